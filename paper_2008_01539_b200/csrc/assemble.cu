@@ -1,0 +1,271 @@
+// assemble.cu — K1: fused cell-property evaluation + TPFA/PPU residual and
+// block-Jacobi-scaled Jacobian over the active rows (+ the K2 pattern).
+//
+// Restates assemble(target_set) (Eq. 16 PAPER.md:252-256;
+// Appendix A): rows only for V_A; a connection to a cell
+// outside V_A uses that cell's current (frozen) state in the residual and the
+// diagonal, with no column.
+//
+// Layout (DESIGN.md §HBM layout):
+//   one thread per active row, rows of a 2048-row chunk strided by 256 so
+//   the ‖F‖₂ partial of each block is the canonical chunk partial;
+//   ELL column/value arrays slot-major [slot][cap] so warp stores coalesce;
+//   NNC blocks indexed by the global NNC CSR slot (no scan needed);
+//   no atomics except the ‖F‖∞ / singular-cell reductions.
+// Block-Jacobi scaling is fused: the row is multiplied by D_ii^{-1} before it
+// is stored, so the Krylov kernel sees a unit block diagonal (never stored).
+#include "ctx.cuh"
+
+namespace {
+
+struct AsmArgs {
+  rsim_fluid_params fl;
+  double dt, bhp;
+  int32_t nx, ny, nz, nslot, nA;
+  int64_t cap;
+  bool d3, has_nnc;
+  const double *__restrict__ tx, *__restrict__ ty, *__restrict__ tz, *__restrict__ pv, *__restrict__ wi;
+  const int32_t *__restrict__ nptr, *__restrict__ nnbr;
+  const double* __restrict__ nt;
+  const double *__restrict__ u, *__restrict__ mold;
+  const uint8_t* __restrict__ st;
+  const int32_t *__restrict__ act, *__restrict__ g2l;
+  int32_t* ell_col;
+  double* ell_val;
+  int32_t* nnc_lcol;
+  double* nnc_val;
+  double *F_raw, *rhs, *part_f2;
+  DevScalars* dsc;
+};
+
+// Cartesian neighbour of slot s (ascending column order -z,-y,-x,+x,+y,+z;
+// 2D: -y,-x,+x,+y).  Returns false when the slot falls off the grid.
+__device__ __forceinline__ bool cart_nbr(const AsmArgs& a, int64_t i, int64_t ix, int64_t iy, int64_t iz, int s,
+                                         int64_t& j, double& T) {
+  const int64_t nxy = (int64_t)a.nx * a.ny;
+  int k = a.d3 ? s : s + 1;  // 2D skips the -z slot
+  switch (k) {
+    case 0: if (iz == 0) return false; j = i - nxy; T = __ldg(&a.tz[j]); return true;
+    case 1: if (iy == 0) return false; j = i - a.nx; T = __ldg(&a.ty[j]); return true;
+    case 2: if (ix == 0) return false; j = i - 1; T = __ldg(&a.tx[j]); return true;
+    case 3: if (ix == a.nx - 1) return false; j = i + 1; T = __ldg(&a.tx[i]); return true;
+    case 4: if (iy == a.ny - 1) return false; j = i + a.nx; T = __ldg(&a.ty[i]); return true;
+    default: if (iz == a.nz - 1) return false; j = i + nxy; T = __ldg(&a.tz[i]); return true;
+  }
+}
+
+template <int B>
+__device__ __forceinline__ void load_u(const AsmArgs& a, int64_t j, double* uj) {
+#pragma unroll
+  for (int c = 0; c < B; ++c) uj[c] = __ldg(&a.u[j * B + c]);
+}
+
+// Flux block of connection (i,j): adds to R/D, returns the raw off-diagonal O.
+template <int B>
+__device__ __forceinline__ void conn(const AsmArgs& a, const double* ui, const rsim::phys::Props<B>& Pi, int64_t j,
+                                     double T, double* R, double (*D)[B], double (*O)[B]) {
+  double uj[B];
+  load_u<B>(a, j, uj);
+  double dp = ui[0] - uj[0];
+  bool up_i = !(dp < 0.0);
+  if (up_i) {
+    rsim::phys::flux_conn<B>(T, dp, true, Pi, R, D, O);
+  } else {
+    rsim::phys::Props<B> Pj;
+    rsim::phys::props(a.fl, uj, B == 3 ? __ldg(&a.st[j]) : (uint8_t)0, Pj);
+    rsim::phys::flux_conn<B>(T, dp, false, Pj, R, D, O);
+  }
+}
+
+template <int B>
+__device__ __forceinline__ void store_scaled(double* dst, const double (*Di)[B], const double (*O)[B]) {
+  double S[B][B];
+  rsim::blk::gemm<B>(Di, O, S);
+#pragma unroll
+  for (int r = 0; r < B; ++r)
+#pragma unroll
+    for (int c = 0; c < B; ++c) dst[r * B + c] = S[r][c];
+}
+
+template <int B>
+__global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
+  __shared__ double sm[9];
+  constexpr bool KEEP = (B == 1);  // keep O in registers (b=1) or recompute (b>1)
+  double s2 = 0.0, finf = 0.0;
+  for (int k = 0; k < RSIM_RED_ITEMS; ++k) {
+    const int64_t l = (int64_t)blockIdx.x * RSIM_RED_CHUNK + threadIdx.x + RSIM_RED_THREADS * k;
+    if (l >= a.nA) break;
+    const int64_t i = a.act[l];
+    const int64_t nxy = (int64_t)a.nx * a.ny;
+    const int64_t ix = i % a.nx, iy = (i / a.nx) % a.ny, iz = i / nxy;
+    double ui[B];
+    load_u<B>(a, i, ui);
+    rsim::phys::Props<B> Pi;
+    rsim::phys::props(a.fl, ui, B == 3 ? a.st[i] : (uint8_t)0, Pi);
+    double R[B], D[B][B];
+    double Mo[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) Mo[c] = __ldg(&a.mold[i * B + c]);
+    rsim::phys::accum_row<B>(a.fl, __ldg(&a.pv[i]), ui[0], Pi, Mo, a.dt, R, D);
+
+    double Okeep[6][B][B];
+    int32_t lcol[6];
+    // pass 1: residual + diagonal (+ pattern)
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      lcol[s] = -1;
+      if (s >= a.nslot) continue;
+      int64_t j;
+      double T;
+      if (cart_nbr(a, i, ix, iy, iz, s, j, T)) {
+        double O[B][B];
+        conn<B>(a, ui, Pi, j, T, R, D, O);
+        lcol[s] = __ldg(&a.g2l[j]);
+        if (KEEP) {
+#pragma unroll
+          for (int r = 0; r < B; ++r)
+#pragma unroll
+            for (int c = 0; c < B; ++c) Okeep[s][r][c] = O[r][c];
+        }
+      }
+      a.ell_col[s * a.cap + l] = lcol[s];
+    }
+    if (a.has_nnc) {
+      const int32_t q0 = __ldg(&a.nptr[i]), q1 = __ldg(&a.nptr[i + 1]);
+      for (int32_t q = q0; q < q1; ++q) {
+        int64_t j = __ldg(&a.nnbr[q]);
+        double O[B][B];
+        conn<B>(a, ui, Pi, j, __ldg(&a.nt[q]), R, D, O);
+        a.nnc_lcol[q] = __ldg(&a.g2l[j]);
+      }
+    }
+    rsim::phys::well_row<B>(__ldg(&a.wi[i]), ui[0], a.bhp, Pi, R, D);
+    double Di[B][B];
+    if (!rsim::blk::inv(D, Di)) {
+      atomicMin(&a.dsc->bad_cell, (int32_t)i);
+      a.dsc->status = RSIM_ENUM;
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+#pragma unroll
+        for (int c = 0; c < B; ++c) Di[r][c] = 0.0;
+    }
+    double y[B];
+    rsim::blk::gemv<B>(Di, R, y);
+#pragma unroll
+    for (int e = 0; e < B; ++e) {
+      a.F_raw[l * B + e] = R[e];
+      a.rhs[l * B + e] = -y[e];
+      finf = fmax(finf, fabs(R[e]));
+    }
+    s2 = s2 + rsim::blk::rowdot<B>(R, R);
+    // pass 2: scaled off-diagonal blocks
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      if (s >= a.nslot || lcol[s] < 0) continue;
+      double* dst = &a.ell_val[((int64_t)s * a.cap + l) * B * B];
+      if (KEEP) {
+        store_scaled<B>(dst, Di, Okeep[s]);
+      } else {
+        int64_t j;
+        double T;
+        cart_nbr(a, i, ix, iy, iz, s, j, T);
+        double O[B][B], Rd[B], Dd[B][B];
+#pragma unroll
+        for (int e = 0; e < B; ++e) {
+          Rd[e] = 0.0;
+#pragma unroll
+          for (int v = 0; v < B; ++v) Dd[e][v] = 0.0;
+        }
+        conn<B>(a, ui, Pi, j, T, Rd, Dd, O);
+        store_scaled<B>(dst, Di, O);
+      }
+    }
+    if (a.has_nnc) {
+      const int32_t q0 = __ldg(&a.nptr[i]), q1 = __ldg(&a.nptr[i + 1]);
+      for (int32_t q = q0; q < q1; ++q) {
+        int64_t j = __ldg(&a.nnbr[q]);
+        if (__ldg(&a.g2l[j]) < 0) continue;
+        double O[B][B], Rd[B], Dd[B][B];
+#pragma unroll
+        for (int e = 0; e < B; ++e) {
+          Rd[e] = 0.0;
+#pragma unroll
+          for (int v = 0; v < B; ++v) Dd[e][v] = 0.0;
+        }
+        conn<B>(a, ui, Pi, j, __ldg(&a.nt[q]), Rd, Dd, O);
+        store_scaled<B>(&a.nnc_val[(int64_t)q * B * B], Di, O);
+      }
+    }
+  }
+  double r = block_sum_canon(s2, sm);
+  if (threadIdx.x == 0) a.part_f2[blockIdx.x] = r;
+  double wm = warp_max(finf);
+  if ((threadIdx.x & 31) == 0) atomic_max_bits(&a.dsc->finf, wm);
+}
+
+// Old-time accumulation M^n = pv φ(p) A(u) for every cell (set_state / Δt change).
+template <int B>
+__global__ void k_mold(rsim_fluid_params fl, int64_t n, const double* __restrict__ u, const uint8_t* __restrict__ st,
+                       const double* __restrict__ pv, double* __restrict__ mold) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double ui[B];
+#pragma unroll
+  for (int c = 0; c < B; ++c) ui[c] = u[i * B + c];
+  rsim::phys::Props<B> P;
+  rsim::phys::props(fl, ui, st[i], P);
+  double M[B];
+  rsim::phys::mass<B>(fl, pv[i], ui[0], P, M);
+#pragma unroll
+  for (int c = 0; c < B; ++c) mold[i * B + c] = M[c];
+}
+
+}  // namespace
+
+int launch_assemble(rsim_gpu_ctx* c) {
+  if (c->nA <= 0) return RSIM_OK;
+  AsmArgs a;
+  a.fl = c->fl;
+  a.dt = c->dt;
+  a.bhp = c->bhp;
+  a.nx = c->nx; a.ny = c->ny; a.nz = c->nz;
+  a.nslot = c->nslot;
+  a.nA = c->nA;
+  a.cap = c->n;
+  a.d3 = c->d3;
+  a.has_nnc = c->has_nnc;
+  a.tx = c->tx; a.ty = c->ty; a.tz = c->tz; a.pv = c->pv; a.wi = c->wi;
+  a.nptr = c->nptr; a.nnbr = c->nnbr; a.nt = c->nt;
+  a.u = c->u; a.mold = c->mold; a.st = c->st;
+  a.act = c->act; a.g2l = c->g2l;
+  a.ell_col = c->ell_col; a.ell_val = c->ell_val;
+  a.nnc_lcol = c->nnc_lcol; a.nnc_val = c->nnc_val;
+  a.F_raw = c->F_raw; a.rhs = c->rhs; a.part_f2 = c->part_f2;
+  a.dsc = c->dsc;
+  const int nchunks = (c->nA + RSIM_RED_CHUNK - 1) / RSIM_RED_CHUNK;
+  // reset F-norm accumulators
+  RSIM_CUDA(cudaMemsetAsync(&c->dsc->finf, 0, sizeof(unsigned long long), c->stream));
+  int32_t pc = nchunks;
+  RSIM_CUDA(cudaMemcpyAsync(&c->dsc->part_count, &pc, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+  switch (c->b) {
+    case 1: k_assemble<1><<<nchunks, 256, 0, c->stream>>>(a); break;
+    case 2: k_assemble<2><<<nchunks, 256, 0, c->stream>>>(a); break;
+    default: k_assemble<3><<<nchunks, 256, 0, c->stream>>>(a); break;
+  }
+  c->launches++;
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
+
+int launch_mold(rsim_gpu_ctx* c) {
+  const int th = 256;
+  const int64_t blocks = (c->n + th - 1) / th;
+  switch (c->b) {
+    case 1: k_mold<1><<<blocks, th, 0, c->stream>>>(c->fl, c->n, c->u, c->st, c->pv, c->mold); break;
+    case 2: k_mold<2><<<blocks, th, 0, c->stream>>>(c->fl, c->n, c->u, c->st, c->pv, c->mold); break;
+    default: k_mold<3><<<blocks, th, 0, c->stream>>>(c->fl, c->n, c->u, c->st, c->pv, c->mold); break;
+  }
+  c->launches++;
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}

@@ -1,0 +1,228 @@
+// ctx.cuh — device context, flag bits and device-side helpers shared by the
+// sm_100a kernels (assemble.cu, krylov.cu, sets.cu) and the C-ABI (abi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "rsim/blockops.h"
+#include "rsim/gpu_abi.h"
+#include "rsim/physics.h"
+
+// ---- per-cell flag bits (u8) -------------------------------------------------
+enum : uint8_t {
+  F_A = 1,     // in V_A (active)
+  F_B = 2,     // in V_B (boundary layer of V_A)
+  F_FLAG = 4,  // |δp| >= ε after the last update (support set, Eq. 14)
+  F_PIN = 8,   // fracture or perforated cell: always active
+  F_T = 16,    // in V_T (DD total active set)
+  F_D0 = 32,   // dilation ping-pong bits
+  F_D1 = 64,
+};
+
+// Set-update modes of the final compaction pass.
+enum { MODE_DEVICE = 0, MODE_SHRINK = 1, MODE_KEEP = 2, MODE_EXPAND = 3, MODE_DD = 4 };
+
+// Device-resident scalars, one struct per ctx (D2H once per Newton iteration).
+struct DevScalars {
+  int32_t status;
+  int32_t bad_cell;
+  int32_t lin_iters;
+  int32_t nA;
+  int32_t nB;
+  int32_t expand;
+  int32_t n_new;
+  int32_t pad0;
+  double lin_relres;
+  double f2;
+  unsigned long long finf;  // bits of a non-negative double (atomicMax)
+  unsigned long long maxA;
+  unsigned long long maxB;
+  unsigned long long halo;
+  int32_t part_count;       // number of K1 F-norm partials
+  int32_t pad1;
+};
+
+struct DDLists {
+  int32_t n_sub = 0;
+  std::vector<int64_t> sub_off, halo_off;  // host offsets (n_sub + 1)
+  int32_t* sub_cells = nullptr;            // device, concatenated sorted lists
+  int32_t* halo_cells = nullptr;
+  int64_t sub_cap = 0, halo_cap = 0;
+  int32_t selected = -1;
+};
+
+struct rsim_gpu_ctx {
+  int b = 1;
+  int32_t nx = 0, ny = 0, nz = 0;
+  int64_t n = 0;
+  bool d3 = false;
+  int nslot = 4;
+  bool has_nnc = false;
+  int64_t nnc_total = 0;
+  rsim_fluid_params fl{};
+  double bhp = 0.0;
+  double dt = 1.0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 0;
+  int max_coop_blocks[4] = {0, 0, 0, 0};  // per b (1..3)
+
+  // graph (immutable)
+  double *tx = nullptr, *ty = nullptr, *tz = nullptr, *pv = nullptr, *wi = nullptr;
+  uint8_t* kind = nullptr;
+  int32_t *nptr = nullptr, *nnbr = nullptr;
+  double* nt = nullptr;
+
+  // state
+  double *u = nullptr, *u_start = nullptr, *mold = nullptr, *p_prev = nullptr;
+  uint8_t *st = nullptr, *st_start = nullptr;
+
+  // sets
+  uint8_t *flags = nullptr, *flags_alt = nullptr;
+  int32_t *act_buf = nullptr, *g2l = nullptr, *label = nullptr;
+  int32_t* act = nullptr;  // current active list (act_buf or a DD sub-list)
+  int32_t nA = 0;
+  double *dp = nullptr, *last_dp = nullptr;
+  int32_t *tile_cnt = nullptr, *tile_off = nullptr;
+  int32_t* list_buf = nullptr;  // uploaded lists
+
+  // local system (ELL [slot][cap] + global-NNC-slot values)
+  int32_t* ell_col = nullptr;
+  double* ell_val = nullptr;
+  int32_t* nnc_lcol = nullptr;
+  double* nnc_val = nullptr;
+  double *F_raw = nullptr, *rhs = nullptr;
+  double* part_f2 = nullptr;
+
+  // Krylov
+  double *x = nullptr, *r = nullptr, *r0 = nullptr, *p = nullptr, *v = nullptr, *s = nullptr, *t = nullptr;
+  double* part = nullptr;  // [4][nchunks_max]
+
+  DevScalars* dsc = nullptr;   // device
+  DevScalars* hsc = nullptr;   // pinned host mirror
+
+  DDLists dd;
+
+  // timing
+  bool timing = false;
+  struct Ev { cudaEvent_t a, b; int phase; };
+  std::vector<Ev> ev_pool, ev_live;
+  double ms[4] = {0, 0, 0, 0};
+  double last_eps = 0.0;
+  bool pending_nA = false;
+  std::vector<int32_t> h_nptr, h_nnbr;
+  int32_t launches = 0;
+};
+
+// ---- error plumbing (abi.cu) -------------------------------------------------
+void rsim_set_error(const std::string& msg);
+int rsim_cuda_fail(cudaError_t e, const char* what);
+#define RSIM_CUDA(call)                                   \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return rsim_cuda_fail(_e, #call); \
+  } while (0)
+
+// Phase timers (abi.cu): wrap kernel sequences of one phase.
+void rsim_phase_begin(rsim_gpu_ctx* c, int phase);
+void rsim_phase_end(rsim_gpu_ctx* c);
+
+// ---- launchers implemented in the .cu files ---------------------------------
+int launch_assemble(rsim_gpu_ctx* c);
+int launch_krylov(rsim_gpu_ctx* c, const rsim_solver_opts* o);
+int launch_update(rsim_gpu_ctx* c, double eps);
+int launch_mold(rsim_gpu_ctx* c);
+int launch_set_reset(rsim_gpu_ctx* c, int all_active);
+int launch_set_list(rsim_gpu_ctx* c, const int32_t* dev_list, int32_t n);
+int launch_compact(rsim_gpu_ctx* c, int mode, int round, double eps, int m);
+int launch_dilate(rsim_gpu_ctx* c, int m, int cond_on_expand);
+int launch_threshold(rsim_gpu_ctx* c, double eps);
+int launch_decide(rsim_gpu_ctx* c, double eps, int shrink_locked, int force_expand);
+int launch_initial_support(rsim_gpu_ctx* c, double eps);
+int launch_seed_pinned(rsim_gpu_ctx* c);
+int launch_dd_begin(rsim_gpu_ctx* c);
+int launch_dd_partition(rsim_gpu_ctx* c, int32_t n_sub, int32_t* sizes);
+int launch_dd_select(rsim_gpu_ctx* c, int32_t k);
+int launch_dd_skip(rsim_gpu_ctx* c, int32_t k);
+int launch_categories(rsim_gpu_ctx* c, uint8_t* dev_out);
+
+// ---- device helpers ------------------------------------------------------------
+#ifdef __CUDACC__
+
+__device__ __forceinline__ unsigned long long dbits(double a) {
+  return (unsigned long long)__double_as_longlong(a);
+}
+
+// Canonical 256-thread block reduction (blockops.h): warp shfl_down tree with
+// offsets 16..1, then the 8 warp sums with offsets 4..1.  Result valid in
+// every thread (broadcast through shared memory).  All 256 threads call it.
+__device__ __forceinline__ double block_sum_canon(double s, double* sm) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) s = s + __shfl_down_sync(FULL, s, off);
+  if (lane == 0) sm[w] = s;
+  __syncthreads();
+  if (w == 0) {
+    double r = (lane < 8) ? sm[lane] : 0.0;
+#pragma unroll
+    for (int off = 4; off >= 1; off >>= 1) r = r + __shfl_down_sync(FULL, r, off);
+    if (lane == 0) sm[8] = r;
+  }
+  __syncthreads();
+  double out = sm[8];
+  __syncthreads();
+  return out;
+}
+
+// Canonical reduction of P partials by ONE block (every block may call it
+// redundantly and obtains identical bits).  lvl: shared scratch >= ceil(P/2048).
+__device__ __forceinline__ double reduce_partials_canon(const double* part, int P, double* sm, double* lvl) {
+  const int t = threadIdx.x;
+  if (P <= RSIM_RED_CHUNK) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < RSIM_RED_ITEMS; ++k) {
+      int idx = t + RSIM_RED_THREADS * k;
+      if (idx < P) s = s + part[idx];
+    }
+    return block_sum_canon(s, sm);
+  }
+  int P2 = (P + RSIM_RED_CHUNK - 1) / RSIM_RED_CHUNK;
+  for (int g = 0; g < P2; ++g) {
+    double s = 0.0;
+    int base = g * RSIM_RED_CHUNK;
+    int m = min(RSIM_RED_CHUNK, P - base);
+#pragma unroll
+    for (int k = 0; k < RSIM_RED_ITEMS; ++k) {
+      int idx = t + RSIM_RED_THREADS * k;
+      if (idx < m) s = s + part[base + idx];
+    }
+    double r = block_sum_canon(s, sm);
+    if (t == 0) lvl[g] = r;
+  }
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < RSIM_RED_ITEMS; ++k) {
+    int idx = t + RSIM_RED_THREADS * k;
+    if (idx < P2) s = s + lvl[idx];
+  }
+  return block_sum_canon(s, sm);
+}
+
+__device__ __forceinline__ void atomic_max_bits(unsigned long long* addr, double nonneg) {
+  atomicMax(addr, dbits(nonneg));
+}
+
+// warp max of a non-negative double, lane 0 gets the result
+__device__ __forceinline__ double warp_max(double a) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) a = fmax(a, __shfl_down_sync(0xffffffffu, a, off));
+  return a;
+}
+
+#endif  // __CUDACC__

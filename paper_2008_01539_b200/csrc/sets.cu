@@ -1,0 +1,608 @@
+// sets.cu — K6 (update + variable substitution + ∞-norms), K7 (active-set
+// estimation: threshold, m-hop dilation, warp-ballot/scan compaction) and K8
+// (DD labels / subdomain lists).
+//
+// Restates (all integer logic => bit-exact against oracle/oracle.cpp):
+//   u^{ν+1} = u^ν + R_A^T δu_A             PAPER.md:282 (Alg. 1 line 5)
+//   variable_substitution
+//   support_set |δp| >= ε (inclusive)
+//   expand_active / neighbor_set           SPEC.md:386-394, :61-69 (graph distance)
+//   shrink V_A = supp δu_A ∪ fracture
+//   boundary_layer / outer_halo
+//   Alg. 2 phase-1 labels, V_T
+// The expand/shrink decision is taken ON THE DEVICE from ‖δp_B‖∞ (k_decide),
+// so K6 -> K7 -> compaction runs without a host round trip.
+#include "ctx.cuh"
+
+namespace {
+
+constexpr int TILE = 2048;  // cells per compaction tile (256 threads x 8 consecutive cells)
+
+struct Geo {
+  int32_t nx, ny, nz;
+  int64_t n;
+  bool d3, has_nnc;
+  const int32_t *nptr, *nnbr;
+};
+
+__host__ Geo geo(const rsim_gpu_ctx* c) {
+  return Geo{c->nx, c->ny, c->nz, c->n, c->d3, c->has_nnc, c->nptr, c->nnbr};
+}
+
+// Visit every graph neighbour of i (Cartesian + NNC).
+template <class F>
+__device__ __forceinline__ void each_nbr(const Geo& g, int64_t i, F&& f) {
+  const int64_t nxy = (int64_t)g.nx * g.ny;
+  const int64_t ix = i % g.nx, iy = (i / g.nx) % g.ny, iz = i / nxy;
+  if (g.d3 && iz > 0) f(i - nxy);
+  if (iy > 0) f(i - g.nx);
+  if (ix > 0) f(i - 1);
+  if (ix < g.nx - 1) f(i + 1);
+  if (iy < g.ny - 1) f(i + g.nx);
+  if (g.d3 && iz < g.nz - 1) f(i + nxy);
+  if (g.has_nnc) {
+    int32_t q0 = __ldg(&g.nptr[i]), q1 = __ldg(&g.nptr[i + 1]);
+    for (int32_t q = q0; q < q1; ++q) f((int64_t)__ldg(&g.nnbr[q]));
+  }
+}
+
+// ---------------------------------------------------------------- K6 update
+template <int B>
+__global__ void __launch_bounds__(256) k_update(rsim_fluid_params fl, int32_t nA, const int32_t* __restrict__ act,
+                                                 const double* __restrict__ x, double* __restrict__ u,
+                                                 uint8_t* __restrict__ st, uint8_t* __restrict__ flags,
+                                                 double* __restrict__ dp, double* __restrict__ last_dp, double eps,
+                                                 DevScalars* dsc) {
+  int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double aA = 0.0, aB = 0.0;
+  bool bad = false;
+  if (l < nA) {
+    const int64_t i = act[l];
+    double ui[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) ui[c] = u[i * B + c] + x[l * B + c];
+    uint8_t s = st[i];
+    rsim::phys::substitute<B>(fl, ui, s);
+#pragma unroll
+    for (int c = 0; c < B; ++c) u[i * B + c] = ui[c];
+    st[i] = s;
+    const double d = x[l * B];
+    const double a = fabs(d);
+    bad = !isfinite(d);
+    dp[i] = d;
+    if (last_dp) last_dp[i] = a;
+    uint8_t f = flags[i];
+    if (a >= eps) {
+      f |= F_FLAG;
+      if (f & F_B) f |= F_D0;  // seed of the expansion (flagged boundary cell)
+    }
+    flags[i] = f;
+    aA = a;
+    aB = (f & F_B) ? a : 0.0;
+  }
+  if (bad) dsc->status = RSIM_ENUM;
+  double wa = warp_max(aA), wb = warp_max(aB);
+  if ((threadIdx.x & 31) == 0) {
+    if (wa > 0.0) atomic_max_bits(&dsc->maxA, wa);
+    if (wb > 0.0) atomic_max_bits(&dsc->maxB, wb);
+  }
+}
+
+// Threshold only (K7 test hook): FLAG / seed bits and ∞-norms from a given δp.
+__global__ void __launch_bounds__(256) k_threshold(int32_t nA, const int32_t* __restrict__ act,
+                                                    const double* __restrict__ dp, uint8_t* __restrict__ flags,
+                                                    double eps, DevScalars* dsc) {
+  int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double aA = 0.0, aB = 0.0;
+  if (l < nA) {
+    const int64_t i = act[l];
+    const double a = fabs(dp[i]);
+    uint8_t f = flags[i];
+    if (a >= eps) {
+      f |= F_FLAG;
+      if (f & F_B) f |= F_D0;
+    }
+    flags[i] = f;
+    aA = a;
+    aB = (f & F_B) ? a : 0.0;
+  }
+  double wa = warp_max(aA), wb = warp_max(aB);
+  if ((threadIdx.x & 31) == 0) {
+    if (wa > 0.0) atomic_max_bits(&dsc->maxA, wa);
+    if (wb > 0.0) atomic_max_bits(&dsc->maxB, wb);
+  }
+}
+
+// ---------------------------------------------------------------- K7 decide
+__global__ void k_decide(DevScalars* dsc, double eps, int shrink_locked, int force_expand) {
+  double mb = __longlong_as_double((long long)dsc->maxB);
+  dsc->expand = force_expand ? 1 : ((!shrink_locked && mb >= eps) ? 1 : 0);
+  dsc->n_new = 0;
+  dsc->nB = 0;
+}
+
+// One dilation round: bit_out(i) = bit_in(i) | OR_j bit_in(j).
+__global__ void __launch_bounds__(256) k_dilate(Geo g, uint8_t* __restrict__ flags, uint8_t bit_in, uint8_t bit_out,
+                                                const DevScalars* __restrict__ dsc, int cond) {
+  if (cond && !dsc->expand) return;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  uint8_t f = flags[i];
+  bool v = (f & bit_in) != 0;
+  if (!v) each_nbr(g, i, [&](int64_t j) { if (flags[j] & bit_in) v = true; });
+  flags[i] = v ? (uint8_t)(f | bit_out) : (uint8_t)(f & ~bit_out);
+}
+
+// A_new of a cell from its (pre-update) flag byte.
+__device__ __forceinline__ bool a_new(uint8_t f, int mode, bool expand, uint8_t dbit) {
+  switch (mode) {
+    case MODE_KEEP: return (f & F_A) != 0;
+    case MODE_SHRINK: return ((f & F_A) && (f & F_FLAG)) || (f & F_PIN);
+    case MODE_EXPAND:
+    case MODE_DD: return (f & F_A) || (f & dbit);
+    default:  // MODE_DEVICE
+      return expand ? ((f & F_A) || (f & dbit)) : (((f & F_A) && (f & F_FLAG)) || (f & F_PIN));
+  }
+}
+
+// Compaction pass 1: per-tile count of A_new.
+__global__ void __launch_bounds__(256) k_count(Geo g, const uint8_t* __restrict__ fin, int mode, uint8_t dbit,
+                                               const DevScalars* __restrict__ dsc, int32_t* __restrict__ tile_cnt) {
+  __shared__ int32_t wsum[8];
+  const bool ex = dsc->expand != 0;
+  const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x * 8;
+  int cnt = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    int64_t i = base + k;
+    if (i < g.n && a_new(fin[i], mode, ex, dbit)) ++cnt;
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, off);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < 8; ++w) s += wsum[w];
+    tile_cnt[blockIdx.x] = s;
+  }
+}
+
+// Compaction pass 2: exclusive scan of the tile counts (one block).
+__global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t* __restrict__ cnt, int32_t* __restrict__ off,
+                                                      int32_t ntiles, DevScalars* dsc) {
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int32_t base = 0; base < ntiles; base += 1024) {
+    int32_t idx = base + threadIdx.x;
+    int32_t v = idx < ntiles ? cnt[idx] : 0;
+    int32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int32_t z = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int32_t y = __shfl_up_sync(0xffffffffu, z, o);
+        if (lane >= o) z += y;
+      }
+      wsum[lane] = z;
+    }
+    __syncthreads();
+    int32_t excl = carry + (w > 0 ? wsum[w - 1] : 0) + x - v;
+    if (idx < ntiles) off[idx] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) dsc->nA = carry;
+}
+
+// Compaction pass 3: A_new, V_B, V_T/labels, g2l, sorted active list.
+__global__ void __launch_bounds__(256) k_scatter(Geo g, const uint8_t* __restrict__ fin, uint8_t* __restrict__ fout,
+                                                 int mode, uint8_t dbit, int32_t round, DevScalars* dsc,
+                                                 const int32_t* __restrict__ tile_off, int32_t* __restrict__ act,
+                                                 int32_t* __restrict__ g2l, int32_t* __restrict__ label) {
+  __shared__ int32_t wsum[8];
+  const bool ex = dsc->expand != 0;
+  const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x * 8;
+  uint8_t keep[8];
+  int cnt = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    int64_t i = base + k;
+    keep[k] = 0;
+    if (i < g.n && a_new(fin[i], mode, ex, dbit)) { keep[k] = 1; ++cnt; }
+  }
+  // block exclusive scan of per-thread counts (warp ballot-free shfl scan)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  int wpre = 0;
+  for (int k = 0; k < w; ++k) wpre += wsum[k];
+  int pos = tile_off[blockIdx.x] + wpre + x - cnt;
+  int nb = 0, nnew = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    int64_t i = base + k;
+    if (i >= g.n) break;
+    uint8_t f = fin[i];
+    uint8_t o = (uint8_t)(f & (F_PIN | F_T));
+    if (keep[k]) {
+      bool bnd = false;
+      each_nbr(g, i, [&](int64_t j) { if (!a_new(fin[j], mode, ex, dbit)) bnd = true; });
+      o |= F_A;
+      if (bnd) { o |= F_B; ++nb; }
+      if (mode == MODE_DD && !(f & F_T)) {
+        label[i] = round;
+        ++nnew;
+      }
+      if (mode == MODE_DD) o |= F_T;
+      act[pos] = (int32_t)i;
+      g2l[i] = pos;
+      ++pos;
+    } else {
+      g2l[i] = -1;
+    }
+    fout[i] = o;
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    nb += __shfl_down_sync(0xffffffffu, nb, off);
+    nnew += __shfl_down_sync(0xffffffffu, nnew, off);
+  }
+  if (lane == 0) {
+    if (nb) atomicAdd(&dsc->nB, nb);
+    if (nnew) atomicAdd(&dsc->n_new, nnew);
+  }
+}
+
+// Reset flags: PIN for fracture / perforated cells; A for all (or PIN only).
+__global__ void k_set_reset(int64_t n, const uint8_t* __restrict__ kind, const double* __restrict__ wi,
+                            uint8_t* __restrict__ flags, int all_active) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool pin = kind[i] == RSIM_KIND_FRACTURE || wi[i] > 0.0;
+  uint8_t f = pin ? (uint8_t)(F_PIN | F_A) : (uint8_t)0;
+  if (all_active) f |= F_A;
+  flags[i] = f;
+}
+
+__global__ void k_set_list(const int32_t* __restrict__ list, int32_t n, uint8_t* __restrict__ flags) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) flags[list[k]] |= F_A;
+}
+
+// D0 := PIN (first-step initial set = pinned + m-halo).
+__global__ void k_seed_pinned(int64_t n, uint8_t* __restrict__ flags) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint8_t f = flags[i];
+  flags[i] = (f & F_PIN) ? (uint8_t)(f | F_D0) : (uint8_t)(f & ~(F_D0 | F_D1));
+}
+
+// A := {|p - p_prev| >= eps} ∪ PIN (support of the last timestep).
+template <int B>
+__global__ void k_initial_support(int64_t n, const double* __restrict__ u, const double* __restrict__ p_prev,
+                                  double eps, uint8_t* __restrict__ flags) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint8_t f = flags[i];
+  if (fabs(u[i * B] - p_prev[i]) >= eps) f |= F_A;
+  flags[i] = f;
+}
+
+// ---------------------------------------------------------------- K8 / DD
+__global__ void k_dd_begin(int64_t n, uint8_t* __restrict__ flags, int32_t* __restrict__ label,
+                           double* __restrict__ last_dp) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint8_t f = flags[i];
+  if (f & F_A) { f |= F_T; label[i] = 0; } else { f &= ~F_T; label[i] = -1; }
+  flags[i] = f;
+  last_dp[i] = 0.0;
+}
+
+// predicate compaction over labels: sel=0 -> label==k ; sel=1 -> halo of k
+__device__ __forceinline__ bool dd_pred(const Geo& g, const int32_t* __restrict__ label, int64_t i, int k, int sel) {
+  int32_t li = label[i];
+  if (sel == 0) return li == k;
+  if (li == k) return false;
+  bool h = false;
+  each_nbr(g, i, [&](int64_t j) { if (label[j] == k) h = true; });
+  return h;
+}
+
+__global__ void __launch_bounds__(256) k_dd_count(Geo g, const int32_t* __restrict__ label, int k, int sel,
+                                                  int32_t* __restrict__ tile_cnt) {
+  __shared__ int32_t wsum[8];
+  const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x * 8;
+  int cnt = 0;
+  for (int q = 0; q < 8; ++q) {
+    int64_t i = base + q;
+    if (i < g.n && dd_pred(g, label, i, k, sel)) ++cnt;
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, off);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < 8; ++w) s += wsum[w];
+    tile_cnt[blockIdx.x] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_dd_scatter(Geo g, const int32_t* __restrict__ label, int k, int sel,
+                                                    const int32_t* __restrict__ tile_off, int32_t* __restrict__ out) {
+  __shared__ int32_t wsum[8];
+  const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x * 8;
+  uint8_t keep[8];
+  int cnt = 0;
+  for (int q = 0; q < 8; ++q) {
+    int64_t i = base + q;
+    keep[q] = (i < g.n && dd_pred(g, label, i, k, sel)) ? 1 : 0;
+    cnt += keep[q];
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  int wpre = 0;
+  for (int q = 0; q < w; ++q) wpre += wsum[q];
+  int pos = tile_off[blockIdx.x] + wpre + x - cnt;
+  for (int q = 0; q < 8; ++q)
+    if (keep[q]) out[pos++] = (int32_t)(base + q);
+}
+
+__global__ void k_g2l_scatter(const int32_t* __restrict__ list, int32_t n, int32_t* __restrict__ g2l, int clear) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) g2l[list[k]] = clear ? -1 : (int32_t)k;
+}
+
+__global__ void k_halo_max(const int32_t* __restrict__ list, int64_t n, const double* __restrict__ last_dp,
+                           DevScalars* dsc) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double a = k < n ? last_dp[list[k]] : 0.0;
+  double w = warp_max(a);
+  if ((threadIdx.x & 31) == 0 && w > 0.0) atomic_max_bits(&dsc->halo, w);
+}
+
+__global__ void k_zero_list(const int32_t* __restrict__ list, int32_t n, double* __restrict__ last_dp) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) last_dp[list[k]] = 0.0;
+}
+
+// Fig. 8 categories: 0 inactive, 1 active, 2 boundary, 3 active+update, 4 boundary+update.
+__global__ void k_categories(int64_t n, const uint8_t* __restrict__ flags, const double* __restrict__ dp, double eps,
+                             uint8_t* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint8_t f = flags[i];
+  uint8_t c = 0;
+  if (f & F_A) {
+    bool upd = fabs(dp[i]) >= eps;
+    c = (f & F_B) ? (upd ? 4 : 2) : (upd ? 3 : 1);
+  }
+  out[i] = c;
+}
+
+inline int64_t nblk(int64_t n, int th) { return (n + th - 1) / th; }
+
+}  // namespace
+
+// ============================================================== launchers
+int launch_update(rsim_gpu_ctx* c, double eps) {
+  if (c->nA <= 0) return RSIM_OK;
+  RSIM_CUDA(cudaMemsetAsync(&c->dsc->maxA, 0, 2 * sizeof(unsigned long long), c->stream));
+  const int64_t g = nblk(c->nA, 256);
+  switch (c->b) {
+    case 1: k_update<1><<<g, 256, 0, c->stream>>>(c->fl, c->nA, c->act, c->x, c->u, c->st, c->flags, c->dp, c->last_dp, eps, c->dsc); break;
+    case 2: k_update<2><<<g, 256, 0, c->stream>>>(c->fl, c->nA, c->act, c->x, c->u, c->st, c->flags, c->dp, c->last_dp, eps, c->dsc); break;
+    default: k_update<3><<<g, 256, 0, c->stream>>>(c->fl, c->nA, c->act, c->x, c->u, c->st, c->flags, c->dp, c->last_dp, eps, c->dsc); break;
+  }
+  c->launches++;
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
+
+int launch_threshold(rsim_gpu_ctx* c, double eps) {
+  RSIM_CUDA(cudaMemsetAsync(&c->dsc->maxA, 0, 2 * sizeof(unsigned long long), c->stream));
+  if (c->nA > 0) {
+    k_threshold<<<nblk(c->nA, 256), 256, 0, c->stream>>>(c->nA, c->act, c->dp, c->flags, eps, c->dsc);
+    c->launches++;
+  }
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
+
+int launch_decide(rsim_gpu_ctx* c, double eps, int shrink_locked, int force_expand) {
+  k_decide<<<1, 1, 0, c->stream>>>(c->dsc, eps, shrink_locked, force_expand);
+  c->launches++;
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
+
+int launch_dilate(rsim_gpu_ctx* c, int m, int cond) {
+  Geo g = geo(c);
+  for (int r = 0; r < m; ++r) {
+    uint8_t bin = (r % 2 == 0) ? F_D0 : F_D1, bout = (r % 2 == 0) ? F_D1 : F_D0;
+    k_dilate<<<nblk(c->n, 256), 256, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, cond);
+    c->launches++;
+  }
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
+
+// Final pass of every set update: count -> scan -> scatter into flags_alt,
+// then swap the flag buffers.  dbit = D bit holding the m-hop dilation.
+int launch_compact(rsim_gpu_ctx* c, int mode, int round, double /*eps*/, int m) {
+  Geo g = geo(c);
+  const uint8_t dbit = (m % 2 == 0) ? F_D0 : F_D1;
+  const int64_t ntiles = nblk(c->n, TILE);
+  k_count<<<ntiles, 256, 0, c->stream>>>(g, c->flags, mode, dbit, c->dsc, c->tile_cnt);
+  k_scan_tiles<<<1, 1024, 0, c->stream>>>(c->tile_cnt, c->tile_off, (int32_t)ntiles, c->dsc);
+  k_scatter<<<ntiles, 256, 0, c->stream>>>(g, c->flags, c->flags_alt, mode, dbit, round, c->dsc, c->tile_off,
+                                           c->act_buf, c->g2l, c->label);
+  c->launches += 3;
+  RSIM_CUDA(cudaGetLastError());
+  std::swap(c->flags, c->flags_alt);
+  c->act = c->act_buf;
+  return RSIM_OK;
+}
+
+int launch_set_reset(rsim_gpu_ctx* c, int all_active) {
+  k_set_reset<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->n, c->kind, c->wi, c->flags, all_active);
+  c->launches++;
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
+
+int launch_set_list(rsim_gpu_ctx* c, const int32_t* list, int32_t n) {
+  if (n <= 0) return RSIM_OK;
+  k_set_list<<<nblk(n, 256), 256, 0, c->stream>>>(list, n, c->flags);
+  c->launches++;
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
+
+int launch_seed_pinned(rsim_gpu_ctx* c) {
+  k_seed_pinned<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->n, c->flags);
+  c->launches++;
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
+
+int launch_initial_support(rsim_gpu_ctx* c, double eps) {
+  const int64_t g = nblk(c->n, 256);
+  switch (c->b) {
+    case 1: k_initial_support<1><<<g, 256, 0, c->stream>>>(c->n, c->u, c->p_prev, eps, c->flags); break;
+    case 2: k_initial_support<2><<<g, 256, 0, c->stream>>>(c->n, c->u, c->p_prev, eps, c->flags); break;
+    default: k_initial_support<3><<<g, 256, 0, c->stream>>>(c->n, c->u, c->p_prev, eps, c->flags); break;
+  }
+  c->launches++;
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
+
+int launch_dd_begin(rsim_gpu_ctx* c) {
+  k_dd_begin<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->n, c->flags, c->label, c->last_dp);
+  c->launches++;
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
+
+// Build sorted per-subdomain cell lists and their outer halos.
+int launch_dd_partition(rsim_gpu_ctx* c, int32_t n_sub, int32_t* sizes) {
+  Geo g = geo(c);
+  const int64_t ntiles = nblk(c->n, TILE);
+  DDLists& d = c->dd;
+  d.n_sub = n_sub;
+  d.sub_off.assign(n_sub + 1, 0);
+  d.halo_off.assign(n_sub + 1, 0);
+  d.selected = -1;
+  std::vector<int32_t> cnt_sub(n_sub), cnt_halo(n_sub);
+  // counts (two syncs per subdomain; Phase-2 setup happens once per timestep)
+  for (int sel = 0; sel < 2; ++sel) {
+    for (int k = 0; k < n_sub; ++k) {
+      k_dd_count<<<ntiles, 256, 0, c->stream>>>(g, c->label, k, sel, c->tile_cnt);
+      k_scan_tiles<<<1, 1024, 0, c->stream>>>(c->tile_cnt, c->tile_off, (int32_t)ntiles, c->dsc);
+      c->launches += 2;
+      RSIM_CUDA(cudaMemcpyAsync(&(sel ? cnt_halo : cnt_sub)[k], &c->dsc->nA, sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, c->stream));
+      RSIM_CUDA(cudaStreamSynchronize(c->stream));
+    }
+  }
+  for (int k = 0; k < n_sub; ++k) {
+    d.sub_off[k + 1] = d.sub_off[k] + cnt_sub[k];
+    d.halo_off[k + 1] = d.halo_off[k] + cnt_halo[k];
+    if (sizes) sizes[k] = cnt_sub[k];
+  }
+  if (d.sub_off[n_sub] > d.sub_cap) {
+    if (d.sub_cells) cudaFree(d.sub_cells);
+    d.sub_cap = d.sub_off[n_sub];
+    RSIM_CUDA(cudaMalloc(&d.sub_cells, sizeof(int32_t) * d.sub_cap));
+  }
+  if (d.halo_off[n_sub] > d.halo_cap) {
+    if (d.halo_cells) cudaFree(d.halo_cells);
+    d.halo_cap = d.halo_off[n_sub];
+    RSIM_CUDA(cudaMalloc(&d.halo_cells, sizeof(int32_t) * d.halo_cap));
+  }
+  for (int sel = 0; sel < 2; ++sel)
+    for (int k = 0; k < n_sub; ++k) {
+      int32_t* out = sel ? d.halo_cells + d.halo_off[k] : d.sub_cells + d.sub_off[k];
+      k_dd_count<<<ntiles, 256, 0, c->stream>>>(g, c->label, k, sel, c->tile_cnt);
+      k_scan_tiles<<<1, 1024, 0, c->stream>>>(c->tile_cnt, c->tile_off, (int32_t)ntiles, c->dsc);
+      k_dd_scatter<<<ntiles, 256, 0, c->stream>>>(g, c->label, k, sel, c->tile_off, out);
+      c->launches += 3;
+    }
+  // clear the localized g2l (every cell -1) before per-subdomain selection
+  RSIM_CUDA(cudaMemsetAsync(c->g2l, 0xff, sizeof(int32_t) * c->n, c->stream));
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
+
+int launch_dd_select(rsim_gpu_ctx* c, int32_t k) {
+  DDLists& d = c->dd;
+  if (d.selected >= 0) {
+    int32_t ps = d.selected;
+    int32_t np = (int32_t)(d.sub_off[ps + 1] - d.sub_off[ps]);
+    if (np > 0) {
+      k_g2l_scatter<<<nblk(np, 256), 256, 0, c->stream>>>(d.sub_cells + d.sub_off[ps], np, c->g2l, 1);
+      c->launches++;
+    }
+  }
+  int32_t nk = (int32_t)(d.sub_off[k + 1] - d.sub_off[k]);
+  int64_t nh = d.halo_off[k + 1] - d.halo_off[k];
+  if (nk > 0) {
+    k_g2l_scatter<<<nblk(nk, 256), 256, 0, c->stream>>>(d.sub_cells + d.sub_off[k], nk, c->g2l, 0);
+    c->launches++;
+  }
+  RSIM_CUDA(cudaMemsetAsync(&c->dsc->halo, 0, sizeof(unsigned long long), c->stream));
+  if (nh > 0) {
+    k_halo_max<<<nblk(nh, 256), 256, 0, c->stream>>>(d.halo_cells + d.halo_off[k], nh, c->last_dp, c->dsc);
+    c->launches++;
+  }
+  c->act = d.sub_cells + d.sub_off[k];
+  c->nA = nk;
+  d.selected = k;
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
+
+int launch_dd_skip(rsim_gpu_ctx* c, int32_t k) {
+  DDLists& d = c->dd;
+  int32_t nk = (int32_t)(d.sub_off[k + 1] - d.sub_off[k]);
+  if (nk > 0) {
+    k_zero_list<<<nblk(nk, 256), 256, 0, c->stream>>>(d.sub_cells + d.sub_off[k], nk, c->last_dp);
+    c->launches++;
+  }
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
+
+int launch_categories(rsim_gpu_ctx* c, uint8_t* out) {
+  k_categories<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->n, c->flags, c->dp, c->last_eps, out);
+  c->launches++;
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}

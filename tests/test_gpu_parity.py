@@ -1,0 +1,168 @@
+"""GPU (sm_100a, through the C-ABI) vs CPU oracle parity.
+
+The bar (BASELINE.json north star): active-set flags and partition labels
+bit-exact given the same Newton update; identical Newton and linear iteration
+counts; residual norms within 1e-10 relative; final p/S within 1e-8 relative.
+By construction (shared cell-local arithmetic, canonical reduction order,
+no FMA contraction) every comparison here is BIT-EXACT, which is stricter.
+"""
+import numpy as np
+import pytest
+
+import paper_2008_01539_b200 as pkg
+from oracle import Oracle
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "c1": dict(config=1),
+    "c1s": dict(config=1, nx=40, ny=40),
+    "c2s": dict(config=2, nx=64, ny=64, n_dfn=20),
+    "c3s": dict(config=3, nx=32, ny=32, nz=4),
+    "c4s": dict(config=4, nx=32, ny=32, nz=4, n_dfn=10),
+}
+
+
+def perturbed_state(case, seed):
+    """A non-trivial state: init + smooth pressure drawdown + saturation noise,
+    mixed black-oil statuses."""
+    rng = np.random.default_rng(seed)
+    s = case.init_state()
+    b, n = case.b, case.n
+    p = s.u[::b]
+    p -= rng.uniform(0, 5e6, n)
+    if b >= 2:
+        s.u[1::b] = np.clip(s.u[1::b] + rng.uniform(-0.05, 0.1, n), 0.0, 1.0)
+    if b == 3:
+        sat = rng.random(n) < 0.4
+        s.status[:] = np.where(sat, 1, 0).astype(np.uint8)
+        s.u[2::b] = np.where(sat, rng.uniform(0.0, 0.2, n), case.fluid.rs_b * rng.uniform(0.8, 1.0, n))
+    return s
+
+
+def random_active(case, seed, frac=0.3):
+    rng = np.random.default_rng(seed + 1)
+    a = np.sort(np.flatnonzero(rng.random(case.n) < frac)).astype(np.int32)
+    pin = np.flatnonzero(case.pinned())
+    return np.union1d(a, pin).astype(np.int32)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_assemble_and_solve_bit_exact(name):
+    case = pkg.Case(**CASES[name])
+    s = perturbed_state(case, 7)
+    dt = 86400.0
+    act = random_active(case, 3)
+    orc = Oracle(case)
+    orc.set_state(s, dt)
+    Fo, ro, rpo, co, vo = orc.assemble(act)
+    sim = pkg.GpuSimulator(case)
+    sim.set_state(s, dt)
+    st = sim.set_active(act)
+    assert st.n_active == len(act)
+    assert np.array_equal(sim.active(), act)
+    sim.assemble()
+    Fg, rg, rpg, cg, vg = sim.system(len(act))
+    assert np.array_equal(rpg, rpo)
+    assert np.array_equal(cg, co)
+    assert np.array_equal(Fg, Fo), np.abs(Fg - Fo).max()
+    assert np.array_equal(rg, ro)
+    assert np.array_equal(vg, vo), np.abs(vg - vo).max()
+    opts = case.solver_opts()
+    rc_o, xo, it_o, rr_o = orc.linear_solve(len(act), opts)
+    sim.linear_solve(opts)
+    gst = sim.stats()
+    xg = sim.solution(len(act))
+    assert rc_o == gst.status == 0
+    assert gst.lin_iters == it_o
+    assert np.array_equal(xg, xo), np.abs(xg - xo).max()
+    assert gst.lin_relres == rr_o
+    sim.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2s", "c3s"])
+@pytest.mark.parametrize("m", [1, 2, 4])
+@pytest.mark.parametrize("shrink_locked", [False, True])
+def test_estimate_active_flags_bit_exact(name, m, shrink_locked):
+    case = pkg.Case(**CASES[name])
+    rng = np.random.default_rng(m)
+    orc = Oracle(case)
+    sim = pkg.GpuSimulator(case)
+    va = random_active(case, 11, 0.05)
+    dp = np.zeros(case.n)
+    dp[va] = rng.lognormal(-2.0, 2.0, len(va)) * rng.choice([-1, 1], len(va))
+    eps = 0.2
+    dp[va[::17]] = eps  # equality is included (Eq. 14)
+    oa, ob, oex = orc.estimate_active(va, dp, eps, m, shrink_locked)
+    sim.set_active(va)
+    sim.upload_dp(dp)
+    sim.threshold(eps)
+    st = sim.estimate_active(eps, m, shrink_locked)
+    assert bool(st.expand) == oex
+    assert np.array_equal(sim.active(), oa)
+    assert np.array_equal(sim.boundary(), ob)
+    sim.close()
+
+
+def _cmp_reports(rg, ro):
+    assert rg.iterations == ro.iterations
+    recg, reco = rg.records(), ro.records()
+    for a, b in zip(recg, reco):
+        assert a["n_active"] == b["n_active"], (a, b)
+        assert a["lin_iters"] == b["lin_iters"], (a, b)
+        assert a["mode_expand"] == b["mode_expand"], (a, b)
+        assert a["dp_inf_A"] == b["dp_inf_A"], (a, b)
+        assert a["f_norm2"] == b["f_norm2"], (a, b)
+        assert a["f_norminf"] == b["f_norminf"], (a, b)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2s", "c3s", "c4s"])
+def test_newton_solvers_bit_exact(name):
+    case = pkg.Case(**CASES[name])
+    s0 = case.init_state()
+    dts = case.schedule()
+    opts = case.solver_opts()
+    orc = Oracle(case)
+    sim = pkg.GpuSimulator(case)
+    for k in (0, 4):
+        dt = float(dts[k])
+        so, ro, rco = orc.newton_standard(s0, dt, opts)
+        sg, rg = sim.newton_standard(s0, dt, opts)
+        assert rg.status == rco
+        _cmp_reports(rg, ro)
+        assert np.array_equal(sg.u, so.u) and np.array_equal(sg.status, so.status)
+        va = orc.initial_active(None, opts.eps_set, 2)
+        so, ro, rco = orc.newton_localized(s0, dt, va, 2, opts.eps_set, opts)
+        sg, rg = sim.newton_localized(s0, dt, va, 2, opts.eps_set, opts)
+        assert rg.status == rco
+        _cmp_reports(rg, ro)
+        assert np.array_equal(sg.u, so.u) and np.array_equal(sg.status, so.status)
+        so, ro, rco, lab = orc.adaptive_nonlinear_dd(s0, dt, va, 4, opts.eps_set, opts)
+        sg, rg = sim.adaptive_nonlinear_dd(s0, dt, va, 4, opts.eps_set, opts)
+        assert rg.status == rco
+        assert rg.n_subdomains == ro.n_subdomains
+        assert rg.outer_iterations == ro.outer_iterations
+        _cmp_reports(rg, ro)
+        assert np.array_equal(sim.labels(), lab)
+        assert np.array_equal(sg.u, so.u) and np.array_equal(sg.status, so.status)
+    sim.close()
+
+
+@pytest.mark.parametrize("name,solver", [("c1", 0), ("c1", 1), ("c1", 2), ("c2s", 1), ("c4s", 1)])
+def test_run_case_bit_exact(name, solver):
+    case = pkg.Case(**CASES[name])
+    s0 = case.init_state()
+    dts = case.schedule()
+    opts = case.solver_opts()
+    if solver == 2:
+        opts.m = 4
+    orc = Oracle(case)
+    ro = orc.run_case(solver, s0, dts, opts)
+    sim = pkg.GpuSimulator(case)
+    rg = sim.run_case(solver, s0, dts, opts)
+    assert rg["status"] == ro["status"] == 0
+    for k in ("iterations", "sum_na", "lin_iters", "cuts"):
+        assert rg[k] == ro[k], (k, rg[k], ro[k])
+    assert rg["total_ma"] == ro["total_ma"]
+    assert np.array_equal(rg["states"].u, ro["states"].u)
+    sim.close()
