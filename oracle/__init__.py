@@ -47,6 +47,11 @@ PROTOS = {
     "orc_initial_active": (C.c_int32, [P, d, C.c_double, C.c_int32, i32]),
     "orc_run_case": (C.c_int, [P, C.c_int32, d, C.c_int32, C.POINTER(A.SolverOpts), i32, d, i64, i32, i32]),
     "orc_full_residual": (C.c_int, [P, d]),
+    "orc_rexp": (C.c_double, [C.c_double]),
+    "orc_corey": (None, [C.c_double, C.c_double, C.c_double, d, d]),
+    "orc_props": (C.c_int, [C.POINTER(A.FluidParams), d, C.c_uint8, d, d, d, d]),
+    "orc_set_u": (C.c_int, [P, d, u8]),
+    "orc_assemble_raw": (C.c_int64, [P, i32, C.c_int32, d, d, i32, i32, d, C.c_int64]),
 }
 
 _lib = None
@@ -84,6 +89,26 @@ def build_matrix_grid(nx, ny, nz, dx, dy, dz, kx, ky, kz):
     if rc != 0:
         raise ValueError("build_matrix_grid: configuration error")
     return tx, ty, tz
+
+
+def rexp(x: float) -> float:
+    return float(lib().orc_rexp(x))
+
+
+def corey(s: float, s_r: float, den: float) -> tuple[float, float]:
+    kr, dkr = C.c_double(), C.c_double()
+    lib().orc_corey(s, s_r, den, C.byref(kr), C.byref(dkr))
+    return kr.value, dkr.value
+
+
+def props(fluid, u, st=0):
+    """(A, dA, L, dL) of one cell (include/rsim/physics.h)."""
+    b = int(fluid.kind)
+    u = np.ascontiguousarray(u, np.float64)
+    Aa, dA, L, dL = np.zeros(b), np.zeros(b * b), np.zeros(b), np.zeros(b * b)
+    lib().orc_props(C.byref(fluid), A.ptr(u, C.c_double), st, A.ptr(Aa, C.c_double), A.ptr(dA, C.c_double),
+                    A.ptr(L, C.c_double), A.ptr(dL, C.c_double))
+    return Aa, dA.reshape(b, b), L, dL.reshape(b, b)
 
 
 class Oracle:
@@ -127,6 +152,23 @@ class Oracle:
         self.L.orc_assemble(self._h, A.ptr(act, C.c_int32), nA, None, None, None, A.ptr(col, C.c_int32),
                             A.ptr(val, C.c_double), nnz)
         return F, rhs, rp, col[:nnz], val[: nnz * b * b]
+
+    def set_u(self, states):
+        self.L.orc_set_u(self._h, A.ptr(states.u, C.c_double), A.ptr(states.status, C.c_uint8))
+
+    def assemble_raw(self, act: np.ndarray):
+        act = np.ascontiguousarray(act, np.int32)
+        nA, b = len(act), self.b
+        F, D, rp = np.zeros(nA * b), np.zeros(nA * b * b), np.zeros(nA + 1, np.int32)
+        nnz = self.L.orc_assemble_raw(self._h, A.ptr(act, C.c_int32), nA, A.ptr(F, C.c_double),
+                                      A.ptr(D, C.c_double), A.ptr(rp, C.c_int32), None, None, 0)
+        if nnz < 0:
+            raise ArithmeticError("singular")
+        col = np.zeros(max(nnz, 1), np.int32)
+        val = np.zeros(max(nnz, 1) * b * b)
+        self.L.orc_assemble_raw(self._h, A.ptr(act, C.c_int32), nA, None, None, None, A.ptr(col, C.c_int32),
+                                A.ptr(val, C.c_double), nnz)
+        return F, D.reshape(nA, b, b), rp, col[:nnz], val[: nnz * b * b].reshape(-1, b, b)
 
     def linear_solve(self, nA: int, opts):
         x = np.zeros(max(nA * self.b, 1))

@@ -83,6 +83,8 @@ struct Model {
   std::vector<int32_t> act, g2l, rowptr, col;
   std::vector<double> val, Fraw, rhs;
   int bad_cell = -1;
+  bool raw = false;            // unscaled assembly (property tests)
+  std::vector<double> diag;    // raw diagonal blocks when raw
 };
 
 // ---------------------------------------------------------------- reductions
@@ -200,6 +202,13 @@ static bool assemble_row(Model& M, int32_t l) {
     }
   });
   phys::well_row<B>(g.wi[i], ui[0], g.bhp, Pi, R, D);
+  if (M.raw) {
+    for (int e = 0; e < B; ++e) {
+      M.Fraw[(int64_t)l * B + e] = R[e];
+      for (int v = 0; v < B; ++v) M.diag[((int64_t)l * B + e) * B + v] = D[e][v];
+    }
+    return true;
+  }
   double Di[B][B];
   if (!blk::inv(D, Di)) return false;
   double y[B];
@@ -240,6 +249,7 @@ static int assemble(Model& M, const int32_t* act, int32_t nA) {
   M.val.assign(nnzb * B * B, 0.0);
   M.Fraw.assign((int64_t)nA * B, 0.0);
   M.rhs.assign((int64_t)nA * B, 0.0);
+  if (M.raw) M.diag.assign((int64_t)nA * B * B, 0.0);
   int32_t bad = -1;
 #pragma omp parallel for schedule(static)
   for (int32_t l = 0; l < nA; ++l)
@@ -859,6 +869,61 @@ int orc_run_case(void* h, int32_t solver, const double* dts, int32_t nsteps, con
   }
   delete rep;
   return status;
+}
+
+double orc_rexp(double x) { return phys::rexp(x); }
+
+void orc_corey(double s, double s_r, double den, double* kr, double* dkr) { phys::corey2(s, s_r, den, *kr, *dkr); }
+
+}  // extern "C"
+
+template <int B>
+static void props_out(const rsim_fluid_params* f, const double* u, uint8_t st, double* A, double* dA, double* L,
+                      double* dL) {
+  phys::Props<B> P;
+  phys::props(*f, u, st, P);
+  for (int e = 0; e < B; ++e) {
+    A[e] = P.A[e];
+    L[e] = P.L[e];
+    for (int v = 0; v < B; ++v) { dA[e * B + v] = P.dA[e][v]; dL[e * B + v] = P.dL[e][v]; }
+  }
+}
+
+extern "C" {
+
+int orc_props(const rsim_fluid_params* f, const double* u, uint8_t st, double* A, double* dA, double* L, double* dL) {
+  switch (f->kind) {
+    case 1: props_out<1>(f, u, st, A, dA, L, dL); return RSIM_OK;
+    case 2: props_out<2>(f, u, st, A, dA, L, dL); return RSIM_OK;
+    case 3: props_out<3>(f, u, st, A, dA, L, dL); return RSIM_OK;
+    default: return RSIM_EARG;
+  }
+}
+
+int orc_set_u(void* h, const double* u, const uint8_t* st) {
+  Model& M = *static_cast<Model*>(h);
+  std::memcpy(M.u.data(), u, sizeof(double) * M.u.size());
+  std::memcpy(M.st.data(), st, M.st.size());
+  return RSIM_OK;
+}
+
+int64_t orc_assemble_raw(void* h, const int32_t* act, int32_t nA, double* F_raw, double* diag, int32_t* rowptr,
+                         int32_t* col, double* val, int64_t cap_nnzb) {
+  Model& M = *static_cast<Model*>(h);
+  M.raw = true;
+  int st = assemble_any(M, act, nA);
+  M.raw = false;
+  if (st < 0) return st;
+  const int B = M.b;
+  int64_t nnzb = M.rowptr[nA];
+  if (F_raw) std::memcpy(F_raw, M.Fraw.data(), sizeof(double) * nA * B);
+  if (diag) std::memcpy(diag, M.diag.data(), sizeof(double) * nA * B * B);
+  if (rowptr) std::memcpy(rowptr, M.rowptr.data(), sizeof(int32_t) * (nA + 1));
+  if (col && val && cap_nnzb >= nnzb) {
+    std::memcpy(col, M.col.data(), sizeof(int32_t) * nnzb);
+    std::memcpy(val, M.val.data(), sizeof(double) * nnzb * B * B);
+  }
+  return nnzb;
 }
 
 int orc_full_residual(void* h, double* F_raw) {

@@ -81,6 +81,18 @@ int orc_run_case(void* h, int32_t solver, const double* dts, int32_t nsteps,
                  const rsim_solver_opts* o, int32_t* total_iters, double* total_ma,
                  int64_t* total_na, int32_t* total_lin, int32_t* n_cuts);
 
+/* Property-suite hooks. */
+double orc_rexp(double x);
+void orc_corey(double s, double s_r, double den, double* kr, double* dkr);
+/* Cell properties for the fluid's b: A[b], dA[b*b], L[b], dL[b*b]. */
+int orc_props(const rsim_fluid_params* f, const double* u, uint8_t st, double* A, double* dA, double* L, double* dL);
+/* Set the current iterate WITHOUT touching the old-time accumulation. */
+int orc_set_u(void* h, const double* u, const uint8_t* st);
+/* Unscaled assembly: raw F, raw diagonal blocks (nA*b*b) and raw
+ * off-diagonal blocks in canonical CSR order.  Returns nnzb. */
+int64_t orc_assemble_raw(void* h, const int32_t* act, int32_t nA, double* F_raw, double* diag,
+                         int32_t* rowptr, int32_t* col, double* val, int64_t cap_nnzb);
+
 /* Residual of the current state on the FULL cell set (for mass balance /
  * restriction tests); F_raw has n*b entries. */
 int orc_full_residual(void* h, double* F_raw);
