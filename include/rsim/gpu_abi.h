@@ -53,6 +53,8 @@ typedef struct {
 } rsim_gpu_stats;
 
 /* ---- context / data movement ------------------------------------------ */
+/* Select the CUDA device of the calling thread (one process per GPU). */
+int rsim_gpu_set_device(int32_t device);
 int rsim_gpu_create(rsim_gpu_ctx** ctx, const rsim_graph_desc* g, const rsim_fluid_params* f);
 int rsim_gpu_destroy(rsim_gpu_ctx* ctx);
 const char* rsim_gpu_last_error(void);
@@ -112,6 +114,25 @@ int rsim_gpu_download_dp(rsim_gpu_ctx* ctx, double* dp_global);
  * [0] set/compaction, [1] assembly, [2] Krylov, [3] update. */
 int rsim_gpu_timers(rsim_gpu_ctx* ctx, int32_t enable, double* ms4, int32_t* launches);
 
+/* Work counters accumulated by the host solvers since the last reset:
+ * [0] rows assembled, [1] Krylov row-iterations Σ n_A·its, [2] Krylov solves,
+ * [3] Krylov launches' rows Σ n_A, [4] set-update passes (full-grid scans). */
+int rsim_gpu_counters(rsim_gpu_ctx* ctx, int64_t* out5, int32_t reset);
+
+/* CUDA events on the ctx stream (bench timing on the launching stream). */
+int rsim_gpu_mark(rsim_gpu_ctx* ctx, int32_t slot);                 /* slot < 64 */
+int rsim_gpu_elapsed(rsim_gpu_ctx* ctx, int32_t a, int32_t b, double* ms);
+/* Write a 512 MB scratch buffer (> 126 MB L2) on the ctx stream. */
+int rsim_gpu_flush_l2(rsim_gpu_ctx* ctx);
+/* Device-side checkpoint of (u, status): 0 = save, 1 = restore. */
+int rsim_gpu_checkpoint(rsim_gpu_ctx* ctx, int32_t restore);
+/* Config-5 style set estimation from an uploaded global δp: seeds =
+ * {|δp| >= eps} over ALL cells, m-hop dilation, compaction (support_set +
+ * neighbor_set + compaction of SPEC.md:359-394 on the whole grid). */
+int rsim_gpu_support_active(rsim_gpu_ctx* ctx, double eps, int32_t m, rsim_gpu_stats* st);
+/* Set p := p_hi - dp_scale * δp (global δp already uploaded), for c5. */
+int rsim_gpu_state_from_dp(rsim_gpu_ctx* ctx, double p_hi, double dp_scale);
+
 /* ---- solver-level entry points (SPEC signatures) ----------------------- */
 /* states in/out are host buffers (u[n*b], status[n]); Δt in seconds. */
 int rsim_newton_standard(rsim_gpu_ctx* ctx, double* u, uint8_t* status, double dt,
@@ -133,6 +154,11 @@ int rsim_adaptive_nonlinear_dd_dev(rsim_gpu_ctx* ctx, const rsim_solver_opts* o,
 int rsim_run_case(rsim_gpu_ctx* ctx, int32_t solver, double* u, uint8_t* status, const double* dts,
                   int32_t nsteps, const rsim_solver_opts* o, int32_t* total_iters, double* total_ma,
                   int64_t* total_na, int32_t* total_lin, int32_t* n_cuts);
+
+/* run_case on the state already resident on the device (no H2D/D2H). */
+int rsim_run_case_dev(rsim_gpu_ctx* ctx, int32_t solver, const double* dts, int32_t nsteps,
+                      const rsim_solver_opts* o, int32_t* total_iters, double* total_ma,
+                      int64_t* total_na, int32_t* total_lin, int32_t* n_cuts);
 
 #ifdef __cplusplus
 }

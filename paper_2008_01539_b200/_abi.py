@@ -109,6 +109,8 @@ PROTOS: dict[str, tuple] = {
     "rsim_case_n_nnc": (C.c_int64, [P]),
     "rsim_case_c5_field": (C.c_double, [P, C.c_double, C.c_int32, C.c_double, dptr, dptr]),
     # gpu_abi.h
+    "rsim_gpu_set_device": (C.c_int, [C.c_int32]),
+    "rsim_gpu_counters": (C.c_int, [P, i64ptr, C.c_int32]),
     "rsim_gpu_create": (C.c_int, [C.POINTER(P), C.POINTER(GraphDesc), C.POINTER(FluidParams)]),
     "rsim_gpu_destroy": (C.c_int, [P]),
     "rsim_gpu_last_error": (C.c_char_p, []),
@@ -138,6 +140,14 @@ PROTOS: dict[str, tuple] = {
     "rsim_gpu_threshold": (C.c_int, [P, C.c_double]),
     "rsim_gpu_download_dp": (C.c_int, [P, dptr]),
     "rsim_gpu_timers": (C.c_int, [P, C.c_int32, dptr, i32ptr]),
+    "rsim_gpu_mark": (C.c_int, [P, C.c_int32]),
+    "rsim_gpu_elapsed": (C.c_int, [P, C.c_int32, C.c_int32, dptr]),
+    "rsim_gpu_flush_l2": (C.c_int, [P]),
+    "rsim_gpu_checkpoint": (C.c_int, [P, C.c_int32]),
+    "rsim_gpu_support_active": (C.c_int, [P, C.c_double, C.c_int32, C.POINTER(GpuStats)]),
+    "rsim_gpu_state_from_dp": (C.c_int, [P, C.c_double, C.c_double]),
+    "rsim_run_case_dev": (C.c_int, [P, C.c_int32, dptr, C.c_int32, C.POINTER(SolverOpts), i32ptr, dptr, i64ptr,
+                                    i32ptr, i32ptr]),
     "rsim_newton_standard": (C.c_int, [P, dptr, u8ptr, C.c_double, C.POINTER(SolverOpts), C.POINTER(NewtonReport)]),
     "rsim_newton_localized": (C.c_int, [P, dptr, u8ptr, C.c_double, i32ptr, C.c_int32, C.c_int32, C.c_double,
                                         C.POINTER(SolverOpts), C.POINTER(NewtonReport)]),

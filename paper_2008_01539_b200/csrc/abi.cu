@@ -150,6 +150,19 @@ int rsim_gpu_device_info(char* name, int32_t cap, int32_t* sm_count, int32_t* ma
   return RSIM_OK;
 }
 
+int rsim_gpu_set_device(int32_t device) {
+  RSIM_CUDA(cudaSetDevice(device));
+  return RSIM_OK;
+}
+
+int rsim_gpu_counters(rsim_gpu_ctx* c, int64_t* out5, int32_t reset) {
+  if (out5)
+    for (int k = 0; k < 5; ++k) out5[k] = c->counters[k];
+  if (reset)
+    for (int k = 0; k < 5; ++k) c->counters[k] = 0;
+  return RSIM_OK;
+}
+
 int rsim_gpu_create(rsim_gpu_ctx** out, const rsim_graph_desc* g, const rsim_fluid_params* f) {
   if (!out || !g || !f || f->kind < 1 || f->kind > 3 || g->nx < 1 || g->ny < 1 || g->nz < 1) {
     rsim_set_error("rsim_gpu_create: bad argument");
@@ -229,10 +242,12 @@ int rsim_gpu_destroy(rsim_gpu_ctx* c) {
                   c->mold, c->p_prev, c->st, c->st_start, c->flags, c->flags_alt, c->act_buf, c->g2l, c->label,
                   c->list_buf, c->dp, c->last_dp, c->tile_cnt, c->tile_off, c->ell_col, c->ell_val, c->nnc_lcol,
                   c->nnc_val, c->F_raw, c->rhs, c->part_f2, c->x, c->r, c->r0, c->p, c->v, c->s, c->t, c->part,
-                  c->dsc, c->dd.sub_cells, c->dd.halo_cells};
+                  c->dsc, c->dd.sub_cells, c->dd.halo_cells, c->u_ckpt, c->st_ckpt, c->l2_scratch, c->pin0};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hsc) cudaFreeHost(c->hsc);
+  for (auto& e : c->marks)
+    if (e) cudaEventDestroy(e);
   for (auto& e : c->ev_pool) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
   for (auto& e : c->ev_live) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -310,6 +325,7 @@ int rsim_gpu_estimate_active(rsim_gpu_ctx* c, double eps, int32_t m, int32_t shr
   TRY(launch_decide(c, eps, shrink_locked, 0));
   TRY(launch_dilate(c, m, 1));
   TRY(launch_compact(c, MODE_DEVICE, 0, eps, m));
+  c->counters[4] += 1;
   rsim_phase_end(c);
   c->pending_nA = true;
   if (st) {
@@ -321,6 +337,7 @@ int rsim_gpu_estimate_active(rsim_gpu_ctx* c, double eps, int32_t m, int32_t shr
 
 int rsim_gpu_assemble(rsim_gpu_ctx* c) {
   rsim_phase_begin(c, 1);
+  c->counters[0] += c->nA;
   TRY(rsim_internal_reset_scalars(c));
   TRY(launch_assemble(c));
   rsim_phase_end(c);
@@ -330,6 +347,8 @@ int rsim_gpu_assemble(rsim_gpu_ctx* c) {
 int rsim_gpu_linear_solve(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   if (!o) return RSIM_EARG;
   rsim_phase_begin(c, 2);
+  c->counters[2] += 1;
+  c->counters[3] += c->nA;
   TRY(launch_krylov(c, o));
   rsim_phase_end(c);
   return RSIM_OK;
@@ -351,6 +370,11 @@ int rsim_gpu_threshold(rsim_gpu_ctx* c, double eps) {
 int rsim_gpu_stats_get(rsim_gpu_ctx* c, rsim_gpu_stats* st) {
   TRY(sync_stats(c));
   fill_stats(c, st);
+  return RSIM_OK;
+}
+
+int rsim_internal_add_row_iters(rsim_gpu_ctx* c, int64_t v) {
+  c->counters[1] += v;
   return RSIM_OK;
 }
 
@@ -500,6 +524,65 @@ int rsim_gpu_timers(rsim_gpu_ctx* c, int32_t enable, double* ms4, int32_t* launc
     c->launches = 0;
   }
   return RSIM_OK;
+}
+
+int rsim_gpu_mark(rsim_gpu_ctx* c, int32_t slot) {
+  if (slot < 0 || slot >= 64) return RSIM_EARG;
+  if (!c->marks[slot]) RSIM_CUDA(cudaEventCreate(&c->marks[slot]));
+  RSIM_CUDA(cudaEventRecord(c->marks[slot], c->stream));
+  return RSIM_OK;
+}
+
+int rsim_gpu_elapsed(rsim_gpu_ctx* c, int32_t a, int32_t b, double* ms) {
+  if (a < 0 || a >= 64 || b < 0 || b >= 64 || !c->marks[a] || !c->marks[b]) return RSIM_EARG;
+  RSIM_CUDA(cudaEventSynchronize(c->marks[b]));
+  float f = 0.f;
+  RSIM_CUDA(cudaEventElapsedTime(&f, c->marks[a], c->marks[b]));
+  *ms = f;
+  return RSIM_OK;
+}
+
+int rsim_gpu_flush_l2(rsim_gpu_ctx* c) {
+  const size_t bytes = 512ull << 20;
+  if (!c->l2_scratch) RSIM_CUDA(cudaMalloc(&c->l2_scratch, bytes));
+  RSIM_CUDA(cudaMemsetAsync(c->l2_scratch, c->launches & 0xff, bytes, c->stream));
+  return RSIM_OK;
+}
+
+int rsim_gpu_checkpoint(rsim_gpu_ctx* c, int32_t restore) {
+  if (!c->u_ckpt) {
+    TRY(dalloc(&c->u_ckpt, c->n * c->b));
+    TRY(dalloc(&c->st_ckpt, c->n));
+  }
+  if (restore) {
+    RSIM_CUDA(cudaMemcpyAsync(c->u, c->u_ckpt, sizeof(double) * c->n * c->b, cudaMemcpyDeviceToDevice, c->stream));
+    RSIM_CUDA(cudaMemcpyAsync(c->st, c->st_ckpt, c->n, cudaMemcpyDeviceToDevice, c->stream));
+  } else {
+    RSIM_CUDA(cudaMemcpyAsync(c->u_ckpt, c->u, sizeof(double) * c->n * c->b, cudaMemcpyDeviceToDevice, c->stream));
+    RSIM_CUDA(cudaMemcpyAsync(c->st_ckpt, c->st, c->n, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  return RSIM_OK;
+}
+
+int rsim_gpu_support_active(rsim_gpu_ctx* c, double eps, int32_t m, rsim_gpu_stats* st) {
+  c->last_eps = eps;
+  rsim_phase_begin(c, 0);
+  TRY(launch_set_reset(c, 0));
+  TRY(launch_seed_support(c, eps));
+  TRY(launch_dilate(c, m, 0));
+  TRY(launch_compact(c, MODE_EXPAND, 0, eps, m));
+  rsim_phase_end(c);
+  c->pending_nA = true;
+  if (st) {
+    TRY(sync_stats(c));
+    fill_stats(c, st);
+  }
+  return RSIM_OK;
+}
+
+int rsim_gpu_state_from_dp(rsim_gpu_ctx* c, double p_hi, double scale) {
+  TRY(launch_state_from_dp(c, p_hi, scale));
+  return begin_step(c, c->dt);
 }
 
 }  // extern "C"

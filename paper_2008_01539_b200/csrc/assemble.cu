@@ -7,8 +7,8 @@
 // diagonal, with no column.
 //
 // Layout (DESIGN.md §HBM layout):
-//   one thread per active row, rows of a 2048-row chunk strided by 256 so
-//   the ‖F‖₂ partial of each block is the canonical chunk partial;
+//   one thread per active row (‖F‖₂ is reduced canonically by the Krylov
+//   kernel's init phase, which reads F anyway);
 //   ELL column/value arrays slot-major [slot][cap] so warp stores coalesce;
 //   NNC blocks indexed by the global NNC CSR slot (no scan needed);
 //   no atomics except the ‖F‖∞ / singular-cell reductions.
@@ -89,12 +89,11 @@ __device__ __forceinline__ void store_scaled(double* dst, const double (*Di)[B],
 
 template <int B>
 __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
-  __shared__ double sm[9];
   constexpr bool KEEP = (B == 1);  // keep O in registers (b=1) or recompute (b>1)
-  double s2 = 0.0, finf = 0.0;
-  for (int k = 0; k < RSIM_RED_ITEMS; ++k) {
-    const int64_t l = (int64_t)blockIdx.x * RSIM_RED_CHUNK + threadIdx.x + RSIM_RED_THREADS * k;
-    if (l >= a.nA) break;
+  double finf = 0.0;
+  {
+    const int64_t l = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (l < a.nA) {
     const int64_t i = a.act[l];
     const int64_t nxy = (int64_t)a.nx * a.ny;
     const int64_t ix = i % a.nx, iy = (i / a.nx) % a.ny, iz = i / nxy;
@@ -157,7 +156,6 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
       a.rhs[l * B + e] = -y[e];
       finf = fmax(finf, fabs(R[e]));
     }
-    s2 = s2 + rsim::blk::rowdot<B>(R, R);
     // pass 2: scaled off-diagonal blocks
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
@@ -196,9 +194,8 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
         store_scaled<B>(&a.nnc_val[(int64_t)q * B * B], Di, O);
       }
     }
+    }
   }
-  double r = block_sum_canon(s2, sm);
-  if (threadIdx.x == 0) a.part_f2[blockIdx.x] = r;
   double wm = warp_max(finf);
   if ((threadIdx.x & 31) == 0) atomic_max_bits(&a.dsc->finf, wm);
 }
@@ -242,15 +239,11 @@ int launch_assemble(rsim_gpu_ctx* c) {
   a.nnc_lcol = c->nnc_lcol; a.nnc_val = c->nnc_val;
   a.F_raw = c->F_raw; a.rhs = c->rhs; a.part_f2 = c->part_f2;
   a.dsc = c->dsc;
-  const int nchunks = (c->nA + RSIM_RED_CHUNK - 1) / RSIM_RED_CHUNK;
-  // reset F-norm accumulators
-  RSIM_CUDA(cudaMemsetAsync(&c->dsc->finf, 0, sizeof(unsigned long long), c->stream));
-  int32_t pc = nchunks;
-  RSIM_CUDA(cudaMemcpyAsync(&c->dsc->part_count, &pc, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+  const int64_t nblocks = (c->nA + 255) / 256;
   switch (c->b) {
-    case 1: k_assemble<1><<<nchunks, 256, 0, c->stream>>>(a); break;
-    case 2: k_assemble<2><<<nchunks, 256, 0, c->stream>>>(a); break;
-    default: k_assemble<3><<<nchunks, 256, 0, c->stream>>>(a); break;
+    case 1: k_assemble<1><<<nblocks, 256, 0, c->stream>>>(a); break;
+    case 2: k_assemble<2><<<nblocks, 256, 0, c->stream>>>(a); break;
+    default: k_assemble<3><<<nblocks, 256, 0, c->stream>>>(a); break;
   }
   c->launches++;
   RSIM_CUDA(cudaGetLastError());

@@ -115,6 +115,12 @@ struct rsim_gpu_ctx {
   bool pending_nA = false;
   std::vector<int32_t> h_nptr, h_nnbr;
   int32_t launches = 0;
+  cudaEvent_t marks[64] = {};
+  double* u_ckpt = nullptr;
+  uint8_t* st_ckpt = nullptr;
+  void* l2_scratch = nullptr;
+  int64_t counters[5] = {0, 0, 0, 0, 0};
+  uint8_t* pin0 = nullptr;  // F_PIN|F_A for pinned cells, 0 elsewhere (reset source)
 };
 
 // ---- error plumbing (abi.cu) -------------------------------------------------
@@ -133,6 +139,9 @@ void rsim_phase_end(rsim_gpu_ctx* c);
 // ---- launchers implemented in the .cu files ---------------------------------
 int launch_assemble(rsim_gpu_ctx* c);
 int launch_krylov(rsim_gpu_ctx* c, const rsim_solver_opts* o);
+// returns RSIM_ENOTAPPLICABLE when the system does not fit one cluster
+constexpr int RSIM_ENOTAPPLICABLE = 100;
+int launch_krylov_dsm(rsim_gpu_ctx* c, const rsim_solver_opts* o);
 int launch_update(rsim_gpu_ctx* c, double eps);
 int launch_mold(rsim_gpu_ctx* c);
 int launch_set_reset(rsim_gpu_ctx* c, int all_active);
@@ -148,6 +157,8 @@ int launch_dd_partition(rsim_gpu_ctx* c, int32_t n_sub, int32_t* sizes);
 int launch_dd_select(rsim_gpu_ctx* c, int32_t k);
 int launch_dd_skip(rsim_gpu_ctx* c, int32_t k);
 int launch_categories(rsim_gpu_ctx* c, uint8_t* dev_out);
+int launch_seed_support(rsim_gpu_ctx* c, double eps);
+int launch_state_from_dp(rsim_gpu_ctx* c, double p_hi, double scale);
 
 // ---- device helpers ------------------------------------------------------------
 #ifdef __CUDACC__

@@ -271,13 +271,21 @@ __global__ void __launch_bounds__(256) k_scatter(Geo g, const uint8_t* __restric
   }
 }
 
-// Reset flags: PIN for fracture / perforated cells; A for all (or PIN only).
-__global__ void k_set_reset(int64_t n, const uint8_t* __restrict__ kind, const double* __restrict__ wi,
-                            uint8_t* __restrict__ flags, int all_active) {
+// Pinned-cell mask (fracture or perforated), computed once per context.
+__global__ void k_pin_mask(int64_t n, const uint8_t* __restrict__ kind, const double* __restrict__ wi,
+                           uint8_t* __restrict__ pin0) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   bool pin = kind[i] == RSIM_KIND_FRACTURE || wi[i] > 0.0;
-  uint8_t f = pin ? (uint8_t)(F_PIN | F_A) : (uint8_t)0;
+  pin0[i] = pin ? (uint8_t)(F_PIN | F_A) : (uint8_t)0;
+}
+
+// Reset flags to the pinned set (A|PIN), or to all-active.
+__global__ void k_set_reset(int64_t n, const uint8_t* __restrict__ pin0, uint8_t* __restrict__ flags,
+                            int all_active) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint8_t f = pin0[i];
   if (all_active) f |= F_A;
   flags[i] = f;
 }
@@ -406,6 +414,22 @@ __global__ void k_categories(int64_t n, const uint8_t* __restrict__ flags, const
   out[i] = c;
 }
 
+// D0 := {|δp| >= eps} over all cells (c5 synthetic update).
+__global__ void k_seed_support(int64_t n, const double* __restrict__ dp, double eps, uint8_t* __restrict__ flags) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint8_t f = flags[i] & (uint8_t)~(F_D0 | F_D1);
+  if (fabs(dp[i]) >= eps) f |= F_D0;
+  flags[i] = f;
+}
+
+template <int B>
+__global__ void k_state_from_dp(int64_t n, const double* __restrict__ dp, double p_hi, double scale,
+                                double* __restrict__ u) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) u[i * B] = p_hi - scale * dp[i];
+}
+
 inline int64_t nblk(int64_t n, int th) { return (n + th - 1) / th; }
 
 }  // namespace
@@ -471,7 +495,12 @@ int launch_compact(rsim_gpu_ctx* c, int mode, int round, double /*eps*/, int m) 
 }
 
 int launch_set_reset(rsim_gpu_ctx* c, int all_active) {
-  k_set_reset<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->n, c->kind, c->wi, c->flags, all_active);
+  if (!c->pin0) {
+    RSIM_CUDA(cudaMalloc(&c->pin0, c->n));
+    k_pin_mask<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->n, c->kind, c->wi, c->pin0);
+    c->launches++;
+  }
+  k_set_reset<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->n, c->pin0, c->flags, all_active);
   c->launches++;
   RSIM_CUDA(cudaGetLastError());
   return RSIM_OK;
@@ -596,6 +625,25 @@ int launch_dd_skip(rsim_gpu_ctx* c, int32_t k) {
     k_zero_list<<<nblk(nk, 256), 256, 0, c->stream>>>(d.sub_cells + d.sub_off[k], nk, c->last_dp);
     c->launches++;
   }
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
+
+int launch_seed_support(rsim_gpu_ctx* c, double eps) {
+  k_seed_support<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->n, c->dp, eps, c->flags);
+  c->launches++;
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
+
+int launch_state_from_dp(rsim_gpu_ctx* c, double p_hi, double scale) {
+  const int64_t g = nblk(c->n, 256);
+  switch (c->b) {
+    case 1: k_state_from_dp<1><<<g, 256, 0, c->stream>>>(c->n, c->dp, p_hi, scale, c->u); break;
+    case 2: k_state_from_dp<2><<<g, 256, 0, c->stream>>>(c->n, c->dp, p_hi, scale, c->u); break;
+    default: k_state_from_dp<3><<<g, 256, 0, c->stream>>>(c->n, c->dp, p_hi, scale, c->u); break;
+  }
+  c->launches++;
   RSIM_CUDA(cudaGetLastError());
   return RSIM_OK;
 }

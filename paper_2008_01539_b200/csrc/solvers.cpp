@@ -24,6 +24,7 @@ int rsim_internal_dd_begin(rsim_gpu_ctx* c);
 int64_t rsim_internal_n(const rsim_gpu_ctx* c);
 int rsim_internal_b(const rsim_gpu_ctx* c);
 int32_t rsim_internal_nA(const rsim_gpu_ctx* c);
+extern "C" int rsim_internal_add_row_iters(rsim_gpu_ctx* c, int64_t v);
 
 namespace {
 
@@ -51,7 +52,8 @@ int local_step(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   return RSIM_OK;
 }
 
-void fill_rec(rsim_iter_record& rec, int32_t nA, const rsim_gpu_stats& s) {
+void fill_rec(rsim_iter_record& rec, int32_t nA, const rsim_gpu_stats& s, rsim_gpu_ctx* c) {
+  rsim_internal_add_row_iters(c, (int64_t)nA * s.lin_iters);
   rec.n_active = nA;
   rec.lin_iters = s.lin_iters;
   rec.dp_inf_A = s.dp_inf_A;
@@ -71,7 +73,7 @@ int standard_dev(rsim_gpu_ctx* c, const rsim_solver_opts* o, rsim_newton_report*
     TRY(rsim_gpu_stats_get(c, &s));
     rsim_iter_record rec{};
     rec.subdomain = -1;
-    fill_rec(rec, (int32_t)n, s);
+    fill_rec(rec, (int32_t)n, s, c);
     rec.dp_inf_B = 0.0;
     rep_push(rep, rec, n);
     if (s.status != RSIM_OK) { rep->status = s.status; return s.status; }
@@ -95,7 +97,7 @@ int localized_dev(rsim_gpu_ctx* c, const rsim_solver_opts* o, rsim_newton_report
     TRY(rsim_gpu_estimate_active(c, o->eps_set, o->m, shrink_locked, &s));
     rsim_iter_record rec{};
     rec.subdomain = -1;
-    fill_rec(rec, nA, s);
+    fill_rec(rec, nA, s, c);
     rec.mode_expand = s.expand;
     rep_push(rep, rec, n);
     if (s.status != RSIM_OK) { rep->status = s.status; return s.status; }
@@ -123,7 +125,7 @@ int dd_dev(rsim_gpu_ctx* c, const rsim_solver_opts* o, rsim_newton_report* rep) 
     TRY(rsim_gpu_dd_expand(c, o->eps_set, o->m, k + 1, &s));
     rsim_iter_record rec{};
     rec.subdomain = -1;
-    fill_rec(rec, nA, s);
+    fill_rec(rec, nA, s, c);
     rec.mode_expand = s.expand;
     rep_push(rep, rec, n);
     if (s.status != RSIM_OK) { rep->status = s.status; return s.status; }
@@ -149,7 +151,7 @@ int dd_dev(rsim_gpu_ctx* c, const rsim_solver_opts* o, rsim_newton_report* rep) 
         TRY(rsim_gpu_stats_get(c, &s));
         rsim_iter_record rec{};
         rec.subdomain = sd;
-        fill_rec(rec, sizes[sd], s);
+        fill_rec(rec, sizes[sd], s, c);
         rec.dp_inf_B = hmax;
         rep_push(rep, rec, n);
         if (s.status != RSIM_OK) { rep->outer_iterations = outer; rep->status = s.status; return s.status; }
@@ -221,13 +223,13 @@ int rsim_adaptive_nonlinear_dd(rsim_gpu_ctx* c, double* u, uint8_t* status, doub
   return r;
 }
 
-int rsim_run_case(rsim_gpu_ctx* c, int32_t solver, double* u, uint8_t* status, const double* dts, int32_t nsteps,
-                  const rsim_solver_opts* o, int32_t* total_iters, double* total_ma, int64_t* total_na,
-                  int32_t* total_lin, int32_t* n_cuts) {
-  if (!c || !u || !status || !dts || !o) return RSIM_EARG;
+int rsim_run_case_dev(rsim_gpu_ctx* c, int32_t solver, const double* dts, int32_t nsteps, const rsim_solver_opts* o,
+                      int32_t* total_iters, double* total_ma, int64_t* total_na, int32_t* total_lin,
+                      int32_t* n_cuts) {
+  if (!c || !dts || !o || nsteps < 1) return RSIM_EARG;
   *total_iters = 0; *total_ma = 0.0; *total_na = 0; *total_lin = 0; *n_cuts = 0;
   rsim_newton_report* rep = new rsim_newton_report;
-  int r = rsim_gpu_set_state(c, u, status, dts[0]);
+  int r = RSIM_OK;
   std::deque<double> q(dts, dts + nsteps);
   bool first = true;
   int status_out = RSIM_OK;
@@ -263,9 +265,18 @@ int rsim_run_case(rsim_gpu_ctx* c, int32_t solver, double* u, uint8_t* status, c
   }
   delete rep;
   if (r != RSIM_OK) return r;
-  int g = rsim_gpu_get_state(c, u, status);
-  if (g != RSIM_OK) return g;
   return status_out;
+}
+
+int rsim_run_case(rsim_gpu_ctx* c, int32_t solver, double* u, uint8_t* status, const double* dts, int32_t nsteps,
+                  const rsim_solver_opts* o, int32_t* total_iters, double* total_ma, int64_t* total_na,
+                  int32_t* total_lin, int32_t* n_cuts) {
+  if (!c || !u || !status || !dts || !o || nsteps < 1) return RSIM_EARG;
+  TRY(rsim_gpu_set_state(c, u, status, dts[0]));
+  int r = rsim_run_case_dev(c, solver, dts, nsteps, o, total_iters, total_ma, total_na, total_lin, n_cuts);
+  if (r == RSIM_ECUDA || r == RSIM_EARG) return r;
+  TRY(rsim_gpu_get_state(c, u, status));
+  return r;
 }
 
 }  // extern "C"

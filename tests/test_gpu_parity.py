@@ -20,6 +20,8 @@ CASES = {
     "c2s": dict(config=2, nx=64, ny=64, n_dfn=20),
     "c3s": dict(config=3, nx=32, ny=32, nz=4),
     "c4s": dict(config=4, nx=32, ny=32, nz=4, n_dfn=10),
+    "c5m": dict(config=5, nx=64, ny=64, nz=8),      # 32768 rows: cooperative-grid Krylov path
+    "c2m": dict(config=2, nx=160, ny=160, n_dfn=30),  # 25600 rows, b=2: cooperative-grid path
 }
 
 
