@@ -5,25 +5,24 @@
  * dot product produce identical bits on both sides.
  *
  * Canonical reduction (sum of per-row values v_0..v_{n-1}):
- *   rows are cut into chunks of RSIM_RED_CHUNK = 2048; inside chunk c,
- *   "thread" t (0..255) sums rows 2048c + t + 256k, k = 0..7, in increasing
- *   k starting from +0.0; the 256 thread sums are combined by the tree
+ *   rows are cut into consecutive chunks of RSIM_RED_CHUNK = 256; inside a
+ *   chunk, "thread" t holds v[256c + t] (+0.0 past the end) and the 256 values
+ *   are combined by the tree
  *     for off in 16,8,4,2,1:  s[lane] += s[lane+off]   (inside each warp)
- *     for off in 4,2,1:       w[k]   += w[k+off]        (over the 8 warps)
+ *     for off in 4,2,1:       w[k]   += w[k+off]        (over the 8 warp sums)
  *   giving one partial per chunk.  If there is more than one chunk the
  *   partials are reduced again with the same rule (recursively).
- * On the GPU this is exactly a 256-thread block doing __shfl_down_sync;
- * oracle/ replays the same tree in plain loops.  Per-row values for b>1
- * are the in-order component sums (row dot = Σ_c a_c b_c, c ascending).
+ * On the GPU a chunk is exactly 8 warps doing __shfl_down_sync, so any CTA
+ * that owns whole chunks reduces them locally; oracle/ replays the same tree
+ * in plain loops.  Per-row values for b>1 are the in-order component sums
+ * (row dot = Σ_c a_c b_c, c ascending).
  */
 #ifndef RSIM_BLOCKOPS_H
 #define RSIM_BLOCKOPS_H
 
 #include "physics.h"
 
-#define RSIM_RED_THREADS 256
-#define RSIM_RED_ITEMS 8
-#define RSIM_RED_CHUNK (RSIM_RED_THREADS * RSIM_RED_ITEMS)
+#define RSIM_RED_CHUNK 256
 
 namespace rsim {
 namespace blk {

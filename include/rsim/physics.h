@@ -217,38 +217,35 @@ RSIM_HD void accum_row(const rsim_fluid_params& f, double pv, double p, const Pr
 
 /* Phase-potential-upwinded TPFA connection (i,j) with Υ = T, dp = p_i − p_j,
  * U = properties of the upwind cell (i when dp >= 0, else j).
- * Adds to R and D (row i); writes the off-diagonal block O = ∂F_ij/∂u_j. */
+ * flux_terms: the residual term Rc = T·L_up·dp, the diagonal term Dc and the
+ * off-diagonal block O = ∂F_ij/∂u_j (not accumulated);
+ * flux_conn: adds Rc to R and Dc to D of row i (the canonical order is the
+ * order in which connections are visited). */
 template <int B>
-RSIM_HD void flux_conn(double T, double dp, bool up_i, const Props<B>& U,
-                       double* R, double (*D)[B], double (*O)[B]) {
+RSIM_HD void flux_terms(double T, double dp, bool up_i, const Props<B>& U, double* Rc, double (*Dc)[B],
+                        double (*O)[B]) {
   for (int e = 0; e < B; ++e) {
     double tl = T * U.L[e];
-    R[e] = R[e] + tl * dp;
+    Rc[e] = tl * dp;
     for (int v = 0; v < B; ++v) {
       double c = (T * U.dL[e][v]) * dp;
       double di = up_i ? c : 0.0;
       double dj = up_i ? 0.0 : c;
       if (v == 0) { di = di + tl; dj = dj - tl; }
-      D[e][v] = D[e][v] + di;
+      Dc[e][v] = di;
       O[e][v] = dj;
     }
   }
 }
 
-/* Residual-only variant for a frozen (inactive) neighbour: the Dirichlet
- * contribution of SPEC.md:272; R gets exactly the same bits as flux_conn. */
 template <int B>
-RSIM_HD void flux_conn_frozen(double T, double dp, bool up_i, const Props<B>& U,
-                              double* R, double (*D)[B]) {
+RSIM_HD void flux_conn(double T, double dp, bool up_i, const Props<B>& U,
+                       double* R, double (*D)[B], double (*O)[B]) {
+  double Rc[B], Dc[B][B];
+  flux_terms<B>(T, dp, up_i, U, Rc, Dc, O);
   for (int e = 0; e < B; ++e) {
-    double tl = T * U.L[e];
-    R[e] = R[e] + tl * dp;
-    for (int v = 0; v < B; ++v) {
-      double c = (T * U.dL[e][v]) * dp;
-      double di = up_i ? c : 0.0;
-      if (v == 0) di = di + tl;
-      D[e][v] = D[e][v] + di;
-    }
+    R[e] = R[e] + Rc[e];
+    for (int v = 0; v < B; ++v) D[e][v] = D[e][v] + Dc[e][v];
   }
 }
 

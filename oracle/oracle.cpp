@@ -88,8 +88,8 @@ struct Model {
 };
 
 // ---------------------------------------------------------------- reductions
-// Canonical reduction (blockops.h): 256 "threads" x 8 items per 2048-row
-// chunk, warp trees with offsets 16..1, then 8 warp sums with offsets 4..1.
+// Canonical reduction (blockops.h): 256-row chunks, warp trees with offsets
+// 16..1, then the 8 warp sums with offsets 4..1; recursive over partials.
 static double chunk_tree(double* t) {
   double w[8];
   for (int wp = 0; wp < 8; ++wp) {
@@ -106,14 +106,7 @@ static double chunk_tree(double* t) {
 template <class RowFn>
 static double chunk_reduce_fn(int64_t base, int64_t m, RowFn&& fn) {
   double t[256];
-  for (int th = 0; th < 256; ++th) {
-    double s = 0.0;
-    for (int k = 0; k < 8; ++k) {
-      int64_t idx = th + 256 * k;
-      if (idx < m) s = s + fn(base + idx);
-    }
-    t[th] = s;
-  }
+  for (int th = 0; th < 256; ++th) t[th] = th < m ? fn(base + th) : 0.0;
   return chunk_tree(t);
 }
 

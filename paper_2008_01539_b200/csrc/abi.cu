@@ -208,7 +208,7 @@ int rsim_gpu_create(rsim_gpu_ctx** out, const rsim_graph_desc* g, const rsim_flu
   TRY(dalloc(&c->part_f2, nchunks));
   TRY(dalloc(&c->x, n * b)); TRY(dalloc(&c->r, n * b)); TRY(dalloc(&c->r0, n * b));
   TRY(dalloc(&c->p, n * b)); TRY(dalloc(&c->v, n * b)); TRY(dalloc(&c->s, n * b)); TRY(dalloc(&c->t, n * b));
-  TRY(dalloc(&c->part, 4 * nchunks));
+  TRY(dalloc(&c->part, 4 * nchunks + 64));
   TRY(dalloc(&c->dsc, 1));
   RSIM_CUDA(cudaMallocHost((void**)&c->hsc, sizeof(DevScalars)));
   std::memset(c->hsc, 0, sizeof(DevScalars));

@@ -87,55 +87,90 @@ __device__ __forceinline__ void store_scaled(double* dst, const double (*Di)[B],
     for (int c = 0; c < B; ++c) dst[r * B + c] = S[r][c];
 }
 
+// 8 lanes per active row: lanes 0..nslot-1 evaluate one Cartesian connection
+// each (neighbour properties, PPU terms, raw off-diagonal block), lane 7 owns
+// the row: accumulation, the connection terms added in canonical slot order,
+// NNC connections, the well, D^{-1}; then every lane stores its scaled block.
+// The terms are computed by physics.h flux_terms() and added in the same order
+// as flux_conn() in the oracle, so rows are bit-identical.
+constexpr int LPR = 8;
+constexpr int RPB = 256 / LPR;
+
 template <int B>
 __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
-  constexpr bool KEEP = (B == 1);  // keep O in registers (b=1) or recompute (b>1)
+  __shared__ double sRc[RPB][6][B];
+  __shared__ double sDc[RPB][6][B * B];
+  __shared__ double sDi[RPB][B * B];
+  __shared__ unsigned char sHas[RPB][6];
+  const int rg = threadIdx.x / LPR, q = threadIdx.x % LPR;
+  const int64_t l = (int64_t)blockIdx.x * RPB + rg;
+  const bool valid = l < a.nA;
   double finf = 0.0;
-  {
-    const int64_t l = (int64_t)blockIdx.x * 256 + threadIdx.x;
-    if (l < a.nA) {
-    const int64_t i = a.act[l];
+  int64_t i = 0, ix = 0, iy = 0, iz = 0;
+  double ui[B];
+  rsim::phys::Props<B> Pi;
+  if (valid) {
+    i = a.act[l];
     const int64_t nxy = (int64_t)a.nx * a.ny;
-    const int64_t ix = i % a.nx, iy = (i / a.nx) % a.ny, iz = i / nxy;
-    double ui[B];
+    ix = i % a.nx; iy = (i / a.nx) % a.ny; iz = i / nxy;
     load_u<B>(a, i, ui);
-    rsim::phys::Props<B> Pi;
     rsim::phys::props(a.fl, ui, B == 3 ? a.st[i] : (uint8_t)0, Pi);
-    double R[B], D[B][B];
-    double Mo[B];
+  }
+  double O[B][B];
+  int32_t lcol = -1;
+  if (valid && q < a.nslot) {
+    int64_t j;
+    double T;
+    bool has = false;
+    if (cart_nbr(a, i, ix, iy, iz, q, j, T)) {
+      double uj[B];
+      load_u<B>(a, j, uj);
+      const double dp = ui[0] - uj[0];
+      const bool up_i = !(dp < 0.0);
+      double Rc[B], Dc[B][B];
+      if (up_i) {
+        rsim::phys::flux_terms<B>(T, dp, true, Pi, Rc, Dc, O);
+      } else {
+        rsim::phys::Props<B> Pj;
+        rsim::phys::props(a.fl, uj, B == 3 ? __ldg(&a.st[j]) : (uint8_t)0, Pj);
+        rsim::phys::flux_terms<B>(T, dp, false, Pj, Rc, Dc, O);
+      }
+#pragma unroll
+      for (int e = 0; e < B; ++e) {
+        sRc[rg][q][e] = Rc[e];
+#pragma unroll
+        for (int v = 0; v < B; ++v) sDc[rg][q][e * B + v] = Dc[e][v];
+      }
+      lcol = __ldg(&a.g2l[j]);
+      has = true;
+    }
+    sHas[rg][q] = has;
+    a.ell_col[q * a.cap + l] = lcol;
+  }
+  __syncwarp();
+  if (valid && q == LPR - 1) {
+    double R[B], D[B][B], Mo[B];
 #pragma unroll
     for (int c = 0; c < B; ++c) Mo[c] = __ldg(&a.mold[i * B + c]);
     rsim::phys::accum_row<B>(a.fl, __ldg(&a.pv[i]), ui[0], Pi, Mo, a.dt, R, D);
-
-    double Okeep[6][B][B];
-    int32_t lcol[6];
-    // pass 1: residual + diagonal (+ pattern)
+    for (int s = 0; s < a.nslot; ++s)
+      if (sHas[rg][s]) {
 #pragma unroll
-    for (int s = 0; s < 6; ++s) {
-      lcol[s] = -1;
-      if (s >= a.nslot) continue;
-      int64_t j;
-      double T;
-      if (cart_nbr(a, i, ix, iy, iz, s, j, T)) {
-        double O[B][B];
-        conn<B>(a, ui, Pi, j, T, R, D, O);
-        lcol[s] = __ldg(&a.g2l[j]);
-        if (KEEP) {
+        for (int e = 0; e < B; ++e) {
+          R[e] = R[e] + sRc[rg][s][e];
 #pragma unroll
-          for (int r = 0; r < B; ++r)
-#pragma unroll
-            for (int c = 0; c < B; ++c) Okeep[s][r][c] = O[r][c];
+          for (int v = 0; v < B; ++v) D[e][v] = D[e][v] + sDc[rg][s][e * B + v];
         }
       }
-      a.ell_col[s * a.cap + l] = lcol[s];
-    }
+    int32_t q0 = 0, q1 = 0;
     if (a.has_nnc) {
-      const int32_t q0 = __ldg(&a.nptr[i]), q1 = __ldg(&a.nptr[i + 1]);
-      for (int32_t q = q0; q < q1; ++q) {
-        int64_t j = __ldg(&a.nnbr[q]);
-        double O[B][B];
-        conn<B>(a, ui, Pi, j, __ldg(&a.nt[q]), R, D, O);
-        a.nnc_lcol[q] = __ldg(&a.g2l[j]);
+      q0 = __ldg(&a.nptr[i]);
+      q1 = __ldg(&a.nptr[i + 1]);
+      for (int32_t qq = q0; qq < q1; ++qq) {
+        const int64_t j = __ldg(&a.nnbr[qq]);
+        double On[B][B];
+        conn<B>(a, ui, Pi, j, __ldg(&a.nt[qq]), R, D, On);
+        a.nnc_lcol[qq] = __ldg(&a.g2l[j]);
       }
     }
     rsim::phys::well_row<B>(__ldg(&a.wi[i]), ui[0], a.bhp, Pi, R, D);
@@ -156,48 +191,35 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
       a.rhs[l * B + e] = -y[e];
       finf = fmax(finf, fabs(R[e]));
     }
-    // pass 2: scaled off-diagonal blocks
 #pragma unroll
-    for (int s = 0; s < 6; ++s) {
-      if (s >= a.nslot || lcol[s] < 0) continue;
-      double* dst = &a.ell_val[((int64_t)s * a.cap + l) * B * B];
-      if (KEEP) {
-        store_scaled<B>(dst, Di, Okeep[s]);
-      } else {
-        int64_t j;
-        double T;
-        cart_nbr(a, i, ix, iy, iz, s, j, T);
-        double O[B][B], Rd[B], Dd[B][B];
+    for (int r = 0; r < B; ++r)
 #pragma unroll
-        for (int e = 0; e < B; ++e) {
-          Rd[e] = 0.0;
+      for (int c = 0; c < B; ++c) sDi[rg][r * B + c] = Di[r][c];
+    for (int32_t qq = q0; qq < q1; ++qq) {  // NNC blocks (rare): recompute + scale
+      const int64_t j = __ldg(&a.nnbr[qq]);
+      if (__ldg(&a.g2l[j]) < 0) continue;
+      double On[B][B], Rd[B], Dd[B][B];
 #pragma unroll
-          for (int v = 0; v < B; ++v) Dd[e][v] = 0.0;
-        }
-        conn<B>(a, ui, Pi, j, T, Rd, Dd, O);
-        store_scaled<B>(dst, Di, O);
+      for (int e = 0; e < B; ++e) {
+        Rd[e] = 0.0;
+#pragma unroll
+        for (int v = 0; v < B; ++v) Dd[e][v] = 0.0;
       }
-    }
-    if (a.has_nnc) {
-      const int32_t q0 = __ldg(&a.nptr[i]), q1 = __ldg(&a.nptr[i + 1]);
-      for (int32_t q = q0; q < q1; ++q) {
-        int64_t j = __ldg(&a.nnbr[q]);
-        if (__ldg(&a.g2l[j]) < 0) continue;
-        double O[B][B], Rd[B], Dd[B][B];
-#pragma unroll
-        for (int e = 0; e < B; ++e) {
-          Rd[e] = 0.0;
-#pragma unroll
-          for (int v = 0; v < B; ++v) Dd[e][v] = 0.0;
-        }
-        conn<B>(a, ui, Pi, j, __ldg(&a.nt[q]), Rd, Dd, O);
-        store_scaled<B>(&a.nnc_val[(int64_t)q * B * B], Di, O);
-      }
-    }
+      conn<B>(a, ui, Pi, j, __ldg(&a.nt[qq]), Rd, Dd, On);
+      store_scaled<B>(&a.nnc_val[(int64_t)qq * B * B], Di, On);
     }
   }
-  double wm = warp_max(finf);
-  if ((threadIdx.x & 31) == 0) atomic_max_bits(&a.dsc->finf, wm);
+  __syncwarp();
+  if (valid && q < a.nslot && lcol >= 0) {
+    double Di[B][B];
+#pragma unroll
+    for (int r = 0; r < B; ++r)
+#pragma unroll
+      for (int c = 0; c < B; ++c) Di[r][c] = sDi[rg][r * B + c];
+    store_scaled<B>(&a.ell_val[((int64_t)q * a.cap + l) * B * B], Di, O);
+  }
+  const double wm = warp_max(finf);
+  if ((threadIdx.x & 31) == 0 && wm > 0.0) atomic_max_bits(&a.dsc->finf, wm);
 }
 
 // Old-time accumulation M^n = pv φ(p) A(u) for every cell (set_state / Δt change).
@@ -239,7 +261,7 @@ int launch_assemble(rsim_gpu_ctx* c) {
   a.nnc_lcol = c->nnc_lcol; a.nnc_val = c->nnc_val;
   a.F_raw = c->F_raw; a.rhs = c->rhs; a.part_f2 = c->part_f2;
   a.dsc = c->dsc;
-  const int64_t nblocks = (c->nA + 255) / 256;
+  const int64_t nblocks = (c->nA + RPB - 1) / RPB;
   switch (c->b) {
     case 1: k_assemble<1><<<nblocks, 256, 0, c->stream>>>(a); break;
     case 2: k_assemble<2><<<nblocks, 256, 0, c->stream>>>(a); break;

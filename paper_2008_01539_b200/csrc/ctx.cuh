@@ -167,62 +167,23 @@ __device__ __forceinline__ unsigned long long dbits(double a) {
   return (unsigned long long)__double_as_longlong(a);
 }
 
-// Canonical 256-thread block reduction (blockops.h): warp shfl_down tree with
-// offsets 16..1, then the 8 warp sums with offsets 4..1.  Result valid in
-// every thread (broadcast through shared memory).  All 256 threads call it.
-__device__ __forceinline__ double block_sum_canon(double s, double* sm) {
-  const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+// Canonical reduction helpers (blockops.h): a 256-row chunk is 8 warps; each
+// warp shuffles 16..1 (lane 0 holds the warp sum), then the 8 warp sums are
+// combined with offsets 4,2,1.
+__device__ __forceinline__ double warp_tree(double v) {
 #pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) s = s + __shfl_down_sync(FULL, s, off);
-  if (lane == 0) sm[w] = s;
-  __syncthreads();
-  if (w == 0) {
-    double r = (lane < 8) ? sm[lane] : 0.0;
-#pragma unroll
-    for (int off = 4; off >= 1; off >>= 1) r = r + __shfl_down_sync(FULL, r, off);
-    if (lane == 0) sm[8] = r;
-  }
-  __syncthreads();
-  double out = sm[8];
-  __syncthreads();
-  return out;
+  for (int off = 16; off >= 1; off >>= 1) v = v + __shfl_down_sync(0xffffffffu, v, off);
+  return v;
 }
-
-// Canonical reduction of P partials by ONE block (every block may call it
-// redundantly and obtains identical bits).  lvl: shared scratch >= ceil(P/2048).
-__device__ __forceinline__ double reduce_partials_canon(const double* part, int P, double* sm, double* lvl) {
-  const int t = threadIdx.x;
-  if (P <= RSIM_RED_CHUNK) {
-    double s = 0.0;
+__device__ __forceinline__ double tree8(const double* w) {
+  double a[8];
 #pragma unroll
-    for (int k = 0; k < RSIM_RED_ITEMS; ++k) {
-      int idx = t + RSIM_RED_THREADS * k;
-      if (idx < P) s = s + part[idx];
-    }
-    return block_sum_canon(s, sm);
-  }
-  int P2 = (P + RSIM_RED_CHUNK - 1) / RSIM_RED_CHUNK;
-  for (int g = 0; g < P2; ++g) {
-    double s = 0.0;
-    int base = g * RSIM_RED_CHUNK;
-    int m = min(RSIM_RED_CHUNK, P - base);
+  for (int k = 0; k < 8; ++k) a[k] = w[k];
 #pragma unroll
-    for (int k = 0; k < RSIM_RED_ITEMS; ++k) {
-      int idx = t + RSIM_RED_THREADS * k;
-      if (idx < m) s = s + part[base + idx];
-    }
-    double r = block_sum_canon(s, sm);
-    if (t == 0) lvl[g] = r;
-  }
-  __syncthreads();
-  double s = 0.0;
+  for (int off = 4; off >= 1; off >>= 1)
 #pragma unroll
-  for (int k = 0; k < RSIM_RED_ITEMS; ++k) {
-    int idx = t + RSIM_RED_THREADS * k;
-    if (idx < P2) s = s + lvl[idx];
-  }
-  return block_sum_canon(s, sm);
+    for (int k = 0; k < off; ++k) a[k] = a[k] + a[k + off];
+  return a[0];
 }
 
 __device__ __forceinline__ void atomic_max_bits(unsigned long long* addr, double nonneg) {

@@ -1,22 +1,17 @@
 // krylov.cu — K3 (SpMV) + K5 (fused vector updates / dot products) inside ONE
-// persistent BiCGSTAB kernel per linear solve.
+// persistent cooperative BiCGSTAB kernel per linear solve (large systems).
 //
 // Replaces solve(J, F) with the north star's BiCGSTAB on
 // the block-Jacobi-scaled system Â = D^{-1}J (unit block diagonal, never
 // stored; block-Jacobi preconditioning is therefore built in).
 //
-// Why persistent: the active systems of the localized solver are small
-// (SURVEY.md §7 H2), where one launch + one host sync per Krylov iteration
-// would dominate.  The whole iteration loop runs on the device; phases are
-// separated by grid-wide barriers (one __syncthreads when the grid is a
-// single CTA), and every block redundantly reduces the chunk partials in the
-// canonical order (blockops.h), so all blocks take the same branch and the
-// result is bit-identical to the CPU oracle.
-//
-// Latency design: 1024-thread CTAs, each owning whole 2048-row chunks with 2
-// rows per thread whose loads are issued together; per-row dot values are
-// staged in shared memory and summed by 256 "canonical" threads, so the
-// reduction order is the canonical one while the loads run 2048-wide.
+// The whole iteration loop runs on the device.  A CTA of 1024 threads owns 4
+// consecutive 256-row canonical chunks per round (one row per thread), so a
+// chunk partial is 8 warp shuffles + an 8-way tree inside the CTA; phases are
+// separated by grid-wide barriers and every CTA reduces the chunk partials
+// with the same canonical tree (blockops.h) — all CTAs take identical
+// branches and the results are bit-identical to oracle/oracle.cpp.
+// Small systems (<= 64 chunks) go to krylov_dsm.cu (one cluster, DSMEM).
 //
 // Element formulas (identical in oracle/oracle.cpp bicgstab()):
 //   p = r + β (p − ω v);  s = r − α v;  x = (x + α p) + ω s;  r = s − ω t.
@@ -30,8 +25,7 @@ namespace cg = cooperative_groups;
 
 namespace {
 
-constexpr int KT = 1024;                   // threads per CTA
-constexpr int RPT = RSIM_RED_CHUNK / KT;   // rows per thread per chunk (2)
+constexpr int KT = 1024;  // threads per CTA = 4 chunks per round
 
 struct KArgs {
   int32_t nA, nslot, maxit, fixed;
@@ -47,167 +41,150 @@ struct KArgs {
   const double* rhs;
   const double* F_raw;
   double *x, *r, *r0, *p, *v, *s, *t;
-  double* part;  // [4][pstride]
-  int32_t pstride;
+  double* part;   // [3][pstride]  level-1 partials
+  double* part2;  // [3][pstride2] level-2 partials (very large systems)
+  int32_t pstride, pstride2;
   DevScalars* dsc;
 };
 
-// 256 canonical threads (warps 0..7) hold the sums; all 1024 threads call it.
-__device__ __forceinline__ double bsum(double s, double* sm) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (w < 8) {
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) s = s + __shfl_down_sync(0xffffffffu, s, off);
-    if (lane == 0) sm[w] = s;
+struct Red {
+  double ws[3][32];  // warp sums of the current round
+  double lvl[3][64];
+  double res[3];
+};
+
+// Per-round commit: warp trees of up to 3 quantities -> 8-way trees -> level-1
+// partials of the 4 chunks of this round.
+__device__ __forceinline__ void commit_round(Red& R, int NQ, const double* val, int64_t chunk0, int64_t nch,
+                                             double* part, int pstride) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int q = 0; q < NQ; ++q) {
+    double v = warp_tree(val[q]);
+    if (lane == 0) R.ws[q][w] = v;
   }
   __syncthreads();
-  if (w == 0) {
-    double r = (lane < 8) ? sm[lane] : 0.0;
-#pragma unroll
-    for (int off = 4; off >= 1; off >>= 1) r = r + __shfl_down_sync(0xffffffffu, r, off);
-    if (lane == 0) sm[8] = r;
+  if ((int)threadIdx.x < 4 * NQ) {
+    const int g = threadIdx.x & 3, q = threadIdx.x >> 2;
+    if (chunk0 + g < nch) part[q * pstride + chunk0 + g] = tree8(&R.ws[q][8 * g]);
   }
   __syncthreads();
-  double out = sm[8];
-  __syncthreads();
-  return out;
 }
 
-// Canonical reduction of P partials (every CTA redundantly; identical bits).
-__device__ __forceinline__ double reduce_parts(const double* part, int P, double* sm, double* lvl) {
-  const int t = threadIdx.x;
-  auto level = [&](const double* src, int m) {
-    double s = 0.0;
-    if (t < RSIM_RED_THREADS) {
-#pragma unroll
-      for (int k = 0; k < RSIM_RED_ITEMS; ++k) {
-        int idx = t + RSIM_RED_THREADS * k;
-        if (idx < m) s = s + src[idx];
-      }
-    }
-    return bsum(s, sm);
-  };
-  if (P <= RSIM_RED_CHUNK) return level(part, P);
-  const int P2 = (P + RSIM_RED_CHUNK - 1) / RSIM_RED_CHUNK;
-  for (int g = 0; g < P2; ++g) {
-    double r = level(part + g * RSIM_RED_CHUNK, min(RSIM_RED_CHUNK, P - g * RSIM_RED_CHUNK));
-    if (t == 0) lvl[g] = r;
+// Canonical reduction of P partials src[0..P) held in global memory, done by
+// ONE CTA (all 1024 threads call it); requires P <= 64*256.  Result in R.res[q].
+__device__ __forceinline__ void reduce_small(Red& R, int q, const double* src, int P) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (P == 1) {
+    if (threadIdx.x == 0) R.res[q] = src[0];
+    __syncthreads();
+    return;
+  }
+  const int P2 = (P + 255) / 256;
+  for (int c0 = 0; c0 < P2; c0 += 4) {  // 4 chunks of 256 partials per pass
+    const int idx = c0 * 256 + threadIdx.x;
+    double v = warp_tree(idx < P ? src[idx] : 0.0);
+    if (lane == 0) R.ws[q][w] = v;
+    __syncthreads();
+    if (threadIdx.x < 4 && c0 + (int)threadIdx.x < P2) R.lvl[q][c0 + threadIdx.x] = tree8(&R.ws[q][8 * threadIdx.x]);
+    __syncthreads();
+  }
+  if (P2 == 1) {
+    if (threadIdx.x == 0) R.res[q] = R.lvl[q][0];
+  } else {
+    double v = warp_tree(threadIdx.x < (unsigned)P2 ? R.lvl[q][threadIdx.x] : 0.0);
+    if (lane == 0 && w < 8) R.ws[q][w] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) R.res[q] = tree8(&R.ws[q][0]);
   }
   __syncthreads();
-  return level(lvl, P2);
 }
 
-// Sum the staged per-row values of one chunk in canonical order -> partial.
-template <int NV>
-__device__ __forceinline__ void chunk_commit(const double* vals, int m, double* sm, double* const* P, int c) {
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < NV; ++q) {
-    double s = 0.0;
-    if (threadIdx.x < RSIM_RED_THREADS) {
-#pragma unroll
-      for (int k = 0; k < RSIM_RED_ITEMS; ++k) {
-        int idx = threadIdx.x + RSIM_RED_THREADS * k;
-        if (idx < m) s = s + vals[q * RSIM_RED_CHUNK + idx];
-      }
-    }
-    double r = bsum(s, sm);
-    if (threadIdx.x == 0) P[q][c] = r;
-  }
-}
-
-// y = Â x for RPT rows of one thread (loads of all rows issued before use).
 template <int B>
-__device__ __forceinline__ void spmv_rows(const KArgs& a, int64_t base, int64_t nr, const double* __restrict__ xin,
-                                          double* __restrict__ yout, double (*acc)[B]) {
+__device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, const double* __restrict__ xin, double* acc) {
   const int32_t* __restrict__ col = a.ell_col;
   const double* __restrict__ val = a.ell_val;
-  int32_t cl[RPT][6];
-  int64_t l[RPT];
+  int32_t cl[6];
 #pragma unroll
-  for (int j = 0; j < RPT; ++j) {
-    l[j] = base + threadIdx.x + KT * j;
-#pragma unroll
-    for (int s = 0; s < 6; ++s) cl[j][s] = (l[j] < nr && s < a.nslot) ? __ldg(&col[s * a.cap + l[j]]) : -1;
-  }
-#pragma unroll
-  for (int j = 0; j < RPT; ++j)
-#pragma unroll
-    for (int c = 0; c < B; ++c) acc[j][c] = l[j] < nr ? xin[l[j] * B + c] : 0.0;
+  for (int s = 0; s < 6; ++s) cl[s] = (s < a.nslot) ? __ldg(&col[s * a.cap + l]) : -1;
+  double xv[6][B];
 #pragma unroll
   for (int s = 0; s < 6; ++s)
+    if (cl[s] >= 0)
 #pragma unroll
-    for (int j = 0; j < RPT; ++j)
-      if (cl[j][s] >= 0)
-        rsim::blk::gemv_acc_flat<B>(&val[((int64_t)s * a.cap + l[j]) * B * B], &xin[(int64_t)cl[j][s] * B], acc[j]);
+      for (int e = 0; e < B; ++e) xv[s][e] = xin[(int64_t)cl[s] * B + e];
+#pragma unroll
+  for (int e = 0; e < B; ++e) acc[e] = xin[l * B + e];
+#pragma unroll
+  for (int s = 0; s < 6; ++s)
+    if (cl[s] >= 0) rsim::blk::gemv_acc_flat<B>(&val[((int64_t)s * a.cap + l) * B * B], xv[s], acc);
   if (a.has_nnc) {
-#pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-      if (l[j] >= nr) continue;
-      int64_t i = a.act[l[j]];
-      int32_t q0 = a.nptr[i], q1 = a.nptr[i + 1];
-      for (int32_t q = q0; q < q1; ++q) {
-        int32_t cc = a.nnc_lcol[q];
-        if (cc >= 0) rsim::blk::gemv_acc_flat<B>(&a.nnc_val[(int64_t)q * B * B], &xin[(int64_t)cc * B], acc[j]);
-      }
+    const int64_t i = a.act[l];
+    const int32_t q0 = a.nptr[i], q1 = a.nptr[i + 1];
+    for (int32_t q = q0; q < q1; ++q) {
+      const int32_t cc = a.nnc_lcol[q];
+      if (cc >= 0) rsim::blk::gemv_acc_flat<B>(&a.nnc_val[(int64_t)q * B * B], &xin[(int64_t)cc * B], acc);
     }
   }
-#pragma unroll
-  for (int j = 0; j < RPT; ++j)
-    if (l[j] < nr)
-#pragma unroll
-      for (int c = 0; c < B; ++c) yout[l[j] * B + c] = acc[j][c];
 }
 
 template <int B>
-__global__ void __launch_bounds__(KT) k_bicgstab(const KArgs a) {
-  __shared__ double vals[2 * RSIM_RED_CHUNK];
-  __shared__ double sm[9];
-  __shared__ double lvl[64];
+__global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
+  __shared__ Red R;
   const bool single = gridDim.x == 1;
   auto sync = [&]() {
     if (single) __syncthreads();
     else cg::this_grid().sync();
   };
   const int64_t nr = a.nA;
-  const int nch = (int)((nr + RSIM_RED_CHUNK - 1) / RSIM_RED_CHUNK);
+  const int64_t nch = (nr + 255) / 256;
+  const int64_t nrounds = (nch + 3) / 4;
   const int tid = threadIdx.x;
-  double* P0 = a.part;
-  double* P1 = a.part + a.pstride;
-  double* P2 = a.part + 2 * a.pstride;
-  double* P3 = a.part + 3 * a.pstride;
-  double* const PP01[2] = {P0, P1};
-  double* const PP23[2] = {P2, P3};
-  double* const PP1[1] = {P1};
 
-  // ---- init: r = r0 = rhs, x = 0;  partials (rhs, rhs) and (F, F)
-  for (int c = blockIdx.x; c < nch; c += gridDim.x) {
-    const int64_t base = (int64_t)c * RSIM_RED_CHUNK;
-#pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-      const int idx = tid + KT * j;
-      const int64_t l = base + idx;
-      double v0 = 0.0, v1 = 0.0;
-      if (l < nr) {
-        double bv[B], fv[B];
-#pragma unroll
-        for (int e = 0; e < B; ++e) { bv[e] = a.rhs[l * B + e]; fv[e] = a.F_raw[l * B + e]; }
-#pragma unroll
-        for (int e = 0; e < B; ++e) { a.r[l * B + e] = bv[e]; a.r0[l * B + e] = bv[e]; a.x[l * B + e] = 0.0; }
-        v0 = rsim::blk::rowdot<B>(bv, bv);
-        v1 = rsim::blk::rowdot<B>(fv, fv);
+  // global canonical reduction of NQ quantities whose level-1 partials are in a.part
+  auto reduce = [&](int NQ) {
+    sync();
+    const int P1 = (int)nch;
+    if (P1 <= 64 * 256) {
+      for (int q = 0; q < NQ; ++q) reduce_small(R, q, a.part + q * a.pstride, P1);
+    } else {
+      // distributed level 2, one more barrier, then the (small) rest per CTA
+      const int P2 = (P1 + 255) / 256;
+      for (int64_t rr = blockIdx.x; rr * 4 < P2; rr += gridDim.x) {
+        const int64_t c2 = rr * 4 + (tid >> 8);
+        const int64_t idx = c2 * 256 + (tid & 255);
+        double v[3] = {0.0, 0.0, 0.0};
+        for (int q = 0; q < NQ; ++q) v[q] = idx < P1 ? a.part[q * a.pstride + idx] : 0.0;
+        commit_round(R, NQ, v, rr * 4, P2, a.part2, a.pstride2);
       }
-      vals[idx] = v0;
-      vals[RSIM_RED_CHUNK + idx] = v1;
+      sync();
+      for (int q = 0; q < NQ; ++q) reduce_small(R, q, a.part2 + q * a.pstride2, P2);
     }
-    chunk_commit<2>(vals, (int)(nr - base < RSIM_RED_CHUNK ? nr - base : RSIM_RED_CHUNK), sm, PP01, c);
+  };
+
+#define ROUNDS_BEGIN                                             \
+  for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) { \
+    const int64_t l = rd * KT + tid;                             \
+    const bool ok = l < nr;                                      \
+    double val[3] = {0.0, 0.0, 0.0};
+#define ROUNDS_END(NQ)                                           \
+  commit_round(R, NQ, val, rd * 4, nch, a.part, a.pstride);      \
   }
-  sync();
-  const double bb = reduce_parts(P0, nch, sm, lvl);
-  if (blockIdx.x == 0) {  // ‖F‖₂ of the assembly (canonical)
-    double f2 = reduce_parts(P1, nch, sm, lvl);
-    if (tid == 0) a.dsc->f2 = sqrt(f2);
+
+  // ---- init: r = r0 = rhs, x = 0;  (rhs, rhs), (F, F)
+  ROUNDS_BEGIN
+  if (ok) {
+    double bv[B], fv[B];
+#pragma unroll
+    for (int e = 0; e < B; ++e) { bv[e] = a.rhs[l * B + e]; fv[e] = a.F_raw[l * B + e]; }
+#pragma unroll
+    for (int e = 0; e < B; ++e) { a.r[l * B + e] = bv[e]; a.r0[l * B + e] = bv[e]; a.x[l * B + e] = 0.0; }
+    val[0] = rsim::blk::rowdot<B>(bv, bv);
+    val[1] = rsim::blk::rowdot<B>(fv, fv);
   }
+  ROUNDS_END(2)
+  reduce(2);
+  const double bb = R.res[0];
+  if (blockIdx.x == 0 && tid == 0) a.dsc->f2 = sqrt(R.res[1]);
   const double bnorm = sqrt(bb);
   if (bnorm == 0.0) {
     if (blockIdx.x == 0 && tid == 0) { a.dsc->lin_iters = 0; a.dsc->lin_relres = 0.0; }
@@ -223,124 +200,92 @@ __global__ void __launch_bounds__(KT) k_bicgstab(const KArgs a) {
   for (it = 1; it <= maxit; ++it) {
     // ---- p update
     const double beta = (it == 1) ? 0.0 : (rho_new / rho) * (alpha / omega);
-    for (int c = blockIdx.x; c < nch; c += gridDim.x) {
+    for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
+      const int64_t l = rd * KT + tid;
+      if (l < nr)
 #pragma unroll
-      for (int j = 0; j < RPT; ++j) {
-        const int64_t l = (int64_t)c * RSIM_RED_CHUNK + tid + KT * j;
-        if (l < nr) {
-#pragma unroll
-          for (int e = 0; e < B; ++e) {
-            const int64_t q = l * B + e;
-            a.p[q] = (it == 1) ? a.r[q] : a.r[q] + beta * (a.p[q] - omega * a.v[q]);
-          }
+        for (int e = 0; e < B; ++e) {
+          const int64_t q = l * B + e;
+          a.p[q] = (it == 1) ? a.r[q] : a.r[q] + beta * (a.p[q] - omega * a.v[q]);
         }
-      }
     }
     sync();
     // ---- v = Â p ; (r0, v)
-    for (int c = blockIdx.x; c < nch; c += gridDim.x) {
-      const int64_t base = (int64_t)c * RSIM_RED_CHUNK;
-      double acc[RPT][B];
-      spmv_rows<B>(a, base, nr, a.p, a.v, acc);
+    ROUNDS_BEGIN
+    if (ok) {
+      double y[B];
+      spmv_row<B>(a, l, a.p, y);
 #pragma unroll
-      for (int j = 0; j < RPT; ++j) {
-        const int idx = tid + KT * j;
-        const int64_t l = base + idx;
-        vals[idx] = (l < nr) ? rsim::blk::rowdot<B>(&a.r0[l * B], acc[j]) : 0.0;
-      }
-      chunk_commit<1>(vals, (int)(nr - base < RSIM_RED_CHUNK ? nr - base : RSIM_RED_CHUNK), sm, &P0, c);
+      for (int e = 0; e < B; ++e) a.v[l * B + e] = y[e];
+      val[0] = rsim::blk::rowdot<B>(&a.r0[l * B], y);
     }
-    sync();
-    const double r0v = reduce_parts(P0, nch, sm, lvl);
+    ROUNDS_END(1)
+    reduce(1);
+    const double r0v = R.res[0];
     if (r0v == 0.0 || !isfinite(r0v)) { status = RSIM_ENUM; break; }
     alpha = rho_new / r0v;
     // ---- s = r − α v ; (s, s)
-    for (int c = blockIdx.x; c < nch; c += gridDim.x) {
-      const int64_t base = (int64_t)c * RSIM_RED_CHUNK;
+    ROUNDS_BEGIN
+    if (ok) {
+      double sv[B];
 #pragma unroll
-      for (int j = 0; j < RPT; ++j) {
-        const int idx = tid + KT * j;
-        const int64_t l = base + idx;
-        double v0 = 0.0;
-        if (l < nr) {
-          double sv[B];
-#pragma unroll
-          for (int e = 0; e < B; ++e) {
-            const int64_t q = l * B + e;
-            sv[e] = a.r[q] - alpha * a.v[q];
-            a.s[q] = sv[e];
-          }
-          v0 = rsim::blk::rowdot<B>(sv, sv);
-        }
-        vals[idx] = v0;
+      for (int e = 0; e < B; ++e) {
+        const int64_t q = l * B + e;
+        sv[e] = a.r[q] - alpha * a.v[q];
+        a.s[q] = sv[e];
       }
-      chunk_commit<1>(vals, (int)(nr - base < RSIM_RED_CHUNK ? nr - base : RSIM_RED_CHUNK), sm, PP1, c);
+      val[0] = rsim::blk::rowdot<B>(sv, sv);
     }
-    sync();
-    const double ss = reduce_parts(P1, nch, sm, lvl);
+    ROUNDS_END(1)
+    reduce(1);
+    const double ss = R.res[0];
     if (!fixed && sqrt(ss) <= tol) {
-      for (int c = blockIdx.x; c < nch; c += gridDim.x)
+      for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
+        const int64_t l = rd * KT + tid;
+        if (l < nr)
 #pragma unroll
-        for (int j = 0; j < RPT; ++j) {
-          const int64_t l = (int64_t)c * RSIM_RED_CHUNK + tid + KT * j;
-          if (l < nr)
-#pragma unroll
-            for (int e = 0; e < B; ++e) a.x[l * B + e] = a.x[l * B + e] + alpha * a.p[l * B + e];
-        }
+          for (int e = 0; e < B; ++e) a.x[l * B + e] = a.x[l * B + e] + alpha * a.p[l * B + e];
+      }
       relres = sqrt(ss) / bnorm;
       status = RSIM_OK;
       break;
     }
     // ---- t = Â s ; (t, s), (t, t)
-    for (int c = blockIdx.x; c < nch; c += gridDim.x) {
-      const int64_t base = (int64_t)c * RSIM_RED_CHUNK;
-      double acc[RPT][B];
-      spmv_rows<B>(a, base, nr, a.s, a.t, acc);
+    ROUNDS_BEGIN
+    if (ok) {
+      double y[B];
+      spmv_row<B>(a, l, a.s, y);
 #pragma unroll
-      for (int j = 0; j < RPT; ++j) {
-        const int idx = tid + KT * j;
-        const int64_t l = base + idx;
-        vals[idx] = (l < nr) ? rsim::blk::rowdot<B>(acc[j], &a.s[l * B]) : 0.0;
-        vals[RSIM_RED_CHUNK + idx] = (l < nr) ? rsim::blk::rowdot<B>(acc[j], acc[j]) : 0.0;
-      }
-      chunk_commit<2>(vals, (int)(nr - base < RSIM_RED_CHUNK ? nr - base : RSIM_RED_CHUNK), sm, PP23, c);
+      for (int e = 0; e < B; ++e) a.t[l * B + e] = y[e];
+      val[0] = rsim::blk::rowdot<B>(y, &a.s[l * B]);
+      val[1] = rsim::blk::rowdot<B>(y, y);
     }
-    sync();
-    const double ts = reduce_parts(P2, nch, sm, lvl);
-    const double tt = reduce_parts(P3, nch, sm, lvl);
+    ROUNDS_END(2)
+    reduce(2);
+    const double ts = R.res[0], tt = R.res[1];
     if (tt == 0.0 || !isfinite(tt)) { status = RSIM_ENUM; break; }
     omega = ts / tt;
     // ---- x, r update ; (r, r), (r0, r)
-    for (int c = blockIdx.x; c < nch; c += gridDim.x) {
-      const int64_t base = (int64_t)c * RSIM_RED_CHUNK;
+    ROUNDS_BEGIN
+    if (ok) {
+      double rv[B], r0v_[B];
 #pragma unroll
-      for (int j = 0; j < RPT; ++j) {
-        const int idx = tid + KT * j;
-        const int64_t l = base + idx;
-        double v0 = 0.0, v1 = 0.0;
-        if (l < nr) {
-          double rv[B], r0v_[B];
-#pragma unroll
-          for (int e = 0; e < B; ++e) {
-            const int64_t q = l * B + e;
-            const double sq = a.s[q];
-            a.x[q] = (a.x[q] + alpha * a.p[q]) + omega * sq;
-            rv[e] = sq - omega * a.t[q];
-            a.r[q] = rv[e];
-            r0v_[e] = a.r0[q];
-          }
-          v0 = rsim::blk::rowdot<B>(rv, rv);
-          v1 = rsim::blk::rowdot<B>(r0v_, rv);
-        }
-        vals[idx] = v0;
-        vals[RSIM_RED_CHUNK + idx] = v1;
+      for (int e = 0; e < B; ++e) {
+        const int64_t q = l * B + e;
+        const double sq = a.s[q];
+        a.x[q] = (a.x[q] + alpha * a.p[q]) + omega * sq;
+        rv[e] = sq - omega * a.t[q];
+        a.r[q] = rv[e];
+        r0v_[e] = a.r0[q];
       }
-      chunk_commit<2>(vals, (int)(nr - base < RSIM_RED_CHUNK ? nr - base : RSIM_RED_CHUNK), sm, PP01, c);
+      val[0] = rsim::blk::rowdot<B>(rv, rv);
+      val[1] = rsim::blk::rowdot<B>(r0v_, rv);
     }
-    sync();
-    const double rr = reduce_parts(P0, nch, sm, lvl);
+    ROUNDS_END(2)
+    reduce(2);
+    const double rr = R.res[0];
     rho = rho_new;
-    rho_new = reduce_parts(P1, nch, sm, lvl);
+    rho_new = R.res[1];
     relres = sqrt(rr) / bnorm;
     if (!fixed && sqrt(rr) <= tol) { status = RSIM_OK; break; }
     if (omega == 0.0 || rho_new == 0.0 || !isfinite(rho_new)) { status = RSIM_ENUM; break; }
@@ -351,16 +296,8 @@ __global__ void __launch_bounds__(KT) k_bicgstab(const KArgs a) {
     a.dsc->lin_relres = relres;
     if (status != RSIM_OK) a.dsc->status = status;
   }
-}
-
-
-int single_max_chunks() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("RSIM_KRYLOV_SINGLE_MAX");
-    v = e ? std::atoi(e) : 2;
-  }
-  return v;
+#undef ROUNDS_BEGIN
+#undef ROUNDS_END
 }
 
 template <int B>
@@ -377,23 +314,19 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.act = c->act; a.nptr = c->nptr; a.nnc_lcol = c->nnc_lcol; a.nnc_val = c->nnc_val;
   a.rhs = c->rhs; a.F_raw = c->F_raw;
   a.x = c->x; a.r = c->r; a.r0 = c->r0; a.p = c->p; a.v = c->v; a.s = c->s; a.t = c->t;
+  a.pstride = (int32_t)((c->n + 255) / 256);
+  a.pstride2 = (a.pstride + 255) / 256;
   a.part = c->part;
-  a.pstride = (int32_t)((c->n + RSIM_RED_CHUNK - 1) / RSIM_RED_CHUNK);
+  a.part2 = c->part + 3 * (int64_t)a.pstride;
   a.dsc = c->dsc;
-  const int nch = (c->nA + RSIM_RED_CHUNK - 1) / RSIM_RED_CHUNK;
-  // small systems: one cluster with matrix + vectors in distributed smem
-  {
-    int r = launch_krylov_dsm(c, o);
-    if (r != RSIM_ENOTAPPLICABLE) return r;
-  }
+  const int64_t nrounds = ((c->nA + 255) / 256 + 3) / 4;
   if (c->max_coop_blocks[B] == 0) {
     int per_sm = 0;
     RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bicgstab<B>, KT, 0));
     c->max_coop_blocks[B] = per_sm * c->sm_count;
     if (c->max_coop_blocks[B] < 1) c->max_coop_blocks[B] = 1;
   }
-  int grid = nch < c->max_coop_blocks[B] ? nch : c->max_coop_blocks[B];
-  if (nch <= single_max_chunks()) grid = 1;
+  int grid = nrounds < c->max_coop_blocks[B] ? (int)nrounds : c->max_coop_blocks[B];
   if (grid < 1) grid = 1;
   void* args[] = {&a};
   if (grid == 1) {
@@ -410,6 +343,10 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
 
 int launch_krylov(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   if (c->nA <= 0) return RSIM_OK;
+  {  // small systems: one cluster with matrix + vectors in distributed smem
+    int r = launch_krylov_dsm(c, o);
+    if (r != RSIM_ENOTAPPLICABLE) return r;
+  }
   switch (c->b) {
     case 1: return launch_b<1>(c, o);
     case 2: return launch_b<2>(c, o);
