@@ -106,21 +106,27 @@ def dist_env():
         int(os.environ.get("LOCAL_RANK", "0"))
 
 
-def init_dist(ws, lr):
+def init_dist(ws, lr, backend="nccl"):
     if ws <= 1:
         return None
     import torch
     import torch.distributed as dist
-    torch.cuda.set_device(lr)
-    dist.init_process_group("nccl", init_method="env://")
+    if backend == "nccl":
+        torch.cuda.set_device(lr)
+    dist.init_process_group(backend, init_method="env://")
     return dist
 
 
+def _dev(dist):
+    return "cuda" if dist.get_backend() == "nccl" else "cpu"
+
+
 def dist_max(dist, v: float) -> float:
+    """Max over ranks (replica timing: the job takes as long as its slowest rank)."""
     if dist is None:
         return v
     import torch
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device=_dev(dist))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -129,7 +135,7 @@ def dist_sum(dist, v: float) -> float:
     if dist is None:
         return v
     import torch
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device=_dev(dist))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 

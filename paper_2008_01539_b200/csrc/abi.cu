@@ -294,7 +294,7 @@ int rsim_gpu_set_active(rsim_gpu_ctx* c, const int32_t* sorted, int32_t n, rsim_
     TRY(h2d(c, c->list_buf, sorted, n));
     TRY(launch_set_list(c, c->list_buf, n));
   }
-  TRY(launch_compact(c, MODE_KEEP, 0, 0.0, 0));
+  TRY(launch_set_update(c, MODE_KEEP, 0, 0.0, 0, 1, 0, 0));
   rsim_phase_end(c);
   c->pending_nA = true;
   TRY(sync_stats(c));
@@ -307,11 +307,10 @@ int rsim_gpu_initial_active(rsim_gpu_ctx* c, int32_t first_step, double eps, int
   TRY(launch_set_reset(c, 0));
   if (first_step) {
     TRY(launch_seed_pinned(c));
-    TRY(launch_dilate(c, m, 0));
-    TRY(launch_compact(c, MODE_EXPAND, 0, eps, m));
+    TRY(launch_set_update(c, MODE_EXPAND, 0, eps, m, 0, 1, 1));
   } else {
     TRY(launch_initial_support(c, eps));
-    TRY(launch_compact(c, MODE_KEEP, 0, eps, 0));
+    TRY(launch_set_update(c, MODE_KEEP, 0, eps, 0, 1, 0, 0));
   }
   rsim_phase_end(c);
   c->pending_nA = true;
@@ -322,9 +321,7 @@ int rsim_gpu_initial_active(rsim_gpu_ctx* c, int32_t first_step, double eps, int
 
 int rsim_gpu_estimate_active(rsim_gpu_ctx* c, double eps, int32_t m, int32_t shrink_locked, rsim_gpu_stats* st) {
   rsim_phase_begin(c, 0);
-  TRY(launch_decide(c, eps, shrink_locked, 0));
-  TRY(launch_dilate(c, m, 1));
-  TRY(launch_compact(c, MODE_DEVICE, 0, eps, m));
+  TRY(launch_set_update(c, MODE_DEVICE, 0, eps, m, shrink_locked, 0, 1));
   c->counters[4] += 1;
   rsim_phase_end(c);
   c->pending_nA = true;
@@ -380,9 +377,7 @@ int rsim_internal_add_row_iters(rsim_gpu_ctx* c, int64_t v) {
 
 int rsim_gpu_dd_expand(rsim_gpu_ctx* c, double eps, int32_t m, int32_t round, rsim_gpu_stats* st) {
   rsim_phase_begin(c, 0);
-  TRY(launch_decide(c, eps, 0, 0));
-  TRY(launch_dilate(c, m, 1));
-  TRY(launch_compact(c, MODE_DD, round, eps, m));
+  TRY(launch_set_update(c, MODE_DD, round, eps, m, 0, 0, 1));
   rsim_phase_end(c);
   c->pending_nA = true;
   TRY(sync_stats(c));
@@ -569,8 +564,7 @@ int rsim_gpu_support_active(rsim_gpu_ctx* c, double eps, int32_t m, rsim_gpu_sta
   rsim_phase_begin(c, 0);
   TRY(launch_set_reset(c, 0));
   TRY(launch_seed_support(c, eps));
-  TRY(launch_dilate(c, m, 0));
-  TRY(launch_compact(c, MODE_EXPAND, 0, eps, m));
+  TRY(launch_set_update(c, MODE_EXPAND, 0, eps, m, 0, 1, 1));
   rsim_phase_end(c);
   c->pending_nA = true;
   if (st) {

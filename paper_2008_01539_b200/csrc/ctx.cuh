@@ -146,10 +146,9 @@ int launch_update(rsim_gpu_ctx* c, double eps);
 int launch_mold(rsim_gpu_ctx* c);
 int launch_set_reset(rsim_gpu_ctx* c, int all_active);
 int launch_set_list(rsim_gpu_ctx* c, const int32_t* dev_list, int32_t n);
-int launch_compact(rsim_gpu_ctx* c, int mode, int round, double eps, int m);
-int launch_dilate(rsim_gpu_ctx* c, int m, int cond_on_expand);
+int launch_set_update(rsim_gpu_ctx* c, int mode, int round, double eps, int m, int shrink_locked, int force_expand,
+                      int do_dilate);
 int launch_threshold(rsim_gpu_ctx* c, double eps);
-int launch_decide(rsim_gpu_ctx* c, double eps, int shrink_locked, int force_expand);
 int launch_initial_support(rsim_gpu_ctx* c, double eps);
 int launch_seed_pinned(rsim_gpu_ctx* c);
 int launch_dd_begin(rsim_gpu_ctx* c);

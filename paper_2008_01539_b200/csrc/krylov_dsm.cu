@@ -34,7 +34,7 @@ namespace {
 constexpr int GMAX = 16;
 
 struct DArgs {
-  int32_t nA, nslot, maxit, fixed, CPB, nch;
+  int32_t nA, nslot, maxit, fixed, CPB, LCPB, nch;
   int64_t cap;
   bool has_nnc;
   double rtol;
@@ -67,13 +67,13 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   double* vv1 = vv0 + RC * B;
   double* mval = vv1 + RC * B;                                    // [NS][RC][B*B]  (MS)
   int32_t* mcol = (int32_t*)(mval + (MS ? NS * RC * B * B : 0));   // [NS][RC]       (MS)
+  int2* nrng = (int2*)(mcol + (MS ? NS * RC : 0));                // [RC] NNC ranges (has_nnc)
 
   __shared__ double* rb[GMAX];
   __shared__ double* pb[2][GMAX];
   __shared__ double* vb[2][GMAX];
-  __shared__ double* cpb[GMAX];
-  __shared__ double cpart[2][3][4];  // [buf][q][local chunk]
-  __shared__ double ws[3][32];
+  __shared__ double* wsb[GMAX];
+  __shared__ double ws[2][3][32];  // [buf][q][warp]: canonical warp sums of this CTA
   __shared__ double res[3];
 
   cg::cluster_group cluster = cg::this_cluster();
@@ -90,38 +90,50 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
     pb[1][tid] = cluster.map_shared_rank(vp1, tid);
     vb[0][tid] = cluster.map_shared_rank(vv0, tid);
     vb[1][tid] = cluster.map_shared_rank(vv1, tid);
-    cpb[tid] = cluster.map_shared_rank(&cpart[0][0][0], tid);
+    wsb[tid] = cluster.map_shared_rank(&ws[0][0][0], tid);
   }
+  const int LSH = 8 + a.LCPB;  // log2(RC)
+  const int RCM = RC - 1;
   const int64_t row0 = (int64_t)rank * RC;
   const int64_t l = row0 + tid;
   const bool valid = l < nr;
   const int lam = tid;
   int wbuf = 0;
 
-  // Canonical reduction of NQ per-row values (one per thread):
-  // chunk partials locally (warp trees + 8-way tree), one cluster barrier,
-  // then the level-2 tree over the <= 64 chunk partials gathered via DSMEM.
+  // Canonical reduction of NQ per-row values (one per thread): warp trees
+  // into shared memory, ONE cluster barrier (which also orders the CTA), then
+  // warp 0 of every CTA gathers the 8 warp sums of each chunk via DSMEM and
+  // finishes the canonical tree (8-way per chunk, then over the chunk
+  // partials); one __syncthreads broadcasts the result.
   auto reduce = [&](int NQ, const double* val) {
     for (int q = 0; q < NQ; ++q) {
       const double v = warp_tree(val[q]);
-      if (lane == 0) ws[q][w] = v;
-    }
-    __syncthreads();
-    if (tid < CPB * NQ) {
-      const int g = tid % CPB, q = tid / CPB;
-      cpart[wbuf][q][g] = tree8(&ws[q][8 * g]);
+      if (lane == 0) ws[wbuf][q][w] = v;
     }
     cluster.sync();
-    if (nch == 1) {
-      if (tid < NQ) res[tid] = cpb[0][(wbuf * 3 + tid) * 4 + 0];
-    } else if (tid < 256) {
+    if (w == 0) {
       for (int q = 0; q < NQ; ++q) {
-        const double v = warp_tree(tid < nch ? cpb[tid / CPB][(wbuf * 3 + q) * 4 + (tid % CPB)] : 0.0);
-        if (lane == 0) ws[q][w] = v;
+        // lane c holds chunk c (and c + 32)
+        double cp[2] = {0.0, 0.0};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = lane + 32 * h;
+          if (c < nch) {
+            const double* src = wsb[c >> a.LCPB] + (wbuf * 3 + q) * 32 + ((c & (CPB - 1)) << 3);
+            double w8[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) w8[k] = src[k];
+            cp[h] = tree8(w8);
+          }
+        }
+        if (nch == 1) {
+          if (lane == 0) res[q] = cp[0];
+        } else {
+          double W[8] = {warp_tree(cp[0]), warp_tree(cp[1]), 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+          if (lane == 0) res[q] = tree8(W);
+        }
       }
     }
-    __syncthreads();
-    if (nch > 1 && tid < NQ) res[tid] = tree8(&ws[tid][0]);
     __syncthreads();
     wbuf ^= 1;
   };
@@ -130,9 +142,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   //   mode 0: p_new_j = r_j + beta (p_old_j - omega v_old_j)   (it > 1)
   //   mode 1: p_new_j = r_j                                     (it == 1)
   //   mode 2: s_j     = r_j - alpha v_new_j
-  auto gather = [&](int mode, int cur, int64_t j, double beta, double omega, double alpha, double* out) {
-    const int g = (int)(j / RC);
-    const int rr = (int)(j - (int64_t)g * RC) * B;
+  auto gather = [&](int mode, int cur, int32_t j, double beta, double omega, double alpha, double* out) {
+    const int g = j >> LSH;
+    const int rr = (j & RCM) * B;
     const bool loc = g == rank;
     const double* R_ = (loc ? vr : rb[g]) + rr;
     if (mode == 1) {
@@ -157,7 +169,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
 #pragma unroll
     for (int s = 0; s < NS; ++s) cl[s] = MS ? mcol[s * RC + lam] : __ldg(&a.ell_col[s * a.cap + l]);
 #pragma unroll
-    for (int s = 0; s < NS; ++s) gather(mode, cur, cl[s] < 0 ? l : cl[s], beta, omega, alpha, xv[s]);
+    for (int s = 0; s < NS; ++s) gather(mode, cur, cl[s] < 0 ? (int32_t)l : cl[s], beta, omega, alpha, xv[s]);
     double acc[B];
 #pragma unroll
     for (int e = 0; e < B; ++e) acc[e] = xown[e];
@@ -168,9 +180,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
         rsim::blk::gemv_acc_flat<B>(M, xv[s], acc);
       }
     if (a.has_nnc) {
-      const int64_t i = a.act[l];
-      const int32_t q0 = a.nptr[i], q1 = a.nptr[i + 1];
-      for (int32_t q = q0; q < q1; ++q) {
+      const int2 rg = nrng[lam];
+      for (int32_t q = rg.x; q < rg.y; ++q) {
         const int32_t c2 = a.nnc_lcol[q];
         if (c2 >= 0) {
           double xn[B];
@@ -200,6 +211,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
       }
       val[0] = rsim::blk::rowdot<B>(bv, bv);
       val[1] = rsim::blk::rowdot<B>(fv, fv);
+      if (a.has_nnc) {
+        const int64_t i = a.act[l];
+        nrng[lam] = make_int2(a.nptr[i], a.nptr[i + 1]);
+      }
       if (MS) {
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
@@ -328,7 +343,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
 
 size_t smem_bytes(int B, int NS, bool MS, int CPB) {
   const size_t R = (size_t)CPB * 256;
-  size_t b = 9 * R * B * sizeof(double);
+  size_t b = 9 * R * B * sizeof(double) + R * sizeof(int2);
   if (MS) b += NS * R * B * B * sizeof(double) + NS * R * sizeof(int32_t);
   return b;
 }
@@ -415,14 +430,14 @@ int launch_krylov_dsm(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.F_raw = c->F_raw;
   a.x = c->x;
   a.dsc = c->dsc;
-  // one chunk per CTA when possible (G = nch <= 16), else 2..4 chunks per CTA
-  int tried[2] = {nch < GMAX ? nch : GMAX, GMAX};
-  for (int k = 0; k < 2; ++k) {
-    const int G = tried[k];
-    if (k == 1 && G == tried[0]) break;
-    const int CPB = (nch + G - 1) / G;
-    if (CPB > 4) continue;
+  // one chunk per CTA when possible (G = nch <= 16), else 2 or 4 chunks per CTA
+  // (powers of two, so the owner of a row is a shift)
+  for (int LCPB = 0; LCPB <= 2; ++LCPB) {
+    const int CPB = 1 << LCPB;
+    const int G = (nch + CPB - 1) / CPB;
+    if (G > GMAX) continue;
     a.CPB = CPB;
+    a.LCPB = LCPB;
     const int TPB = 256 * CPB;
     bool ok = false;
     int r;

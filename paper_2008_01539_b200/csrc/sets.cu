@@ -10,8 +10,8 @@
 //   shrink V_A = supp δu_A ∪ fracture
 //   boundary_layer / outer_halo
 //   Alg. 2 phase-1 labels, V_T
-// The expand/shrink decision is taken ON THE DEVICE from ‖δp_B‖∞ (k_decide),
-// so K6 -> K7 -> compaction runs without a host round trip.
+// The expand/shrink decision is taken ON THE DEVICE from ‖δp_B‖∞ (each K7
+// kernel evaluates it), so K6 -> K7 -> compaction runs without a host round trip.
 #include "ctx.cuh"
 
 namespace {
@@ -113,24 +113,22 @@ __global__ void __launch_bounds__(256) k_threshold(int32_t nA, const int32_t* __
   }
 }
 
-// ---------------------------------------------------------------- K7 decide
-__global__ void k_decide(DevScalars* dsc, double eps, int shrink_locked, int force_expand) {
-  double mb = __longlong_as_double((long long)dsc->maxB);
-  dsc->expand = force_expand ? 1 : ((!shrink_locked && mb >= eps) ? 1 : 0);
-  dsc->n_new = 0;
-  dsc->nB = 0;
-}
+// ---------------------------------------------------------------- K7
+// Set-update parameters shared by the dilation / count / scatter kernels.  The
+// expand/shrink decision is evaluated by every thread from ‖δp_B‖∞ (written by
+// K6 or k_threshold), so no separate decision kernel or host round trip.
+struct SetMode {
+  int mode;          // MODE_*
+  uint8_t dbit;      // D bit that holds the m-hop dilation
+  double eps;
+  int shrink_locked;
+  int force_expand;
+};
 
-// One dilation round: bit_out(i) = bit_in(i) | OR_j bit_in(j).
-__global__ void __launch_bounds__(256) k_dilate(Geo g, uint8_t* __restrict__ flags, uint8_t bit_in, uint8_t bit_out,
-                                                const DevScalars* __restrict__ dsc, int cond) {
-  if (cond && !dsc->expand) return;
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= g.n) return;
-  uint8_t f = flags[i];
-  bool v = (f & bit_in) != 0;
-  if (!v) each_nbr(g, i, [&](int64_t j) { if (flags[j] & bit_in) v = true; });
-  flags[i] = v ? (uint8_t)(f | bit_out) : (uint8_t)(f & ~bit_out);
+__device__ __forceinline__ bool decide_expand(const SetMode& M, const DevScalars* dsc) {
+  if (M.force_expand) return true;
+  const double mb = __longlong_as_double((long long)dsc->maxB);
+  return !M.shrink_locked && mb >= M.eps;
 }
 
 // A_new of a cell from its (pre-update) flag byte.
@@ -145,126 +143,119 @@ __device__ __forceinline__ bool a_new(uint8_t f, int mode, bool expand, uint8_t 
   }
 }
 
-// Compaction pass 1: per-tile count of A_new.
-__global__ void __launch_bounds__(256) k_count(Geo g, const uint8_t* __restrict__ fin, int mode, uint8_t dbit,
-                                               const DevScalars* __restrict__ dsc, int32_t* __restrict__ tile_cnt) {
-  __shared__ int32_t wsum[8];
-  const bool ex = dsc->expand != 0;
-  const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x * 8;
-  int cnt = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    int64_t i = base + k;
-    if (i < g.n && a_new(fin[i], mode, ex, dbit)) ++cnt;
+// One dilation round bit_out(i) = bit_in(i) | OR_j bit_in(j) (skipped when the
+// device decided to shrink).  With COUNT the same pass also counts A_new per
+// 256-cell tile (compaction pass 1), which needs only the cell's own bits.
+template <bool COUNT>
+__global__ void __launch_bounds__(256) k_dilate(Geo g, uint8_t* __restrict__ flags, uint8_t bit_in, uint8_t bit_out,
+                                                const DevScalars* __restrict__ dsc, SetMode M, int do_dilate,
+                                                int32_t* __restrict__ tile_cnt) {
+  const bool ex = decide_expand(M, dsc);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool keep = false;
+  if (i < g.n) {
+    uint8_t f = flags[i];
+    if (do_dilate && ((M.mode == MODE_DEVICE || M.mode == MODE_DD) ? ex : true)) {
+      bool v = (f & bit_in) != 0;
+      if (!v) each_nbr(g, i, [&](int64_t j) { if (flags[j] & bit_in) v = true; });
+      f = v ? (uint8_t)(f | bit_out) : (uint8_t)(f & ~bit_out);
+      flags[i] = f;
+    }
+    if (COUNT) keep = a_new(f, M.mode, ex, M.dbit);
   }
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, off);
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int s = 0;
-    for (int w = 0; w < 8; ++w) s += wsum[w];
-    tile_cnt[blockIdx.x] = s;
+  if (COUNT) {
+    const int cnt = __syncthreads_count(keep);
+    if (threadIdx.x == 0) tile_cnt[blockIdx.x] = cnt;
   }
 }
 
-// Compaction pass 2: exclusive scan of the tile counts (one block).
+// Compaction pass 2: exclusive scan of the tile counts (one block, strips of
+// consecutive tiles per thread).  Also publishes the decision + n_A and
+// resets the counters of pass 3.
 __global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t* __restrict__ cnt, int32_t* __restrict__ off,
-                                                      int32_t ntiles, DevScalars* dsc) {
+                                                      int32_t ntiles, DevScalars* dsc, SetMode M) {
   __shared__ int32_t wsum[32];
-  __shared__ int32_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int32_t base = 0; base < ntiles; base += 1024) {
-    int32_t idx = base + threadIdx.x;
-    int32_t v = idx < ntiles ? cnt[idx] : 0;
-    int32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[w] = x;
-    __syncthreads();
-    if (w == 0) {
-      int32_t z = wsum[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int32_t y = __shfl_up_sync(0xffffffffu, z, o);
-        if (lane >= o) z += y;
-      }
-      wsum[lane] = z;
-    }
-    __syncthreads();
-    int32_t excl = carry + (w > 0 ? wsum[w - 1] : 0) + x - v;
-    if (idx < ntiles) off[idx] = excl;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = excl + v;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) dsc->nA = carry;
-}
-
-// Compaction pass 3: A_new, V_B, V_T/labels, g2l, sorted active list.
-__global__ void __launch_bounds__(256) k_scatter(Geo g, const uint8_t* __restrict__ fin, uint8_t* __restrict__ fout,
-                                                 int mode, uint8_t dbit, int32_t round, DevScalars* dsc,
-                                                 const int32_t* __restrict__ tile_off, int32_t* __restrict__ act,
-                                                 int32_t* __restrict__ g2l, int32_t* __restrict__ label) {
-  __shared__ int32_t wsum[8];
-  const bool ex = dsc->expand != 0;
-  const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x * 8;
-  uint8_t keep[8];
-  int cnt = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    int64_t i = base + k;
-    keep[k] = 0;
-    if (i < g.n && a_new(fin[i], mode, ex, dbit)) { keep[k] = 1; ++cnt; }
-  }
-  // block exclusive scan of per-thread counts (warp ballot-free shfl scan)
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int x = cnt;
+  const int32_t per = (ntiles + 1023) / 1024;
+  const int32_t b0 = threadIdx.x * per;
+  int32_t tot = 0;
+  for (int32_t k = 0; k < per; ++k)
+    if (b0 + k < ntiles) tot += cnt[b0 + k];
+  int32_t x = tot;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, x, o);
+    int32_t y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
   if (lane == 31) wsum[w] = x;
   __syncthreads();
-  int wpre = 0;
-  for (int k = 0; k < w; ++k) wpre += wsum[k];
-  int pos = tile_off[blockIdx.x] + wpre + x - cnt;
-  int nb = 0, nnew = 0;
+  if (w == 0) {
+    int32_t z = wsum[lane];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    int64_t i = base + k;
-    if (i >= g.n) break;
-    uint8_t f = fin[i];
+    for (int o = 1; o < 32; o <<= 1) {
+      int32_t y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    wsum[lane] = z;
+  }
+  __syncthreads();
+  int32_t run = (w > 0 ? wsum[w - 1] : 0) + x - tot;
+  for (int32_t k = 0; k < per; ++k)
+    if (b0 + k < ntiles) {
+      off[b0 + k] = run;
+      run += cnt[b0 + k];
+    }
+  if (threadIdx.x == 1023) {
+    dsc->nA = wsum[31];
+    dsc->expand = decide_expand(M, dsc) ? 1 : 0;
+    dsc->nB = 0;
+    dsc->n_new = 0;
+  }
+}
+
+// Compaction pass 3 (one cell per thread, 256-cell tiles): A_new, V_B,
+// V_T/labels, g2l, sorted active list (warp ballot + block scan).
+__global__ void __launch_bounds__(256) k_scatter(Geo g, const uint8_t* __restrict__ fin, uint8_t* __restrict__ fout,
+                                                 SetMode M, int32_t round, DevScalars* dsc,
+                                                 const int32_t* __restrict__ tile_off, int32_t* __restrict__ act,
+                                                 int32_t* __restrict__ g2l, int32_t* __restrict__ label) {
+  __shared__ int32_t wcnt[8];
+  const bool ex = decide_expand(M, dsc);
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint8_t f = 0;
+  bool keep = false;
+  if (i < g.n) {
+    f = fin[i];
+    keep = a_new(f, M.mode, ex, M.dbit);
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, keep);
+  if (lane == 0) wcnt[w] = __popc(bal);
+  __syncthreads();
+  int pre = 0;
+  for (int k = 0; k < w; ++k) pre += wcnt[k];
+  int nb = 0, nnew = 0;
+  if (i < g.n) {
     uint8_t o = (uint8_t)(f & (F_PIN | F_T));
-    if (keep[k]) {
+    if (keep) {
       bool bnd = false;
-      each_nbr(g, i, [&](int64_t j) { if (!a_new(fin[j], mode, ex, dbit)) bnd = true; });
+      each_nbr(g, i, [&](int64_t j) { if (!a_new(fin[j], M.mode, ex, M.dbit)) bnd = true; });
       o |= F_A;
-      if (bnd) { o |= F_B; ++nb; }
-      if (mode == MODE_DD && !(f & F_T)) {
-        label[i] = round;
-        ++nnew;
+      if (bnd) { o |= F_B; nb = 1; }
+      if (M.mode == MODE_DD) {
+        if (!(f & F_T)) { label[i] = round; nnew = 1; }
+        o |= F_T;
       }
-      if (mode == MODE_DD) o |= F_T;
+      const int pos = tile_off[blockIdx.x] + pre + __popc(bal & ((1u << lane) - 1u));
       act[pos] = (int32_t)i;
       g2l[i] = pos;
-      ++pos;
     } else {
       g2l[i] = -1;
     }
     fout[i] = o;
   }
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-    nb += __shfl_down_sync(0xffffffffu, nb, off);
-    nnew += __shfl_down_sync(0xffffffffu, nnew, off);
-  }
+  nb = __reduce_add_sync(0xffffffffu, nb);
+  nnew = __reduce_add_sync(0xffffffffu, nnew);
   if (lane == 0) {
     if (nb) atomicAdd(&dsc->nB, nb);
     if (nnew) atomicAdd(&dsc->n_new, nnew);
@@ -459,35 +450,35 @@ int launch_threshold(rsim_gpu_ctx* c, double eps) {
   return RSIM_OK;
 }
 
-int launch_decide(rsim_gpu_ctx* c, double eps, int shrink_locked, int force_expand) {
-  k_decide<<<1, 1, 0, c->stream>>>(c->dsc, eps, shrink_locked, force_expand);
-  c->launches++;
-  RSIM_CUDA(cudaGetLastError());
-  return RSIM_OK;
-}
-
-int launch_dilate(rsim_gpu_ctx* c, int m, int cond) {
+// Full set update: [m-1 dilation rounds] + [round m fused with the tile count]
+// + scan + scatter.  4 launches for m = 2, no host round trip.
+int launch_set_update(rsim_gpu_ctx* c, int mode, int round, double eps, int m, int shrink_locked, int force_expand,
+                      int do_dilate) {
   Geo g = geo(c);
-  for (int r = 0; r < m; ++r) {
+  SetMode M;
+  M.mode = mode;
+  M.dbit = (m % 2 == 0) ? F_D0 : F_D1;
+  M.eps = eps;
+  M.shrink_locked = shrink_locked;
+  M.force_expand = force_expand;
+  const int64_t ntiles = nblk(c->n, 256);
+  const int rounds = do_dilate ? m : 0;
+  for (int r = 0; r + 1 < rounds; ++r) {
     uint8_t bin = (r % 2 == 0) ? F_D0 : F_D1, bout = (r % 2 == 0) ? F_D1 : F_D0;
-    k_dilate<<<nblk(c->n, 256), 256, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, cond);
+    k_dilate<false><<<ntiles, 256, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, 1, c->tile_cnt);
     c->launches++;
   }
-  RSIM_CUDA(cudaGetLastError());
-  return RSIM_OK;
-}
-
-// Final pass of every set update: count -> scan -> scatter into flags_alt,
-// then swap the flag buffers.  dbit = D bit holding the m-hop dilation.
-int launch_compact(rsim_gpu_ctx* c, int mode, int round, double /*eps*/, int m) {
-  Geo g = geo(c);
-  const uint8_t dbit = (m % 2 == 0) ? F_D0 : F_D1;
-  const int64_t ntiles = nblk(c->n, TILE);
-  k_count<<<ntiles, 256, 0, c->stream>>>(g, c->flags, mode, dbit, c->dsc, c->tile_cnt);
-  k_scan_tiles<<<1, 1024, 0, c->stream>>>(c->tile_cnt, c->tile_off, (int32_t)ntiles, c->dsc);
-  k_scatter<<<ntiles, 256, 0, c->stream>>>(g, c->flags, c->flags_alt, mode, dbit, round, c->dsc, c->tile_off,
-                                           c->act_buf, c->g2l, c->label);
-  c->launches += 3;
+  {
+    const int r = rounds - 1;
+    uint8_t bin = (r % 2 == 0) ? F_D0 : F_D1, bout = (r % 2 == 0) ? F_D1 : F_D0;
+    k_dilate<true><<<ntiles, 256, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, rounds > 0 ? 1 : 0,
+                                                  c->tile_cnt);
+    c->launches++;
+  }
+  k_scan_tiles<<<1, 1024, 0, c->stream>>>(c->tile_cnt, c->tile_off, (int32_t)ntiles, c->dsc, M);
+  k_scatter<<<ntiles, 256, 0, c->stream>>>(g, c->flags, c->flags_alt, M, round, c->dsc, c->tile_off, c->act_buf,
+                                           c->g2l, c->label);
+  c->launches += 2;
   RSIM_CUDA(cudaGetLastError());
   std::swap(c->flags, c->flags_alt);
   c->act = c->act_buf;
@@ -554,7 +545,7 @@ int launch_dd_partition(rsim_gpu_ctx* c, int32_t n_sub, int32_t* sizes) {
   for (int sel = 0; sel < 2; ++sel) {
     for (int k = 0; k < n_sub; ++k) {
       k_dd_count<<<ntiles, 256, 0, c->stream>>>(g, c->label, k, sel, c->tile_cnt);
-      k_scan_tiles<<<1, 1024, 0, c->stream>>>(c->tile_cnt, c->tile_off, (int32_t)ntiles, c->dsc);
+      k_scan_tiles<<<1, 1024, 0, c->stream>>>(c->tile_cnt, c->tile_off, (int32_t)ntiles, c->dsc, SetMode{MODE_KEEP, 0, 0.0, 1, 0});
       c->launches += 2;
       RSIM_CUDA(cudaMemcpyAsync(&(sel ? cnt_halo : cnt_sub)[k], &c->dsc->nA, sizeof(int32_t),
                                 cudaMemcpyDeviceToHost, c->stream));
@@ -580,7 +571,7 @@ int launch_dd_partition(rsim_gpu_ctx* c, int32_t n_sub, int32_t* sizes) {
     for (int k = 0; k < n_sub; ++k) {
       int32_t* out = sel ? d.halo_cells + d.halo_off[k] : d.sub_cells + d.sub_off[k];
       k_dd_count<<<ntiles, 256, 0, c->stream>>>(g, c->label, k, sel, c->tile_cnt);
-      k_scan_tiles<<<1, 1024, 0, c->stream>>>(c->tile_cnt, c->tile_off, (int32_t)ntiles, c->dsc);
+      k_scan_tiles<<<1, 1024, 0, c->stream>>>(c->tile_cnt, c->tile_off, (int32_t)ntiles, c->dsc, SetMode{MODE_KEEP, 0, 0.0, 1, 0});
       k_dd_scatter<<<ntiles, 256, 0, c->stream>>>(g, c->label, k, sel, c->tile_off, out);
       c->launches += 3;
     }
