@@ -119,6 +119,9 @@ int rsim_gpu_timers(rsim_gpu_ctx* ctx, int32_t enable, double* ms4, int32_t* lau
  * [3] Krylov launches' rows Σ n_A, [4] set-update passes (full-grid scans). */
 int rsim_gpu_counters(rsim_gpu_ctx* ctx, int64_t* out5, int32_t reset);
 
+/* Debug: cycle counters of the cluster Krylov phases (RSIM_KTRACE=1 at create). */
+int rsim_gpu_ktrace(rsim_gpu_ctx* ctx, unsigned long long* out8);
+
 /* CUDA events on the ctx stream (bench timing on the launching stream). */
 int rsim_gpu_mark(rsim_gpu_ctx* ctx, int32_t slot);                 /* slot < 64 */
 int rsim_gpu_elapsed(rsim_gpu_ctx* ctx, int32_t a, int32_t b, double* ms);

@@ -141,6 +141,7 @@ PROTOS: dict[str, tuple] = {
     "rsim_gpu_download_dp": (C.c_int, [P, dptr]),
     "rsim_gpu_timers": (C.c_int, [P, C.c_int32, dptr, i32ptr]),
     "rsim_gpu_mark": (C.c_int, [P, C.c_int32]),
+    "rsim_gpu_ktrace": (C.c_int, [P, C.POINTER(C.c_ulonglong)]),
     "rsim_gpu_elapsed": (C.c_int, [P, C.c_int32, C.c_int32, dptr]),
     "rsim_gpu_flush_l2": (C.c_int, [P]),
     "rsim_gpu_checkpoint": (C.c_int, [P, C.c_int32]),

@@ -4,6 +4,7 @@
 // device rsim_gpu_create fails with RSIM_ECUDA.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -232,6 +233,17 @@ int rsim_gpu_create(rsim_gpu_ctx** out, const rsim_graph_desc* g, const rsim_flu
   RSIM_CUDA(cudaStreamSynchronize(c->stream));
   c->act = c->act_buf;
   c->nA = 0;
+  if (const char* e = std::getenv("RSIM_KTRACE"); e && *e == '1') {
+    TRY(dalloc(&c->ktrace, 8));
+    RSIM_CUDA(cudaMemset(c->ktrace, 0, 8 * sizeof(unsigned long long)));
+  }
+  return RSIM_OK;
+}
+
+int rsim_gpu_ktrace(rsim_gpu_ctx* c, unsigned long long* out8) {
+  if (!c->ktrace) return RSIM_EARG;
+  RSIM_CUDA(cudaMemcpy(out8, c->ktrace, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  RSIM_CUDA(cudaMemset(c->ktrace, 0, 8 * sizeof(unsigned long long)));
   return RSIM_OK;
 }
 
@@ -242,7 +254,7 @@ int rsim_gpu_destroy(rsim_gpu_ctx* c) {
                   c->mold, c->p_prev, c->st, c->st_start, c->flags, c->flags_alt, c->act_buf, c->g2l, c->label,
                   c->list_buf, c->dp, c->last_dp, c->tile_cnt, c->tile_off, c->ell_col, c->ell_val, c->nnc_lcol,
                   c->nnc_val, c->F_raw, c->rhs, c->part_f2, c->x, c->r, c->r0, c->p, c->v, c->s, c->t, c->part,
-                  c->dsc, c->dd.sub_cells, c->dd.halo_cells, c->u_ckpt, c->st_ckpt, c->l2_scratch, c->pin0};
+                  c->dsc, c->dd.sub_cells, c->dd.halo_cells, c->u_ckpt, c->st_ckpt, c->l2_scratch, c->pin0, c->ktrace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hsc) cudaFreeHost(c->hsc);

@@ -121,6 +121,7 @@ struct rsim_gpu_ctx {
   void* l2_scratch = nullptr;
   int64_t counters[5] = {0, 0, 0, 0, 0};
   uint8_t* pin0 = nullptr;  // F_PIN|F_A for pinned cells, 0 elsewhere (reset source)
+  unsigned long long* ktrace = nullptr;  // Krylov phase cycle counters (debug, RSIM_KTRACE=1)
 };
 
 // ---- error plumbing (abi.cu) -------------------------------------------------
@@ -172,6 +173,17 @@ __device__ __forceinline__ unsigned long long dbits(double a) {
 __device__ __forceinline__ double warp_tree(double v) {
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) v = v + __shfl_down_sync(0xffffffffu, v, off);
+  return v;
+}
+// warp_tree for a warp whose lanes >= n hold structural +0.0 (n warp-uniform):
+// the additions of a structural zero are done locally (v + 0.0, same bits as
+// adding the shuffled +0.0), only the offsets that can reach data shuffle.
+__device__ __forceinline__ double warp_tree_n(double v, int n) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    if (off >= n) v = v + 0.0;
+    else v = v + __shfl_down_sync(0xffffffffu, v, off);
+  }
   return v;
 }
 __device__ __forceinline__ double tree8(const double* w) {

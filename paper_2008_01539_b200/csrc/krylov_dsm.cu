@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <map>
 #include <tuple>
+#include <type_traits>
 
 #include "ctx.cuh"
 
@@ -32,6 +33,8 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int GMAX = 16;
+constexpr int NNCMAX = 256;             // NNC entries cached in smem per CTA
+constexpr int NNC_GLOBAL = 0x40000000;  // flag in the range end: entries stay in global
 
 struct DArgs {
   int32_t nA, nslot, maxit, fixed, CPB, LCPB, nch;
@@ -48,6 +51,7 @@ struct DArgs {
   const double* F_raw;
   double* x;
   DevScalars* dsc;
+  unsigned long long* trace;  // optional [8] cycle accumulators (RSIM_KTRACE)
 };
 
 template <int B, int NS, bool MS, int MAXT>
@@ -68,6 +72,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   double* mval = vv1 + RC * B;                                    // [NS][RC][B*B]  (MS)
   int32_t* mcol = (int32_t*)(mval + (MS ? NS * RC * B * B : 0));   // [NS][RC]       (MS)
   int2* nrng = (int2*)(mcol + (MS ? NS * RC : 0));                // [RC] NNC ranges (has_nnc)
+  double* nsv = (double*)(nrng + RC);                              // [NNCMAX][B*B] NNC blocks
+  int32_t* nsc = (int32_t*)(nsv + NNCMAX * B * B);                 // [NNCMAX] NNC local columns
+  __shared__ int nnc_cnt;
 
   __shared__ double* rb[GMAX];
   __shared__ double* pb[2][GMAX];
@@ -105,33 +112,42 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   // warp 0 of every CTA gathers the 8 warp sums of each chunk via DSMEM and
   // finishes the canonical tree (8-way per chunk, then over the chunk
   // partials); one __syncthreads broadcasts the result.
-  auto reduce = [&](int NQ, const double* val) {
-    for (int q = 0; q < NQ; ++q) {
-      const double v = warp_tree(val[q]);
-      if (lane == 0) ws[wbuf][q][w] = v;
-    }
-    cluster.sync();
-    if (w == 0) {
-      for (int q = 0; q < NQ; ++q) {
-        // lane c holds chunk c (and c + 32)
-        double cp[2] = {0.0, 0.0};
+  auto csync = [&]() {
+    if (G == 1) __syncthreads();
+    else cluster.sync();
+  };
+  auto reduce = [&](auto NQc, const double* val) {
+    constexpr int NQ = decltype(NQc)::value;
+    double v[NQ];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = lane + 32 * h;
-          if (c < nch) {
-            const double* src = wsb[c >> a.LCPB] + (wbuf * 3 + q) * 32 + ((c & (CPB - 1)) << 3);
-            double w8[8];
+    for (int q = 0; q < NQ; ++q) v[q] = val[q];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) w8[k] = src[k];
-            cp[h] = tree8(w8);
-          }
+    for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) v[q] = v[q] + __shfl_down_sync(0xffffffffu, v[q], off);
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) ws[wbuf][q][w] = v[q];
+    csync();
+    if (w < NQ) {  // warp q finishes quantity q
+      const int q = w;
+      double cp[2] = {0.0, 0.0};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // lane c holds chunk c (and c + 32)
+        const int c = lane + 32 * h;
+        if (c < nch) {
+          const double* src = wsb[c >> a.LCPB] + (wbuf * 3 + q) * 32 + ((c & (CPB - 1)) << 3);
+          double w8[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) w8[k] = src[k];
+          cp[h] = tree8(w8);
         }
-        if (nch == 1) {
-          if (lane == 0) res[q] = cp[0];
-        } else {
-          double W[8] = {warp_tree(cp[0]), warp_tree(cp[1]), 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-          if (lane == 0) res[q] = tree8(W);
-        }
+      }
+      if (nch == 1) {
+        if (lane == 0) res[q] = cp[0];
+      } else {
+        double W[8] = {warp_tree_n(cp[0], nch), warp_tree_n(cp[1], nch - 32), 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        if (lane == 0) res[q] = tree8(W);
       }
     }
     __syncthreads();
@@ -181,12 +197,20 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
       }
     if (a.has_nnc) {
       const int2 rg = nrng[lam];
-      for (int32_t q = rg.x; q < rg.y; ++q) {
-        const int32_t c2 = a.nnc_lcol[q];
-        if (c2 >= 0) {
+      if (rg.y & NNC_GLOBAL) {
+        for (int32_t q = rg.x; q < (rg.y & ~NNC_GLOBAL); ++q) {
+          const int32_t c2 = a.nnc_lcol[q];
+          if (c2 >= 0) {
+            double xn[B];
+            gather(mode, cur, c2, beta, omega, alpha, xn);
+            rsim::blk::gemv_acc_flat<B>(&a.nnc_val[(int64_t)q * B * B], xn, acc);
+          }
+        }
+      } else {
+        for (int32_t q = rg.x; q < rg.y; ++q) {
           double xn[B];
-          gather(mode, cur, c2, beta, omega, alpha, xn);
-          rsim::blk::gemv_acc_flat<B>(&a.nnc_val[(int64_t)q * B * B], xn, acc);
+          gather(mode, cur, nsc[q], beta, omega, alpha, xn);
+          rsim::blk::gemv_acc_flat<B>(&nsv[q * B * B], xn, acc);
         }
       }
     }
@@ -195,6 +219,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   };
 
   // ---- load: matrix rows (MS), rhs -> r, r0; x = 0; (b,b), (F,F)
+  if (tid == 0) nnc_cnt = 0;
+  __syncthreads();
   {
     double val[3] = {0.0, 0.0, 0.0};
     if (valid) {
@@ -211,9 +237,26 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
       }
       val[0] = rsim::blk::rowdot<B>(bv, bv);
       val[1] = rsim::blk::rowdot<B>(fv, fv);
-      if (a.has_nnc) {
+      if (a.has_nnc) {  // cache this row's active NNC blocks in smem (order preserved)
         const int64_t i = a.act[l];
-        nrng[lam] = make_int2(a.nptr[i], a.nptr[i + 1]);
+        const int32_t q0 = a.nptr[i], q1 = a.nptr[i + 1];
+        int k = 0;
+        for (int32_t q = q0; q < q1; ++q) k += a.nnc_lcol[q] >= 0;
+        const int base = k ? atomicAdd(&nnc_cnt, k) : 0;
+        if (base + k <= NNCMAX) {
+          int m = base;
+          for (int32_t q = q0; q < q1; ++q) {
+            const int32_t c2 = a.nnc_lcol[q];
+            if (c2 < 0) continue;
+            nsc[m] = c2;
+#pragma unroll
+            for (int e = 0; e < B * B; ++e) nsv[m * B * B + e] = a.nnc_val[(int64_t)q * B * B + e];
+            ++m;
+          }
+          nrng[lam] = make_int2(base, base + k);
+        } else {
+          nrng[lam] = make_int2(q0, q1 | NNC_GLOBAL);
+        }
       }
       if (MS) {
 #pragma unroll
@@ -227,7 +270,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
         }
       }
     }
-    reduce(2, val);
+    reduce(std::integral_constant<int, 2>{}, val);
   }
   const double bb = res[0];
   if (rank == 0 && tid == 0) a.dsc->f2 = sqrt(res[1]);
@@ -242,7 +285,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   int cur = 0;  // buffer holding the current iteration's p, v
   if (bnorm != 0.0) {
     status = RSIM_ENOCONV;
+    unsigned long long tc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const bool tr = a.trace && rank == 0 && tid == 0;
+    long long t0 = clock64();
+#define KT_MARK(k) do { if (tr) { long long t1 = clock64(); tc[k] += (unsigned long long)(t1 - t0); t0 = t1; } } while (0)
     for (it = 1; it <= maxit; ++it) {
+      KT_MARK(7);
       const double beta = (it == 1) ? 0.0 : (rho_new / rho) * (alpha / omega);
       double* vpc = cur ? vp1 : vp0;
       double* vvc = cur ? vv1 : vv0;
@@ -265,7 +313,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
           for (int e = 0; e < B; ++e) vvc[lam * B + e] = y[e];
           val[0] = rsim::blk::rowdot<B>(&vr0[lam * B], y);
         }
-        reduce(1, val);
+        KT_MARK(0);
+        reduce(std::integral_constant<int, 1>{}, val);
+        KT_MARK(1);
       }
       const double r0v = res[0];
       if (r0v == 0.0 || !isfinite(r0v)) { status = RSIM_ENUM; break; }
@@ -289,7 +339,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
           val[1] = rsim::blk::rowdot<B>(y, sv);
           val[2] = rsim::blk::rowdot<B>(y, y);
         }
-        reduce(3, val);
+        KT_MARK(2);
+        reduce(std::integral_constant<int, 3>{}, val);
+        KT_MARK(3);
       }
       const double ssn = res[0], ts = res[1], tt = res[2];
       if (!fixed && sqrt(ssn) <= tol) {
@@ -318,7 +370,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
           val[0] = rsim::blk::rowdot<B>(rv, rv);
           val[1] = rsim::blk::rowdot<B>(&vr0[lam * B], rv);
         }
-        reduce(2, val);
+        KT_MARK(4);
+        reduce(std::integral_constant<int, 2>{}, val);
+        KT_MARK(5);
       }
       const double rr = res[0];
       rho = rho_new;
@@ -329,6 +383,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
       cur ^= 1;
     }
     if (it > maxit) { it = maxit; status = fixed ? RSIM_OK : RSIM_ENOCONV; }
+    if (tr)
+      for (int k = 0; k < 8; ++k) atomicAdd(&a.trace[k], tc[k]);
+#undef KT_MARK
   }
   if (valid)
 #pragma unroll
@@ -343,7 +400,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
 
 size_t smem_bytes(int B, int NS, bool MS, int CPB) {
   const size_t R = (size_t)CPB * 256;
-  size_t b = 9 * R * B * sizeof(double) + R * sizeof(int2);
+  size_t b = 9 * R * B * sizeof(double) + R * sizeof(int2) + NNCMAX * (B * B * sizeof(double) + sizeof(int32_t));
   if (MS) b += NS * R * B * B * sizeof(double) + NS * R * sizeof(int32_t);
   return b;
 }
@@ -429,6 +486,7 @@ int launch_krylov_dsm(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.rhs = c->rhs;
   a.F_raw = c->F_raw;
   a.x = c->x;
+  a.trace = c->ktrace;
   a.dsc = c->dsc;
   // one chunk per CTA when possible (G = nch <= 16), else 2 or 4 chunks per CTA
   // (powers of two, so the owner of a row is a shift)
