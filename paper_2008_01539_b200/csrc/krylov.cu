@@ -13,6 +13,9 @@
 // branches and the results are bit-identical to oracle/oracle.cpp.
 // Small systems (<= 64 chunks) go to krylov_dsm.cu (one cluster, DSMEM).
 //
+// Per iteration 3 grid barriers: the p- and s-updates of neighbours are
+// recomputed at the gather site (p, v double-buffered), (s,s) is reduced
+// together with (t,s), (t,t).
 // Element formulas (identical in oracle/oracle.cpp bicgstab()):
 //   p = r + β (p − ω v);  s = r − α v;  x = (x + α p) + ω s;  r = s − ω t.
 #include <cooperative_groups.h>
@@ -40,7 +43,7 @@ struct KArgs {
   const double* nnc_val;
   const double* rhs;
   const double* F_raw;
-  double *x, *r, *r0, *p, *v, *s, *t;
+  double *x, *r, *r0, *p, *v, *s, *t, *p2, *v2;
   double* part;   // [3][pstride]  level-1 partials
   double* part2;  // [3][pstride2] level-2 partials (very large systems)
   int32_t pstride, pstride2;
@@ -99,8 +102,27 @@ __device__ __forceinline__ void reduce_small(Red& R, int q, const double* src, i
   __syncthreads();
 }
 
+// Neighbour value of the vector being multiplied, recomputed from vectors
+// that are read-only in the current phase (same formula as the owner, so the
+// same bits):  mode 0: p_j = r_j + β (p_old_j − ω v_old_j);  mode 1: p_j = r_j;
+// mode 2: s_j = r_j − α v_j.
 template <int B>
-__device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, const double* __restrict__ xin, double* acc) {
+__device__ __forceinline__ void nbr_val(int mode, const double* __restrict__ r, const double* __restrict__ po,
+                                        const double* __restrict__ vo, int64_t j, double beta, double omega,
+                                        double alpha, double* out) {
+#pragma unroll
+  for (int e = 0; e < B; ++e) {
+    const int64_t q = j * B + e;
+    if (mode == 1) out[e] = r[q];
+    else if (mode == 0) out[e] = r[q] + beta * (po[q] - omega * vo[q]);
+    else out[e] = r[q] - alpha * vo[q];
+  }
+}
+
+template <int B>
+__device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, const double* __restrict__ r,
+                                         const double* __restrict__ po, const double* __restrict__ vo, double beta,
+                                         double omega, double alpha, const double* own, double* acc) {
   const int32_t* __restrict__ col = a.ell_col;
   const double* __restrict__ val = a.ell_val;
   int32_t cl[6];
@@ -109,11 +131,9 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, const double
   double xv[6][B];
 #pragma unroll
   for (int s = 0; s < 6; ++s)
-    if (cl[s] >= 0)
+    if (cl[s] >= 0) nbr_val<B>(mode, r, po, vo, cl[s], beta, omega, alpha, xv[s]);
 #pragma unroll
-      for (int e = 0; e < B; ++e) xv[s][e] = xin[(int64_t)cl[s] * B + e];
-#pragma unroll
-  for (int e = 0; e < B; ++e) acc[e] = xin[l * B + e];
+  for (int e = 0; e < B; ++e) acc[e] = own[e];
 #pragma unroll
   for (int s = 0; s < 6; ++s)
     if (cl[s] >= 0) rsim::blk::gemv_acc_flat<B>(&val[((int64_t)s * a.cap + l) * B * B], xv[s], acc);
@@ -122,7 +142,11 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, const double
     const int32_t q0 = a.nptr[i], q1 = a.nptr[i + 1];
     for (int32_t q = q0; q < q1; ++q) {
       const int32_t cc = a.nnc_lcol[q];
-      if (cc >= 0) rsim::blk::gemv_acc_flat<B>(&a.nnc_val[(int64_t)q * B * B], &xin[(int64_t)cc * B], acc);
+      if (cc >= 0) {
+        double xn[B];
+        nbr_val<B>(mode, r, po, vo, cc, beta, omega, alpha, xn);
+        rsim::blk::gemv_acc_flat<B>(&a.nnc_val[(int64_t)q * B * B], xn, acc);
+      }
     }
   }
 }
@@ -197,26 +221,24 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   int status = RSIM_ENOCONV;
   int it = 0;
   double relres = 0.0;
+  int cur = 0;  // which (p, v) buffer pair holds the current iterate
   for (it = 1; it <= maxit; ++it) {
-    // ---- p update
     const double beta = (it == 1) ? 0.0 : (rho_new / rho) * (alpha / omega);
-    for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
-      const int64_t l = rd * KT + tid;
-      if (l < nr)
-#pragma unroll
-        for (int e = 0; e < B; ++e) {
-          const int64_t q = l * B + e;
-          a.p[q] = (it == 1) ? a.r[q] : a.r[q] + beta * (a.p[q] - omega * a.v[q]);
-        }
-    }
-    sync();
-    // ---- v = Â p ; (r0, v)
+    double* pc = cur ? a.p2 : a.p;
+    double* vc = cur ? a.v2 : a.v;
+    const double* po = cur ? a.p : a.p2;
+    const double* vo = cur ? a.v : a.v2;
+    // ---- p = r + β(p − ωv) (own, and recomputed for neighbours); v = Â p; (r0, v)
     ROUNDS_BEGIN
     if (ok) {
-      double y[B];
-      spmv_row<B>(a, l, a.p, y);
+      double pown[B];
+      nbr_val<B>(it == 1 ? 1 : 0, a.r, po, vo, l, beta, omega, 0.0, pown);
 #pragma unroll
-      for (int e = 0; e < B; ++e) a.v[l * B + e] = y[e];
+      for (int e = 0; e < B; ++e) pc[l * B + e] = pown[e];
+      double y[B];
+      spmv_row<B>(a, l, it == 1 ? 1 : 0, a.r, po, vo, beta, omega, 0.0, pown, y);
+#pragma unroll
+      for (int e = 0; e < B; ++e) vc[l * B + e] = y[e];
       val[0] = rsim::blk::rowdot<B>(&a.r0[l * B], y);
     }
     ROUNDS_END(1)
@@ -224,45 +246,33 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     const double r0v = R.res[0];
     if (r0v == 0.0 || !isfinite(r0v)) { status = RSIM_ENUM; break; }
     alpha = rho_new / r0v;
-    // ---- s = r − α v ; (s, s)
+    // ---- s = r − α v (own + recomputed); t = Â s; (s,s), (t,s), (t,t)
     ROUNDS_BEGIN
     if (ok) {
       double sv[B];
+      nbr_val<B>(2, a.r, po, vc, l, 0.0, 0.0, alpha, sv);
+      double y[B];
+      spmv_row<B>(a, l, 2, a.r, po, vc, 0.0, 0.0, alpha, sv, y);
 #pragma unroll
-      for (int e = 0; e < B; ++e) {
-        const int64_t q = l * B + e;
-        sv[e] = a.r[q] - alpha * a.v[q];
-        a.s[q] = sv[e];
-      }
+      for (int e = 0; e < B; ++e) { a.s[l * B + e] = sv[e]; a.t[l * B + e] = y[e]; }
       val[0] = rsim::blk::rowdot<B>(sv, sv);
+      val[1] = rsim::blk::rowdot<B>(y, sv);
+      val[2] = rsim::blk::rowdot<B>(y, y);
     }
-    ROUNDS_END(1)
-    reduce(1);
-    const double ss = R.res[0];
+    ROUNDS_END(3)
+    reduce(3);
+    const double ss = R.res[0], ts = R.res[1], tt = R.res[2];
     if (!fixed && sqrt(ss) <= tol) {
       for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
         const int64_t l = rd * KT + tid;
         if (l < nr)
 #pragma unroll
-          for (int e = 0; e < B; ++e) a.x[l * B + e] = a.x[l * B + e] + alpha * a.p[l * B + e];
+          for (int e = 0; e < B; ++e) a.x[l * B + e] = a.x[l * B + e] + alpha * pc[l * B + e];
       }
       relres = sqrt(ss) / bnorm;
       status = RSIM_OK;
       break;
     }
-    // ---- t = Â s ; (t, s), (t, t)
-    ROUNDS_BEGIN
-    if (ok) {
-      double y[B];
-      spmv_row<B>(a, l, a.s, y);
-#pragma unroll
-      for (int e = 0; e < B; ++e) a.t[l * B + e] = y[e];
-      val[0] = rsim::blk::rowdot<B>(y, &a.s[l * B]);
-      val[1] = rsim::blk::rowdot<B>(y, y);
-    }
-    ROUNDS_END(2)
-    reduce(2);
-    const double ts = R.res[0], tt = R.res[1];
     if (tt == 0.0 || !isfinite(tt)) { status = RSIM_ENUM; break; }
     omega = ts / tt;
     // ---- x, r update ; (r, r), (r0, r)
@@ -273,7 +283,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       for (int e = 0; e < B; ++e) {
         const int64_t q = l * B + e;
         const double sq = a.s[q];
-        a.x[q] = (a.x[q] + alpha * a.p[q]) + omega * sq;
+        a.x[q] = (a.x[q] + alpha * pc[q]) + omega * sq;
         rv[e] = sq - omega * a.t[q];
         a.r[q] = rv[e];
         r0v_[e] = a.r0[q];
@@ -289,6 +299,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     relres = sqrt(rr) / bnorm;
     if (!fixed && sqrt(rr) <= tol) { status = RSIM_OK; break; }
     if (omega == 0.0 || rho_new == 0.0 || !isfinite(rho_new)) { status = RSIM_ENUM; break; }
+    cur ^= 1;
   }
   if (it > maxit) { it = maxit; status = fixed ? RSIM_OK : RSIM_ENOCONV; }
   if (blockIdx.x == 0 && tid == 0) {
@@ -314,6 +325,7 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.act = c->act; a.nptr = c->nptr; a.nnc_lcol = c->nnc_lcol; a.nnc_val = c->nnc_val;
   a.rhs = c->rhs; a.F_raw = c->F_raw;
   a.x = c->x; a.r = c->r; a.r0 = c->r0; a.p = c->p; a.v = c->v; a.s = c->s; a.t = c->t;
+  a.p2 = c->p2; a.v2 = c->v2;
   a.pstride = (int32_t)((c->n + 255) / 256);
   a.pstride2 = (a.pstride + 255) / 256;
   a.part = c->part;

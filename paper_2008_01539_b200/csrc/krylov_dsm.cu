@@ -4,8 +4,9 @@
 // rows), so a Krylov iteration is bound by latency, not HBM.  This kernel runs
 // the whole solve inside ONE thread-block cluster of G <= 16 CTAs:
 //
-//   * CTA g owns the contiguous local rows [g*RC, (g+1)*RC), RC = CPB*256, i.e.
-//     CPB whole 256-row canonical chunks (blockops.h); a chunk partial is 8
+//   * CTA g owns the contiguous local rows [g*RC, (g+1)*RC), RC = 64..1024
+//     (RC/32 canonical warps, blockops.h); canonical warp sums are local, a
+//     chunk partial is the 8-way tree of 8 warp sums
 //     warp shuffles + an 8-way tree inside the CTA, and only the <= 64 chunk
 //     partials cross DSMEM (one cluster barrier per reduction);
 //   * the Krylov vectors and (when it fits) the ELL rows of each CTA live in
@@ -37,7 +38,7 @@ constexpr int NNCMAX = 256;             // NNC entries cached in smem per CTA
 constexpr int NNC_GLOBAL = 0x40000000;  // flag in the range end: entries stay in global
 
 struct DArgs {
-  int32_t nA, nslot, maxit, fixed, CPB, LCPB, nch;
+  int32_t nA, nslot, maxit, fixed, LRC, nch;
   int64_t cap;
   bool has_nnc;
   double rtol;
@@ -57,15 +58,12 @@ struct DArgs {
 template <int B, int NS, bool MS, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   extern __shared__ __align__(16) double dyn[];
-  const int RC = a.CPB * 256;
-  // own rows: r, r0, x, s, t, p[2], v[2]  (p, v double-buffered: neighbours
-  // read the previous iterate while the owner writes the new one)
+  const int RC = 1 << a.LRC;
+  // shared (read by neighbours): r, p[2], v[2]  (p, v double-buffered:
+  // neighbours read the previous iterate while the owner writes the new one);
+  // own-row-only vectors r0, x, s, t live in registers.
   double* vr = dyn;
-  double* vr0 = vr + RC * B;
-  double* vx = vr0 + RC * B;
-  double* vs = vx + RC * B;
-  double* vt = vs + RC * B;
-  double* vp0 = vt + RC * B;
+  double* vp0 = vr + RC * B;
   double* vp1 = vp0 + RC * B;
   double* vv0 = vp1 + RC * B;
   double* vv1 = vv0 + RC * B;
@@ -90,7 +88,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   const int w = tid >> 5, lane = tid & 31;
   const int64_t nr = a.nA;
   const int nch = a.nch;
-  const int CPB = a.CPB;
+  const int LWPC = a.LRC - 5;  // log2(warps per CTA)
   if (tid < G) {
     rb[tid] = cluster.map_shared_rank(vr, tid);
     pb[0][tid] = cluster.map_shared_rank(vp0, tid);
@@ -99,7 +97,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
     vb[1][tid] = cluster.map_shared_rank(vv1, tid);
     wsb[tid] = cluster.map_shared_rank(&ws[0][0][0], tid);
   }
-  const int LSH = 8 + a.LCPB;  // log2(RC)
+  const int LSH = a.LRC;  // log2(RC)
   const int RCM = RC - 1;
   const int64_t row0 = (int64_t)rank * RC;
   const int64_t l = row0 + tid;
@@ -129,17 +127,19 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
 #pragma unroll
       for (int q = 0; q < NQ; ++q) ws[wbuf][q][w] = v[q];
     csync();
-    if (w < NQ) {  // warp q finishes quantity q
-      const int q = w;
+    for (int q = w; q < NQ; q += (1 << LWPC)) {  // warp w finishes quantities w, w+WPC, ...
       double cp[2] = {0.0, 0.0};
 #pragma unroll
       for (int h = 0; h < 2; ++h) {  // lane c holds chunk c (and c + 32)
         const int c = lane + 32 * h;
         if (c < nch) {
-          const double* src = wsb[c >> a.LCPB] + (wbuf * 3 + q) * 32 + ((c & (CPB - 1)) << 3);
           double w8[8];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) w8[k] = src[k];
+          for (int k = 0; k < 8; ++k) {  // canonical warp 8c+k lives on CTA gw >> LWPC
+            const int gw = (c << 3) | k;
+            w8[k] = ((int64_t)gw << 5) < nr ? wsb[gw >> LWPC][(wbuf * 3 + q) * 32 + (gw & ((1 << LWPC) - 1))]
+                                            : 0.0;  // warp entirely past n_A: structural zero
+          }
           cp[h] = tree8(w8);
         }
       }
@@ -218,6 +218,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
     for (int e = 0; e < B; ++e) y[e] = acc[e];
   };
 
+  double r0r[B], xr[B], sr[B], tr_[B];
+#pragma unroll
+  for (int e = 0; e < B; ++e) { r0r[e] = 0.0; xr[e] = 0.0; sr[e] = 0.0; tr_[e] = 0.0; }
   // ---- load: matrix rows (MS), rhs -> r, r0; x = 0; (b,b), (F,F)
   if (tid == 0) nnc_cnt = 0;
   __syncthreads();
@@ -230,8 +233,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
         bv[e] = a.rhs[l * B + e];
         fv[e] = a.F_raw[l * B + e];
         vr[lam * B + e] = bv[e];
-        vr0[lam * B + e] = bv[e];
-        vx[lam * B + e] = 0.0;
+        r0r[e] = bv[e];
+        xr[e] = 0.0;
         vp0[lam * B + e] = 0.0; vp1[lam * B + e] = 0.0;
         vv0[lam * B + e] = 0.0; vv1[lam * B + e] = 0.0;
       }
@@ -311,7 +314,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
           spmv(it == 1 ? 1 : 0, cur, pown, beta, omega, 0.0, y);
 #pragma unroll
           for (int e = 0; e < B; ++e) vvc[lam * B + e] = y[e];
-          val[0] = rsim::blk::rowdot<B>(&vr0[lam * B], y);
+          val[0] = rsim::blk::rowdot<B>(r0r, y);
         }
         KT_MARK(0);
         reduce(std::integral_constant<int, 1>{}, val);
@@ -329,12 +332,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
           for (int e = 0; e < B; ++e) {
             const int q = lam * B + e;
             sv[e] = vr[q] - alpha * vvc[q];
-            vs[q] = sv[e];
+            sr[e] = sv[e];
           }
           double y[B];
           spmv(2, cur, sv, 0.0, 0.0, alpha, y);
 #pragma unroll
-          for (int e = 0; e < B; ++e) vt[lam * B + e] = y[e];
+          for (int e = 0; e < B; ++e) tr_[e] = y[e];
           val[0] = rsim::blk::rowdot<B>(sv, sv);
           val[1] = rsim::blk::rowdot<B>(y, sv);
           val[2] = rsim::blk::rowdot<B>(y, y);
@@ -347,7 +350,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
       if (!fixed && sqrt(ssn) <= tol) {
         if (valid)
 #pragma unroll
-          for (int e = 0; e < B; ++e) vx[lam * B + e] = vx[lam * B + e] + alpha * vpc[lam * B + e];
+          for (int e = 0; e < B; ++e) xr[e] = xr[e] + alpha * vpc[lam * B + e];
         relres = sqrt(ssn) / bnorm;
         status = RSIM_OK;
         break;
@@ -362,13 +365,13 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
 #pragma unroll
           for (int e = 0; e < B; ++e) {
             const int q = lam * B + e;
-            const double sq = vs[q];
-            vx[q] = (vx[q] + alpha * vpc[q]) + omega * sq;
-            rv[e] = sq - omega * vt[q];
+            const double sq = sr[e];
+            xr[e] = (xr[e] + alpha * vpc[q]) + omega * sq;
+            rv[e] = sq - omega * tr_[e];
             vr[q] = rv[e];
           }
           val[0] = rsim::blk::rowdot<B>(rv, rv);
-          val[1] = rsim::blk::rowdot<B>(&vr0[lam * B], rv);
+          val[1] = rsim::blk::rowdot<B>(r0r, rv);
         }
         KT_MARK(4);
         reduce(std::integral_constant<int, 2>{}, val);
@@ -389,7 +392,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   }
   if (valid)
 #pragma unroll
-    for (int e = 0; e < B; ++e) a.x[l * B + e] = vx[lam * B + e];
+    for (int e = 0; e < B; ++e) a.x[l * B + e] = xr[e];
   if (rank == 0 && tid == 0) {
     a.dsc->lin_iters = it;
     a.dsc->lin_relres = relres;
@@ -398,9 +401,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   cluster.sync();  // keep every CTA's shared memory alive until all remote reads are done
 }
 
-size_t smem_bytes(int B, int NS, bool MS, int CPB) {
-  const size_t R = (size_t)CPB * 256;
-  size_t b = 9 * R * B * sizeof(double) + R * sizeof(int2) + NNCMAX * (B * B * sizeof(double) + sizeof(int32_t));
+size_t smem_bytes(int B, int NS, bool MS, int LRC) {
+  const size_t R = (size_t)1 << LRC;
+  size_t b = 5 * R * B * sizeof(double) + R * sizeof(int2) + NNCMAX * (B * B * sizeof(double) + sizeof(int32_t));
   if (MS) b += NS * R * B * B * sizeof(double) + NS * R * sizeof(int32_t);
   return b;
 }
@@ -439,7 +442,7 @@ int launch_t(rsim_gpu_ctx* c, const DArgs& a, int G, int TPB, size_t smem, bool*
 
 template <int B, int NS>
 int launch_bn(rsim_gpu_ctx* c, DArgs& a, int G, int TPB, bool* ok) {
-  const size_t with_m = smem_bytes(B, NS, true, a.CPB), without = smem_bytes(B, NS, false, a.CPB);
+  const size_t with_m = smem_bytes(B, NS, true, a.LRC), without = smem_bytes(B, NS, false, a.LRC);
   const size_t cap = 220 * 1024;
   if (with_m <= cap) {
     int r = TPB <= 512 ? launch_t<B, NS, true, 512>(c, a, G, TPB, with_m, ok)
@@ -490,13 +493,19 @@ int launch_krylov_dsm(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.dsc = c->dsc;
   // one chunk per CTA when possible (G = nch <= 16), else 2 or 4 chunks per CTA
   // (powers of two, so the owner of a row is a shift)
-  for (int LCPB = 0; LCPB <= 2; ++LCPB) {
-    const int CPB = 1 << LCPB;
-    const int G = (nch + CPB - 1) / CPB;
+  // rows per CTA: the smallest power of two >= 64 that fits the system in
+  // <= 16 CTAs (more CTAs = shorter per-CTA critical path)
+  static int minl = -1;
+  if (minl < 0) {
+    const char* e = std::getenv("RSIM_DSM_MINLRC");
+    minl = e ? std::atoi(e) : 6;
+  }
+  for (int LRC = minl; LRC <= 10; ++LRC) {
+    const int RC = 1 << LRC;
+    const int G = (c->nA + RC - 1) / RC;
     if (G > GMAX) continue;
-    a.CPB = CPB;
-    a.LCPB = LCPB;
-    const int TPB = 256 * CPB;
+    a.LRC = LRC;
+    const int TPB = RC;
     bool ok = false;
     int r;
     switch (c->b * 10 + c->nslot) {
