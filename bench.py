@@ -168,7 +168,7 @@ def bytes_k7(n, nA, m):
 WORKLOAD = {"config": 2, "solver": 1, "name": "c2_oilwater_256x256_dfn40_localized_newton_30steps"}
 
 
-def run_reference(args, rank, ws):
+def run_reference(args, rank, ws):  # noqa: C901
     """--impl reference: the CPU oracle (port of SPEC + Algorithms 1-2) on all host threads."""
     if rank != 0:
         return
@@ -181,6 +181,8 @@ def run_reference(args, rank, ws):
     s0 = case.init_state()
     dts = case.schedule()
     opts = case.solver_opts()
+    if args.precond is not None:
+        opts.precond = args.precond
     orc = Oracle(case)
     for _ in range(args.warmup):
         orc.run_case(WORKLOAD["solver"], s0, dts, opts)
@@ -298,6 +300,8 @@ def main():
     ap.add_argument("--c5", default="0.05,1.0", help="config-5 active fractions ('' to skip)")
     ap.add_argument("--c5-reps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--precond", type=int, default=None,
+                    help="0 block-Jacobi, 2 block-Jacobi + first-order Neumann polynomial (default: case default)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, ws, lr = dist_env()
@@ -315,6 +319,8 @@ def main():
     s0 = case.init_state()
     dts = case.schedule()
     opts = case.solver_opts()
+    if args.precond is not None:
+        opts.precond = args.precond
     sim = pkg.GpuSimulator(case)
     L, ctx = sim.L, sim._ctx
     b, D = case.b, (3 if case.nz > 1 else 2)

@@ -36,7 +36,7 @@ enum { RSIM_KIND_MATRIX = 0, RSIM_KIND_FRACTURE = 1 };
 
 /* Linear solver selectors. */
 enum { RSIM_LIN_BICGSTAB = 0, RSIM_LIN_GMRES = 1 };
-enum { RSIM_PREC_BJACOBI = 0, RSIM_PREC_ILU0 = 1 };
+enum { RSIM_PREC_BJACOBI = 0, RSIM_PREC_ILU0 = 1, RSIM_PREC_NEUMANN1 = 2 };
 
 /* Return codes of every C-ABI call. */
 enum {

@@ -286,7 +286,15 @@ static double dotc(int64_t nrows, const double* a, const double* b) {
 template <int B>
 static int bicgstab(const Model& M, const rsim_solver_opts& o, double* x, int32_t* iters, double* relres) {
   const int64_t nr = M.nA, N = nr * B;
-  std::vector<double> r(M.rhs), r0(M.rhs), p(N, 0.0), v(N, 0.0), s(N), t(N);
+  const bool neu = o.precond == RSIM_PREC_NEUMANN1;
+  std::vector<double> r(M.rhs), r0(M.rhs), p(N, 0.0), v(N, 0.0), s(N), t(N), ph, sh, y;
+  if (neu) { ph.assign(N, 0.0); sh.assign(N, 0.0); y.assign(N, 0.0); }
+  // M^{-1} z = z + (z - Â z): first-order Neumann polynomial on the unit-diagonal system
+  auto prec = [&](const std::vector<double>& z, std::vector<double>& out) {
+    spmv<B>(M, z.data(), y.data());
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < N; ++e) out[e] = z[e] + (z[e] - y[e]);
+  };
   std::fill(x, x + N, 0.0);
   double bb = dotc<B>(nr, r.data(), r.data());
   double bnorm = std::sqrt(bb);
@@ -306,28 +314,30 @@ static int bicgstab(const Model& M, const rsim_solver_opts& o, double* x, int32_
 #pragma omp parallel for schedule(static)
       for (int64_t e = 0; e < N; ++e) p[e] = r[e] + beta * (p[e] - omega * v[e]);
     }
-    spmv<B>(M, p.data(), v.data());
+    const std::vector<double>& pp = neu ? (prec(p, ph), ph) : p;
+    spmv<B>(M, pp.data(), v.data());
     double r0v = dotc<B>(nr, r0.data(), v.data());
     if (r0v == 0.0 || !std::isfinite(r0v)) { *iters = it; return RSIM_ENUM; }
     alpha = rho_new / r0v;
 #pragma omp parallel for schedule(static)
     for (int64_t e = 0; e < N; ++e) s[e] = r[e] - alpha * v[e];
+    const std::vector<double>& ss_ = neu ? (prec(s, sh), sh) : s;
+    spmv<B>(M, ss_.data(), t.data());
     double ss = dotc<B>(nr, s.data(), s.data());
+    double ts = dotc<B>(nr, t.data(), s.data());
+    double tt = dotc<B>(nr, t.data(), t.data());
     if (!fixed && std::sqrt(ss) <= tol) {
 #pragma omp parallel for schedule(static)
-      for (int64_t e = 0; e < N; ++e) x[e] = x[e] + alpha * p[e];
+      for (int64_t e = 0; e < N; ++e) x[e] = x[e] + alpha * pp[e];
       *iters = it;
       *relres = std::sqrt(ss) / bnorm;
       return RSIM_OK;
     }
-    spmv<B>(M, s.data(), t.data());
-    double ts = dotc<B>(nr, t.data(), s.data());
-    double tt = dotc<B>(nr, t.data(), t.data());
     if (tt == 0.0 || !std::isfinite(tt)) { *iters = it; return RSIM_ENUM; }
     omega = ts / tt;
 #pragma omp parallel for schedule(static)
     for (int64_t e = 0; e < N; ++e) {
-      x[e] = (x[e] + alpha * p[e]) + omega * s[e];
+      x[e] = (x[e] + alpha * pp[e]) + omega * ss_[e];
       r[e] = s[e] - omega * t[e];
     }
     double rr = dotc<B>(nr, r.data(), r.data());

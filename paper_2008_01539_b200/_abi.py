@@ -17,7 +17,7 @@ LIB_PATH = Path(__file__).resolve().parent / "lib" / "librsim.so"
 RSIM_OK, RSIM_EARG, RSIM_ECUDA, RSIM_ENUM, RSIM_ENOCONV = 0, 1, 2, 3, 4
 FLUID_SINGLE, FLUID_OILWATER, FLUID_BLACKOIL = 1, 2, 3
 LIN_BICGSTAB, LIN_GMRES = 0, 1
-PREC_BJACOBI, PREC_ILU0 = 0, 1
+PREC_BJACOBI, PREC_ILU0, PREC_NEUMANN1 = 0, 1, 2
 MAX_ITER_RECORDS = 4096
 
 dptr = C.POINTER(C.c_double)

@@ -210,6 +210,7 @@ int rsim_gpu_create(rsim_gpu_ctx** out, const rsim_graph_desc* g, const rsim_flu
   TRY(dalloc(&c->x, n * b)); TRY(dalloc(&c->r, n * b)); TRY(dalloc(&c->r0, n * b));
   TRY(dalloc(&c->p, n * b)); TRY(dalloc(&c->v, n * b)); TRY(dalloc(&c->s, n * b)); TRY(dalloc(&c->t, n * b));
   TRY(dalloc(&c->p2, n * b)); TRY(dalloc(&c->v2, n * b));
+  TRY(dalloc(&c->ph, n * b)); TRY(dalloc(&c->sh, n * b));
   TRY(dalloc(&c->part, 4 * nchunks + 64));
   TRY(dalloc(&c->dsc, 1));
   RSIM_CUDA(cudaMallocHost((void**)&c->hsc, sizeof(DevScalars)));
@@ -254,7 +255,7 @@ int rsim_gpu_destroy(rsim_gpu_ctx* c) {
   void* ptrs[] = {c->tx, c->ty, c->tz, c->pv, c->wi, c->kind, c->nptr, c->nnbr, c->nt, c->u, c->u_start,
                   c->mold, c->p_prev, c->st, c->st_start, c->flags, c->flags_alt, c->act_buf, c->g2l, c->label,
                   c->list_buf, c->dp, c->last_dp, c->tile_cnt, c->tile_off, c->ell_col, c->ell_val, c->nnc_lcol,
-                  c->nnc_val, c->F_raw, c->rhs, c->part_f2, c->x, c->r, c->r0, c->p, c->v, c->s, c->t, c->p2, c->v2, c->part,
+                  c->nnc_val, c->F_raw, c->rhs, c->part_f2, c->x, c->r, c->r0, c->p, c->v, c->s, c->t, c->p2, c->v2, c->ph, c->sh, c->part,
                   c->dsc, c->dd.sub_cells, c->dd.halo_cells, c->u_ckpt, c->st_ckpt, c->l2_scratch, c->pin0, c->ktrace};
   for (void* p : ptrs)
     if (p) cudaFree(p);

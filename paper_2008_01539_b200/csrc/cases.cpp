@@ -416,7 +416,7 @@ int rsim_case_solver_opts(const rsim_case* c, rsim_solver_opts* o) {
   o->max_newton = 25;
   o->max_outer = 50;
   o->lin_method = RSIM_LIN_BICGSTAB;
-  o->precond = RSIM_PREC_BJACOBI;
+  o->precond = RSIM_PREC_NEUMANN1;  // block-Jacobi scaling + 1st-order Neumann polynomial
   o->lin_maxit = 4000;
   o->lin_rtol = 1e-9;
   o->eps_p = c->eps;

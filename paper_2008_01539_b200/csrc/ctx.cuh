@@ -100,6 +100,7 @@ struct rsim_gpu_ctx {
   // Krylov
   double *x = nullptr, *r = nullptr, *r0 = nullptr, *p = nullptr, *v = nullptr, *s = nullptr, *t = nullptr;
   double *p2 = nullptr, *v2 = nullptr;  // second buffers of p, v (fused Krylov)
+  double *ph = nullptr, *sh = nullptr;  // M^-1 p, M^-1 s (Neumann-1 preconditioner)
   double* part = nullptr;  // [4][nchunks_max]
 
   DevScalars* dsc = nullptr;   // device

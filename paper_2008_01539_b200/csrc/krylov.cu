@@ -43,7 +43,8 @@ struct KArgs {
   const double* nnc_val;
   const double* rhs;
   const double* F_raw;
-  double *x, *r, *r0, *p, *v, *s, *t, *p2, *v2;
+  double *x, *r, *r0, *p, *v, *s, *t, *p2, *v2, *ph, *sh;
+  int32_t neu;
   double* part;   // [3][pstride]  level-1 partials
   double* part2;  // [3][pstride2] level-2 partials (very large systems)
   int32_t pstride, pstride2;
@@ -105,7 +106,7 @@ __device__ __forceinline__ void reduce_small(Red& R, int q, const double* src, i
 // Neighbour value of the vector being multiplied, recomputed from vectors
 // that are read-only in the current phase (same formula as the owner, so the
 // same bits):  mode 0: p_j = r_j + β (p_old_j − ω v_old_j);  mode 1: p_j = r_j;
-// mode 2: s_j = r_j − α v_j.
+// mode 2: s_j = r_j − α v_j;  mode 3: x_j read directly from `po`.
 template <int B>
 __device__ __forceinline__ void nbr_val(int mode, const double* __restrict__ r, const double* __restrict__ po,
                                         const double* __restrict__ vo, int64_t j, double beta, double omega,
@@ -113,7 +114,8 @@ __device__ __forceinline__ void nbr_val(int mode, const double* __restrict__ r, 
 #pragma unroll
   for (int e = 0; e < B; ++e) {
     const int64_t q = j * B + e;
-    if (mode == 1) out[e] = r[q];
+    if (mode == 3) out[e] = po[q];
+    else if (mode == 1) out[e] = r[q];
     else if (mode == 0) out[e] = r[q] + beta * (po[q] - omega * vo[q]);
     else out[e] = r[q] - alpha * vo[q];
   }
@@ -228,15 +230,36 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     double* vc = cur ? a.v2 : a.v;
     const double* po = cur ? a.p : a.p2;
     const double* vo = cur ? a.v : a.v2;
-    // ---- p = r + β(p − ωv) (own, and recomputed for neighbours); v = Â p; (r0, v)
+    // ---- p = r + β(p − ωv) (own, and recomputed for neighbours)
+    //      BJ: v = Â p;  Neumann-1: ph = p + (p − Â p), barrier, v = Â ph;  (r0, v)
+    if (a.neu) {
+      for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
+        const int64_t l = rd * KT + tid;
+        if (l < nr) {
+          double pown[B], y[B];
+          nbr_val<B>(it == 1 ? 1 : 0, a.r, po, vo, l, beta, omega, 0.0, pown);
+          spmv_row<B>(a, l, it == 1 ? 1 : 0, a.r, po, vo, beta, omega, 0.0, pown, y);
+#pragma unroll
+          for (int e = 0; e < B; ++e) {
+            pc[l * B + e] = pown[e];
+            a.ph[l * B + e] = pown[e] + (pown[e] - y[e]);
+          }
+        }
+      }
+      sync();
+    }
     ROUNDS_BEGIN
     if (ok) {
-      double pown[B];
-      nbr_val<B>(it == 1 ? 1 : 0, a.r, po, vo, l, beta, omega, 0.0, pown);
-#pragma unroll
-      for (int e = 0; e < B; ++e) pc[l * B + e] = pown[e];
       double y[B];
-      spmv_row<B>(a, l, it == 1 ? 1 : 0, a.r, po, vo, beta, omega, 0.0, pown, y);
+      if (a.neu) {
+        spmv_row<B>(a, l, 3, a.r, a.ph, vo, 0.0, 0.0, 0.0, &a.ph[l * B], y);
+      } else {
+        double pown[B];
+        nbr_val<B>(it == 1 ? 1 : 0, a.r, po, vo, l, beta, omega, 0.0, pown);
+#pragma unroll
+        for (int e = 0; e < B; ++e) pc[l * B + e] = pown[e];
+        spmv_row<B>(a, l, it == 1 ? 1 : 0, a.r, po, vo, beta, omega, 0.0, pown, y);
+      }
 #pragma unroll
       for (int e = 0; e < B; ++e) vc[l * B + e] = y[e];
       val[0] = rsim::blk::rowdot<B>(&a.r0[l * B], y);
@@ -246,15 +269,39 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     const double r0v = R.res[0];
     if (r0v == 0.0 || !isfinite(r0v)) { status = RSIM_ENUM; break; }
     alpha = rho_new / r0v;
-    // ---- s = r − α v (own + recomputed); t = Â s; (s,s), (t,s), (t,t)
+    // ---- s = r − α v (own + recomputed)
+    //      BJ: t = Â s;  Neumann-1: sh = s + (s − Â s), barrier, t = Â sh;  (s,s), (t,s), (t,t)
+    if (a.neu) {
+      for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
+        const int64_t l = rd * KT + tid;
+        if (l < nr) {
+          double sv[B], y[B];
+          nbr_val<B>(2, a.r, po, vc, l, 0.0, 0.0, alpha, sv);
+          spmv_row<B>(a, l, 2, a.r, po, vc, 0.0, 0.0, alpha, sv, y);
+#pragma unroll
+          for (int e = 0; e < B; ++e) {
+            a.s[l * B + e] = sv[e];
+            a.sh[l * B + e] = sv[e] + (sv[e] - y[e]);
+          }
+        }
+      }
+      sync();
+    }
     ROUNDS_BEGIN
     if (ok) {
-      double sv[B];
-      nbr_val<B>(2, a.r, po, vc, l, 0.0, 0.0, alpha, sv);
-      double y[B];
-      spmv_row<B>(a, l, 2, a.r, po, vc, 0.0, 0.0, alpha, sv, y);
+      double sv[B], y[B];
+      if (a.neu) {
 #pragma unroll
-      for (int e = 0; e < B; ++e) { a.s[l * B + e] = sv[e]; a.t[l * B + e] = y[e]; }
+        for (int e = 0; e < B; ++e) sv[e] = a.s[l * B + e];
+        spmv_row<B>(a, l, 3, a.r, a.sh, vc, 0.0, 0.0, 0.0, &a.sh[l * B], y);
+      } else {
+        nbr_val<B>(2, a.r, po, vc, l, 0.0, 0.0, alpha, sv);
+        spmv_row<B>(a, l, 2, a.r, po, vc, 0.0, 0.0, alpha, sv, y);
+#pragma unroll
+        for (int e = 0; e < B; ++e) a.s[l * B + e] = sv[e];
+      }
+#pragma unroll
+      for (int e = 0; e < B; ++e) a.t[l * B + e] = y[e];
       val[0] = rsim::blk::rowdot<B>(sv, sv);
       val[1] = rsim::blk::rowdot<B>(y, sv);
       val[2] = rsim::blk::rowdot<B>(y, y);
@@ -262,12 +309,14 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     ROUNDS_END(3)
     reduce(3);
     const double ss = R.res[0], ts = R.res[1], tt = R.res[2];
+    const double* phv = a.neu ? a.ph : pc;
+    const double* shv = a.neu ? a.sh : a.s;
     if (!fixed && sqrt(ss) <= tol) {
       for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
         const int64_t l = rd * KT + tid;
         if (l < nr)
 #pragma unroll
-          for (int e = 0; e < B; ++e) a.x[l * B + e] = a.x[l * B + e] + alpha * pc[l * B + e];
+          for (int e = 0; e < B; ++e) a.x[l * B + e] = a.x[l * B + e] + alpha * phv[l * B + e];
       }
       relres = sqrt(ss) / bnorm;
       status = RSIM_OK;
@@ -283,7 +332,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       for (int e = 0; e < B; ++e) {
         const int64_t q = l * B + e;
         const double sq = a.s[q];
-        a.x[q] = (a.x[q] + alpha * pc[q]) + omega * sq;
+        a.x[q] = (a.x[q] + alpha * phv[q]) + omega * shv[q];
         rv[e] = sq - omega * a.t[q];
         a.r[q] = rv[e];
         r0v_[e] = a.r0[q];
@@ -325,7 +374,8 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.act = c->act; a.nptr = c->nptr; a.nnc_lcol = c->nnc_lcol; a.nnc_val = c->nnc_val;
   a.rhs = c->rhs; a.F_raw = c->F_raw;
   a.x = c->x; a.r = c->r; a.r0 = c->r0; a.p = c->p; a.v = c->v; a.s = c->s; a.t = c->t;
-  a.p2 = c->p2; a.v2 = c->v2;
+  a.p2 = c->p2; a.v2 = c->v2; a.ph = c->ph; a.sh = c->sh;
+  a.neu = o->precond == RSIM_PREC_NEUMANN1;
   a.pstride = (int32_t)((c->n + 255) / 256);
   a.pstride2 = (a.pstride + 255) / 256;
   a.part = c->part;

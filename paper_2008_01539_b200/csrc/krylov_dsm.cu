@@ -38,7 +38,7 @@ constexpr int NNCMAX = 256;             // NNC entries cached in smem per CTA
 constexpr int NNC_GLOBAL = 0x40000000;  // flag in the range end: entries stay in global
 
 struct DArgs {
-  int32_t nA, nslot, maxit, fixed, LRC, nch;
+  int32_t nA, nslot, maxit, fixed, LRC, nch, neu;
   int64_t cap;
   bool has_nnc;
   double rtol;
@@ -67,7 +67,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   double* vp1 = vp0 + RC * B;
   double* vv0 = vp1 + RC * B;
   double* vv1 = vv0 + RC * B;
-  double* mval = vv1 + RC * B;                                    // [NS][RC][B*B]  (MS)
+  double* vph = vv1 + RC * B;  // M^-1 p  (Neumann-1 preconditioner only)
+  double* vsh = vph + RC * B;  // M^-1 s
+  double* mval = vsh + RC * B;                                    // [NS][RC][B*B]  (MS)
   int32_t* mcol = (int32_t*)(mval + (MS ? NS * RC * B * B : 0));   // [NS][RC]       (MS)
   int2* nrng = (int2*)(mcol + (MS ? NS * RC : 0));                // [RC] NNC ranges (has_nnc)
   double* nsv = (double*)(nrng + RC);                              // [NNCMAX][B*B] NNC blocks
@@ -78,6 +80,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   __shared__ double* pb[2][GMAX];
   __shared__ double* vb[2][GMAX];
   __shared__ double* wsb[GMAX];
+  __shared__ double* phb[GMAX];
+  __shared__ double* shb[GMAX];
   __shared__ double ws[2][3][32];  // [buf][q][warp]: canonical warp sums of this CTA
   __shared__ double res[3];
 
@@ -96,6 +100,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
     vb[0][tid] = cluster.map_shared_rank(vv0, tid);
     vb[1][tid] = cluster.map_shared_rank(vv1, tid);
     wsb[tid] = cluster.map_shared_rank(&ws[0][0][0], tid);
+    phb[tid] = cluster.map_shared_rank(vph, tid);
+    shb[tid] = cluster.map_shared_rank(vsh, tid);
   }
   const int LSH = a.LRC;  // log2(RC)
   const int RCM = RC - 1;
@@ -158,10 +164,17 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   //   mode 0: p_new_j = r_j + beta (p_old_j - omega v_old_j)   (it > 1)
   //   mode 1: p_new_j = r_j                                     (it == 1)
   //   mode 2: s_j     = r_j - alpha v_new_j
+  //   mode 3: (M^-1 p)_j, mode 4: (M^-1 s)_j   (stored by the owner, Neumann-1)
   auto gather = [&](int mode, int cur, int32_t j, double beta, double omega, double alpha, double* out) {
     const int g = j >> LSH;
     const int rr = (j & RCM) * B;
     const bool loc = g == rank;
+    if (mode >= 3) {
+      const double* X_ = (mode == 3 ? (loc ? vph : phb[g]) : (loc ? vsh : shb[g])) + rr;
+#pragma unroll
+      for (int e = 0; e < B; ++e) out[e] = X_[e];
+      return;
+    }
     const double* R_ = (loc ? vr : rb[g]) + rr;
     if (mode == 1) {
 #pragma unroll
@@ -299,19 +312,35 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
       double* vvc = cur ? vv1 : vv0;
       const double* vpo = cur ? vp0 : vp1;
       const double* vvo = cur ? vv0 : vv1;
-      // ---- p = r + β (p − ω v) (own + recomputed for neighbours); v = Â p; (r0, v)
+      // ---- p = r + β (p − ω v) (own + recomputed for neighbours)
+      //      BJ:  v = Â p;   Neumann-1: ph = p + (p − Â p), barrier, v = Â ph;  (r0, v)
+      double phr[B];
       {
         double val[3] = {0.0, 0.0, 0.0};
+        double pown[B], y[B];
         if (valid) {
-          double pown[B];
 #pragma unroll
           for (int e = 0; e < B; ++e) {
             const int q = lam * B + e;
             pown[e] = (it == 1) ? vr[q] : vr[q] + beta * (vpo[q] - omega * vvo[q]);
             vpc[q] = pown[e];
           }
-          double y[B];
           spmv(it == 1 ? 1 : 0, cur, pown, beta, omega, 0.0, y);
+        }
+        if (a.neu) {
+          if (valid)
+#pragma unroll
+            for (int e = 0; e < B; ++e) {
+              phr[e] = pown[e] + (pown[e] - y[e]);
+              vph[lam * B + e] = phr[e];
+            }
+          csync();
+          if (valid) spmv(3, cur, phr, 0.0, 0.0, 0.0, y);
+        } else {
+#pragma unroll
+          for (int e = 0; e < B; ++e) phr[e] = pown[e];
+        }
+        if (valid) {
 #pragma unroll
           for (int e = 0; e < B; ++e) vvc[lam * B + e] = y[e];
           val[0] = rsim::blk::rowdot<B>(r0r, y);
@@ -323,23 +352,35 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
       const double r0v = res[0];
       if (r0v == 0.0 || !isfinite(r0v)) { status = RSIM_ENUM; break; }
       alpha = rho_new / r0v;
-      // ---- s = r − α v (own + recomputed for neighbours); t = Â s; (s,s), (t,s), (t,t)
+      // ---- s = r − α v (own + recomputed for neighbours)
+      //      BJ: t = Â s;  Neumann-1: sh = s + (s − Â s), barrier, t = Â sh;  (s,s), (t,s), (t,t)
+      double shr[B];
       {
         double val[3] = {0.0, 0.0, 0.0};
+        double y[B];
         if (valid) {
-          double sv[B];
 #pragma unroll
-          for (int e = 0; e < B; ++e) {
-            const int q = lam * B + e;
-            sv[e] = vr[q] - alpha * vvc[q];
-            sr[e] = sv[e];
-          }
-          double y[B];
-          spmv(2, cur, sv, 0.0, 0.0, alpha, y);
+          for (int e = 0; e < B; ++e) sr[e] = vr[lam * B + e] - alpha * vvc[lam * B + e];
+          spmv(2, cur, sr, 0.0, 0.0, alpha, y);
+        }
+        if (a.neu) {
+          if (valid)
+#pragma unroll
+            for (int e = 0; e < B; ++e) {
+              shr[e] = sr[e] + (sr[e] - y[e]);
+              vsh[lam * B + e] = shr[e];
+            }
+          csync();
+          if (valid) spmv(4, cur, shr, 0.0, 0.0, 0.0, y);
+        } else {
+#pragma unroll
+          for (int e = 0; e < B; ++e) shr[e] = sr[e];
+        }
+        if (valid) {
 #pragma unroll
           for (int e = 0; e < B; ++e) tr_[e] = y[e];
-          val[0] = rsim::blk::rowdot<B>(sv, sv);
-          val[1] = rsim::blk::rowdot<B>(y, sv);
+          val[0] = rsim::blk::rowdot<B>(sr, sr);
+          val[1] = rsim::blk::rowdot<B>(y, sr);
           val[2] = rsim::blk::rowdot<B>(y, y);
         }
         KT_MARK(2);
@@ -350,7 +391,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
       if (!fixed && sqrt(ssn) <= tol) {
         if (valid)
 #pragma unroll
-          for (int e = 0; e < B; ++e) xr[e] = xr[e] + alpha * vpc[lam * B + e];
+          for (int e = 0; e < B; ++e) xr[e] = xr[e] + alpha * phr[e];
         relres = sqrt(ssn) / bnorm;
         status = RSIM_OK;
         break;
@@ -364,11 +405,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
           double rv[B];
 #pragma unroll
           for (int e = 0; e < B; ++e) {
-            const int q = lam * B + e;
-            const double sq = sr[e];
-            xr[e] = (xr[e] + alpha * vpc[q]) + omega * sq;
-            rv[e] = sq - omega * tr_[e];
-            vr[q] = rv[e];
+            xr[e] = (xr[e] + alpha * phr[e]) + omega * shr[e];
+            rv[e] = sr[e] - omega * tr_[e];
+            vr[lam * B + e] = rv[e];
           }
           val[0] = rsim::blk::rowdot<B>(rv, rv);
           val[1] = rsim::blk::rowdot<B>(r0r, rv);
@@ -403,7 +442,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
 
 size_t smem_bytes(int B, int NS, bool MS, int LRC) {
   const size_t R = (size_t)1 << LRC;
-  size_t b = 5 * R * B * sizeof(double) + R * sizeof(int2) + NNCMAX * (B * B * sizeof(double) + sizeof(int32_t));
+  size_t b = 7 * R * B * sizeof(double) + R * sizeof(int2) + NNCMAX * (B * B * sizeof(double) + sizeof(int32_t));
   if (MS) b += NS * R * B * B * sizeof(double) + NS * R * sizeof(int32_t);
   return b;
 }
@@ -476,6 +515,7 @@ int launch_krylov_dsm(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.nslot = c->nslot;
   a.maxit = o->lin_maxit;
   a.fixed = o->fixed_lin_iters;
+  a.neu = o->precond == RSIM_PREC_NEUMANN1;
   a.nch = nch;
   a.cap = c->n;
   a.has_nnc = c->has_nnc;

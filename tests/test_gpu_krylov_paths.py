@@ -22,20 +22,20 @@ def _state(case, seed):
     return s
 
 
-def _check(case, act, its=None, seed=1):
+def _check(case, act, its=None, seed=1, precond=0):
     if act is not None:
         act = np.union1d(act, np.flatnonzero(case.pinned())).astype(np.int32)
     s = _state(case, seed)
     dt = 86400.0
     orc = Oracle(case)
     orc.set_state(s, dt)
-    Fo, ro, rpo, co, vo = orc.assemble(act)
+    Fo, ro, rpo, co, vo = orc.assemble(np.arange(case.n, dtype=np.int32) if act is None else act)
     sim = pkg.GpuSimulator(case)
     sim.set_state(s, dt)
     st = sim.set_active(act)
     assert st.n_active == (case.n if act is None else len(act))
     sim.assemble()
-    opts = case.solver_opts()
+    opts = case.solver_opts(precond=precond)
     if its:
         opts.fixed_lin_iters = its
         opts.lin_maxit = its
@@ -52,37 +52,41 @@ def _check(case, act, its=None, seed=1):
     sim.close()
 
 
+@pytest.mark.parametrize("precond", [pkg.PREC_BJACOBI, pkg.PREC_NEUMANN1])
 @pytest.mark.parametrize("nA", [1, 17, 63, 64, 65, 200, 257, 1000, 2049, 4095, 8191, 12000, 16384])
-def test_cluster_path_exact_sizes(nA):
+def test_cluster_path_exact_sizes(nA, precond):
     # config 5 has no pinned (fracture/well) cells, so |V_A| is exactly nA
     case = pkg.Case(5, nx=160, ny=160, nz=1)
     rng = np.random.default_rng(nA)
     act = np.sort(rng.choice(case.n, nA, replace=False)).astype(np.int32)
-    _check(case, act)
+    _check(case, act, precond=precond)
 
 
+@pytest.mark.parametrize("precond", [pkg.PREC_BJACOBI, pkg.PREC_NEUMANN1])
 @pytest.mark.parametrize("nA", [100, 1500, 5000, 15000])
-def test_cluster_path_b2_with_nnc(nA):
+def test_cluster_path_b2_with_nnc(nA, precond):
     case = pkg.Case(2, nx=160, ny=160, n_dfn=30)
     assert case.n_nnc > 0
     rng = np.random.default_rng(nA)
     act = np.union1d(rng.choice(case.n, nA, replace=False), np.flatnonzero(case.pinned())).astype(np.int32)
-    _check(case, act)
+    _check(case, act, precond=precond)
 
 
+@pytest.mark.parametrize("precond", [pkg.PREC_BJACOBI, pkg.PREC_NEUMANN1])
 @pytest.mark.parametrize("cfg,nA", [(dict(config=1), 300), (dict(config=3, nx=48, ny=48, nz=8), 5000),
                                     (dict(config=4, nx=40, ny=40, nz=4, n_dfn=6), 3000)])
-def test_cluster_path_b1_b3_3d(cfg, nA):
+def test_cluster_path_b1_b3_3d(cfg, nA, precond):
     case = pkg.Case(**cfg)
     rng = np.random.default_rng(nA)
     act = np.sort(rng.choice(case.n, min(nA, case.n), replace=False)).astype(np.int32)
-    _check(case, act)
+    _check(case, act, precond=precond)
 
 
+@pytest.mark.parametrize("precond", [pkg.PREC_BJACOBI, pkg.PREC_NEUMANN1])
 @pytest.mark.parametrize("cfg", [dict(config=2, nx=200, ny=200, n_dfn=40), dict(config=4, nx=48, ny=48, nz=8, n_dfn=8)])
-def test_grid_path_full_set(cfg):
+def test_grid_path_full_set(cfg, precond):
     case = pkg.Case(**cfg)
-    _check(case, None)
+    _check(case, None, precond=precond)
 
 
 def test_grid_path_distributed_level2_reduction():

@@ -150,12 +150,13 @@ def test_newton_solvers_bit_exact(name):
     sim.close()
 
 
-@pytest.mark.parametrize("name,solver", [("c1", 0), ("c1", 1), ("c1", 2), ("c2s", 1), ("c4s", 1)])
-def test_run_case_bit_exact(name, solver):
+@pytest.mark.parametrize("name,solver,precond", [("c1", 0, 0), ("c1", 1, 0), ("c1", 2, 0), ("c2s", 1, 0), ("c4s", 1, 0),
+                                                 ("c1", 1, 2), ("c2s", 1, 2), ("c2s", 2, 2), ("c4s", 1, 2)])
+def test_run_case_bit_exact(name, solver, precond):
     case = pkg.Case(**CASES[name])
     s0 = case.init_state()
     dts = case.schedule()
-    opts = case.solver_opts()
+    opts = case.solver_opts(precond=precond)
     if solver == 2:
         opts.m = 4
     orc = Oracle(case)
