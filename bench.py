@@ -242,7 +242,7 @@ def c5_sweep(pkg, fractions, reps, hbm):
     sim = pkg.GpuSimulator(case)
     L, ctx = sim.L, sim._ctx
     n, b, s = case.n, 1, 6
-    opts = case.solver_opts(fixed_lin_iters=50, lin_maxit=50)
+    opts = case.solver_opts(fixed_lin_iters=50, lin_maxit=50, precond=pkg.PREC_BJACOBI)  # Jacobi
     out = []
     s0 = case.init_state()
     sim.set_state(s0, 86400.0)
@@ -341,14 +341,16 @@ def main():
     for _ in range(args.warmup):
         L.rsim_gpu_checkpoint(ctx, 1)
         run_dev()
-    # ---- device-resident timed region
-    L.rsim_gpu_timers(ctx, 1, None, None)
+    # ---- device-resident timed region (phase timers OFF: no extra events)
+    L.rsim_gpu_timers(ctx, 0, None, None)
     cnt = np.zeros(5, np.int64)
     L.rsim_gpu_counters(ctx, A.ptr(cnt, C.c_int64), 1)
+    launches0 = C.c_int32()
     barrier(dist)
     L.rsim_gpu_stats_get(ctx, C.byref(pkg.GpuStats()))
     tot_ms, tot_na = 0.0, 0
     with Clocks(lr) as clk:
+        L.rsim_gpu_timers(ctx, -1, None, C.byref(launches0))
         for _ in range(args.steps):
             L.rsim_gpu_checkpoint(ctx, 1)
             L.rsim_gpu_flush_l2(ctx)
@@ -358,15 +360,23 @@ def main():
             v = C.c_double()
             L.rsim_gpu_elapsed(ctx, 0, 1, C.byref(v))
             tot_ms += v.value
+        launches1 = C.c_int32()
+        L.rsim_gpu_timers(ctx, -1, None, C.byref(launches1))
     barrier(dist)
-    phase_ms = np.zeros(4)
-    launches = C.c_int32()
-    L.rsim_gpu_timers(ctx, 0, A.ptr(phase_ms, C.c_double), C.byref(launches))
     L.rsim_gpu_counters(ctx, A.ptr(cnt, C.c_int64), 1)
     n_iters, n_lin, iters_per_run = it.value, lin.value, it.value
     t_max = dist_max(dist, tot_ms)
     na_all = dist_sum(dist, float(tot_na))
     value = na_all / (t_max / 1e3)
+    n_launch = int(launches1.value - launches0.value)
+    # ---- phase breakdown (separate pass with per-phase CUDA events; not part of `value`)
+    L.rsim_gpu_timers(ctx, 1, None, None)
+    L.rsim_gpu_checkpoint(ctx, 1)
+    L.rsim_gpu_flush_l2(ctx)
+    run_dev()
+    phase_ms = np.zeros(4)
+    L.rsim_gpu_timers(ctx, 0, A.ptr(phase_ms, C.c_double), None)
+    phase_ms *= args.steps  # per-run breakdown scaled to the timed steps
 
     # ---- e2e through the public C-ABI entry point with pinned host buffers
     import torch
@@ -424,7 +434,7 @@ def main():
                    "parallelism": f"replicas x{ws}"},
         "e2e": {"value": e2e_v, "unit": "active-cell iters/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "api": "rsim_run_case (C-ABI), pinned host buffers"},
-        "gpu_launches": int(launches.value),
+        "gpu_launches": n_launch,
         "roofline": roof,
         "clocks": clk.summary(),
     }

@@ -284,9 +284,9 @@ static double dotc(int64_t nrows, const double* a, const double* b) {
 // Element formulas and reduction order are the contract the GPU kernel
 // (csrc/krylov.cu) follows.
 template <int B>
-static int bicgstab(const Model& M, const rsim_solver_opts& o, double* x, int32_t* iters, double* relres) {
+static int bicgstab_once(const Model& M, const rsim_solver_opts& o, bool neu, double* x, int32_t* iters,
+                         double* relres) {
   const int64_t nr = M.nA, N = nr * B;
-  const bool neu = o.precond == RSIM_PREC_NEUMANN1;
   std::vector<double> r(M.rhs), r0(M.rhs), p(N, 0.0), v(N, 0.0), s(N), t(N), ph, sh, y;
   if (neu) { ph.assign(N, 0.0); sh.assign(N, 0.0); y.assign(N, 0.0); }
   // M^{-1} z = z + (z - Â z): first-order Neumann polynomial on the unit-diagonal system
@@ -349,6 +349,22 @@ static int bicgstab(const Model& M, const rsim_solver_opts& o, double* x, int32_
     if (omega == 0.0 || rho_new == 0.0 || !std::isfinite(rho_new)) return RSIM_ENUM;
   }
   return fixed ? RSIM_OK : RSIM_ENOCONV;
+}
+
+// Neumann-1 preconditioned solve with a deterministic fallback: if it breaks
+// down or hits the cap, the solve restarts from x0 = 0 with block-Jacobi only
+// (the Neumann polynomial is not guaranteed positive on non-M-matrix blocks,
+// e.g. black-oil).  Iterations of both attempts are reported.
+template <int B>
+static int bicgstab(const Model& M, const rsim_solver_opts& o, double* x, int32_t* iters, double* relres) {
+  const bool neu = o.precond == RSIM_PREC_NEUMANN1;
+  int st = bicgstab_once<B>(M, o, neu, x, iters, relres);
+  if (neu && (st == RSIM_ENUM || st == RSIM_ENOCONV)) {
+    int32_t it2 = 0;
+    st = bicgstab_once<B>(M, o, false, x, &it2, relres);
+    *iters += it2;
+  }
+  return st;
 }
 
 static int linsolve_any(const Model& M, const rsim_solver_opts& o, double* x, int32_t* it, double* rr) {

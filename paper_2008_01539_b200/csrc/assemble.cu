@@ -95,6 +95,7 @@ __device__ __forceinline__ void store_scaled(double* dst, const double (*Di)[B],
 // as flux_conn() in the oracle, so rows are bit-identical.
 constexpr int LPR = 8;
 constexpr int RPB = 256 / LPR;
+constexpr int64_t kRowKernelMin = 148 * 2048;  // rows: switch to one thread per row
 
 template <int B>
 __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
@@ -222,6 +223,115 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
   if ((threadIdx.x & 31) == 0 && wm > 0.0) atomic_max_bits(&a.dsc->finf, wm);
 }
 
+// One thread per active row (large active sets: memory-bound, the 8-lane
+// variant's redundant property evaluations cost more than they hide).
+// b = 1 keeps the raw off-diagonal blocks in registers; b > 1 recomputes them
+// in a second pass (same physics.h calls => same bits).
+template <int B>
+__global__ void __launch_bounds__(256) k_assemble_row(const AsmArgs a) {
+  constexpr bool KEEP = (B == 1);
+  double finf = 0.0;
+  const int64_t l = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (l < a.nA) {
+    const int64_t i = a.act[l];
+    const int64_t nxy = (int64_t)a.nx * a.ny;
+    const int64_t ix = i % a.nx, iy = (i / a.nx) % a.ny, iz = i / nxy;
+    double ui[B];
+    load_u<B>(a, i, ui);
+    rsim::phys::Props<B> Pi;
+    rsim::phys::props(a.fl, ui, B == 3 ? a.st[i] : (uint8_t)0, Pi);
+    double R[B], D[B][B], Mo[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) Mo[c] = __ldg(&a.mold[i * B + c]);
+    rsim::phys::accum_row<B>(a.fl, __ldg(&a.pv[i]), ui[0], Pi, Mo, a.dt, R, D);
+    double Okeep[6][B][B];
+    int32_t lcol[6];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      lcol[s] = -1;
+      if (s >= a.nslot) continue;
+      int64_t j;
+      double T;
+      if (cart_nbr(a, i, ix, iy, iz, s, j, T)) {
+        double O[B][B];
+        conn<B>(a, ui, Pi, j, T, R, D, O);
+        lcol[s] = __ldg(&a.g2l[j]);
+        if (KEEP)
+#pragma unroll
+          for (int r = 0; r < B; ++r)
+#pragma unroll
+            for (int c = 0; c < B; ++c) Okeep[s][r][c] = O[r][c];
+      }
+      a.ell_col[s * a.cap + l] = lcol[s];
+    }
+    int32_t q0 = 0, q1 = 0;
+    if (a.has_nnc) {
+      q0 = __ldg(&a.nptr[i]);
+      q1 = __ldg(&a.nptr[i + 1]);
+      for (int32_t q = q0; q < q1; ++q) {
+        const int64_t j = __ldg(&a.nnbr[q]);
+        double O[B][B];
+        conn<B>(a, ui, Pi, j, __ldg(&a.nt[q]), R, D, O);
+        a.nnc_lcol[q] = __ldg(&a.g2l[j]);
+      }
+    }
+    rsim::phys::well_row<B>(__ldg(&a.wi[i]), ui[0], a.bhp, Pi, R, D);
+    double Di[B][B];
+    if (!rsim::blk::inv(D, Di)) {
+      atomicMin(&a.dsc->bad_cell, (int32_t)i);
+      a.dsc->status = RSIM_ENUM;
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+#pragma unroll
+        for (int c = 0; c < B; ++c) Di[r][c] = 0.0;
+    }
+    double y[B];
+    rsim::blk::gemv<B>(Di, R, y);
+#pragma unroll
+    for (int e = 0; e < B; ++e) {
+      a.F_raw[l * B + e] = R[e];
+      a.rhs[l * B + e] = -y[e];
+      finf = fmax(finf, fabs(R[e]));
+    }
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      if (s >= a.nslot || lcol[s] < 0) continue;
+      double* dst = &a.ell_val[((int64_t)s * a.cap + l) * B * B];
+      if (KEEP) {
+        store_scaled<B>(dst, Di, Okeep[s]);
+      } else {
+        int64_t j;
+        double T;
+        cart_nbr(a, i, ix, iy, iz, s, j, T);
+        double O[B][B], Rd[B], Dd[B][B];
+#pragma unroll
+        for (int e = 0; e < B; ++e) {
+          Rd[e] = 0.0;
+#pragma unroll
+          for (int v = 0; v < B; ++v) Dd[e][v] = 0.0;
+        }
+        conn<B>(a, ui, Pi, j, T, Rd, Dd, O);
+        store_scaled<B>(dst, Di, O);
+      }
+    }
+    for (int32_t q = q0; q < q1; ++q) {
+      const int64_t j = __ldg(&a.nnbr[q]);
+      if (__ldg(&a.g2l[j]) < 0) continue;
+      double O[B][B], Rd[B], Dd[B][B];
+#pragma unroll
+      for (int e = 0; e < B; ++e) {
+        Rd[e] = 0.0;
+#pragma unroll
+        for (int v = 0; v < B; ++v) Dd[e][v] = 0.0;
+      }
+      conn<B>(a, ui, Pi, j, __ldg(&a.nt[q]), Rd, Dd, O);
+      store_scaled<B>(&a.nnc_val[(int64_t)q * B * B], Di, O);
+    }
+  }
+  const double wm = warp_max(finf);
+  if ((threadIdx.x & 31) == 0 && wm > 0.0) atomic_max_bits(&a.dsc->finf, wm);
+}
+
 // Old-time accumulation M^n = pv φ(p) A(u) for every cell (set_state / Δt change).
 template <int B>
 __global__ void k_mold(rsim_fluid_params fl, int64_t n, const double* __restrict__ u, const uint8_t* __restrict__ st,
@@ -261,11 +371,21 @@ int launch_assemble(rsim_gpu_ctx* c) {
   a.nnc_lcol = c->nnc_lcol; a.nnc_val = c->nnc_val;
   a.F_raw = c->F_raw; a.rhs = c->rhs; a.part_f2 = c->part_f2;
   a.dsc = c->dsc;
-  const int64_t nblocks = (c->nA + RPB - 1) / RPB;
-  switch (c->b) {
-    case 1: k_assemble<1><<<nblocks, 256, 0, c->stream>>>(a); break;
-    case 2: k_assemble<2><<<nblocks, 256, 0, c->stream>>>(a); break;
-    default: k_assemble<3><<<nblocks, 256, 0, c->stream>>>(a); break;
+  // small active sets: 8 lanes per row (latency); large: one thread per row (bandwidth)
+  if (c->nA < kRowKernelMin) {
+    const int64_t nblocks = (c->nA + RPB - 1) / RPB;
+    switch (c->b) {
+      case 1: k_assemble<1><<<nblocks, 256, 0, c->stream>>>(a); break;
+      case 2: k_assemble<2><<<nblocks, 256, 0, c->stream>>>(a); break;
+      default: k_assemble<3><<<nblocks, 256, 0, c->stream>>>(a); break;
+    }
+  } else {
+    const int64_t nblocks = (c->nA + 255) / 256;
+    switch (c->b) {
+      case 1: k_assemble_row<1><<<nblocks, 256, 0, c->stream>>>(a); break;
+      case 2: k_assemble_row<2><<<nblocks, 256, 0, c->stream>>>(a); break;
+      default: k_assemble_row<3><<<nblocks, 256, 0, c->stream>>>(a); break;
+    }
   }
   c->launches++;
   RSIM_CUDA(cudaGetLastError());

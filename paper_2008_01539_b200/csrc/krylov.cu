@@ -29,6 +29,7 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int KT = 1024;  // threads per CTA = 4 chunks per round
+constexpr int64_t kFuseMaxRows = 1 << 20;  // recompute-fusion only while latency-bound
 
 struct KArgs {
   int32_t nA, nslot, maxit, fixed;
@@ -44,7 +45,7 @@ struct KArgs {
   const double* rhs;
   const double* F_raw;
   double *x, *r, *r0, *p, *v, *s, *t, *p2, *v2, *ph, *sh;
-  int32_t neu;
+  int32_t neu, fuse;
   double* part;   // [3][pstride]  level-1 partials
   double* part2;  // [3][pstride2] level-2 partials (very large systems)
   int32_t pstride, pstride2;
@@ -224,41 +225,84 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   int it = 0;
   double relres = 0.0;
   int cur = 0;  // which (p, v) buffer pair holds the current iterate
+  // fuse: neighbours' p and s are recomputed at the gather site (fewer grid
+  // barriers, latency regime); !fuse: owners store p and s, then a barrier,
+  // then plain gathers (less memory traffic, bandwidth regime).
+  const bool fuse = a.fuse != 0;
+  int it_total = 0;
+  // attempt 0: as configured; attempt 1 (only after a Neumann-1 breakdown or
+  // cap): block-Jacobi only, restarted from x0 = 0 (same rule as the oracle)
+  for (int attempt = 0; attempt < (a.neu ? 2 : 1); ++attempt) {
+  const bool neu = a.neu && attempt == 0;
+  if (attempt) {
+    for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
+      const int64_t l = rd * KT + tid;
+      if (l < nr)
+#pragma unroll
+        for (int e = 0; e < B; ++e) {
+          a.r[l * B + e] = a.rhs[l * B + e];
+          a.x[l * B + e] = 0.0;
+        }
+    }
+    rho = 1.0; alpha = 1.0; omega = 1.0; rho_new = bb;
+    cur = 0;
+    status = RSIM_ENOCONV;
+    sync();
+  }
   for (it = 1; it <= maxit; ++it) {
     const double beta = (it == 1) ? 0.0 : (rho_new / rho) * (alpha / omega);
     double* pc = cur ? a.p2 : a.p;
     double* vc = cur ? a.v2 : a.v;
     const double* po = cur ? a.p : a.p2;
     const double* vo = cur ? a.v : a.v2;
-    // ---- p = r + β(p − ωv) (own, and recomputed for neighbours)
-    //      BJ: v = Â p;  Neumann-1: ph = p + (p − Â p), barrier, v = Â ph;  (r0, v)
-    if (a.neu) {
+    const int pmode = it == 1 ? 1 : 0;
+    if (!fuse) {  // p = r + β (p − ω v), stored, then visible to all
       for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
         const int64_t l = rd * KT + tid;
         if (l < nr) {
-          double pown[B], y[B];
-          nbr_val<B>(it == 1 ? 1 : 0, a.r, po, vo, l, beta, omega, 0.0, pown);
-          spmv_row<B>(a, l, it == 1 ? 1 : 0, a.r, po, vo, beta, omega, 0.0, pown, y);
+          double pown[B];
+          nbr_val<B>(pmode, a.r, po, vo, l, beta, omega, 0.0, pown);
 #pragma unroll
-          for (int e = 0; e < B; ++e) {
-            pc[l * B + e] = pown[e];
-            a.ph[l * B + e] = pown[e] + (pown[e] - y[e]);
-          }
+          for (int e = 0; e < B; ++e) pc[l * B + e] = pown[e];
         }
       }
       sync();
     }
+    if (neu) {  // ph = p + (p − Â p), stored, barrier
+      for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
+        const int64_t l = rd * KT + tid;
+        if (l < nr) {
+          double pown[B], y[B];
+          if (fuse) {
+            nbr_val<B>(pmode, a.r, po, vo, l, beta, omega, 0.0, pown);
+            spmv_row<B>(a, l, pmode, a.r, po, vo, beta, omega, 0.0, pown, y);
+#pragma unroll
+            for (int e = 0; e < B; ++e) pc[l * B + e] = pown[e];
+          } else {
+#pragma unroll
+            for (int e = 0; e < B; ++e) pown[e] = pc[l * B + e];
+            spmv_row<B>(a, l, 3, a.r, pc, vo, 0.0, 0.0, 0.0, pown, y);
+          }
+#pragma unroll
+          for (int e = 0; e < B; ++e) a.ph[l * B + e] = pown[e] + (pown[e] - y[e]);
+        }
+      }
+      sync();
+    }
+    // ---- v = Â p (BJ) or v = Â ph (Neumann-1); (r0, v)
     ROUNDS_BEGIN
     if (ok) {
       double y[B];
-      if (a.neu) {
+      if (neu) {
         spmv_row<B>(a, l, 3, a.r, a.ph, vo, 0.0, 0.0, 0.0, &a.ph[l * B], y);
-      } else {
+      } else if (fuse) {
         double pown[B];
-        nbr_val<B>(it == 1 ? 1 : 0, a.r, po, vo, l, beta, omega, 0.0, pown);
+        nbr_val<B>(pmode, a.r, po, vo, l, beta, omega, 0.0, pown);
 #pragma unroll
         for (int e = 0; e < B; ++e) pc[l * B + e] = pown[e];
-        spmv_row<B>(a, l, it == 1 ? 1 : 0, a.r, po, vo, beta, omega, 0.0, pown, y);
+        spmv_row<B>(a, l, pmode, a.r, po, vo, beta, omega, 0.0, pown, y);
+      } else {
+        spmv_row<B>(a, l, 3, a.r, pc, vo, 0.0, 0.0, 0.0, &pc[l * B], y);
       }
 #pragma unroll
       for (int e = 0; e < B; ++e) vc[l * B + e] = y[e];
@@ -269,36 +313,53 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     const double r0v = R.res[0];
     if (r0v == 0.0 || !isfinite(r0v)) { status = RSIM_ENUM; break; }
     alpha = rho_new / r0v;
-    // ---- s = r − α v (own + recomputed)
-    //      BJ: t = Â s;  Neumann-1: sh = s + (s − Â s), barrier, t = Â sh;  (s,s), (t,s), (t,t)
-    if (a.neu) {
+    if (!fuse) {  // s = r − α v, stored, barrier
+      for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
+        const int64_t l = rd * KT + tid;
+        if (l < nr)
+#pragma unroll
+          for (int e = 0; e < B; ++e) a.s[l * B + e] = a.r[l * B + e] - alpha * vc[l * B + e];
+      }
+      sync();
+    }
+    if (neu) {  // sh = s + (s − Â s), stored, barrier
       for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
         const int64_t l = rd * KT + tid;
         if (l < nr) {
           double sv[B], y[B];
-          nbr_val<B>(2, a.r, po, vc, l, 0.0, 0.0, alpha, sv);
-          spmv_row<B>(a, l, 2, a.r, po, vc, 0.0, 0.0, alpha, sv, y);
+          if (fuse) {
+            nbr_val<B>(2, a.r, po, vc, l, 0.0, 0.0, alpha, sv);
+            spmv_row<B>(a, l, 2, a.r, po, vc, 0.0, 0.0, alpha, sv, y);
 #pragma unroll
-          for (int e = 0; e < B; ++e) {
-            a.s[l * B + e] = sv[e];
-            a.sh[l * B + e] = sv[e] + (sv[e] - y[e]);
+            for (int e = 0; e < B; ++e) a.s[l * B + e] = sv[e];
+          } else {
+#pragma unroll
+            for (int e = 0; e < B; ++e) sv[e] = a.s[l * B + e];
+            spmv_row<B>(a, l, 3, a.r, a.s, vc, 0.0, 0.0, 0.0, sv, y);
           }
+#pragma unroll
+          for (int e = 0; e < B; ++e) a.sh[l * B + e] = sv[e] + (sv[e] - y[e]);
         }
       }
       sync();
     }
+    // ---- t = Â s (BJ) or t = Â sh (Neumann-1); (s,s), (t,s), (t,t)
     ROUNDS_BEGIN
     if (ok) {
       double sv[B], y[B];
-      if (a.neu) {
+      if (neu) {
 #pragma unroll
         for (int e = 0; e < B; ++e) sv[e] = a.s[l * B + e];
         spmv_row<B>(a, l, 3, a.r, a.sh, vc, 0.0, 0.0, 0.0, &a.sh[l * B], y);
-      } else {
+      } else if (fuse) {
         nbr_val<B>(2, a.r, po, vc, l, 0.0, 0.0, alpha, sv);
         spmv_row<B>(a, l, 2, a.r, po, vc, 0.0, 0.0, alpha, sv, y);
 #pragma unroll
         for (int e = 0; e < B; ++e) a.s[l * B + e] = sv[e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < B; ++e) sv[e] = a.s[l * B + e];
+        spmv_row<B>(a, l, 3, a.r, a.s, vc, 0.0, 0.0, 0.0, sv, y);
       }
 #pragma unroll
       for (int e = 0; e < B; ++e) a.t[l * B + e] = y[e];
@@ -309,8 +370,8 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     ROUNDS_END(3)
     reduce(3);
     const double ss = R.res[0], ts = R.res[1], tt = R.res[2];
-    const double* phv = a.neu ? a.ph : pc;
-    const double* shv = a.neu ? a.sh : a.s;
+    const double* phv = neu ? a.ph : pc;
+    const double* shv = neu ? a.sh : a.s;
     if (!fixed && sqrt(ss) <= tol) {
       for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
         const int64_t l = rd * KT + tid;
@@ -351,6 +412,10 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     cur ^= 1;
   }
   if (it > maxit) { it = maxit; status = fixed ? RSIM_OK : RSIM_ENOCONV; }
+  it_total += it;
+  if (!(neu && (status == RSIM_ENUM || status == RSIM_ENOCONV))) break;
+  }
+  it = it_total;
   if (blockIdx.x == 0 && tid == 0) {
     a.dsc->lin_iters = it;
     a.dsc->lin_relres = relres;
@@ -376,6 +441,7 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.x = c->x; a.r = c->r; a.r0 = c->r0; a.p = c->p; a.v = c->v; a.s = c->s; a.t = c->t;
   a.p2 = c->p2; a.v2 = c->v2; a.ph = c->ph; a.sh = c->sh;
   a.neu = o->precond == RSIM_PREC_NEUMANN1;
+  a.fuse = c->nA <= kFuseMaxRows ? 1 : 0;
   a.pstride = (int32_t)((c->n + 255) / 256);
   a.pstride2 = (a.pstride + 255) / 256;
   a.part = c->part;

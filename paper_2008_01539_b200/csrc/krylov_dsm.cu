@@ -305,6 +305,23 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
     const bool tr = a.trace && rank == 0 && tid == 0;
     long long t0 = clock64();
 #define KT_MARK(k) do { if (tr) { long long t1 = clock64(); tc[k] += (unsigned long long)(t1 - t0); t0 = t1; } } while (0)
+    int it_total = 0;
+    // attempt 0: as configured; attempt 1 (only after a Neumann-1 breakdown or
+    // cap): block-Jacobi only, restarted from x0 = 0 (same rule as the oracle)
+    for (int attempt = 0; attempt < (a.neu ? 2 : 1); ++attempt) {
+    const bool neu = a.neu && attempt == 0;
+    if (attempt) {
+      if (valid)
+#pragma unroll
+        for (int e = 0; e < B; ++e) {
+          vr[lam * B + e] = a.rhs[l * B + e];
+          xr[e] = 0.0;
+        }
+      rho = 1.0; alpha = 1.0; omega = 1.0; rho_new = bb;
+      cur = 0;
+      status = RSIM_ENOCONV;
+      csync();
+    }
     for (it = 1; it <= maxit; ++it) {
       KT_MARK(7);
       const double beta = (it == 1) ? 0.0 : (rho_new / rho) * (alpha / omega);
@@ -327,7 +344,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
           }
           spmv(it == 1 ? 1 : 0, cur, pown, beta, omega, 0.0, y);
         }
-        if (a.neu) {
+        if (neu) {
           if (valid)
 #pragma unroll
             for (int e = 0; e < B; ++e) {
@@ -363,7 +380,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
           for (int e = 0; e < B; ++e) sr[e] = vr[lam * B + e] - alpha * vvc[lam * B + e];
           spmv(2, cur, sr, 0.0, 0.0, alpha, y);
         }
-        if (a.neu) {
+        if (neu) {
           if (valid)
 #pragma unroll
             for (int e = 0; e < B; ++e) {
@@ -425,6 +442,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
       cur ^= 1;
     }
     if (it > maxit) { it = maxit; status = fixed ? RSIM_OK : RSIM_ENOCONV; }
+    it_total += it;
+    if (!(neu && (status == RSIM_ENUM || status == RSIM_ENOCONV))) break;
+    }
+    it = it_total;
     if (tr)
       for (int k = 0; k < 8; ++k) atomicAdd(&a.trace[k], tc[k]);
 #undef KT_MARK
@@ -463,18 +484,27 @@ int launch_t(rsim_gpu_ctx* c, const DArgs& a, int G, int TPB, size_t smem, bool*
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  // the dynamic-smem attribute is a per-kernel maximum: only ever raise it
+  static size_t attr_max = 0;
+  auto ensure_attr = [&](size_t need) -> cudaError_t {
+    if (need <= attr_max) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(k_krylov_dsm<B, NS, MS, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)need);
+    if (e == cudaSuccess) attr_max = need;
+    return e;
+  };
   auto itf = fits.find(key);
   if (itf == fits.end()) {
-    cudaFuncSetAttribute(k_krylov_dsm<B, NS, MS, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    bool f = ensure_attr(smem) == cudaSuccess;
     cudaFuncSetAttribute(k_krylov_dsm<B, NS, MS, MAXT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     int ncl = 0;
-    bool f = cudaOccupancyMaxActiveClusters(&ncl, k_krylov_dsm<B, NS, MS, MAXT>, &cfg) == cudaSuccess && ncl >= 1;
+    f = f && cudaOccupancyMaxActiveClusters(&ncl, k_krylov_dsm<B, NS, MS, MAXT>, &cfg) == cudaSuccess && ncl >= 1;
     cudaGetLastError();
     itf = fits.emplace(key, f).first;
   }
   *ok = itf->second;
   if (!*ok) return RSIM_OK;
-  RSIM_CUDA(cudaFuncSetAttribute(k_krylov_dsm<B, NS, MS, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  RSIM_CUDA(ensure_attr(smem));
   RSIM_CUDA(cudaLaunchKernelEx(&cfg, k_krylov_dsm<B, NS, MS, MAXT>, a));
   return RSIM_OK;
 }

@@ -28,6 +28,6 @@ else:
     for k in range(2):
         sim.L.rsim_gpu_support_active(sim._ctx, 1e-3, 2, C.byref(st))
         sim.assemble()
-        sim.linear_solve(case.solver_opts(fixed_lin_iters=50, lin_maxit=50))
+        sim.linear_solve(case.solver_opts(fixed_lin_iters=50, lin_maxit=50, precond=0))
         s2 = sim.stats()
     print("c5", frac, st.n_active, s2.lin_iters)

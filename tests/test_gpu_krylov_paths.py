@@ -89,8 +89,18 @@ def test_grid_path_full_set(cfg, precond):
     _check(case, None, precond=precond)
 
 
-def test_grid_path_distributed_level2_reduction():
-    # > 64*256*256 rows => level-2 partials reduced across CTAs (extra barrier)
+@pytest.mark.parametrize("precond", [pkg.PREC_BJACOBI, pkg.PREC_NEUMANN1])
+def test_grid_path_distributed_level2_reduction(precond):
+    # > 64*256*256 rows => level-2 partials reduced across CTAs (extra barrier);
+    # > 2^20 rows => the unfused (store, barrier, gather) Krylov variant
     case = pkg.Case(5, nx=256, ny=128, nz=140)
     assert case.n > 64 * 256 * 256
-    _check(case, None, its=3)
+    _check(case, None, its=3, precond=precond)
+
+
+@pytest.mark.parametrize("precond", [pkg.PREC_BJACOBI, pkg.PREC_NEUMANN1])
+def test_grid_path_unfused_converged(precond):
+    # unfused variant run to convergence (early-exit branch) on 1.3 M rows, b=2
+    case = pkg.Case(3, nx=160, ny=128, nz=64)
+    assert case.n > (1 << 20)
+    _check(case, None, precond=precond)
