@@ -120,7 +120,8 @@ int rsim_gpu_timers(rsim_gpu_ctx* ctx, int32_t enable, double* ms4, int32_t* lau
 int rsim_gpu_counters(rsim_gpu_ctx* ctx, int64_t* out5, int32_t reset);
 
 /* Debug: cycle counters of the cluster Krylov phases (RSIM_KTRACE=1 at create). */
-int rsim_gpu_ktrace(rsim_gpu_ctx* ctx, unsigned long long* out8);
+#define RSIM_KTRACE_N 136 /* 8 phase counters (CTA 0) + 16 CTAs x 8 per-CTA counters */
+int rsim_gpu_ktrace(rsim_gpu_ctx* ctx, unsigned long long* out);
 
 /* CUDA events on the ctx stream (bench timing on the launching stream). */
 int rsim_gpu_mark(rsim_gpu_ctx* ctx, int32_t slot);                 /* slot < 64 */

@@ -304,6 +304,9 @@ static int bicgstab_once(const Model& M, const rsim_solver_opts& o, bool neu, do
   const bool fixed = o.fixed_lin_iters > 0;
   const int maxit = fixed ? o.fixed_lin_iters : o.lin_maxit;
   const double tol = o.lin_rtol * bnorm;
+  // Two global reductions per iteration: (r0,v) travels with
+  // the LAGGED (r,r) of the previous iterate, and rho_{k+1} = (r0,s) - w (r0,t)
+  // is formed from quantities reduced together with (s,s), (t,s), (t,t).
   double rho = 1.0, alpha = 1.0, omega = 1.0, rho_new = bb;
   for (int it = 1; it <= maxit; ++it) {
     if (it == 1) {
@@ -317,6 +320,14 @@ static int bicgstab_once(const Model& M, const rsim_solver_opts& o, bool neu, do
     const std::vector<double>& pp = neu ? (prec(p, ph), ph) : p;
     spmv<B>(M, pp.data(), v.data());
     double r0v = dotc<B>(nr, r0.data(), v.data());
+    if (it > 1) {  // convergence of the previous iterate (reduced with (r0,v))
+      const double rr = dotc<B>(nr, r.data(), r.data());
+      if (!fixed && std::sqrt(rr) <= tol) {
+        *iters = it - 1;
+        *relres = std::sqrt(rr) / bnorm;
+        return RSIM_OK;
+      }
+    }
     if (r0v == 0.0 || !std::isfinite(r0v)) { *iters = it; return RSIM_ENUM; }
     alpha = rho_new / r0v;
 #pragma omp parallel for schedule(static)
@@ -326,6 +337,8 @@ static int bicgstab_once(const Model& M, const rsim_solver_opts& o, bool neu, do
     double ss = dotc<B>(nr, s.data(), s.data());
     double ts = dotc<B>(nr, t.data(), s.data());
     double tt = dotc<B>(nr, t.data(), t.data());
+    double r0s = dotc<B>(nr, r0.data(), s.data());
+    double r0t = dotc<B>(nr, r0.data(), t.data());
     if (!fixed && std::sqrt(ss) <= tol) {
 #pragma omp parallel for schedule(static)
       for (int64_t e = 0; e < N; ++e) x[e] = x[e] + alpha * pp[e];
@@ -340,13 +353,15 @@ static int bicgstab_once(const Model& M, const rsim_solver_opts& o, bool neu, do
       x[e] = (x[e] + alpha * pp[e]) + omega * ss_[e];
       r[e] = s[e] - omega * t[e];
     }
-    double rr = dotc<B>(nr, r.data(), r.data());
     rho = rho_new;
-    rho_new = dotc<B>(nr, r0.data(), r.data());
+    rho_new = r0s - omega * r0t;
     *iters = it;
+    if (omega == 0.0 || rho_new == 0.0 || !std::isfinite(rho_new)) return RSIM_ENUM;
+  }
+  {  // iteration cap: residual of the last iterate
+    const double rr = dotc<B>(nr, r.data(), r.data());
     *relres = std::sqrt(rr) / bnorm;
     if (!fixed && std::sqrt(rr) <= tol) return RSIM_OK;
-    if (omega == 0.0 || rho_new == 0.0 || !std::isfinite(rho_new)) return RSIM_ENUM;
   }
   return fixed ? RSIM_OK : RSIM_ENOCONV;
 }

@@ -8,11 +8,12 @@ fallback for any kernel.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "librsim.so"
+LIB_PATH = Path(os.environ.get("RSIM_LIB") or (Path(__file__).resolve().parent / "lib" / "librsim.so"))  # RSIM_LIB: A/B experiments only
 
 RSIM_OK, RSIM_EARG, RSIM_ECUDA, RSIM_ENUM, RSIM_ENOCONV = 0, 1, 2, 3, 4
 FLUID_SINGLE, FLUID_OILWATER, FLUID_BLACKOIL = 1, 2, 3

@@ -211,7 +211,7 @@ int rsim_gpu_create(rsim_gpu_ctx** out, const rsim_graph_desc* g, const rsim_flu
   TRY(dalloc(&c->p, n * b)); TRY(dalloc(&c->v, n * b)); TRY(dalloc(&c->s, n * b)); TRY(dalloc(&c->t, n * b));
   TRY(dalloc(&c->p2, n * b)); TRY(dalloc(&c->v2, n * b));
   TRY(dalloc(&c->ph, n * b)); TRY(dalloc(&c->sh, n * b));
-  TRY(dalloc(&c->part, 4 * nchunks + 64));
+  TRY(dalloc(&c->part, 6 * nchunks + 64));  // 5 level-1 + 5 level-2 partial rows
   TRY(dalloc(&c->dsc, 1));
   RSIM_CUDA(cudaMallocHost((void**)&c->hsc, sizeof(DevScalars)));
   std::memset(c->hsc, 0, sizeof(DevScalars));
@@ -236,16 +236,16 @@ int rsim_gpu_create(rsim_gpu_ctx** out, const rsim_graph_desc* g, const rsim_flu
   c->act = c->act_buf;
   c->nA = 0;
   if (const char* e = std::getenv("RSIM_KTRACE"); e && *e == '1') {
-    TRY(dalloc(&c->ktrace, 8));
-    RSIM_CUDA(cudaMemset(c->ktrace, 0, 8 * sizeof(unsigned long long)));
+    TRY(dalloc(&c->ktrace, RSIM_KTRACE_N));
+    RSIM_CUDA(cudaMemset(c->ktrace, 0, RSIM_KTRACE_N * sizeof(unsigned long long)));
   }
   return RSIM_OK;
 }
 
-int rsim_gpu_ktrace(rsim_gpu_ctx* c, unsigned long long* out8) {
+int rsim_gpu_ktrace(rsim_gpu_ctx* c, unsigned long long* out) {
   if (!c->ktrace) return RSIM_EARG;
-  RSIM_CUDA(cudaMemcpy(out8, c->ktrace, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-  RSIM_CUDA(cudaMemset(c->ktrace, 0, 8 * sizeof(unsigned long long)));
+  RSIM_CUDA(cudaMemcpy(out, c->ktrace, RSIM_KTRACE_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  RSIM_CUDA(cudaMemset(c->ktrace, 0, RSIM_KTRACE_N * sizeof(unsigned long long)));
   return RSIM_OK;
 }
 

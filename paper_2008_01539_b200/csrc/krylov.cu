@@ -46,16 +46,16 @@ struct KArgs {
   const double* F_raw;
   double *x, *r, *r0, *p, *v, *s, *t, *p2, *v2, *ph, *sh;
   int32_t neu, fuse;
-  double* part;   // [3][pstride]  level-1 partials
-  double* part2;  // [3][pstride2] level-2 partials (very large systems)
+  double* part;   // [5][pstride]  level-1 partials
+  double* part2;  // [5][pstride2] level-2 partials (very large systems)
   int32_t pstride, pstride2;
   DevScalars* dsc;
 };
 
 struct Red {
-  double ws[3][32];  // warp sums of the current round
-  double lvl[3][64];
-  double res[3];
+  double ws[5][32];  // warp sums of the current round
+  double lvl[5][64];
+  double res[5];
 };
 
 // Per-round commit: warp trees of up to 3 quantities -> 8-way trees -> level-1
@@ -104,27 +104,31 @@ __device__ __forceinline__ void reduce_small(Red& R, int q, const double* src, i
   __syncthreads();
 }
 
+// Vectors a gather may read (read-only in the current phase).
+struct Vecs {
+  const double *r, *po, *vo, *s, *t;
+};
+
 // Neighbour value of the vector being multiplied, recomputed from vectors
 // that are read-only in the current phase (same formula as the owner, so the
-// same bits):  mode 0: p_j = r_j + β (p_old_j − ω v_old_j);  mode 1: p_j = r_j;
-// mode 2: s_j = r_j − α v_j;  mode 3: x_j read directly from `po`.
+// same bits):  mode 0: p_j = (s_j − ω t_j) + β (p_old_j − ω v_old_j), the
+// previous iterate's r recomputed from its s, t;  mode 1: p_j = r_j;
+// mode 2: s_j = r_j − α v_j (vo = current v);  mode 3: x_j read directly from `po`.
 template <int B>
-__device__ __forceinline__ void nbr_val(int mode, const double* __restrict__ r, const double* __restrict__ po,
-                                        const double* __restrict__ vo, int64_t j, double beta, double omega,
-                                        double alpha, double* out) {
+__device__ __forceinline__ void nbr_val(int mode, const Vecs& X, int64_t j, double beta, double omega, double alpha,
+                                        double* out) {
 #pragma unroll
   for (int e = 0; e < B; ++e) {
     const int64_t q = j * B + e;
-    if (mode == 3) out[e] = po[q];
-    else if (mode == 1) out[e] = r[q];
-    else if (mode == 0) out[e] = r[q] + beta * (po[q] - omega * vo[q]);
-    else out[e] = r[q] - alpha * vo[q];
+    if (mode == 3) out[e] = X.po[q];
+    else if (mode == 1) out[e] = X.r[q];
+    else if (mode == 0) out[e] = (X.s[q] - omega * X.t[q]) + beta * (X.po[q] - omega * X.vo[q]);
+    else out[e] = X.r[q] - alpha * X.vo[q];
   }
 }
 
 template <int B>
-__device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, const double* __restrict__ r,
-                                         const double* __restrict__ po, const double* __restrict__ vo, double beta,
+__device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, const Vecs& X, double beta,
                                          double omega, double alpha, const double* own, double* acc) {
   const int32_t* __restrict__ col = a.ell_col;
   const double* __restrict__ val = a.ell_val;
@@ -134,7 +138,7 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
   double xv[6][B];
 #pragma unroll
   for (int s = 0; s < 6; ++s)
-    if (cl[s] >= 0) nbr_val<B>(mode, r, po, vo, cl[s], beta, omega, alpha, xv[s]);
+    if (cl[s] >= 0) nbr_val<B>(mode, X, cl[s], beta, omega, alpha, xv[s]);
 #pragma unroll
   for (int e = 0; e < B; ++e) acc[e] = own[e];
 #pragma unroll
@@ -147,7 +151,7 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
       const int32_t cc = a.nnc_lcol[q];
       if (cc >= 0) {
         double xn[B];
-        nbr_val<B>(mode, r, po, vo, cc, beta, omega, alpha, xn);
+        nbr_val<B>(mode, X, cc, beta, omega, alpha, xn);
         rsim::blk::gemv_acc_flat<B>(&a.nnc_val[(int64_t)q * B * B], xn, acc);
       }
     }
@@ -179,7 +183,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       for (int64_t rr = blockIdx.x; rr * 4 < P2; rr += gridDim.x) {
         const int64_t c2 = rr * 4 + (tid >> 8);
         const int64_t idx = c2 * 256 + (tid & 255);
-        double v[3] = {0.0, 0.0, 0.0};
+        double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         for (int q = 0; q < NQ; ++q) v[q] = idx < P1 ? a.part[q * a.pstride + idx] : 0.0;
         commit_round(R, NQ, v, rr * 4, P2, a.part2, a.pstride2);
       }
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) { \
     const int64_t l = rd * KT + tid;                             \
     const bool ok = l < nr;                                      \
-    double val[3] = {0.0, 0.0, 0.0};
+    double val[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #define ROUNDS_END(NQ)                                           \
   commit_round(R, NQ, val, rd * 4, nch, a.part, a.pstride);      \
   }
@@ -256,12 +260,13 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     const double* po = cur ? a.p : a.p2;
     const double* vo = cur ? a.v : a.v2;
     const int pmode = it == 1 ? 1 : 0;
+    const Vecs V0{a.r, po, vo, a.s, a.t};  // p_j = (s_j − ω t_j) + β (p_old_j − ω v_old_j)
     if (!fuse) {  // p = r + β (p − ω v), stored, then visible to all
       for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
         const int64_t l = rd * KT + tid;
         if (l < nr) {
           double pown[B];
-          nbr_val<B>(pmode, a.r, po, vo, l, beta, omega, 0.0, pown);
+          nbr_val<B>(pmode, V0, l, beta, omega, 0.0, pown);
 #pragma unroll
           for (int e = 0; e < B; ++e) pc[l * B + e] = pown[e];
         }
@@ -274,14 +279,14 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
         if (l < nr) {
           double pown[B], y[B];
           if (fuse) {
-            nbr_val<B>(pmode, a.r, po, vo, l, beta, omega, 0.0, pown);
-            spmv_row<B>(a, l, pmode, a.r, po, vo, beta, omega, 0.0, pown, y);
+            nbr_val<B>(pmode, V0, l, beta, omega, 0.0, pown);
+            spmv_row<B>(a, l, pmode, V0, beta, omega, 0.0, pown, y);
 #pragma unroll
             for (int e = 0; e < B; ++e) pc[l * B + e] = pown[e];
           } else {
 #pragma unroll
             for (int e = 0; e < B; ++e) pown[e] = pc[l * B + e];
-            spmv_row<B>(a, l, 3, a.r, pc, vo, 0.0, 0.0, 0.0, pown, y);
+            spmv_row<B>(a, l, 3, Vecs{a.r, pc, vo, a.s, a.t}, 0.0, 0.0, 0.0, pown, y);
           }
 #pragma unroll
           for (int e = 0; e < B; ++e) a.ph[l * B + e] = pown[e] + (pown[e] - y[e]);
@@ -289,30 +294,38 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       }
       sync();
     }
-    // ---- v = Â p (BJ) or v = Â ph (Neumann-1); (r0, v)
+    // ---- v = Â p (BJ) or v = Â ph (Neumann-1); (r0, v) and the lagged (r, r)
     ROUNDS_BEGIN
     if (ok) {
       double y[B];
       if (neu) {
-        spmv_row<B>(a, l, 3, a.r, a.ph, vo, 0.0, 0.0, 0.0, &a.ph[l * B], y);
+        spmv_row<B>(a, l, 3, Vecs{a.r, a.ph, vo, a.s, a.t}, 0.0, 0.0, 0.0, &a.ph[l * B], y);
       } else if (fuse) {
         double pown[B];
-        nbr_val<B>(pmode, a.r, po, vo, l, beta, omega, 0.0, pown);
+        nbr_val<B>(pmode, V0, l, beta, omega, 0.0, pown);
 #pragma unroll
         for (int e = 0; e < B; ++e) pc[l * B + e] = pown[e];
-        spmv_row<B>(a, l, pmode, a.r, po, vo, beta, omega, 0.0, pown, y);
+        spmv_row<B>(a, l, pmode, V0, beta, omega, 0.0, pown, y);
       } else {
-        spmv_row<B>(a, l, 3, a.r, pc, vo, 0.0, 0.0, 0.0, &pc[l * B], y);
+        spmv_row<B>(a, l, 3, Vecs{a.r, pc, vo, a.s, a.t}, 0.0, 0.0, 0.0, &pc[l * B], y);
       }
 #pragma unroll
       for (int e = 0; e < B; ++e) vc[l * B + e] = y[e];
       val[0] = rsim::blk::rowdot<B>(&a.r0[l * B], y);
+      val[1] = rsim::blk::rowdot<B>(&a.r[l * B], &a.r[l * B]);
     }
-    ROUNDS_END(1)
-    reduce(1);
+    ROUNDS_END(2)
+    reduce(2);
+    if (it > 1 && !fixed && sqrt(R.res[1]) <= tol) {  // previous iterate converged
+      relres = sqrt(R.res[1]) / bnorm;
+      status = RSIM_OK;
+      --it;
+      break;
+    }
     const double r0v = R.res[0];
     if (r0v == 0.0 || !isfinite(r0v)) { status = RSIM_ENUM; break; }
     alpha = rho_new / r0v;
+    const Vecs V2{a.r, po, vc, a.s, a.t};  // s_j = r_j − α v_j
     if (!fuse) {  // s = r − α v, stored, barrier
       for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
         const int64_t l = rd * KT + tid;
@@ -328,14 +341,12 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
         if (l < nr) {
           double sv[B], y[B];
           if (fuse) {
-            nbr_val<B>(2, a.r, po, vc, l, 0.0, 0.0, alpha, sv);
-            spmv_row<B>(a, l, 2, a.r, po, vc, 0.0, 0.0, alpha, sv, y);
-#pragma unroll
-            for (int e = 0; e < B; ++e) a.s[l * B + e] = sv[e];
+            nbr_val<B>(2, V2, l, 0.0, 0.0, alpha, sv);
+            spmv_row<B>(a, l, 2, V2, 0.0, 0.0, alpha, sv, y);
           } else {
 #pragma unroll
             for (int e = 0; e < B; ++e) sv[e] = a.s[l * B + e];
-            spmv_row<B>(a, l, 3, a.r, a.s, vc, 0.0, 0.0, 0.0, sv, y);
+            spmv_row<B>(a, l, 3, Vecs{a.r, a.s, vc, a.s, a.t}, 0.0, 0.0, 0.0, sv, y);
           }
 #pragma unroll
           for (int e = 0; e < B; ++e) a.sh[l * B + e] = sv[e] + (sv[e] - y[e]);
@@ -343,33 +354,38 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       }
       sync();
     }
-    // ---- t = Â s (BJ) or t = Â sh (Neumann-1); (s,s), (t,s), (t,t)
+    // ---- t = Â s (BJ) or t = Â sh (Neumann-1); (s,s), (t,s), (t,t), (r0,s), (r0,t)
     ROUNDS_BEGIN
     if (ok) {
       double sv[B], y[B];
       if (neu) {
+        if (fuse) nbr_val<B>(2, V2, l, 0.0, 0.0, alpha, sv);
+        else
 #pragma unroll
-        for (int e = 0; e < B; ++e) sv[e] = a.s[l * B + e];
-        spmv_row<B>(a, l, 3, a.r, a.sh, vc, 0.0, 0.0, 0.0, &a.sh[l * B], y);
+          for (int e = 0; e < B; ++e) sv[e] = a.s[l * B + e];
+        spmv_row<B>(a, l, 3, Vecs{a.r, a.sh, vc, a.s, a.t}, 0.0, 0.0, 0.0, &a.sh[l * B], y);
       } else if (fuse) {
-        nbr_val<B>(2, a.r, po, vc, l, 0.0, 0.0, alpha, sv);
-        spmv_row<B>(a, l, 2, a.r, po, vc, 0.0, 0.0, alpha, sv, y);
-#pragma unroll
-        for (int e = 0; e < B; ++e) a.s[l * B + e] = sv[e];
+        nbr_val<B>(2, V2, l, 0.0, 0.0, alpha, sv);
+        spmv_row<B>(a, l, 2, V2, 0.0, 0.0, alpha, sv, y);
       } else {
 #pragma unroll
         for (int e = 0; e < B; ++e) sv[e] = a.s[l * B + e];
-        spmv_row<B>(a, l, 3, a.r, a.s, vc, 0.0, 0.0, 0.0, sv, y);
+        spmv_row<B>(a, l, 3, Vecs{a.r, a.s, vc, a.s, a.t}, 0.0, 0.0, 0.0, sv, y);
       }
+      if (fuse)
+#pragma unroll
+        for (int e = 0; e < B; ++e) a.s[l * B + e] = sv[e];
 #pragma unroll
       for (int e = 0; e < B; ++e) a.t[l * B + e] = y[e];
       val[0] = rsim::blk::rowdot<B>(sv, sv);
       val[1] = rsim::blk::rowdot<B>(y, sv);
       val[2] = rsim::blk::rowdot<B>(y, y);
+      val[3] = rsim::blk::rowdot<B>(&a.r0[l * B], sv);
+      val[4] = rsim::blk::rowdot<B>(&a.r0[l * B], y);
     }
-    ROUNDS_END(3)
-    reduce(3);
-    const double ss = R.res[0], ts = R.res[1], tt = R.res[2];
+    ROUNDS_END(5)
+    reduce(5);
+    const double ss = R.res[0], ts = R.res[1], tt = R.res[2], r0s = R.res[3], r0t = R.res[4];
     const double* phv = neu ? a.ph : pc;
     const double* shv = neu ? a.sh : a.s;
     if (!fixed && sqrt(ss) <= tol) {
@@ -385,33 +401,32 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     }
     if (tt == 0.0 || !isfinite(tt)) { status = RSIM_ENUM; break; }
     omega = ts / tt;
-    // ---- x, r update ; (r, r), (r0, r)
-    ROUNDS_BEGIN
-    if (ok) {
-      double rv[B], r0v_[B];
+    // ---- x, r update (own rows, no barrier: neighbours recompute r from s, t
+    //      until the next reduction, and the next p-pass reads only its own r)
+    for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
+      const int64_t l = rd * KT + tid;
+      if (l < nr)
 #pragma unroll
-      for (int e = 0; e < B; ++e) {
-        const int64_t q = l * B + e;
-        const double sq = a.s[q];
-        a.x[q] = (a.x[q] + alpha * phv[q]) + omega * shv[q];
-        rv[e] = sq - omega * a.t[q];
-        a.r[q] = rv[e];
-        r0v_[e] = a.r0[q];
-      }
-      val[0] = rsim::blk::rowdot<B>(rv, rv);
-      val[1] = rsim::blk::rowdot<B>(r0v_, rv);
+        for (int e = 0; e < B; ++e) {
+          const int64_t q = l * B + e;
+          a.x[q] = (a.x[q] + alpha * phv[q]) + omega * shv[q];
+          a.r[q] = a.s[q] - omega * a.t[q];
+        }
     }
-    ROUNDS_END(2)
-    reduce(2);
-    const double rr = R.res[0];
     rho = rho_new;
-    rho_new = R.res[1];
-    relres = sqrt(rr) / bnorm;
-    if (!fixed && sqrt(rr) <= tol) { status = RSIM_OK; break; }
+    rho_new = r0s - omega * r0t;
     if (omega == 0.0 || rho_new == 0.0 || !isfinite(rho_new)) { status = RSIM_ENUM; break; }
     cur ^= 1;
   }
-  if (it > maxit) { it = maxit; status = fixed ? RSIM_OK : RSIM_ENOCONV; }
+  if (it > maxit) {  // iteration cap: residual of the last iterate (one more reduction)
+    it = maxit;
+    ROUNDS_BEGIN
+    if (ok) val[0] = rsim::blk::rowdot<B>(&a.r[l * B], &a.r[l * B]);
+    ROUNDS_END(1)
+    reduce(1);
+    relres = sqrt(R.res[0]) / bnorm;
+    status = (fixed || sqrt(R.res[0]) <= tol) ? RSIM_OK : RSIM_ENOCONV;
+  }
   it_total += it;
   if (!(neu && (status == RSIM_ENUM || status == RSIM_ENOCONV))) break;
   }
@@ -445,7 +460,7 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.pstride = (int32_t)((c->n + 255) / 256);
   a.pstride2 = (a.pstride + 255) / 256;
   a.part = c->part;
-  a.part2 = c->part + 3 * (int64_t)a.pstride;
+  a.part2 = c->part + 5 * (int64_t)a.pstride;
   a.dsc = c->dsc;
   const int64_t nrounds = ((c->nA + 255) / 256 + 3) / 4;
   if (c->max_coop_blocks[B] == 0) {

@@ -5,18 +5,21 @@
 // the whole solve inside ONE thread-block cluster of G <= 16 CTAs:
 //
 //   * CTA g owns the contiguous local rows [g*RC, (g+1)*RC), RC = 64..1024
-//     (RC/32 canonical warps, blockops.h); canonical warp sums are local, a
-//     chunk partial is the 8-way tree of 8 warp sums
-//     warp shuffles + an 8-way tree inside the CTA, and only the <= 64 chunk
-//     partials cross DSMEM (one cluster barrier per reduction);
+//     (RC/32 canonical warps, blockops.h); a reduction is warp shuffles into
+//     shared memory, one cluster barrier, then a DSMEM gather of the canonical
+//     warp sums and the canonical tree (identical in every CTA);
 //   * the Krylov vectors and (when it fits) the ELL rows of each CTA live in
 //     its shared memory for the whole solve — global traffic is the initial
 //     load and the final store of x;
-//   * SpMV reads neighbour entries from the owning CTA (own smem when local —
-//     the usual case since the active list is sorted by cell — DSMEM else);
-//   * the p- and s-updates are recomputed at the gather site from r, p_old,
-//     v_old (same formulas, same bits), so an iteration needs 3 cluster
-//     barriers instead of 5.
+//   * every neighbour's tagged shared address (own CTA: ld.shared, peer CTA:
+//     ld.shared::cluster) is resolved once per solve;
+//   * the neighbours' p (via r = s − ω t) and s are recomputed at the gather
+//     site (same formulas, same bits), and BiCGSTAB runs with two reductions
+//     per iteration ((r0,v) with the lagged (r,r); (s,s), (t,s), (t,t),
+//     (r0,s), (r0,t) with ρ = (r0,s) − ω (r0,t)): 2 cluster barriers per
+//     iteration, 4 with the Neumann-1 preconditioner;
+//   * cluster barriers are relaxed (no GPU-scope fence) after a __syncthreads
+//     that drains the CTA's shared stores — see csync().
 // Element formulas and reduction order are those of oracle/oracle.cpp
 // bicgstab(); results are bit-identical to it and to krylov.cu.
 
@@ -33,6 +36,13 @@ namespace cg = cooperative_groups;
 
 namespace {
 
+// ---- shared::cluster addressing (PTX; sm_90+)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int r) {
+  uint32_t o;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(o) : "r"(a), "r"(r));
+  return o;
+}
 constexpr int GMAX = 16;
 constexpr int NNCMAX = 256;             // NNC entries cached in smem per CTA
 constexpr int NNC_GLOBAL = 0x40000000;  // flag in the range end: entries stay in global
@@ -55,35 +65,45 @@ struct DArgs {
   unsigned long long* trace;  // optional [8] cycle accumulators (RSIM_KTRACE)
 };
 
+// Cluster loads of a row's B components (shared::cluster address; B = 3 is padded to 4).
+// Row loads of B components through a generic pointer into this CTA's or a
+// peer CTA's shared memory (the hardware routes a peer window to DSMEM).
+// B = 3 rows are padded to 4 doubles, so every row starts 16-byte aligned.
+template <int B>
+__device__ __forceinline__ void ldg_row(const double* p, double* o) {
+  if constexpr (B == 1) {
+    o[0] = p[0];
+  } else {
+    const double2 v = *reinterpret_cast<const double2*>(p);
+    o[0] = v.x;
+    o[1] = v.y;
+    if constexpr (B == 3) o[2] = p[2];
+  }
+}
+
 template <int B, int NS, bool MS, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
+  // Shared layout (identical in every CTA, so a neighbour row's cluster
+  // address is mapa(base, owner) + row offset, computed once per solve):
+  //   V[RC][9][BP]: per row r, p0, p1, v0, v1, ph, sh, s, t (p, v
+  //   double-buffered: neighbours read the previous iterate while the owner
+  //   writes the new one; s, t feed the neighbours' recompute of r)
+  //   mval[NS][RC][B*B] (MS), NNC ranges, NNC blocks + cluster addresses.
+  // Own-row-only vectors r0, x, s, t live in registers.
+  constexpr int BP = (B == 3) ? 4 : B;
+  constexpr int ROWD = 9 * BP;
+  constexpr uint32_t ROWB = ROWD * 8;
+  constexpr int O_R = 0, O_P = 1, O_V = 3, O_PH = 5, O_SH = 6, O_S = 7, O_T = 8;
   extern __shared__ __align__(16) double dyn[];
   const int RC = 1 << a.LRC;
-  // shared (read by neighbours): r, p[2], v[2]  (p, v double-buffered:
-  // neighbours read the previous iterate while the owner writes the new one);
-  // own-row-only vectors r0, x, s, t live in registers.
-  double* vr = dyn;
-  double* vp0 = vr + RC * B;
-  double* vp1 = vp0 + RC * B;
-  double* vv0 = vp1 + RC * B;
-  double* vv1 = vv0 + RC * B;
-  double* vph = vv1 + RC * B;  // M^-1 p  (Neumann-1 preconditioner only)
-  double* vsh = vph + RC * B;  // M^-1 s
-  double* mval = vsh + RC * B;                                    // [NS][RC][B*B]  (MS)
-  int32_t* mcol = (int32_t*)(mval + (MS ? NS * RC * B * B : 0));   // [NS][RC]       (MS)
-  int2* nrng = (int2*)(mcol + (MS ? NS * RC : 0));                // [RC] NNC ranges (has_nnc)
-  double* nsv = (double*)(nrng + RC);                              // [NNCMAX][B*B] NNC blocks
-  int32_t* nsc = (int32_t*)(nsv + NNCMAX * B * B);                 // [NNCMAX] NNC local columns
+  double* V = dyn;
+  double* mval = V + RC * ROWD;                                     // [NS][RC][B*B]  (MS)
+  int2* nrng = (int2*)(mval + (MS ? NS * RC * B * B : 0));          // [RC] NNC ranges (has_nnc)
+  double* nsv = (double*)(nrng + RC);                               // [NNCMAX][B*B] NNC blocks
+  const double** nsa = (const double**)(nsv + NNCMAX * B * B);       // [NNCMAX] NNC row pointers
   __shared__ int nnc_cnt;
-
-  __shared__ double* rb[GMAX];
-  __shared__ double* pb[2][GMAX];
-  __shared__ double* vb[2][GMAX];
-  __shared__ double* wsb[GMAX];
-  __shared__ double* phb[GMAX];
-  __shared__ double* shb[GMAX];
-  __shared__ double ws[2][3][32];  // [buf][q][warp]: canonical warp sums of this CTA
-  __shared__ double res[3];
+  __shared__ double ws[2][5][32];  // [buf][q][warp]: canonical warp sums of this CTA
+  __shared__ double res_s[5];
 
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
@@ -93,34 +113,44 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   const int64_t nr = a.nA;
   const int nch = a.nch;
   const int LWPC = a.LRC - 5;  // log2(warps per CTA)
-  if (tid < G) {
-    rb[tid] = cluster.map_shared_rank(vr, tid);
-    pb[0][tid] = cluster.map_shared_rank(vp0, tid);
-    pb[1][tid] = cluster.map_shared_rank(vp1, tid);
-    vb[0][tid] = cluster.map_shared_rank(vv0, tid);
-    vb[1][tid] = cluster.map_shared_rank(vv1, tid);
-    wsb[tid] = cluster.map_shared_rank(&ws[0][0][0], tid);
-    phb[tid] = cluster.map_shared_rank(vph, tid);
-    shb[tid] = cluster.map_shared_rank(vsh, tid);
-  }
+  const uint32_t ws_u32 = smem_u32(&ws[0][0][0]);
   const int LSH = a.LRC;  // log2(RC)
   const int RCM = RC - 1;
-  const int64_t row0 = (int64_t)rank * RC;
-  const int64_t l = row0 + tid;
+  const int64_t l = (int64_t)rank * RC + tid;
   const bool valid = l < nr;
   const int lam = tid;
+  double* Vo = V + lam * ROWD;  // own row
+  // generic pointer to local row j's vector block (own CTA or a peer's window)
+  auto caddr = [&](int32_t j) -> const double* {
+    const int g = j >> LSH;
+    const double* base = g == rank ? V : cluster.map_shared_rank(V, g);
+    return base + (size_t)(j & RCM) * ROWD;
+  };
   int wbuf = 0;
 
-  // Canonical reduction of NQ per-row values (one per thread): warp trees
-  // into shared memory, ONE cluster barrier (which also orders the CTA), then
-  // warp 0 of every CTA gathers the 8 warp sums of each chunk via DSMEM and
-  // finishes the canonical tree (8-way per chunk, then over the chunk
-  // partials); one __syncthreads broadcasts the result.
+  // Cluster-wide barrier after which every CTA's earlier shared-memory writes
+  // are visible to DSMEM reads: __syncthreads drains this CTA's pending shared
+  // stores, then a relaxed cluster barrier (no GPU-scope fence: nothing in the
+  // solve loop writes global memory, and DSMEM reads are served by the owner
+  // SM's shared memory, not a cache).  ~160 cycles against ~400 for
+  // cluster.sync() with its MEMBAR.GPU (scripts/micro/xchg.cu).
+  __shared__ unsigned long long tc[8];  // RSIM_KTRACE cycle accumulators (rank 0, thread 0)
+  __shared__ unsigned long long tcr[8];  // per-CTA: [0,1] csync wait, [2,3] spmv, [4] reduce tail (warp 0 / last warp)
+  const bool tr = a.trace && rank == 0 && tid == 0;
+  const int trw = (a.trace && lane == 0) ? (w == 0 ? 1 : (w == (RC >> 5) - 1 ? 2 : 0)) : 0;
+  if (a.trace && tid < 8) tcr[tid] = 0;
   auto csync = [&]() {
-    if (G == 1) __syncthreads();
-    else cluster.sync();
+    const long long tb = (tr || trw) ? clock64() : 0;
+    __syncthreads();
+    if (G > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
+    if (tr) tc[6] += (unsigned long long)(clock64() - tb);
+    if (trw) tcr[trw - 1] += (unsigned long long)(clock64() - tb);
   };
-  auto reduce = [&](auto NQc, const double* val) {
+  // Canonical reduction of NQ per-row values (one per thread): warp trees into
+  // shared memory, ONE cluster barrier, then warp q of every CTA gathers the 8
+  // warp sums of each chunk via DSMEM and finishes the canonical tree (8-way
+  // per chunk, then over the chunk partials); one __syncthreads broadcasts.
+  auto reduce = [&](auto NQc, const double* val, double* out) {
     constexpr int NQ = decltype(NQc)::value;
     double v[NQ];
 #pragma unroll
@@ -133,6 +163,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
 #pragma unroll
       for (int q = 0; q < NQ; ++q) ws[wbuf][q][w] = v[q];
     csync();
+    const long long t_tail = trw == 1 ? clock64() : 0;
     for (int q = w; q < NQ; q += (1 << LWPC)) {  // warp w finishes quantities w, w+WPC, ...
       double cp[2] = {0.0, 0.0};
 #pragma unroll
@@ -143,68 +174,83 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) {  // canonical warp 8c+k lives on CTA gw >> LWPC
             const int gw = (c << 3) | k;
-            w8[k] = ((int64_t)gw << 5) < nr ? wsb[gw >> LWPC][(wbuf * 3 + q) * 32 + (gw & ((1 << LWPC) - 1))]
-                                            : 0.0;  // warp entirely past n_A: structural zero
+            double x = 0.0;  // warp entirely past n_A: structural zero
+            if (((int64_t)gw << 5) < nr) {
+              const uint32_t ad = mapa_u32(ws_u32, gw >> LWPC) + (uint32_t)(((wbuf * 5 + q) * 32 + (gw & ((1 << LWPC) - 1))) * 8);
+              asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(x) : "r"(ad) : "memory");
+            }
+            w8[k] = x;
           }
           cp[h] = tree8(w8);
         }
       }
       if (nch == 1) {
-        if (lane == 0) res[q] = cp[0];
+        if (lane == 0) res_s[q] = cp[0];
       } else {
         double W[8] = {warp_tree_n(cp[0], nch), warp_tree_n(cp[1], nch - 32), 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-        if (lane == 0) res[q] = tree8(W);
+        if (lane == 0) res_s[q] = tree8(W);
       }
     }
     __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) out[q] = res_s[q];
+    if (trw == 1) tcr[4] += (unsigned long long)(clock64() - t_tail);
     wbuf ^= 1;
   };
+  auto xbar = [&]() { csync(); };
+
+  // neighbour rows: cluster address per Cartesian slot (bit s of nmask = present)
+  const double* na[NS];
+  uint32_t nmask = 0;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) na[s] = nullptr;
 
   // neighbour value of the vector being multiplied, recomputed at the gather site:
-  //   mode 0: p_new_j = r_j + beta (p_old_j - omega v_old_j)   (it > 1)
+  //   mode 0: p_new_j = (s_j - omega t_j) + beta (p_old_j - omega v_old_j)   (it > 1)
   //   mode 1: p_new_j = r_j                                     (it == 1)
   //   mode 2: s_j     = r_j - alpha v_new_j
   //   mode 3: (M^-1 p)_j, mode 4: (M^-1 s)_j   (stored by the owner, Neumann-1)
-  auto gather = [&](int mode, int cur, int32_t j, double beta, double omega, double alpha, double* out) {
-    const int g = j >> LSH;
-    const int rr = (j & RCM) * B;
-    const bool loc = g == rank;
-    if (mode >= 3) {
-      const double* X_ = (mode == 3 ? (loc ? vph : phb[g]) : (loc ? vsh : shb[g])) + rr;
+  auto gather = [&](auto MODEc, const double* ad, int offo, double beta, double omega, double alpha, double* out) {
+    constexpr int MODE = decltype(MODEc)::value;
+    if constexpr (MODE == 3) {
+      ldg_row<B>(ad + O_PH * BP, out);
+    } else if constexpr (MODE == 4) {
+      ldg_row<B>(ad + O_SH * BP, out);
+    } else if constexpr (MODE == 1) {
+      ldg_row<B>(ad + O_R * BP, out);
+    } else if constexpr (MODE == 0) {  // r_j = s_j − ω t_j (previous iterate); offo: old p (v 2 vectors later)
+      double S_[B], T_[B], P_[B], V_[B];
+      ldg_row<B>(ad + O_S * BP, S_);
+      ldg_row<B>(ad + O_T * BP, T_);
+      ldg_row<B>(ad + offo, P_);
+      ldg_row<B>(ad + offo + 2 * BP, V_);
 #pragma unroll
-      for (int e = 0; e < B; ++e) out[e] = X_[e];
-      return;
-    }
-    const double* R_ = (loc ? vr : rb[g]) + rr;
-    if (mode == 1) {
-#pragma unroll
-      for (int e = 0; e < B; ++e) out[e] = R_[e];
-    } else if (mode == 0) {
-      const double* P_ = (loc ? (cur ? vp0 : vp1) : pb[cur ^ 1][g]) + rr;
-      const double* V_ = (loc ? (cur ? vv0 : vv1) : vb[cur ^ 1][g]) + rr;
-#pragma unroll
-      for (int e = 0; e < B; ++e) out[e] = R_[e] + beta * (P_[e] - omega * V_[e]);
-    } else {
-      const double* V_ = (loc ? (cur ? vv1 : vv0) : vb[cur][g]) + rr;
+      for (int e = 0; e < B; ++e) {
+        const double rj = S_[e] - omega * T_[e];
+        out[e] = rj + beta * (P_[e] - omega * V_[e]);
+      }
+    } else {  // offo: the current v
+      double R_[B], V_[B];
+      ldg_row<B>(ad + O_R * BP, R_);
+      ldg_row<B>(ad + offo, V_);
 #pragma unroll
       for (int e = 0; e < B; ++e) out[e] = R_[e] - alpha * V_[e];
     }
   };
 
-  // y = xown + Σ_slots Â_s x_col (+ NNC)
-  auto spmv = [&](int mode, int cur, const double* xown, double beta, double omega, double alpha, double* y) {
-    int32_t cl[NS];
+  // y = xown + Σ_slots Â_s x_col (+ NNC), canonical order
+  auto spmv = [&](auto MODEc, int offo, const double* xown, double beta, double omega, double alpha, double* y) {
+    const long long t_sp = trw ? clock64() : 0;
     double xv[NS][B];
 #pragma unroll
-    for (int s = 0; s < NS; ++s) cl[s] = MS ? mcol[s * RC + lam] : __ldg(&a.ell_col[s * a.cap + l]);
-#pragma unroll
-    for (int s = 0; s < NS; ++s) gather(mode, cur, cl[s] < 0 ? (int32_t)l : cl[s], beta, omega, alpha, xv[s]);
+    for (int s = 0; s < NS; ++s)
+      if (nmask & (1u << s)) gather(MODEc, na[s], offo, beta, omega, alpha, xv[s]);
     double acc[B];
 #pragma unroll
     for (int e = 0; e < B; ++e) acc[e] = xown[e];
 #pragma unroll
     for (int s = 0; s < NS; ++s)
-      if (cl[s] >= 0) {
+      if (nmask & (1u << s)) {
         const double* M = MS ? &mval[((size_t)s * RC + lam) * B * B] : &a.ell_val[((int64_t)s * a.cap + l) * B * B];
         rsim::blk::gemv_acc_flat<B>(M, xv[s], acc);
       }
@@ -215,26 +261,28 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
           const int32_t c2 = a.nnc_lcol[q];
           if (c2 >= 0) {
             double xn[B];
-            gather(mode, cur, c2, beta, omega, alpha, xn);
+            gather(MODEc, caddr(c2), offo, beta, omega, alpha, xn);
             rsim::blk::gemv_acc_flat<B>(&a.nnc_val[(int64_t)q * B * B], xn, acc);
           }
         }
       } else {
         for (int32_t q = rg.x; q < rg.y; ++q) {
           double xn[B];
-          gather(mode, cur, nsc[q], beta, omega, alpha, xn);
+          gather(MODEc, nsa[q], offo, beta, omega, alpha, xn);
           rsim::blk::gemv_acc_flat<B>(&nsv[q * B * B], xn, acc);
         }
       }
     }
 #pragma unroll
     for (int e = 0; e < B; ++e) y[e] = acc[e];
+    if (trw) tcr[1 + trw] += (unsigned long long)(clock64() - t_sp);
   };
 
   double r0r[B], xr[B], sr[B], tr_[B];
+  double res[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int e = 0; e < B; ++e) { r0r[e] = 0.0; xr[e] = 0.0; sr[e] = 0.0; tr_[e] = 0.0; }
-  // ---- load: matrix rows (MS), rhs -> r, r0; x = 0; (b,b), (F,F)
+  // ---- load: matrix rows (MS), neighbour addresses, rhs -> r, r0; x = 0; (b,b), (F,F)
   if (tid == 0) nnc_cnt = 0;
   __syncthreads();
   {
@@ -245,11 +293,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
       for (int e = 0; e < B; ++e) {
         bv[e] = a.rhs[l * B + e];
         fv[e] = a.F_raw[l * B + e];
-        vr[lam * B + e] = bv[e];
+        Vo[O_R * BP + e] = bv[e];
         r0r[e] = bv[e];
         xr[e] = 0.0;
-        vp0[lam * B + e] = 0.0; vp1[lam * B + e] = 0.0;
-        vv0[lam * B + e] = 0.0; vv1[lam * B + e] = 0.0;
+        Vo[O_P * BP + e] = 0.0; Vo[(O_P + 1) * BP + e] = 0.0;
+        Vo[O_V * BP + e] = 0.0; Vo[(O_V + 1) * BP + e] = 0.0;
       }
       val[0] = rsim::blk::rowdot<B>(bv, bv);
       val[1] = rsim::blk::rowdot<B>(fv, fv);
@@ -264,7 +312,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
           for (int32_t q = q0; q < q1; ++q) {
             const int32_t c2 = a.nnc_lcol[q];
             if (c2 < 0) continue;
-            nsc[m] = c2;
+            nsa[m] = caddr(c2);
 #pragma unroll
             for (int e = 0; e < B * B; ++e) nsv[m * B * B + e] = a.nnc_val[(int64_t)q * B * B + e];
             ++m;
@@ -274,19 +322,21 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
           nrng[lam] = make_int2(q0, q1 | NNC_GLOBAL);
         }
       }
-      if (MS) {
 #pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          const int32_t cl = (s < a.nslot) ? a.ell_col[s * a.cap + l] : -1;
-          mcol[s * RC + lam] = cl;
-          if (cl >= 0)
+      for (int s = 0; s < NS; ++s) {
+        const int32_t cl = a.ell_col[s * a.cap + l];
+        if (cl >= 0) {
+          nmask |= 1u << s;
+          na[s] = caddr(cl);
+          if (a.trace && (cl >> LSH) != rank) atomicAdd(&tcr[5], 1ull);
+          if (MS)
 #pragma unroll
             for (int e = 0; e < B * B; ++e)
               mval[((size_t)s * RC + lam) * B * B + e] = a.ell_val[((int64_t)s * a.cap + l) * B * B + e];
         }
       }
     }
-    reduce(std::integral_constant<int, 2>{}, val);
+    reduce(std::integral_constant<int, 2>{}, val, res);
   }
   const double bb = res[0];
   if (rank == 0 && tid == 0) a.dsc->f2 = sqrt(res[1]);
@@ -301,8 +351,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   int cur = 0;  // buffer holding the current iteration's p, v
   if (bnorm != 0.0) {
     status = RSIM_ENOCONV;
-    unsigned long long tc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const bool tr = a.trace && rank == 0 && tid == 0;
+    if (tr)
+      for (int k = 0; k < 8; ++k) tc[k] = 0;
     long long t0 = clock64();
 #define KT_MARK(k) do { if (tr) { long long t1 = clock64(); tc[k] += (unsigned long long)(t1 - t0); t0 = t1; } } while (0)
     int it_total = 0;
@@ -314,97 +364,117 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
       if (valid)
 #pragma unroll
         for (int e = 0; e < B; ++e) {
-          vr[lam * B + e] = a.rhs[l * B + e];
+          Vo[O_R * BP + e] = a.rhs[l * B + e];
           xr[e] = 0.0;
         }
       rho = 1.0; alpha = 1.0; omega = 1.0; rho_new = bb;
       cur = 0;
       status = RSIM_ENOCONV;
-      csync();
+      xbar();
     }
     for (it = 1; it <= maxit; ++it) {
       KT_MARK(7);
       const double beta = (it == 1) ? 0.0 : (rho_new / rho) * (alpha / omega);
-      double* vpc = cur ? vp1 : vp0;
-      double* vvc = cur ? vv1 : vv0;
-      const double* vpo = cur ? vp0 : vp1;
-      const double* vvo = cur ? vv0 : vv1;
-      // ---- p = r + β (p − ω v) (own + recomputed for neighbours)
-      //      BJ:  v = Â p;   Neumann-1: ph = p + (p − Â p), barrier, v = Â ph;  (r0, v)
+      double* Pc = Vo + (O_P + cur) * BP;          // own p (this iteration)
+      double* Vc = Vo + (O_V + cur) * BP;          // own v (this iteration)
+      const double* Po = Vo + (O_P + (cur ^ 1)) * BP;
+      const double* Vold = Vo + (O_V + (cur ^ 1)) * BP;
+      const int off_po = (O_P + (cur ^ 1)) * BP;  // neighbours' old p
+      const int off_vc = (O_V + cur) * BP;        // neighbours' current v
+      // ---- p = r + β (p − ω v) (own; neighbours recompute r = s − ω t and p)
+      //      BJ:  v = Â p;   Neumann-1: ph = p + (p − Â p), barrier, v = Â ph
+      //      reduce (r0, v) and the lagged (r, r) of the previous iterate
       double phr[B];
       {
-        double val[3] = {0.0, 0.0, 0.0};
-        double pown[B], y[B];
+        double val[2] = {0.0, 0.0};
+        double pown[B], y[B], rown[B];
         if (valid) {
 #pragma unroll
           for (int e = 0; e < B; ++e) {
-            const int q = lam * B + e;
-            pown[e] = (it == 1) ? vr[q] : vr[q] + beta * (vpo[q] - omega * vvo[q]);
-            vpc[q] = pown[e];
+            rown[e] = Vo[O_R * BP + e];
+            pown[e] = (it == 1) ? rown[e] : rown[e] + beta * (Po[e] - omega * Vold[e]);
+            Pc[e] = pown[e];
           }
-          spmv(it == 1 ? 1 : 0, cur, pown, beta, omega, 0.0, y);
+          if (it == 1) spmv(std::integral_constant<int, 1>{}, 0, pown, beta, omega, 0.0, y);
+          else spmv(std::integral_constant<int, 0>{}, off_po, pown, beta, omega, 0.0, y);
         }
         if (neu) {
           if (valid)
 #pragma unroll
             for (int e = 0; e < B; ++e) {
               phr[e] = pown[e] + (pown[e] - y[e]);
-              vph[lam * B + e] = phr[e];
+              Vo[O_PH * BP + e] = phr[e];
             }
-          csync();
-          if (valid) spmv(3, cur, phr, 0.0, 0.0, 0.0, y);
+          xbar();
+          if (valid) spmv(std::integral_constant<int, 3>{}, 0, phr, 0.0, 0.0, 0.0, y);
         } else {
 #pragma unroll
           for (int e = 0; e < B; ++e) phr[e] = pown[e];
         }
         if (valid) {
 #pragma unroll
-          for (int e = 0; e < B; ++e) vvc[lam * B + e] = y[e];
+          for (int e = 0; e < B; ++e) Vc[e] = y[e];
           val[0] = rsim::blk::rowdot<B>(r0r, y);
+          val[1] = rsim::blk::rowdot<B>(rown, rown);
         }
         KT_MARK(0);
-        reduce(std::integral_constant<int, 1>{}, val);
+        reduce(std::integral_constant<int, 2>{}, val, res);
         KT_MARK(1);
+      }
+      if (it > 1 && !fixed && sqrt(res[1]) <= tol) {  // previous iterate converged
+        relres = sqrt(res[1]) / bnorm;
+        status = RSIM_OK;
+        --it;
+        break;
       }
       const double r0v = res[0];
       if (r0v == 0.0 || !isfinite(r0v)) { status = RSIM_ENUM; break; }
       alpha = rho_new / r0v;
-      // ---- s = r − α v (own + recomputed for neighbours)
-      //      BJ: t = Â s;  Neumann-1: sh = s + (s − Â s), barrier, t = Â sh;  (s,s), (t,s), (t,t)
+      // ---- s = r − α v (own + recomputed for neighbours; stored for the next r recompute)
+      //      BJ: t = Â s;  Neumann-1: sh = s + (s − Â s), barrier, t = Â sh
+      //      reduce (s,s), (t,s), (t,t), (r0,s), (r0,t)
       double shr[B];
       {
-        double val[3] = {0.0, 0.0, 0.0};
+        double val[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         double y[B];
         if (valid) {
 #pragma unroll
-          for (int e = 0; e < B; ++e) sr[e] = vr[lam * B + e] - alpha * vvc[lam * B + e];
-          spmv(2, cur, sr, 0.0, 0.0, alpha, y);
+          for (int e = 0; e < B; ++e) {
+            sr[e] = Vo[O_R * BP + e] - alpha * Vc[e];
+            Vo[O_S * BP + e] = sr[e];
+          }
+          spmv(std::integral_constant<int, 2>{}, off_vc, sr, 0.0, 0.0, alpha, y);
         }
         if (neu) {
           if (valid)
 #pragma unroll
             for (int e = 0; e < B; ++e) {
               shr[e] = sr[e] + (sr[e] - y[e]);
-              vsh[lam * B + e] = shr[e];
+              Vo[O_SH * BP + e] = shr[e];
             }
-          csync();
-          if (valid) spmv(4, cur, shr, 0.0, 0.0, 0.0, y);
+          xbar();
+          if (valid) spmv(std::integral_constant<int, 4>{}, 0, shr, 0.0, 0.0, 0.0, y);
         } else {
 #pragma unroll
           for (int e = 0; e < B; ++e) shr[e] = sr[e];
         }
         if (valid) {
 #pragma unroll
-          for (int e = 0; e < B; ++e) tr_[e] = y[e];
+          for (int e = 0; e < B; ++e) {
+            tr_[e] = y[e];
+            Vo[O_T * BP + e] = y[e];
+          }
           val[0] = rsim::blk::rowdot<B>(sr, sr);
           val[1] = rsim::blk::rowdot<B>(y, sr);
           val[2] = rsim::blk::rowdot<B>(y, y);
+          val[3] = rsim::blk::rowdot<B>(r0r, sr);
+          val[4] = rsim::blk::rowdot<B>(r0r, y);
         }
         KT_MARK(2);
-        reduce(std::integral_constant<int, 3>{}, val);
+        reduce(std::integral_constant<int, 5>{}, val, res);
         KT_MARK(3);
       }
-      const double ssn = res[0], ts = res[1], tt = res[2];
+      const double ssn = res[0], ts = res[1], tt = res[2], r0s = res[3], r0t = res[4];
       if (!fixed && sqrt(ssn) <= tol) {
         if (valid)
 #pragma unroll
@@ -415,33 +485,32 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
       }
       if (tt == 0.0 || !isfinite(tt)) { status = RSIM_ENUM; break; }
       omega = ts / tt;
-      // ---- x, r update ; (r, r), (r0, r)
-      {
-        double val[3] = {0.0, 0.0, 0.0};
-        if (valid) {
-          double rv[B];
+      // ---- x, r update (own rows; neighbours recompute r from s, t)
+      if (valid)
 #pragma unroll
-          for (int e = 0; e < B; ++e) {
-            xr[e] = (xr[e] + alpha * phr[e]) + omega * shr[e];
-            rv[e] = sr[e] - omega * tr_[e];
-            vr[lam * B + e] = rv[e];
-          }
-          val[0] = rsim::blk::rowdot<B>(rv, rv);
-          val[1] = rsim::blk::rowdot<B>(r0r, rv);
+        for (int e = 0; e < B; ++e) {
+          xr[e] = (xr[e] + alpha * phr[e]) + omega * shr[e];
+          Vo[O_R * BP + e] = sr[e] - omega * tr_[e];
         }
-        KT_MARK(4);
-        reduce(std::integral_constant<int, 2>{}, val);
-        KT_MARK(5);
-      }
-      const double rr = res[0];
+      KT_MARK(4);
       rho = rho_new;
-      rho_new = res[1];
-      relres = sqrt(rr) / bnorm;
-      if (!fixed && sqrt(rr) <= tol) { status = RSIM_OK; break; }
+      rho_new = r0s - omega * r0t;
       if (omega == 0.0 || rho_new == 0.0 || !isfinite(rho_new)) { status = RSIM_ENUM; break; }
       cur ^= 1;
     }
-    if (it > maxit) { it = maxit; status = fixed ? RSIM_OK : RSIM_ENOCONV; }
+    if (it > maxit) {  // iteration cap: residual of the last iterate (one more reduction)
+      it = maxit;
+      double val[1] = {0.0};
+      if (valid) {
+        double rv[B];
+#pragma unroll
+        for (int e = 0; e < B; ++e) rv[e] = Vo[O_R * BP + e];
+        val[0] = rsim::blk::rowdot<B>(rv, rv);
+      }
+      reduce(std::integral_constant<int, 1>{}, val, res);
+      relres = sqrt(res[0]) / bnorm;
+      status = (fixed || sqrt(res[0]) <= tol) ? RSIM_OK : RSIM_ENOCONV;
+    }
     it_total += it;
     if (!(neu && (status == RSIM_ENUM || status == RSIM_ENOCONV))) break;
     }
@@ -453,6 +522,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   if (valid)
 #pragma unroll
     for (int e = 0; e < B; ++e) a.x[l * B + e] = xr[e];
+  if (a.trace) {
+    if (valid) atomicAdd(&tcr[6], 1ull);
+    __syncthreads();
+    if (tid < 8) atomicAdd(&a.trace[8 + rank * 8 + tid], tcr[tid]);
+  }
   if (rank == 0 && tid == 0) {
     a.dsc->lin_iters = it;
     a.dsc->lin_relres = relres;
@@ -463,8 +537,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
 
 size_t smem_bytes(int B, int NS, bool MS, int LRC) {
   const size_t R = (size_t)1 << LRC;
-  size_t b = 7 * R * B * sizeof(double) + R * sizeof(int2) + NNCMAX * (B * B * sizeof(double) + sizeof(int32_t));
-  if (MS) b += NS * R * B * B * sizeof(double) + NS * R * sizeof(int32_t);
+  const size_t BP = (B == 3) ? 4 : B;
+  size_t b = 9 * R * BP * sizeof(double) + R * sizeof(int2) + NNCMAX * (B * B * sizeof(double) + sizeof(const double*));
+  if (MS) b += NS * R * B * B * sizeof(double);
   return b;
 }
 
@@ -509,18 +584,27 @@ int launch_t(rsim_gpu_ctx* c, const DArgs& a, int G, int TPB, size_t smem, bool*
   return RSIM_OK;
 }
 
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return (e && *e) ? std::atoi(e) : dflt;
+}
+
 template <int B, int NS>
 int launch_bn(rsim_gpu_ctx* c, DArgs& a, int G, int TPB, bool* ok) {
+  static const int tmin = env_int("RSIM_DSM_MINT", 0);  // experiments: smallest MAXT variant to use
+  const int sel = TPB < tmin ? tmin : TPB;  // template variant (blockDim stays TPB)
   const size_t with_m = smem_bytes(B, NS, true, a.LRC), without = smem_bytes(B, NS, false, a.LRC);
   const size_t cap = 220 * 1024;
   if (with_m <= cap) {
-    int r = TPB <= 512 ? launch_t<B, NS, true, 512>(c, a, G, TPB, with_m, ok)
-                       : launch_t<B, NS, true, 1024>(c, a, G, TPB, with_m, ok);
+    int r = sel <= 256   ? launch_t<B, NS, true, 256>(c, a, G, TPB, with_m, ok)
+            : sel <= 512 ? launch_t<B, NS, true, 512>(c, a, G, TPB, with_m, ok)
+                         : launch_t<B, NS, true, 1024>(c, a, G, TPB, with_m, ok);
     if (r != RSIM_OK || *ok) return r;
   }
   if (without <= cap)
-    return TPB <= 512 ? launch_t<B, NS, false, 512>(c, a, G, TPB, without, ok)
-                      : launch_t<B, NS, false, 1024>(c, a, G, TPB, without, ok);
+    return sel <= 256   ? launch_t<B, NS, false, 256>(c, a, G, TPB, without, ok)
+           : sel <= 512 ? launch_t<B, NS, false, 512>(c, a, G, TPB, without, ok)
+                        : launch_t<B, NS, false, 1024>(c, a, G, TPB, without, ok);
   *ok = false;
   return RSIM_OK;
 }

@@ -3,7 +3,7 @@ os.environ["RSIM_KTRACE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2008_01539_b200 as pkg
-for cfg, nA in ((1, 250), (2, 1400), (2, 3000)):
+for cfg, nA in ((1, 250), (2, 1400), (2, 3000), (2, 6000)):
     case = pkg.Case(cfg)
     sim = pkg.GpuSimulator(case)
     rng = np.random.default_rng(0)
@@ -17,5 +17,5 @@ for cfg, nA in ((1, 250), (2, 1400), (2, 3000)):
     sim.linear_solve(o); sim.stats()
     sim.L.rsim_gpu_ktrace(sim._ctx, buf)
     v = [buf[k] / 100 for k in range(8)]
-    names = ["spmvV", "redV", "spmvT", "redT", "xr", "redXR", "-", "loophead"]
+    names = ["spmvV", "redV", "spmvT", "redT", "xr", "redXR", "in_csync", "loophead"]
     print(cfg, nA, {n: round(x) for n, x in zip(names, v)}, "total/iter cycles", round(sum(v)))
