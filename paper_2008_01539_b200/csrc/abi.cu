@@ -165,7 +165,8 @@ int rsim_gpu_counters(rsim_gpu_ctx* c, int64_t* out5, int32_t reset) {
 }
 
 int rsim_gpu_create(rsim_gpu_ctx** out, const rsim_graph_desc* g, const rsim_fluid_params* f) {
-  if (!out || !g || !f || f->kind < 1 || f->kind > 3 || g->nx < 1 || g->ny < 1 || g->nz < 1) {
+  if (!out || !g || !f || f->kind < 1 || f->kind > 3 || g->nx < 1 || g->ny < 1 || g->nz < 1 ||
+      (int64_t)g->nx * g->ny * g->nz >= ((int64_t)1 << 31)) {  // cell ids are int32 (CSR, act, g2l)
     rsim_set_error("rsim_gpu_create: bad argument");
     return RSIM_EARG;
   }

@@ -143,44 +143,177 @@ __device__ __forceinline__ bool a_new(uint8_t f, int mode, bool expand, uint8_t 
   }
 }
 
-// One dilation round bit_out(i) = bit_in(i) | OR_j bit_in(j) (skipped when the
-// device decided to shrink).  With COUNT the same pass also counts A_new per
-// 256-cell tile (compaction pass 1), which needs only the cell's own bits.
-template <bool COUNT>
-__global__ void __launch_bounds__(256) k_dilate(Geo g, uint8_t* __restrict__ flags, uint8_t bit_in, uint8_t bit_out,
-                                                const DevScalars* __restrict__ dsc, SetMode M, int do_dilate,
-                                                int32_t* __restrict__ tile_cnt) {
-  const bool ex = decide_expand(M, dsc);
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  bool keep = false;
-  if (i < g.n) {
-    uint8_t f = flags[i];
-    if (do_dilate && ((M.mode == MODE_DEVICE || M.mode == MODE_DD) ? ex : true)) {
-      bool v = (f & bit_in) != 0;
-      if (!v) each_nbr(g, i, [&](int64_t j) { if (flags[j] & bit_in) v = true; });
-      f = v ? (uint8_t)(f | bit_out) : (uint8_t)(f & ~bit_out);
-      flags[i] = f;
-    }
-    if (COUNT) keep = a_new(f, M.mode, ex, M.dbit);
-  }
-  if (COUNT) {
-    const int cnt = __syncthreads_count(keep);
-    if (threadIdx.x == 0) tile_cnt[blockIdx.x] = cnt;
+// The same predicate on 4 flag bytes at once: bit 0 of every byte of the result.
+__device__ __forceinline__ uint32_t bitpos(uint32_t bit) { return (uint32_t)__ffs((int)bit) - 1u; }
+__device__ __forceinline__ uint32_t lanes(uint32_t w, uint32_t bit) { return (w >> bitpos(bit)) & 0x01010101u; }
+__device__ __forceinline__ uint32_t a_new4(uint32_t w, int mode, bool expand, uint8_t dbit) {
+  const uint32_t A = lanes(w, F_A);
+  const uint32_t grow = A | lanes(w, dbit);
+  const uint32_t shrink = (A & lanes(w, F_FLAG)) | lanes(w, F_PIN);
+  switch (mode) {
+    case MODE_KEEP: return A;
+    case MODE_SHRINK: return shrink;
+    case MODE_EXPAND:
+    case MODE_DD: return grow;
+    default: return expand ? grow : shrink;
   }
 }
 
-// Compaction pass 2: exclusive scan of the tile counts (one block, strips of
-// consecutive tiles per thread).  Also publishes the decision + n_A and
-// resets the counters of pass 3.
+// 4 consecutive cells per thread, 1024-cell tiles per 256-thread block.  With
+// nx % 4 == 0 (every configuration) the 4 cells share one x-row and are
+// processed as one 32-bit word of flag bytes: the ±x neighbours are byte
+// shifts (plus one byte of the adjacent words), ±y/±z are the words one row /
+// one plane away — no per-cell index arithmetic, coalesced 4-byte accesses.
+// Otherwise a per-cell path with the same semantics.
+constexpr int K7T = 256;
+constexpr int K7TILE = 4 * K7T;
+
+struct Geo4 {
+  int32_t nx, ny, nz;
+  int64_t n, nw;  // cells, 4-cell words
+  int32_t wrow;   // words per x-row (nx / 4, vec4 only)
+  int64_t wplane; // words per plane
+  bool d3, has_nnc, vec4;
+  const int32_t *nptr, *nnbr;
+};
+
+__host__ Geo4 geo4(const rsim_gpu_ctx* c) {
+  Geo4 g;
+  g.nx = c->nx; g.ny = c->ny; g.nz = c->nz;
+  g.n = c->n;
+  g.nw = (c->n + 3) / 4;
+  g.vec4 = (c->nx % 4) == 0;
+  g.wrow = c->nx / 4;
+  g.wplane = (int64_t)g.wrow * c->ny;
+  g.d3 = c->d3; g.has_nnc = c->has_nnc;
+  g.nptr = c->nptr; g.nnbr = c->nnbr;
+  return g;
+}
+
+// OR over the graph neighbours of the 4 cells of word t of per-byte bit-0
+// lanes produced by `L(word index)`; `edge` is the lane value for a missing
+// (off-grid) neighbour; `comb` combines (OR for dilation, AND for "all keep").
+template <class LF, class CF>
+__device__ __forceinline__ uint32_t nbr_lanes4(const Geo4& g, int64_t t, uint32_t self, uint32_t edge, LF&& L,
+                                                CF&& comb) {
+  const uint32_t row = (uint32_t)t / (uint32_t)g.wrow;  // n < 2^31 (checked at create)
+  const int32_t xw = (int32_t)((uint32_t)t - row * (uint32_t)g.wrow);
+  const uint32_t iz_ = row / (uint32_t)g.ny;
+  const int32_t iy = (int32_t)(row - iz_ * (uint32_t)g.ny);
+  const int32_t iz = (int32_t)iz_;
+  uint32_t acc;
+  // -x / +x: byte shifts, the outermost byte from the adjacent word (or the edge value)
+  const uint32_t lft = (self << 8) | (xw > 0 ? (L(t - 1) >> 24) : (edge & 0xFFu));
+  const uint32_t rgt = (self >> 8) | (xw < g.wrow - 1 ? ((L(t + 1) & 0xFFu) << 24) : (edge & 0xFF000000u));
+  acc = comb(lft, rgt);
+  acc = comb(acc, iy > 0 ? L(t - g.wrow) : edge);
+  acc = comb(acc, iy < g.ny - 1 ? L(t + g.wrow) : edge);
+  if (g.d3) {
+    acc = comb(acc, iz > 0 ? L(t - g.wplane) : edge);
+    acc = comb(acc, iz < g.nz - 1 ? L(t + g.wplane) : edge);
+  }
+  return acc;
+}
+
+// graph neighbours of one cell (scalar path / NNC), 32-bit coordinates
+template <class F>
+__device__ __forceinline__ void each_nbr32(const Geo4& g, int64_t i, F&& f) {
+  const uint32_t nxy = (uint32_t)g.nx * (uint32_t)g.ny;
+  const int32_t iz = (int32_t)((uint32_t)i / nxy);
+  const int32_t rem = (int32_t)((uint32_t)i - (uint32_t)iz * nxy);
+  const int32_t iy = rem / g.nx, ix = rem - iy * g.nx;
+  if (g.d3 && iz > 0) f(i - nxy);
+  if (iy > 0) f(i - g.nx);
+  if (ix > 0) f(i - 1);
+  if (ix < g.nx - 1) f(i + 1);
+  if (iy < g.ny - 1) f(i + g.nx);
+  if (g.d3 && iz < g.nz - 1) f(i + nxy);
+  if (g.has_nnc) {
+    const int32_t q0 = __ldg(&g.nptr[i]), q1 = __ldg(&g.nptr[i + 1]);
+    for (int32_t q = q0; q < q1; ++q) f((int64_t)__ldg(&g.nnbr[q]));
+  }
+}
+
+__device__ __forceinline__ int block_sum256(int v, int* sh8) {
+  v = __reduce_add_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0) sh8[threadIdx.x >> 5] = v;
+  __syncthreads();
+  int s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += sh8[k];
+  return s;
+}
+
+// One dilation round bit_out(i) = bit_in(i) | OR_j bit_in(j) (skipped when the
+// device decided to shrink).  With COUNT the same pass also counts A_new per
+// 1024-cell tile (compaction pass 1), which needs only the cell's own bits.
+template <bool COUNT>
+__global__ void __launch_bounds__(K7T) k_dilate(Geo4 g, uint8_t* __restrict__ flags, uint8_t bit_in, uint8_t bit_out,
+                                                const DevScalars* __restrict__ dsc, SetMode M, int do_dilate,
+                                                int32_t* __restrict__ tile_cnt) {
+  __shared__ int sh8[8];
+  const bool ex = decide_expand(M, dsc);
+  const bool dil = do_dilate && ((M.mode == MODE_DEVICE || M.mode == MODE_DD) ? ex : true);
+  const int64_t t = (int64_t)blockIdx.x * K7T + threadIdx.x;
+  int cnt = 0;
+  if (g.vec4) {
+    if (t < g.nw) {
+      uint32_t* fw = reinterpret_cast<uint32_t*>(flags);
+      uint32_t w = fw[t];
+      if (dil) {
+        const uint32_t in = lanes(w, bit_in);
+        auto L = [&](int64_t u) { return lanes(__ldcg(&fw[u]), bit_in); };
+        uint32_t out = in | nbr_lanes4(g, t, in, 0u, L, [](uint32_t x, uint32_t y) { return x | y; });
+        if (g.has_nnc) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int64_t i = 4 * t + k;
+            const int32_t q0 = __ldg(&g.nptr[i]), q1 = __ldg(&g.nptr[i + 1]);
+            for (int32_t q = q0; q < q1; ++q)
+              if (flags[__ldg(&g.nnbr[q])] & bit_in) out |= 1u << (8 * k);
+          }
+        }
+        w = (w & ~(0x01010101u * bit_out)) | (out * bit_out);
+        fw[t] = w;
+      }
+      if (COUNT) cnt = __popc(a_new4(w, M.mode, ex, M.dbit));
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t i = 4 * t + k;
+      if (i >= g.n) break;
+      uint8_t f = flags[i];
+      if (dil) {
+        bool v = (f & bit_in) != 0;
+        if (!v) each_nbr32(g, i, [&](int64_t j) { if (flags[j] & bit_in) v = true; });
+        f = v ? (uint8_t)(f | bit_out) : (uint8_t)(f & ~bit_out);
+        flags[i] = f;
+      }
+      if (COUNT) cnt += a_new(f, M.mode, ex, M.dbit) ? 1 : 0;
+    }
+  }
+  if (COUNT) {
+    const int s = block_sum256(cnt, sh8);
+    if (threadIdx.x == 0) tile_cnt[blockIdx.x] = s;
+  }
+}
+
+// Compaction pass 2: exclusive scan of the tile counts (one block; counts
+// staged through shared memory, strips of consecutive tiles per thread).
+// Also publishes the decision + n_A and resets the counters of pass 3.
 __global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t* __restrict__ cnt, int32_t* __restrict__ off,
                                                       int32_t ntiles, DevScalars* dsc, SetMode M) {
+  extern __shared__ int32_t scnt[];
   __shared__ int32_t wsum[32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int32_t k = threadIdx.x; k < ntiles; k += 1024) scnt[k] = cnt[k];
+  __syncthreads();
   const int32_t per = (ntiles + 1023) / 1024;
   const int32_t b0 = threadIdx.x * per;
   int32_t tot = 0;
   for (int32_t k = 0; k < per; ++k)
-    if (b0 + k < ntiles) tot += cnt[b0 + k];
+    if (b0 + k < ntiles) tot += scnt[b0 + k];
   int32_t x = tot;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -202,9 +335,12 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t* __restrict__
   int32_t run = (w > 0 ? wsum[w - 1] : 0) + x - tot;
   for (int32_t k = 0; k < per; ++k)
     if (b0 + k < ntiles) {
-      off[b0 + k] = run;
-      run += cnt[b0 + k];
+      const int32_t c = scnt[b0 + k];
+      scnt[b0 + k] = run;
+      run += c;
     }
+  __syncthreads();
+  for (int32_t k = threadIdx.x; k < ntiles; k += 1024) off[k] = scnt[k];
   if (threadIdx.x == 1023) {
     dsc->nA = wsum[31];
     dsc->expand = decide_expand(M, dsc) ? 1 : 0;
@@ -213,52 +349,106 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t* __restrict__
   }
 }
 
-// Compaction pass 3 (one cell per thread, 256-cell tiles): A_new, V_B,
-// V_T/labels, g2l, sorted active list (warp ballot + block scan).
-__global__ void __launch_bounds__(256) k_scatter(Geo g, const uint8_t* __restrict__ fin, uint8_t* __restrict__ fout,
+// Compaction pass 3 (4 cells per thread, 1024-cell tiles): A_new, V_B,
+// V_T/labels, g2l, sorted active list (block scan of the per-thread counts).
+__global__ void __launch_bounds__(K7T) k_scatter(Geo4 g, const uint8_t* __restrict__ fin, uint8_t* __restrict__ fout,
                                                  SetMode M, int32_t round, DevScalars* dsc,
                                                  const int32_t* __restrict__ tile_off, int32_t* __restrict__ act,
                                                  int32_t* __restrict__ g2l, int32_t* __restrict__ label) {
-  __shared__ int32_t wcnt[8];
+  __shared__ int32_t wpre[8];
+  __shared__ int sh8[8];
   const bool ex = decide_expand(M, dsc);
-  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int64_t t = (int64_t)blockIdx.x * K7T + threadIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint8_t f = 0;
-  bool keep = false;
-  if (i < g.n) {
-    f = fin[i];
-    keep = a_new(f, M.mode, ex, M.dbit);
+  uint32_t keep = 0, bnd = 0, f4 = 0;
+  if (g.vec4) {
+    if (t < g.nw) {
+      const uint32_t* fw = reinterpret_cast<const uint32_t*>(fin);
+      f4 = fw[t];
+      keep = a_new4(f4, M.mode, ex, M.dbit);
+      if (keep) {
+        auto L = [&](int64_t u) { return a_new4(__ldg(&fw[u]), M.mode, ex, M.dbit); };
+        const uint32_t all = nbr_lanes4(g, t, keep, 0x01010101u, L, [](uint32_t x, uint32_t y) { return x & y; });
+        bnd = keep & ~all & 0x01010101u;
+        if (g.has_nnc)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (!((keep >> (8 * k)) & 1u) || ((bnd >> (8 * k)) & 1u)) continue;
+            const int64_t i = 4 * t + k;
+            const int32_t q0 = __ldg(&g.nptr[i]), q1 = __ldg(&g.nptr[i + 1]);
+            for (int32_t q = q0; q < q1; ++q)
+              if (!a_new(fin[__ldg(&g.nnbr[q])], M.mode, ex, M.dbit)) { bnd |= 1u << (8 * k); break; }
+          }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t i = 4 * t + k;
+      if (i >= g.n) break;
+      const uint8_t f = fin[i];
+      f4 |= (uint32_t)f << (8 * k);
+      if (a_new(f, M.mode, ex, M.dbit)) {
+        keep |= 1u << (8 * k);
+        bool b = false;
+        each_nbr32(g, i, [&](int64_t j) { if (!a_new(fin[j], M.mode, ex, M.dbit)) b = true; });
+        if (b) bnd |= 1u << (8 * k);
+      }
+    }
   }
-  const unsigned bal = __ballot_sync(0xffffffffu, keep);
-  if (lane == 0) wcnt[w] = __popc(bal);
+  // block exclusive scan of the per-thread counts (0..4)
+  const int c = __popc(keep);
+  int x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wpre[w] = x;
   __syncthreads();
-  int pre = 0;
-  for (int k = 0; k < w; ++k) pre += wcnt[k];
-  int nb = 0, nnew = 0;
-  if (i < g.n) {
-    uint8_t o = (uint8_t)(f & (F_PIN | F_T));
-    if (keep) {
-      bool bnd = false;
-      each_nbr(g, i, [&](int64_t j) { if (!a_new(fin[j], M.mode, ex, M.dbit)) bnd = true; });
+  int pre = x - c;
+  for (int k = 0; k < w; ++k) pre += wpre[k];
+  int32_t pos = tile_off[blockIdx.x] + pre;
+  int nnew = 0;
+  const int64_t i0 = 4 * t;
+  int32_t gl[4];
+  uint32_t out = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t f = (f4 >> (8 * k)) & 0xFFu;
+    uint32_t o = f & (F_PIN | F_T);
+    gl[k] = -1;
+    if ((keep >> (8 * k)) & 1u) {
       o |= F_A;
-      if (bnd) { o |= F_B; nb = 1; }
+      if ((bnd >> (8 * k)) & 1u) o |= F_B;
       if (M.mode == MODE_DD) {
-        if (!(f & F_T)) { label[i] = round; nnew = 1; }
+        if (!(f & F_T)) { label[i0 + k] = round; ++nnew; }
         o |= F_T;
       }
-      const int pos = tile_off[blockIdx.x] + pre + __popc(bal & ((1u << lane) - 1u));
-      act[pos] = (int32_t)i;
-      g2l[i] = pos;
-    } else {
-      g2l[i] = -1;
+      act[pos] = (int32_t)(i0 + k);
+      gl[k] = pos++;
     }
-    fout[i] = o;
+    out |= o << (8 * k);
   }
-  nb = __reduce_add_sync(0xffffffffu, nb);
-  nnew = __reduce_add_sync(0xffffffffu, nnew);
-  if (lane == 0) {
+  if (g.vec4) {
+    if (t < g.nw) {
+      reinterpret_cast<uint32_t*>(fout)[t] = out;
+      reinterpret_cast<int4*>(g2l)[t] = make_int4(gl[0], gl[1], gl[2], gl[3]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (i0 + k < g.n) {
+        fout[i0 + k] = (uint8_t)((out >> (8 * k)) & 0xFFu);
+        g2l[i0 + k] = gl[k];
+      }
+  }
+  const int nb = block_sum256(__popc(bnd), sh8);
+  __syncthreads();
+  const int nn = block_sum256(nnew, sh8);
+  if (threadIdx.x == 0) {
     if (nb) atomicAdd(&dsc->nB, nb);
-    if (nnew) atomicAdd(&dsc->n_new, nnew);
+    if (nn) atomicAdd(&dsc->n_new, nn);
   }
 }
 
@@ -452,33 +642,50 @@ int launch_threshold(rsim_gpu_ctx* c, double eps) {
 
 // Full set update: [m-1 dilation rounds] + [round m fused with the tile count]
 // + scan + scatter.  4 launches for m = 2, no host round trip.
+// single-block tile scan (counts staged in dynamic shared memory)
+static int launch_scan_tiles(rsim_gpu_ctx* c, int64_t ntiles, const SetMode& M) {
+  const size_t smem = (size_t)ntiles * sizeof(int32_t);
+  if (smem > 220 * 1024) {
+    rsim_set_error("set update: grid too large for the single-block tile scan");
+    return RSIM_EARG;
+  }
+  static size_t attr = 48 * 1024;
+  if (smem > attr) {
+    RSIM_CUDA(cudaFuncSetAttribute(k_scan_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    attr = 220 * 1024;
+  }
+  k_scan_tiles<<<1, 1024, smem, c->stream>>>(c->tile_cnt, c->tile_off, (int32_t)ntiles, c->dsc, M);
+  c->launches++;
+  return RSIM_OK;
+}
+
 int launch_set_update(rsim_gpu_ctx* c, int mode, int round, double eps, int m, int shrink_locked, int force_expand,
                       int do_dilate) {
-  Geo g = geo(c);
+  Geo4 g = geo4(c);
   SetMode M;
   M.mode = mode;
   M.dbit = (m % 2 == 0) ? F_D0 : F_D1;
   M.eps = eps;
   M.shrink_locked = shrink_locked;
   M.force_expand = force_expand;
-  const int64_t ntiles = nblk(c->n, 256);
+  const int64_t ntiles = nblk(c->n, K7TILE);
   const int rounds = do_dilate ? m : 0;
   for (int r = 0; r + 1 < rounds; ++r) {
     uint8_t bin = (r % 2 == 0) ? F_D0 : F_D1, bout = (r % 2 == 0) ? F_D1 : F_D0;
-    k_dilate<false><<<ntiles, 256, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, 1, c->tile_cnt);
+    k_dilate<false><<<ntiles, K7T, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, 1, c->tile_cnt);
     c->launches++;
   }
   {
     const int r = rounds - 1;
     uint8_t bin = (r % 2 == 0) ? F_D0 : F_D1, bout = (r % 2 == 0) ? F_D1 : F_D0;
-    k_dilate<true><<<ntiles, 256, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, rounds > 0 ? 1 : 0,
+    k_dilate<true><<<ntiles, K7T, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, rounds > 0 ? 1 : 0,
                                                   c->tile_cnt);
     c->launches++;
   }
-  k_scan_tiles<<<1, 1024, 0, c->stream>>>(c->tile_cnt, c->tile_off, (int32_t)ntiles, c->dsc, M);
-  k_scatter<<<ntiles, 256, 0, c->stream>>>(g, c->flags, c->flags_alt, M, round, c->dsc, c->tile_off, c->act_buf,
+  { const int r = launch_scan_tiles(c, ntiles, M); if (r != RSIM_OK) return r; }
+  k_scatter<<<ntiles, K7T, 0, c->stream>>>(g, c->flags, c->flags_alt, M, round, c->dsc, c->tile_off, c->act_buf,
                                            c->g2l, c->label);
-  c->launches += 2;
+  c->launches++;
   RSIM_CUDA(cudaGetLastError());
   std::swap(c->flags, c->flags_alt);
   c->act = c->act_buf;
@@ -545,8 +752,8 @@ int launch_dd_partition(rsim_gpu_ctx* c, int32_t n_sub, int32_t* sizes) {
   for (int sel = 0; sel < 2; ++sel) {
     for (int k = 0; k < n_sub; ++k) {
       k_dd_count<<<ntiles, 256, 0, c->stream>>>(g, c->label, k, sel, c->tile_cnt);
-      k_scan_tiles<<<1, 1024, 0, c->stream>>>(c->tile_cnt, c->tile_off, (int32_t)ntiles, c->dsc, SetMode{MODE_KEEP, 0, 0.0, 1, 0});
-      c->launches += 2;
+      { const int r = launch_scan_tiles(c, ntiles, SetMode{MODE_KEEP, 0, 0.0, 1, 0}); if (r != RSIM_OK) return r; }
+      c->launches += 1;
       RSIM_CUDA(cudaMemcpyAsync(&(sel ? cnt_halo : cnt_sub)[k], &c->dsc->nA, sizeof(int32_t),
                                 cudaMemcpyDeviceToHost, c->stream));
       RSIM_CUDA(cudaStreamSynchronize(c->stream));
@@ -571,9 +778,9 @@ int launch_dd_partition(rsim_gpu_ctx* c, int32_t n_sub, int32_t* sizes) {
     for (int k = 0; k < n_sub; ++k) {
       int32_t* out = sel ? d.halo_cells + d.halo_off[k] : d.sub_cells + d.sub_off[k];
       k_dd_count<<<ntiles, 256, 0, c->stream>>>(g, c->label, k, sel, c->tile_cnt);
-      k_scan_tiles<<<1, 1024, 0, c->stream>>>(c->tile_cnt, c->tile_off, (int32_t)ntiles, c->dsc, SetMode{MODE_KEEP, 0, 0.0, 1, 0});
+      { const int r = launch_scan_tiles(c, ntiles, SetMode{MODE_KEEP, 0, 0.0, 1, 0}); if (r != RSIM_OK) return r; }
       k_dd_scatter<<<ntiles, 256, 0, c->stream>>>(g, c->label, k, sel, c->tile_off, out);
-      c->launches += 3;
+      c->launches += 2;
     }
   // clear the localized g2l (every cell -1) before per-subdomain selection
   RSIM_CUDA(cudaMemsetAsync(c->g2l, 0xff, sizeof(int32_t) * c->n, c->stream));
