@@ -203,7 +203,12 @@ int rsim_gpu_create(rsim_gpu_ctx** out, const rsim_graph_desc* g, const rsim_flu
   TRY(dalloc(&c->act_buf, n)); TRY(dalloc(&c->g2l, n)); TRY(dalloc(&c->label, n));
   TRY(dalloc(&c->list_buf, n));
   TRY(dalloc(&c->dp, n)); TRY(dalloc(&c->last_dp, n));
-  TRY(dalloc(&c->tile_cnt, nchunks)); TRY(dalloc(&c->tile_off, nchunks));
+  {  // compaction tiles: K7 uses one tile per (x-row, 1024-cell segment), K8 one per 2048 cells
+    const int64_t wrow = (g->nx + 3) / 4, bs = wrow >= 256 ? 256 : ((wrow + 31) / 32) * 32;
+    const int64_t k7 = (int64_t)g->ny * g->nz * ((wrow + bs - 1) / bs);
+    const int64_t nt = (k7 > nchunks ? k7 : nchunks) + 1;
+    TRY(dalloc(&c->tile_cnt, nt)); TRY(dalloc(&c->tile_off, nt));
+  }
   TRY(dalloc(&c->ell_col, c->nslot * n)); TRY(dalloc(&c->ell_val, c->nslot * n * b * b));
   TRY(dalloc(&c->nnc_lcol, c->nnc_total)); TRY(dalloc(&c->nnc_val, c->nnc_total * b * b));
   TRY(dalloc(&c->F_raw, n * b)); TRY(dalloc(&c->rhs, n * b));
@@ -577,8 +582,7 @@ int rsim_gpu_checkpoint(rsim_gpu_ctx* c, int32_t restore) {
 int rsim_gpu_support_active(rsim_gpu_ctx* c, double eps, int32_t m, rsim_gpu_stats* st) {
   c->last_eps = eps;
   rsim_phase_begin(c, 0);
-  TRY(launch_set_reset(c, 0));
-  TRY(launch_seed_support(c, eps));
+  TRY(launch_reset_seed(c, eps));
   TRY(launch_set_update(c, MODE_EXPAND, 0, eps, m, 0, 1, 1));
   rsim_phase_end(c);
   c->pending_nA = true;

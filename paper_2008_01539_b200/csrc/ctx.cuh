@@ -160,6 +160,7 @@ int launch_dd_select(rsim_gpu_ctx* c, int32_t k);
 int launch_dd_skip(rsim_gpu_ctx* c, int32_t k);
 int launch_categories(rsim_gpu_ctx* c, uint8_t* dev_out);
 int launch_seed_support(rsim_gpu_ctx* c, double eps);
+int launch_reset_seed(rsim_gpu_ctx* c, double eps);
 int launch_state_from_dp(rsim_gpu_ctx* c, double p_hi, double scale);
 
 // ---- device helpers ------------------------------------------------------------

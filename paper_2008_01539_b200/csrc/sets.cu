@@ -159,20 +159,20 @@ __device__ __forceinline__ uint32_t a_new4(uint32_t w, int mode, bool expand, ui
   }
 }
 
-// 4 consecutive cells per thread, 1024-cell tiles per 256-thread block.  With
-// nx % 4 == 0 (every configuration) the 4 cells share one x-row and are
-// processed as one 32-bit word of flag bytes: the ±x neighbours are byte
-// shifts (plus one byte of the adjacent words), ±y/±z are the words one row /
-// one plane away — no per-cell index arithmetic, coalesced 4-byte accesses.
-// Otherwise a per-cell path with the same semantics.
-constexpr int K7T = 256;
-constexpr int K7TILE = 4 * K7T;
-
+// K7 work mapping: block (row, seg) covers x-row `row` (= iy + ny*iz) and
+// 4-cell groups [seg*bs, (seg+1)*bs) of it, thread = 4 consecutive cells.  The
+// tile of the compaction is the block, tile id = row*nseg + seg (global cell
+// order).  With nx % 4 == 0 (every configuration) a group is one 32-bit word
+// of flag bytes: ±x neighbours are byte shifts (plus one byte of the adjacent
+// words), ±y/±z the words one row / one plane away — coalesced 4-byte
+// accesses, no per-cell index arithmetic.  Otherwise a per-cell path with the
+// same semantics and the same tiles.
 struct Geo4 {
   int32_t nx, ny, nz;
-  int64_t n, nw;  // cells, 4-cell words
-  int32_t wrow;   // words per x-row (nx / 4, vec4 only)
-  int64_t wplane; // words per plane
+  int64_t n;
+  int32_t wrow;    // 4-cell groups per x-row
+  int64_t wplane;  // groups per plane (vec4)
+  int32_t bs, nseg;
   bool d3, has_nnc, vec4;
   const int32_t *nptr, *nnbr;
 };
@@ -181,47 +181,58 @@ __host__ Geo4 geo4(const rsim_gpu_ctx* c) {
   Geo4 g;
   g.nx = c->nx; g.ny = c->ny; g.nz = c->nz;
   g.n = c->n;
-  g.nw = (c->n + 3) / 4;
   g.vec4 = (c->nx % 4) == 0;
-  g.wrow = c->nx / 4;
+  g.wrow = (c->nx + 3) / 4;
   g.wplane = (int64_t)g.wrow * c->ny;
+  g.bs = g.wrow >= 256 ? 256 : ((g.wrow + 31) / 32) * 32;
+  g.nseg = (g.wrow + g.bs - 1) / g.bs;
   g.d3 = c->d3; g.has_nnc = c->has_nnc;
   g.nptr = c->nptr; g.nnbr = c->nnbr;
   return g;
 }
+__host__ dim3 k7_grid(const Geo4& g) { return dim3((unsigned)(g.ny * g.nz), (unsigned)g.nseg, 1); }
+__host__ int64_t k7_tiles(const Geo4& g) { return (int64_t)g.ny * g.nz * g.nseg; }
 
-// OR over the graph neighbours of the 4 cells of word t of per-byte bit-0
-// lanes produced by `L(word index)`; `edge` is the lane value for a missing
-// (off-grid) neighbour; `comb` combines (OR for dilation, AND for "all keep").
+struct Pos4 {
+  int32_t row, iy, iz, xw;  // x-row, its y/z, group index in the row
+  int64_t t;                // vec4: word index
+  bool ok;
+};
+__device__ __forceinline__ Pos4 pos4(const Geo4& g) {
+  Pos4 p;
+  p.row = blockIdx.x;
+  p.iz = p.row / g.ny;
+  p.iy = p.row - p.iz * g.ny;
+  p.xw = blockIdx.y * g.bs + threadIdx.x;
+  p.ok = p.xw < g.wrow;
+  p.t = (int64_t)p.row * g.wrow + p.xw;
+  return p;
+}
+__device__ __forceinline__ int32_t tile_id(const Geo4& g) { return blockIdx.x * g.nseg + blockIdx.y; }
+
+// Combine over the graph neighbours of the 4 cells of group p of per-byte
+// bit-0 lanes produced by `L(word index)`; `edge` is the lane value of a
+// missing (off-grid) neighbour; `comb` is OR (dilation) or AND ("all keep").
 template <class LF, class CF>
-__device__ __forceinline__ uint32_t nbr_lanes4(const Geo4& g, int64_t t, uint32_t self, uint32_t edge, LF&& L,
+__device__ __forceinline__ uint32_t nbr_lanes4(const Geo4& g, const Pos4& p, uint32_t self, uint32_t edge, LF&& L,
                                                 CF&& comb) {
-  const uint32_t row = (uint32_t)t / (uint32_t)g.wrow;  // n < 2^31 (checked at create)
-  const int32_t xw = (int32_t)((uint32_t)t - row * (uint32_t)g.wrow);
-  const uint32_t iz_ = row / (uint32_t)g.ny;
-  const int32_t iy = (int32_t)(row - iz_ * (uint32_t)g.ny);
-  const int32_t iz = (int32_t)iz_;
-  uint32_t acc;
-  // -x / +x: byte shifts, the outermost byte from the adjacent word (or the edge value)
-  const uint32_t lft = (self << 8) | (xw > 0 ? (L(t - 1) >> 24) : (edge & 0xFFu));
-  const uint32_t rgt = (self >> 8) | (xw < g.wrow - 1 ? ((L(t + 1) & 0xFFu) << 24) : (edge & 0xFF000000u));
-  acc = comb(lft, rgt);
-  acc = comb(acc, iy > 0 ? L(t - g.wrow) : edge);
-  acc = comb(acc, iy < g.ny - 1 ? L(t + g.wrow) : edge);
+  const int64_t t = p.t;
+  const uint32_t lft = (self << 8) | (p.xw > 0 ? (L(t - 1) >> 24) : (edge & 0xFFu));
+  const uint32_t rgt = (self >> 8) | (p.xw < g.wrow - 1 ? ((L(t + 1) & 0xFFu) << 24) : (edge & 0xFF000000u));
+  uint32_t acc = comb(lft, rgt);
+  acc = comb(acc, p.iy > 0 ? L(t - g.wrow) : edge);
+  acc = comb(acc, p.iy < g.ny - 1 ? L(t + g.wrow) : edge);
   if (g.d3) {
-    acc = comb(acc, iz > 0 ? L(t - g.wplane) : edge);
-    acc = comb(acc, iz < g.nz - 1 ? L(t + g.wplane) : edge);
+    acc = comb(acc, p.iz > 0 ? L(t - g.wplane) : edge);
+    acc = comb(acc, p.iz < g.nz - 1 ? L(t + g.wplane) : edge);
   }
   return acc;
 }
 
-// graph neighbours of one cell (scalar path / NNC), 32-bit coordinates
+// graph neighbours of cell (ix, iy, iz) = i (scalar path / NNC)
 template <class F>
-__device__ __forceinline__ void each_nbr32(const Geo4& g, int64_t i, F&& f) {
-  const uint32_t nxy = (uint32_t)g.nx * (uint32_t)g.ny;
-  const int32_t iz = (int32_t)((uint32_t)i / nxy);
-  const int32_t rem = (int32_t)((uint32_t)i - (uint32_t)iz * nxy);
-  const int32_t iy = rem / g.nx, ix = rem - iy * g.nx;
+__device__ __forceinline__ void each_nbr_xyz(const Geo4& g, int64_t i, int32_t ix, int32_t iy, int32_t iz, F&& f) {
+  const int64_t nxy = (int64_t)g.nx * g.ny;
   if (g.d3 && iz > 0) f(i - nxy);
   if (iy > 0) f(i - g.nx);
   if (ix > 0) f(i - 1);
@@ -234,68 +245,70 @@ __device__ __forceinline__ void each_nbr32(const Geo4& g, int64_t i, F&& f) {
   }
 }
 
-__device__ __forceinline__ int block_sum256(int v, int* sh8) {
+__device__ __forceinline__ int block_sum(int v, int* sh8) {
   v = __reduce_add_sync(0xffffffffu, v);
   if ((threadIdx.x & 31) == 0) sh8[threadIdx.x >> 5] = v;
   __syncthreads();
   int s = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) s += sh8[k];
+  for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += sh8[k];
   return s;
 }
 
 // One dilation round bit_out(i) = bit_in(i) | OR_j bit_in(j) (skipped when the
 // device decided to shrink).  With COUNT the same pass also counts A_new per
-// 1024-cell tile (compaction pass 1), which needs only the cell's own bits.
+// tile (compaction pass 1), which needs only the cell's own bits.
 template <bool COUNT>
-__global__ void __launch_bounds__(K7T) k_dilate(Geo4 g, uint8_t* __restrict__ flags, uint8_t bit_in, uint8_t bit_out,
+__global__ void __launch_bounds__(256) k_dilate(Geo4 g, uint8_t* __restrict__ flags, uint8_t bit_in, uint8_t bit_out,
                                                 const DevScalars* __restrict__ dsc, SetMode M, int do_dilate,
                                                 int32_t* __restrict__ tile_cnt) {
   __shared__ int sh8[8];
   const bool ex = decide_expand(M, dsc);
   const bool dil = do_dilate && ((M.mode == MODE_DEVICE || M.mode == MODE_DD) ? ex : true);
-  const int64_t t = (int64_t)blockIdx.x * K7T + threadIdx.x;
+  const Pos4 p = pos4(g);
   int cnt = 0;
-  if (g.vec4) {
-    if (t < g.nw) {
+  if (p.ok) {
+    if (g.vec4) {
       uint32_t* fw = reinterpret_cast<uint32_t*>(flags);
-      uint32_t w = fw[t];
+      uint32_t w = fw[p.t];
       if (dil) {
         const uint32_t in = lanes(w, bit_in);
-        auto L = [&](int64_t u) { return lanes(__ldcg(&fw[u]), bit_in); };
-        uint32_t out = in | nbr_lanes4(g, t, in, 0u, L, [](uint32_t x, uint32_t y) { return x | y; });
+        // bit_in is not written by this pass, so plain (L1-cached) loads are safe
+        auto L = [&](int64_t u) { return lanes(fw[u], bit_in); };
+        uint32_t out = in | nbr_lanes4(g, p, in, 0u, L, [](uint32_t x, uint32_t y) { return x | y; });
         if (g.has_nnc) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const int64_t i = 4 * t + k;
+            const int64_t i = 4 * p.t + k;
             const int32_t q0 = __ldg(&g.nptr[i]), q1 = __ldg(&g.nptr[i + 1]);
             for (int32_t q = q0; q < q1; ++q)
               if (flags[__ldg(&g.nnbr[q])] & bit_in) out |= 1u << (8 * k);
           }
         }
         w = (w & ~(0x01010101u * bit_out)) | (out * bit_out);
-        fw[t] = w;
+        fw[p.t] = w;
       }
       if (COUNT) cnt = __popc(a_new4(w, M.mode, ex, M.dbit));
-    }
-  } else {
+    } else {
+      const int64_t rb = (int64_t)p.row * g.nx;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int64_t i = 4 * t + k;
-      if (i >= g.n) break;
-      uint8_t f = flags[i];
-      if (dil) {
-        bool v = (f & bit_in) != 0;
-        if (!v) each_nbr32(g, i, [&](int64_t j) { if (flags[j] & bit_in) v = true; });
-        f = v ? (uint8_t)(f | bit_out) : (uint8_t)(f & ~bit_out);
-        flags[i] = f;
+      for (int k = 0; k < 4; ++k) {
+        const int32_t ix = 4 * p.xw + k;
+        if (ix >= g.nx) break;
+        const int64_t i = rb + ix;
+        uint8_t f = flags[i];
+        if (dil) {
+          bool v = (f & bit_in) != 0;
+          if (!v) each_nbr_xyz(g, i, ix, p.iy, p.iz, [&](int64_t j) { if (flags[j] & bit_in) v = true; });
+          f = v ? (uint8_t)(f | bit_out) : (uint8_t)(f & ~bit_out);
+          flags[i] = f;
+        }
+        if (COUNT) cnt += a_new(f, M.mode, ex, M.dbit) ? 1 : 0;
       }
-      if (COUNT) cnt += a_new(f, M.mode, ex, M.dbit) ? 1 : 0;
     }
   }
   if (COUNT) {
-    const int s = block_sum256(cnt, sh8);
-    if (threadIdx.x == 0) tile_cnt[blockIdx.x] = s;
+    const int s = block_sum(cnt, sh8);
+    if (threadIdx.x == 0) tile_cnt[tile_id(g)] = s;
   }
 }
 
@@ -349,54 +362,56 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t* __restrict__
   }
 }
 
-// Compaction pass 3 (4 cells per thread, 1024-cell tiles): A_new, V_B,
-// V_T/labels, g2l, sorted active list (block scan of the per-thread counts).
-__global__ void __launch_bounds__(K7T) k_scatter(Geo4 g, const uint8_t* __restrict__ fin, uint8_t* __restrict__ fout,
+// Compaction pass 3 (same tiles): A_new, V_B, V_T/labels, g2l, sorted
+// active list (block scan of the per-thread counts 0..4).
+__global__ void __launch_bounds__(256) k_scatter(Geo4 g, const uint8_t* __restrict__ fin, uint8_t* __restrict__ fout,
                                                  SetMode M, int32_t round, DevScalars* dsc,
                                                  const int32_t* __restrict__ tile_off, int32_t* __restrict__ act,
                                                  int32_t* __restrict__ g2l, int32_t* __restrict__ label) {
   __shared__ int32_t wpre[8];
   __shared__ int sh8[8];
   const bool ex = decide_expand(M, dsc);
-  const int64_t t = (int64_t)blockIdx.x * K7T + threadIdx.x;
+  const Pos4 p = pos4(g);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t keep = 0, bnd = 0, f4 = 0;
-  if (g.vec4) {
-    if (t < g.nw) {
+  const int64_t rb = (int64_t)p.row * g.nx;
+  if (p.ok) {
+    if (g.vec4) {
       const uint32_t* fw = reinterpret_cast<const uint32_t*>(fin);
-      f4 = fw[t];
+      f4 = fw[p.t];
       keep = a_new4(f4, M.mode, ex, M.dbit);
       if (keep) {
         auto L = [&](int64_t u) { return a_new4(__ldg(&fw[u]), M.mode, ex, M.dbit); };
-        const uint32_t all = nbr_lanes4(g, t, keep, 0x01010101u, L, [](uint32_t x, uint32_t y) { return x & y; });
+        const uint32_t all = nbr_lanes4(g, p, keep, 0x01010101u, L, [](uint32_t x, uint32_t y) { return x & y; });
         bnd = keep & ~all & 0x01010101u;
         if (g.has_nnc)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             if (!((keep >> (8 * k)) & 1u) || ((bnd >> (8 * k)) & 1u)) continue;
-            const int64_t i = 4 * t + k;
+            const int64_t i = 4 * p.t + k;
             const int32_t q0 = __ldg(&g.nptr[i]), q1 = __ldg(&g.nptr[i + 1]);
             for (int32_t q = q0; q < q1; ++q)
               if (!a_new(fin[__ldg(&g.nnbr[q])], M.mode, ex, M.dbit)) { bnd |= 1u << (8 * k); break; }
           }
       }
-    }
-  } else {
+    } else {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int64_t i = 4 * t + k;
-      if (i >= g.n) break;
-      const uint8_t f = fin[i];
-      f4 |= (uint32_t)f << (8 * k);
-      if (a_new(f, M.mode, ex, M.dbit)) {
-        keep |= 1u << (8 * k);
-        bool b = false;
-        each_nbr32(g, i, [&](int64_t j) { if (!a_new(fin[j], M.mode, ex, M.dbit)) b = true; });
-        if (b) bnd |= 1u << (8 * k);
+      for (int k = 0; k < 4; ++k) {
+        const int32_t ix = 4 * p.xw + k;
+        if (ix >= g.nx) break;
+        const int64_t i = rb + ix;
+        const uint8_t f = fin[i];
+        f4 |= (uint32_t)f << (8 * k);
+        if (a_new(f, M.mode, ex, M.dbit)) {
+          keep |= 1u << (8 * k);
+          bool b = false;
+          each_nbr_xyz(g, i, ix, p.iy, p.iz, [&](int64_t j) { if (!a_new(fin[j], M.mode, ex, M.dbit)) b = true; });
+          if (b) bnd |= 1u << (8 * k);
+        }
       }
     }
   }
-  // block exclusive scan of the per-thread counts (0..4)
+  // block exclusive scan of the per-thread counts
   const int c = __popc(keep);
   int x = c;
 #pragma unroll
@@ -408,9 +423,9 @@ __global__ void __launch_bounds__(K7T) k_scatter(Geo4 g, const uint8_t* __restri
   __syncthreads();
   int pre = x - c;
   for (int k = 0; k < w; ++k) pre += wpre[k];
-  int32_t pos = tile_off[blockIdx.x] + pre;
+  int32_t pos = tile_off[tile_id(g)] + pre;
   int nnew = 0;
-  const int64_t i0 = 4 * t;
+  const int64_t i0 = rb + 4 * (int64_t)p.xw;
   int32_t gl[4];
   uint32_t out = 0;
 #pragma unroll
@@ -430,22 +445,22 @@ __global__ void __launch_bounds__(K7T) k_scatter(Geo4 g, const uint8_t* __restri
     }
     out |= o << (8 * k);
   }
-  if (g.vec4) {
-    if (t < g.nw) {
-      reinterpret_cast<uint32_t*>(fout)[t] = out;
-      reinterpret_cast<int4*>(g2l)[t] = make_int4(gl[0], gl[1], gl[2], gl[3]);
-    }
-  } else {
+  if (p.ok) {
+    if (g.vec4) {
+      reinterpret_cast<uint32_t*>(fout)[p.t] = out;
+      reinterpret_cast<int4*>(g2l)[p.t] = make_int4(gl[0], gl[1], gl[2], gl[3]);
+    } else {
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (i0 + k < g.n) {
-        fout[i0 + k] = (uint8_t)((out >> (8 * k)) & 0xFFu);
-        g2l[i0 + k] = gl[k];
-      }
+      for (int k = 0; k < 4; ++k)
+        if (4 * p.xw + k < g.nx) {
+          fout[i0 + k] = (uint8_t)((out >> (8 * k)) & 0xFFu);
+          g2l[i0 + k] = gl[k];
+        }
+    }
   }
-  const int nb = block_sum256(__popc(bnd), sh8);
+  const int nb = block_sum(__popc(bnd), sh8);
   __syncthreads();
-  const int nn = block_sum256(nnew, sh8);
+  const int nn = block_sum(nnew, sh8);
   if (threadIdx.x == 0) {
     if (nb) atomicAdd(&dsc->nB, nb);
     if (nn) atomicAdd(&dsc->n_new, nn);
@@ -461,14 +476,43 @@ __global__ void k_pin_mask(int64_t n, const uint8_t* __restrict__ kind, const do
   pin0[i] = pin ? (uint8_t)(F_PIN | F_A) : (uint8_t)0;
 }
 
-// Reset flags to the pinned set (A|PIN), or to all-active.
+// Reset flags to the pinned set (A|PIN), or to all-active: 16 cells per
+// thread (uint4), scalar tail.
 __global__ void k_set_reset(int64_t n, const uint8_t* __restrict__ pin0, uint8_t* __restrict__ flags,
                             int all_active) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  uint8_t f = pin0[i];
-  if (all_active) f |= F_A;
-  flags[i] = f;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n16 = n / 16;
+  if (t < n16) {
+    uint4 v = reinterpret_cast<const uint4*>(pin0)[t];
+    if (all_active) {
+      const uint32_t a = 0x01010101u * F_A;
+      v.x |= a; v.y |= a; v.z |= a; v.w |= a;
+    }
+    reinterpret_cast<uint4*>(flags)[t] = v;
+  } else if (t == n16) {
+    for (int64_t i = 16 * n16; i < n; ++i) flags[i] = (uint8_t)(pin0[i] | (all_active ? F_A : 0));
+  }
+}
+
+// Support-set seed for an externally given δp (config 5):
+// flags = pinned set | D0 where |δp| >= ε  (reset + seed in one pass, 4 cells
+// per thread: one flag word, two double2 loads).
+__global__ void k_reset_seed(int64_t n, const uint8_t* __restrict__ pin0, const double* __restrict__ dp, double eps,
+                             uint8_t* __restrict__ flags) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n4 = n / 4;
+  if (t < n4) {
+    uint32_t w = reinterpret_cast<const uint32_t*>(pin0)[t];
+    const double2 a = reinterpret_cast<const double2*>(dp)[2 * t];
+    const double2 b = reinterpret_cast<const double2*>(dp)[2 * t + 1];
+    if (fabs(a.x) >= eps) w |= (uint32_t)F_D0;
+    if (fabs(a.y) >= eps) w |= (uint32_t)F_D0 << 8;
+    if (fabs(b.x) >= eps) w |= (uint32_t)F_D0 << 16;
+    if (fabs(b.y) >= eps) w |= (uint32_t)F_D0 << 24;
+    reinterpret_cast<uint32_t*>(flags)[t] = w;
+  } else if (t == n4) {
+    for (int64_t i = 4 * n4; i < n; ++i) flags[i] = (uint8_t)(pin0[i] | (fabs(dp[i]) >= eps ? F_D0 : 0));
+  }
 }
 
 __global__ void k_set_list(const int32_t* __restrict__ list, int32_t n, uint8_t* __restrict__ flags) {
@@ -661,29 +705,30 @@ static int launch_scan_tiles(rsim_gpu_ctx* c, int64_t ntiles, const SetMode& M) 
 
 int launch_set_update(rsim_gpu_ctx* c, int mode, int round, double eps, int m, int shrink_locked, int force_expand,
                       int do_dilate) {
-  Geo4 g = geo4(c);
+  const Geo4 g = geo4(c);
+  const dim3 grid = k7_grid(g);
   SetMode M;
   M.mode = mode;
   M.dbit = (m % 2 == 0) ? F_D0 : F_D1;
   M.eps = eps;
   M.shrink_locked = shrink_locked;
   M.force_expand = force_expand;
-  const int64_t ntiles = nblk(c->n, K7TILE);
+  const int64_t ntiles = k7_tiles(g);
   const int rounds = do_dilate ? m : 0;
   for (int r = 0; r + 1 < rounds; ++r) {
     uint8_t bin = (r % 2 == 0) ? F_D0 : F_D1, bout = (r % 2 == 0) ? F_D1 : F_D0;
-    k_dilate<false><<<ntiles, K7T, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, 1, c->tile_cnt);
+    k_dilate<false><<<grid, g.bs, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, 1, c->tile_cnt);
     c->launches++;
   }
   {
     const int r = rounds - 1;
     uint8_t bin = (r % 2 == 0) ? F_D0 : F_D1, bout = (r % 2 == 0) ? F_D1 : F_D0;
-    k_dilate<true><<<ntiles, K7T, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, rounds > 0 ? 1 : 0,
+    k_dilate<true><<<grid, g.bs, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, rounds > 0 ? 1 : 0,
                                                   c->tile_cnt);
     c->launches++;
   }
   { const int r = launch_scan_tiles(c, ntiles, M); if (r != RSIM_OK) return r; }
-  k_scatter<<<ntiles, K7T, 0, c->stream>>>(g, c->flags, c->flags_alt, M, round, c->dsc, c->tile_off, c->act_buf,
+  k_scatter<<<grid, g.bs, 0, c->stream>>>(g, c->flags, c->flags_alt, M, round, c->dsc, c->tile_off, c->act_buf,
                                            c->g2l, c->label);
   c->launches++;
   RSIM_CUDA(cudaGetLastError());
@@ -692,13 +737,19 @@ int launch_set_update(rsim_gpu_ctx* c, int mode, int round, double eps, int m, i
   return RSIM_OK;
 }
 
-int launch_set_reset(rsim_gpu_ctx* c, int all_active) {
+static int ensure_pin0(rsim_gpu_ctx* c) {
   if (!c->pin0) {
-    RSIM_CUDA(cudaMalloc(&c->pin0, c->n));
+    RSIM_CUDA(cudaMalloc(&c->pin0, c->n + 16));
     k_pin_mask<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->n, c->kind, c->wi, c->pin0);
     c->launches++;
   }
-  k_set_reset<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->n, c->pin0, c->flags, all_active);
+  return RSIM_OK;
+}
+#define TRY_K7(x) do { const int r_ = (x); if (r_ != RSIM_OK) return r_; } while (0)
+
+int launch_set_reset(rsim_gpu_ctx* c, int all_active) {
+  TRY_K7(ensure_pin0(c));
+  k_set_reset<<<nblk(c->n / 16 + 1, 256), 256, 0, c->stream>>>(c->n, c->pin0, c->flags, all_active);
   c->launches++;
   RSIM_CUDA(cudaGetLastError());
   return RSIM_OK;
@@ -823,6 +874,15 @@ int launch_dd_skip(rsim_gpu_ctx* c, int32_t k) {
     k_zero_list<<<nblk(nk, 256), 256, 0, c->stream>>>(d.sub_cells + d.sub_off[k], nk, c->last_dp);
     c->launches++;
   }
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
+
+// flags := pinned | D0 where |δp| >= ε  (set reset + support seed, one pass)
+int launch_reset_seed(rsim_gpu_ctx* c, double eps) {
+  TRY_K7(ensure_pin0(c));
+  k_reset_seed<<<nblk(c->n / 4 + 1, 256), 256, 0, c->stream>>>(c->n, c->pin0, c->dp, eps, c->flags);
+  c->launches++;
   RSIM_CUDA(cudaGetLastError());
   return RSIM_OK;
 }
