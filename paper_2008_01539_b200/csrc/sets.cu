@@ -317,16 +317,17 @@ __global__ void __launch_bounds__(256) k_dilate(Geo4 g, uint8_t* __restrict__ fl
 // Also publishes the decision + n_A and resets the counters of pass 3.
 __global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t* __restrict__ cnt, int32_t* __restrict__ off,
                                                       int32_t ntiles, DevScalars* dsc, SetMode M) {
-  extern __shared__ int32_t scnt[];
+  extern __shared__ int32_t scnt[];  // padded: entry i at i + i/32 (conflict-free strips)
   __shared__ int32_t wsum[32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int32_t k = threadIdx.x; k < ntiles; k += 1024) scnt[k] = cnt[k];
+  auto P = [](int32_t i) { return i + (i >> 5); };
+  for (int32_t k = threadIdx.x; k < ntiles; k += 1024) scnt[P(k)] = cnt[k];
   __syncthreads();
   const int32_t per = (ntiles + 1023) / 1024;
   const int32_t b0 = threadIdx.x * per;
   int32_t tot = 0;
   for (int32_t k = 0; k < per; ++k)
-    if (b0 + k < ntiles) tot += scnt[b0 + k];
+    if (b0 + k < ntiles) tot += scnt[P(b0 + k)];
   int32_t x = tot;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -348,12 +349,12 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t* __restrict__
   int32_t run = (w > 0 ? wsum[w - 1] : 0) + x - tot;
   for (int32_t k = 0; k < per; ++k)
     if (b0 + k < ntiles) {
-      const int32_t c = scnt[b0 + k];
-      scnt[b0 + k] = run;
+      const int32_t c = scnt[P(b0 + k)];
+      scnt[P(b0 + k)] = run;
       run += c;
     }
   __syncthreads();
-  for (int32_t k = threadIdx.x; k < ntiles; k += 1024) off[k] = scnt[k];
+  for (int32_t k = threadIdx.x; k < ntiles; k += 1024) off[k] = scnt[P(k)];
   if (threadIdx.x == 1023) {
     dsc->nA = wsum[31];
     dsc->expand = decide_expand(M, dsc) ? 1 : 0;
@@ -464,6 +465,216 @@ __global__ void __launch_bounds__(256) k_scatter(Geo4 g, const uint8_t* __restri
   if (threadIdx.x == 0) {
     if (nb) atomicAdd(&dsc->nB, nb);
     if (nn) atomicAdd(&dsc->n_new, nn);
+  }
+}
+
+// ---- row-group variants (vec4 grids): a thread owns the same 4-cell group in
+// RG consecutive x-rows of one plane.  The ±y neighbour words of the group
+// column are loaded once and reused by the RG rows, the ±x neighbours come
+// from the adjacent lanes by warp shuffles (a load only at warp edges), the
+// ±z neighbours are loads.  Tiles are unchanged (one per x-row segment), so a
+// block produces RG tile counts / scans.
+constexpr int RG = 4;
+
+struct PosRG {
+  int32_t iz, iy0, xw, nrow;  // plane, first row, group in row, rows in this group (<= RG)
+  int64_t t0;                 // word index of (iy0, xw)
+  bool ok;
+};
+__device__ __forceinline__ PosRG pos_rg(const Geo4& g) {
+  PosRG p;
+  const int32_t gpp = (g.ny + RG - 1) / RG;  // row groups per plane
+  p.iz = blockIdx.x / gpp;
+  p.iy0 = (blockIdx.x - p.iz * gpp) * RG;
+  p.nrow = g.ny - p.iy0 < RG ? g.ny - p.iy0 : RG;
+  p.xw = blockIdx.y * g.bs + threadIdx.x;
+  p.ok = p.xw < g.wrow;
+  p.t0 = ((int64_t)p.iz * g.ny + p.iy0) * g.wrow + p.xw;
+  return p;
+}
+__host__ dim3 rg_grid(const Geo4& g) { return dim3((unsigned)(((g.ny + RG - 1) / RG) * g.nz), (unsigned)g.nseg, 1); }
+
+// per-byte lanes of the x-neighbours of `in` (row word of this lane): the lanes
+// of the left / right word come from lane-1 / lane+1, or a load at warp edges.
+template <class LF>
+__device__ __forceinline__ uint32_t xnbr_lanes(const Geo4& g, const PosRG& p, int64_t t, bool valid, uint32_t in,
+                                               uint32_t edge, bool or_mode, LF&& L) {
+  const int lane = threadIdx.x & 31;
+  uint32_t lw = __shfl_up_sync(0xffffffffu, in, 1);
+  uint32_t rw = __shfl_down_sync(0xffffffffu, in, 1);
+  if (lane == 0) lw = (valid && p.xw > 0) ? L(t - 1) : 0u;
+  if (lane == 31) rw = (valid && p.xw < g.wrow - 1) ? L(t + 1) : 0u;
+  const uint32_t lft = (in << 8) | (p.xw > 0 ? (lw >> 24) : (edge & 0xFFu));
+  const uint32_t rgt = (in >> 8) | (p.xw < g.wrow - 1 ? ((rw & 0xFFu) << 24) : (edge & 0xFF000000u));
+  return or_mode ? (lft | rgt) : (lft & rgt);
+}
+
+template <bool COUNT>
+__global__ void __launch_bounds__(256) k_dilate_rg(Geo4 g, uint8_t* __restrict__ flags, uint8_t bit_in,
+                                                   uint8_t bit_out, const DevScalars* __restrict__ dsc, SetMode M,
+                                                   int do_dilate, int32_t* __restrict__ tile_cnt) {
+  __shared__ int sh[8][RG];
+  const bool ex = decide_expand(M, dsc);
+  const bool dil = do_dilate && ((M.mode == MODE_DEVICE || M.mode == MODE_DD) ? ex : true);
+  const PosRG p = pos_rg(g);
+  uint32_t* fw = reinterpret_cast<uint32_t*>(flags);
+  auto L = [&](int64_t u) { return lanes(fw[u], bit_in); };  // bit_in is not written by this pass
+  uint32_t col[RG + 2];
+  uint32_t own[RG];
+#pragma unroll
+  for (int j = 0; j < RG + 2; ++j) {
+    const int32_t iy = p.iy0 - 1 + j;
+    const bool in_rows = iy >= 0 && iy < g.ny && (j == 0 || j == RG + 1 || j - 1 < p.nrow);
+    uint32_t wv = 0;
+    if (p.ok && in_rows) wv = fw[p.t0 + (int64_t)(j - 1) * g.wrow];
+    if (j >= 1 && j <= RG) own[j - 1] = wv;
+    col[j] = lanes(wv, bit_in);
+  }
+  int cnt[RG];
+#pragma unroll
+  for (int k = 0; k < RG; ++k) {
+    cnt[k] = 0;
+    const int64_t t = p.t0 + (int64_t)k * g.wrow;
+    uint32_t w = own[k];
+    if (dil) {
+      const uint32_t in = col[k + 1];
+      uint32_t out = in | xnbr_lanes(g, p, t, p.ok && k < p.nrow, in, 0u, true, L) | col[k] | col[k + 2];
+      if (p.ok && k < p.nrow) {
+        if (g.d3) {
+          if (p.iz > 0) out |= L(t - g.wplane);
+          if (p.iz < g.nz - 1) out |= L(t + g.wplane);
+        }
+        if (g.has_nnc) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int64_t i = 4 * t + e;
+            const int32_t q0 = __ldg(&g.nptr[i]), q1 = __ldg(&g.nptr[i + 1]);
+            for (int32_t q = q0; q < q1; ++q)
+              if (flags[__ldg(&g.nnbr[q])] & bit_in) out |= 1u << (8 * e);
+          }
+        }
+        w = (w & ~(0x01010101u * bit_out)) | (out * bit_out);
+        fw[t] = w;
+      }
+    }
+    if (COUNT && p.ok && k < p.nrow) cnt[k] = __popc(a_new4(w, M.mode, ex, M.dbit));
+  }
+  if (COUNT) {
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < RG; ++k) {
+      const int v = __reduce_add_sync(0xffffffffu, cnt[k]);
+      if (lane == 0) sh[wi][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < p.nrow) {
+      int s = 0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) s += sh[q][threadIdx.x];
+      const int32_t row = p.iz * g.ny + p.iy0 + threadIdx.x;
+      tile_cnt[row * g.nseg + blockIdx.y] = s;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_scatter_rg(Geo4 g, const uint8_t* __restrict__ fin,
+                                                    uint8_t* __restrict__ fout, SetMode M, int32_t round,
+                                                    DevScalars* dsc, const int32_t* __restrict__ tile_off,
+                                                    int32_t* __restrict__ act, int32_t* __restrict__ g2l,
+                                                    int32_t* __restrict__ label) {
+  __shared__ unsigned long long wpre[8];
+  __shared__ int sh8[8];
+  const bool ex = decide_expand(M, dsc);
+  const PosRG p = pos_rg(g);
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const uint32_t* fw = reinterpret_cast<const uint32_t*>(fin);
+  auto K = [&](int64_t u) { return a_new4(__ldg(&fw[u]), M.mode, ex, M.dbit); };
+  uint32_t kc[RG + 2], own[RG];
+#pragma unroll
+  for (int j = 0; j < RG + 2; ++j) {
+    const int32_t iy = p.iy0 - 1 + j;
+    const bool row_ok = iy >= 0 && iy < g.ny && (j == 0 || j == RG + 1 || j - 1 < p.nrow);
+    uint32_t wv = 0;
+    if (p.ok && row_ok) wv = __ldg(&fw[p.t0 + (int64_t)(j - 1) * g.wrow]);
+    if (j >= 1 && j <= RG) own[j - 1] = wv;
+    // off-grid rows count as "keep" for the boundary test (no neighbour there)
+    kc[j] = (iy >= 0 && iy < g.ny) ? a_new4(wv, M.mode, ex, M.dbit) : 0x01010101u;
+  }
+  uint32_t keep[RG], bnd[RG];
+  unsigned long long packed = 0;  // 16-bit per-row counts
+#pragma unroll
+  for (int k = 0; k < RG; ++k) {
+    const int64_t t = p.t0 + (int64_t)k * g.wrow;
+    const bool rok = p.ok && k < p.nrow;
+    keep[k] = rok ? kc[k + 1] : 0u;
+    const uint32_t xa = xnbr_lanes(g, p, t, rok, keep[k], 0x01010101u, false, K);
+    bnd[k] = 0;
+    if (keep[k]) {
+      uint32_t all = xa & kc[k] & kc[k + 2];
+      if (g.d3) {
+        all &= p.iz > 0 ? K(t - g.wplane) : 0x01010101u;
+        all &= p.iz < g.nz - 1 ? K(t + g.wplane) : 0x01010101u;
+      }
+      bnd[k] = keep[k] & ~all & 0x01010101u;
+      if (g.has_nnc)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (!((keep[k] >> (8 * e)) & 1u) || ((bnd[k] >> (8 * e)) & 1u)) continue;
+          const int64_t i = 4 * t + e;
+          const int32_t q0 = __ldg(&g.nptr[i]), q1 = __ldg(&g.nptr[i + 1]);
+          for (int32_t q = q0; q < q1; ++q)
+            if (!a_new(fin[__ldg(&g.nnbr[q])], M.mode, ex, M.dbit)) { bnd[k] |= 1u << (8 * e); break; }
+        }
+    }
+    packed |= (unsigned long long)__popc(keep[k]) << (16 * k);
+  }
+  // block exclusive scan of the packed per-row counts (row sums <= 4*256 < 2^16)
+  unsigned long long x = packed;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wpre[wi] = x;
+  __syncthreads();
+  unsigned long long pre = x - packed;
+  for (int q = 0; q < wi; ++q) pre += wpre[q];
+  int nb = 0, nnew = 0;
+#pragma unroll
+  for (int k = 0; k < RG; ++k) {
+    if (!(p.ok && k < p.nrow)) continue;
+    const int64_t t = p.t0 + (int64_t)k * g.wrow;
+    const int32_t row = p.iz * g.ny + p.iy0 + k;
+    int32_t pos = tile_off[row * g.nseg + blockIdx.y] + (int32_t)((pre >> (16 * k)) & 0xFFFFu);
+    const int64_t i0 = 4 * t;
+    int32_t gl[4];
+    uint32_t out = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t f = (own[k] >> (8 * e)) & 0xFFu;
+      uint32_t o = f & (F_PIN | F_T);
+      gl[e] = -1;
+      if ((keep[k] >> (8 * e)) & 1u) {
+        o |= F_A;
+        if ((bnd[k] >> (8 * e)) & 1u) o |= F_B;
+        if (M.mode == MODE_DD) {
+          if (!(f & F_T)) { label[i0 + e] = round; ++nnew; }
+          o |= F_T;
+        }
+        act[pos] = (int32_t)(i0 + e);
+        gl[e] = pos++;
+      }
+      out |= o << (8 * e);
+    }
+    reinterpret_cast<uint32_t*>(fout)[t] = out;
+    reinterpret_cast<int4*>(g2l)[t] = make_int4(gl[0], gl[1], gl[2], gl[3]);
+    nb += __popc(bnd[k]);
+  }
+  const int nbs = block_sum(nb, sh8);
+  __syncthreads();
+  const int nns = block_sum(nnew, sh8);
+  if (threadIdx.x == 0) {
+    if (nbs) atomicAdd(&dsc->nB, nbs);
+    if (nns) atomicAdd(&dsc->n_new, nns);
   }
 }
 
@@ -688,7 +899,7 @@ int launch_threshold(rsim_gpu_ctx* c, double eps) {
 // + scan + scatter.  4 launches for m = 2, no host round trip.
 // single-block tile scan (counts staged in dynamic shared memory)
 static int launch_scan_tiles(rsim_gpu_ctx* c, int64_t ntiles, const SetMode& M) {
-  const size_t smem = (size_t)ntiles * sizeof(int32_t);
+  const size_t smem = (size_t)(ntiles + ntiles / 32 + 1) * sizeof(int32_t);
   if (smem > 220 * 1024) {
     rsim_set_error("set update: grid too large for the single-block tile scan");
     return RSIM_EARG;
@@ -715,21 +926,34 @@ int launch_set_update(rsim_gpu_ctx* c, int mode, int round, double eps, int m, i
   M.force_expand = force_expand;
   const int64_t ntiles = k7_tiles(g);
   const int rounds = do_dilate ? m : 0;
+  const dim3 grg = rg_grid(g);
+  // row groups reuse the ±y words RG-fold but give RG-fold fewer blocks: only
+  // for grids large enough to fill the GPU many times over
+  const bool use_rg = g.vec4 && (int64_t)grg.x * grg.y >= 16 * 148;
   for (int r = 0; r + 1 < rounds; ++r) {
     uint8_t bin = (r % 2 == 0) ? F_D0 : F_D1, bout = (r % 2 == 0) ? F_D1 : F_D0;
-    k_dilate<false><<<grid, g.bs, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, 1, c->tile_cnt);
+    if (use_rg) k_dilate_rg<false><<<grg, g.bs, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, 1, c->tile_cnt);
+    else k_dilate<false><<<grid, g.bs, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, 1, c->tile_cnt);
     c->launches++;
   }
   {
     const int r = rounds - 1;
     uint8_t bin = (r % 2 == 0) ? F_D0 : F_D1, bout = (r % 2 == 0) ? F_D1 : F_D0;
-    k_dilate<true><<<grid, g.bs, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, rounds > 0 ? 1 : 0,
-                                                  c->tile_cnt);
+    if (use_rg)
+      k_dilate_rg<true><<<grg, g.bs, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, rounds > 0 ? 1 : 0,
+                                                     c->tile_cnt);
+    else
+      k_dilate<true><<<grid, g.bs, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, rounds > 0 ? 1 : 0,
+                                                   c->tile_cnt);
     c->launches++;
   }
   { const int r = launch_scan_tiles(c, ntiles, M); if (r != RSIM_OK) return r; }
-  k_scatter<<<grid, g.bs, 0, c->stream>>>(g, c->flags, c->flags_alt, M, round, c->dsc, c->tile_off, c->act_buf,
-                                           c->g2l, c->label);
+  if (use_rg)
+    k_scatter_rg<<<grg, g.bs, 0, c->stream>>>(g, c->flags, c->flags_alt, M, round, c->dsc, c->tile_off, c->act_buf,
+                                              c->g2l, c->label);
+  else
+    k_scatter<<<grid, g.bs, 0, c->stream>>>(g, c->flags, c->flags_alt, M, round, c->dsc, c->tile_off, c->act_buf,
+                                            c->g2l, c->label);
   c->launches++;
   RSIM_CUDA(cudaGetLastError());
   std::swap(c->flags, c->flags_alt);
