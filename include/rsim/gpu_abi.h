@@ -119,6 +119,10 @@ int rsim_gpu_timers(rsim_gpu_ctx* ctx, int32_t enable, double* ms4, int32_t* lau
  * [3] Krylov launches' rows Σ n_A, [4] set-update passes (full-grid scans). */
 int rsim_gpu_counters(rsim_gpu_ctx* ctx, int64_t* out5, int32_t reset);
 
+/* Debug flags: bit 0 = the large-set assembly also stores the raw residual F
+ * (otherwise only ‖F‖ partials are kept; rsim_gpu_download_system needs F). */
+int rsim_gpu_set_debug(rsim_gpu_ctx* ctx, int32_t flags);
+
 /* Debug: cycle counters of the cluster Krylov phases (RSIM_KTRACE=1 at create). */
 #define RSIM_KTRACE_N 136 /* 8 phase counters (CTA 0) + 16 CTAs x 8 per-CTA counters */
 int rsim_gpu_ktrace(rsim_gpu_ctx* ctx, unsigned long long* out);

@@ -69,7 +69,17 @@ RSIM_HD double rexp(double x) {
   q = q * r + 0.5;
   q = q * r + 1.0;
   q = q * r + 1.0;
-  return ldexp(q, (int)kd);
+  const int k = (int)kd;
+  if (k > -1000 && k < 1000) {  // q·2^k is a normal number: exact, the same bits as ldexp
+#if defined(__CUDA_ARCH__)
+    return q * __longlong_as_double((long long)(k + 1023) << 52);
+#else
+    union { long long i; double d; } e;
+    e.i = (long long)(k + 1023) << 52;
+    return q * e.d;
+#endif
+  }
+  return ldexp(q, k);
 }
 
 /* Quadratic Corey curve on the normalised saturation (s − s_r)/den,

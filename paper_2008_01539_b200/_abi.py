@@ -143,6 +143,7 @@ PROTOS: dict[str, tuple] = {
     "rsim_gpu_timers": (C.c_int, [P, C.c_int32, dptr, i32ptr]),
     "rsim_gpu_mark": (C.c_int, [P, C.c_int32]),
     "rsim_gpu_ktrace": (C.c_int, [P, C.POINTER(C.c_ulonglong)]),
+    "rsim_gpu_set_debug": (C.c_int, [P, C.c_int32]),
     "rsim_gpu_elapsed": (C.c_int, [P, C.c_int32, C.c_int32, dptr]),
     "rsim_gpu_flush_l2": (C.c_int, [P]),
     "rsim_gpu_checkpoint": (C.c_int, [P, C.c_int32]),
@@ -173,6 +174,8 @@ def lib() -> C.CDLL:
             raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback exists)")
         L = C.CDLL(str(LIB_PATH))
         for name, (res, args) in PROTOS.items():
+            if os.environ.get("RSIM_LIB") and not hasattr(L, name):
+                continue  # A/B against an older build: tolerate symbols it predates
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args

@@ -248,6 +248,12 @@ int rsim_gpu_create(rsim_gpu_ctx** out, const rsim_graph_desc* g, const rsim_flu
   return RSIM_OK;
 }
 
+int rsim_gpu_set_debug(rsim_gpu_ctx* c, int32_t flags) {
+  if (!c) return RSIM_EARG;
+  c->keep_F = (flags & 1) != 0;
+  return RSIM_OK;
+}
+
 int rsim_gpu_ktrace(rsim_gpu_ctx* c, unsigned long long* out) {
   if (!c->ktrace) return RSIM_EARG;
   RSIM_CUDA(cudaMemcpy(out, c->ktrace, RSIM_KTRACE_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
@@ -470,6 +476,7 @@ int rsim_gpu_download_boundary(rsim_gpu_ctx* c, int32_t* vb, int32_t* n) {
 int64_t rsim_gpu_download_system(rsim_gpu_ctx* c, double* F_raw, double* rhs, int32_t* rowptr, int32_t* col,
                                  double* val, int64_t cap_nnzb) {
   const int64_t nA = c->nA, b = c->b, bb = b * b, cap = c->n;
+  TRY(launch_materialize_cols(c));
   RSIM_CUDA(cudaStreamSynchronize(c->stream));
   std::vector<int32_t> ecol(c->nslot * nA), act(nA);
   std::vector<double> eval(c->nslot * nA * bb);
@@ -485,7 +492,13 @@ int64_t rsim_gpu_download_system(rsim_gpu_ctx* c, double* F_raw, double* rhs, in
     RSIM_CUDA(cudaMemcpy(nlcol.data(), c->nnc_lcol, sizeof(int32_t) * c->nnc_total, cudaMemcpyDeviceToHost));
     RSIM_CUDA(cudaMemcpy(nval.data(), c->nnc_val, sizeof(double) * c->nnc_total * bb, cudaMemcpyDeviceToHost));
   }
-  if (F_raw) RSIM_CUDA(cudaMemcpy(F_raw, c->F_raw, sizeof(double) * nA * b, cudaMemcpyDeviceToHost));
+  if (F_raw) {
+    if (c->f2_parts && !c->keep_F) {
+      rsim_set_error("download_system: raw residual not stored (large assembly; enable rsim_gpu_set_debug bit 0)");
+      return -RSIM_EARG;
+    }
+    RSIM_CUDA(cudaMemcpy(F_raw, c->F_raw, sizeof(double) * nA * b, cudaMemcpyDeviceToHost));
+  }
   if (rhs) RSIM_CUDA(cudaMemcpy(rhs, c->rhs, sizeof(double) * nA * b, cudaMemcpyDeviceToHost));
   int64_t nnz = 0;
   for (int64_t l = 0; l < nA; ++l) {

@@ -35,6 +35,7 @@ struct AsmArgs {
   int32_t* nnc_lcol;
   double* nnc_val;
   double *F_raw, *rhs, *part_f2;
+  bool keep_F;  // row kernel: store the raw residual (debug downloads only)
   DevScalars* dsc;
 };
 
@@ -225,45 +226,95 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
 
 // One thread per active row (large active sets: memory-bound, the 8-lane
 // variant's redundant property evaluations cost more than they hide).
-// b = 1 keeps the raw off-diagonal blocks in registers; b > 1 recomputes them
-// in a second pass (same physics.h calls => same bits).
-template <int B>
+// Every neighbour load (face Υ, u_j, g2l_j, status_j) is issued before any
+// arithmetic so a thread keeps ~4·nslot loads in flight; the ELL / residual
+// stores are streaming (st.global.cs) so they do not evict the neighbour
+// working set from L2.  b = 1 keeps the raw off-diagonal blocks in registers;
+// b > 1 recomputes them in a second pass (same physics.h calls => same bits).
+// FULL (V_A = all cells): act is the identity, every in-grid neighbour is
+// active with local index = global index, so neither act / g2l are read nor
+// the structural ELL columns stored (consumers use implicit_col()).
+template <int B, bool FULL>
 __global__ void __launch_bounds__(256) k_assemble_row(const AsmArgs a) {
   constexpr bool KEEP = (B == 1);
-  double finf = 0.0;
+  __shared__ double wsf[8];
+  double finf = 0.0, ff = 0.0;
   const int64_t l = (int64_t)blockIdx.x * 256 + threadIdx.x;
   if (l < a.nA) {
-    const int64_t i = a.act[l];
-    const int64_t nxy = (int64_t)a.nx * a.ny;
-    const int64_t ix = i % a.nx, iy = (i / a.nx) % a.ny, iz = i / nxy;
-    double ui[B];
-    load_u<B>(a, i, ui);
-    rsim::phys::Props<B> Pi;
-    rsim::phys::props(a.fl, ui, B == 3 ? a.st[i] : (uint8_t)0, Pi);
-    double R[B], D[B][B], Mo[B];
-#pragma unroll
-    for (int c = 0; c < B; ++c) Mo[c] = __ldg(&a.mold[i * B + c]);
-    rsim::phys::accum_row<B>(a.fl, __ldg(&a.pv[i]), ui[0], Pi, Mo, a.dt, R, D);
-    double Okeep[6][B][B];
-    int32_t lcol[6];
+    const int64_t i = FULL ? l : (int64_t)a.act[l];
+    // 32-bit coordinates (n < 2^31, checked at create)
+    const uint32_t nxy = (uint32_t)a.nx * (uint32_t)a.ny;
+    const uint32_t iz = (uint32_t)i / nxy;
+    const uint32_t rem = (uint32_t)i - iz * nxy;
+    const uint32_t iy = rem / (uint32_t)a.nx, ix = rem - iy * (uint32_t)a.nx;
+    // ---- neighbour indices and all loads up front
+    int64_t jn[6];
+    bool has[6];
+    double Tn[6], un[6][B];
+    int32_t gn[6];
+    uint8_t sn[6];
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
-      lcol[s] = -1;
+      has[s] = false;
+      jn[s] = i;
+      Tn[s] = 0.0;
+      gn[s] = -1;
+      sn[s] = 0;
       if (s >= a.nslot) continue;
-      int64_t j;
-      double T;
-      if (cart_nbr(a, i, ix, iy, iz, s, j, T)) {
-        double O[B][B];
-        conn<B>(a, ui, Pi, j, T, R, D, O);
-        lcol[s] = __ldg(&a.g2l[j]);
-        if (KEEP)
-#pragma unroll
-          for (int r = 0; r < B; ++r)
-#pragma unroll
-            for (int c = 0; c < B; ++c) Okeep[s][r][c] = O[r][c];
+      const int k = a.d3 ? s : s + 1;  // 2D skips the -z slot
+      switch (k) {
+        case 0: has[s] = iz > 0; jn[s] = i - nxy; break;
+        case 1: has[s] = iy > 0; jn[s] = i - a.nx; break;
+        case 2: has[s] = ix > 0; jn[s] = i - 1; break;
+        case 3: has[s] = ix < (uint32_t)a.nx - 1; jn[s] = i + 1; break;
+        case 4: has[s] = iy < (uint32_t)a.ny - 1; jn[s] = i + a.nx; break;
+        default: has[s] = iz < (uint32_t)a.nz - 1; jn[s] = i + nxy; break;
       }
-      a.ell_col[s * a.cap + l] = lcol[s];
     }
+#pragma unroll
+    for (int s = 0; s < 6; ++s)
+      if (has[s]) {
+        const int k = a.d3 ? s : s + 1;
+        const double* tf = (k == 0 || k == 5) ? a.tz : ((k == 1 || k == 4) ? a.ty : a.tx);
+        Tn[s] = __ldg(&tf[k < 3 ? jn[s] : i]);  // face Υ stored at the lower cell
+        load_u<B>(a, jn[s], un[s]);
+        gn[s] = FULL ? (int32_t)jn[s] : __ldg(&a.g2l[jn[s]]);
+        if (B == 3) sn[s] = __ldg(&a.st[jn[s]]);
+      }
+    double ui[B], Mo[B];
+    load_u<B>(a, i, ui);
+#pragma unroll
+    for (int c = 0; c < B; ++c) Mo[c] = __ldg(&a.mold[i * B + c]);
+    const double pv = __ldg(&a.pv[i]), wi = __ldg(&a.wi[i]);
+    const uint8_t sti = B == 3 ? a.st[i] : (uint8_t)0;
+    // ---- arithmetic (canonical order: accumulation, slots ascending, NNC, well)
+    rsim::phys::Props<B> Pi;
+    rsim::phys::props(a.fl, ui, sti, Pi);
+    double R[B], D[B][B];
+    rsim::phys::accum_row<B>(a.fl, pv, ui[0], Pi, Mo, a.dt, R, D);
+    double Okeep[6][B][B];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      if (!has[s]) continue;
+      double O[B][B];
+      const double dp = ui[0] - un[s][0];
+      if (!(dp < 0.0)) {
+        rsim::phys::flux_conn<B>(Tn[s], dp, true, Pi, R, D, O);
+      } else {
+        rsim::phys::Props<B> Pj;
+        rsim::phys::props(a.fl, un[s], sn[s], Pj);
+        rsim::phys::flux_conn<B>(Tn[s], dp, false, Pj, R, D, O);
+      }
+      if (KEEP)
+#pragma unroll
+        for (int r = 0; r < B; ++r)
+#pragma unroll
+          for (int c = 0; c < B; ++c) Okeep[s][r][c] = O[r][c];
+    }
+    if (!FULL)
+#pragma unroll
+      for (int s = 0; s < 6; ++s)
+        if (s < a.nslot) __stcs(&a.ell_col[s * a.cap + l], has[s] ? gn[s] : -1);
     int32_t q0 = 0, q1 = 0;
     if (a.has_nnc) {
       q0 = __ldg(&a.nptr[i]);
@@ -275,7 +326,7 @@ __global__ void __launch_bounds__(256) k_assemble_row(const AsmArgs a) {
         a.nnc_lcol[q] = __ldg(&a.g2l[j]);
       }
     }
-    rsim::phys::well_row<B>(__ldg(&a.wi[i]), ui[0], a.bhp, Pi, R, D);
+    rsim::phys::well_row<B>(wi, ui[0], a.bhp, Pi, R, D);
     double Di[B][B];
     if (!rsim::blk::inv(D, Di)) {
       atomicMin(&a.dsc->bad_cell, (int32_t)i);
@@ -289,30 +340,44 @@ __global__ void __launch_bounds__(256) k_assemble_row(const AsmArgs a) {
     rsim::blk::gemv<B>(Di, R, y);
 #pragma unroll
     for (int e = 0; e < B; ++e) {
-      a.F_raw[l * B + e] = R[e];
-      a.rhs[l * B + e] = -y[e];
+      if (a.keep_F) __stcs(&a.F_raw[l * B + e], R[e]);
+      __stcs(&a.rhs[l * B + e], -y[e]);
       finf = fmax(finf, fabs(R[e]));
     }
+    ff = rsim::blk::rowdot<B>(R, R);
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
-      if (s >= a.nslot || lcol[s] < 0) continue;
+      if (!has[s] || gn[s] < 0) continue;
       double* dst = &a.ell_val[((int64_t)s * a.cap + l) * B * B];
+      double O[B][B];
       if (KEEP) {
-        store_scaled<B>(dst, Di, Okeep[s]);
+#pragma unroll
+        for (int r = 0; r < B; ++r)
+#pragma unroll
+          for (int c = 0; c < B; ++c) O[r][c] = Okeep[s][r][c];
       } else {
-        int64_t j;
-        double T;
-        cart_nbr(a, i, ix, iy, iz, s, j, T);
-        double O[B][B], Rd[B], Dd[B][B];
+        double Rd[B], Dd[B][B];
 #pragma unroll
         for (int e = 0; e < B; ++e) {
           Rd[e] = 0.0;
 #pragma unroll
           for (int v = 0; v < B; ++v) Dd[e][v] = 0.0;
         }
-        conn<B>(a, ui, Pi, j, T, Rd, Dd, O);
-        store_scaled<B>(dst, Di, O);
+        const double dp = ui[0] - un[s][0];
+        if (!(dp < 0.0)) {
+          rsim::phys::flux_conn<B>(Tn[s], dp, true, Pi, Rd, Dd, O);
+        } else {
+          rsim::phys::Props<B> Pj;
+          rsim::phys::props(a.fl, un[s], sn[s], Pj);
+          rsim::phys::flux_conn<B>(Tn[s], dp, false, Pj, Rd, Dd, O);
+        }
       }
+      double S[B][B];
+      rsim::blk::gemm<B>(Di, O, S);
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+#pragma unroll
+        for (int c = 0; c < B; ++c) __stcs(&dst[r * B + c], S[r][c]);
     }
     for (int32_t q = q0; q < q1; ++q) {
       const int64_t j = __ldg(&a.nnbr[q]);
@@ -330,6 +395,13 @@ __global__ void __launch_bounds__(256) k_assemble_row(const AsmArgs a) {
   }
   const double wm = warp_max(finf);
   if ((threadIdx.x & 31) == 0 && wm > 0.0) atomic_max_bits(&a.dsc->finf, wm);
+  // canonical chunk partial of (F, F): this block IS local chunk blockIdx.x
+  // (256 rows; rows past n_A hold +0.0) — the Krylov init reduces these
+  // instead of re-reading F
+  const double wsum = warp_tree(ff);
+  if ((threadIdx.x & 31) == 0) wsf[threadIdx.x >> 5] = wsum;
+  __syncthreads();
+  if (threadIdx.x == 0) a.part_f2[blockIdx.x] = tree8(wsf);
 }
 
 // Old-time accumulation M^n = pv φ(p) A(u) for every cell (set_state / Δt change).
@@ -349,7 +421,27 @@ __global__ void k_mold(rsim_fluid_params fl, int64_t n, const double* __restrict
   for (int c = 0; c < B; ++c) mold[i * B + c] = M[c];
 }
 
+// debug download of an implicit-column assembly: write the structural columns
+__global__ void k_materialize_cols(int32_t nx, int32_t ny, int32_t nz, bool d3, int nslot, int64_t n,
+                                   int32_t* __restrict__ ell_col) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t cl[6];
+  implicit_cols(nx, ny, nz, d3, i, cl);
+  for (int s = 0; s < nslot; ++s) ell_col[s * n + i] = cl[s];
+}
+
 }  // namespace
+
+int launch_materialize_cols(rsim_gpu_ctx* c) {
+  if (!c->cols_implicit) return RSIM_OK;
+  k_materialize_cols<<<(c->n + 255) / 256, 256, 0, c->stream>>>(c->nx, c->ny, c->nz, c->d3, c->nslot, c->n,
+                                                                c->ell_col);
+  c->launches++;
+  c->cols_implicit = false;
+  RSIM_CUDA(cudaGetLastError());
+  return RSIM_OK;
+}
 
 int launch_assemble(rsim_gpu_ctx* c) {
   if (c->nA <= 0) return RSIM_OK;
@@ -370,8 +462,11 @@ int launch_assemble(rsim_gpu_ctx* c) {
   a.ell_col = c->ell_col; a.ell_val = c->ell_val;
   a.nnc_lcol = c->nnc_lcol; a.nnc_val = c->nnc_val;
   a.F_raw = c->F_raw; a.rhs = c->rhs; a.part_f2 = c->part_f2;
+  a.keep_F = c->keep_F;
   a.dsc = c->dsc;
   // small active sets: 8 lanes per row (latency); large: one thread per row (bandwidth)
+  c->cols_implicit = false;
+  c->f2_parts = c->nA >= kRowKernelMin;  // row kernel: (F,F) as canonical chunk partials
   if (c->nA < kRowKernelMin) {
     const int64_t nblocks = (c->nA + RPB - 1) / RPB;
     switch (c->b) {
@@ -381,10 +476,15 @@ int launch_assemble(rsim_gpu_ctx* c) {
     }
   } else {
     const int64_t nblocks = (c->nA + 255) / 256;
-    switch (c->b) {
-      case 1: k_assemble_row<1><<<nblocks, 256, 0, c->stream>>>(a); break;
-      case 2: k_assemble_row<2><<<nblocks, 256, 0, c->stream>>>(a); break;
-      default: k_assemble_row<3><<<nblocks, 256, 0, c->stream>>>(a); break;
+    const bool full = c->nA == c->n;
+    c->cols_implicit = full;
+    switch (c->b * 2 + (full ? 1 : 0)) {
+      case 2: k_assemble_row<1, false><<<nblocks, 256, 0, c->stream>>>(a); break;
+      case 3: k_assemble_row<1, true><<<nblocks, 256, 0, c->stream>>>(a); break;
+      case 4: k_assemble_row<2, false><<<nblocks, 256, 0, c->stream>>>(a); break;
+      case 5: k_assemble_row<2, true><<<nblocks, 256, 0, c->stream>>>(a); break;
+      case 6: k_assemble_row<3, false><<<nblocks, 256, 0, c->stream>>>(a); break;
+      default: k_assemble_row<3, true><<<nblocks, 256, 0, c->stream>>>(a); break;
     }
   }
   c->launches++;

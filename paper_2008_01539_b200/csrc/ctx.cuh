@@ -62,6 +62,9 @@ struct rsim_gpu_ctx {
   bool d3 = false;
   int nslot = 4;
   bool has_nnc = false;
+  bool cols_implicit = false;  // last assembly: V_A = all cells, ELL columns not stored (structural)
+  bool f2_parts = false;       // last assembly left (F,F) chunk partials in part_f2 (F_raw only if keep_F)
+  bool keep_F = false;         // debug: the row kernel also stores the raw residual
   int64_t nnc_total = 0;
   rsim_fluid_params fl{};
   double bhp = 0.0;
@@ -161,6 +164,7 @@ int launch_dd_skip(rsim_gpu_ctx* c, int32_t k);
 int launch_categories(rsim_gpu_ctx* c, uint8_t* dev_out);
 int launch_seed_support(rsim_gpu_ctx* c, double eps);
 int launch_reset_seed(rsim_gpu_ctx* c, double eps);
+int launch_materialize_cols(rsim_gpu_ctx* c);
 int launch_state_from_dp(rsim_gpu_ctx* c, double p_hi, double scale);
 
 // ---- device helpers ------------------------------------------------------------
@@ -173,6 +177,23 @@ __device__ __forceinline__ unsigned long long dbits(double a) {
 // Canonical reduction helpers (blockops.h): a 256-row chunk is 8 warps; each
 // warp shuffles 16..1 (lane 0 holds the warp sum), then the 8 warp sums are
 // combined with offsets 4,2,1.
+// Full active set (V_A = all cells, local == global index): the ELL columns
+// of cell i are structural — the Cartesian neighbours in slot order, -1 off-grid.
+__device__ __forceinline__ void implicit_cols(int32_t nx, int32_t ny, int32_t nz, bool d3, int64_t i, int32_t* cl) {
+  const uint32_t nxy = (uint32_t)nx * (uint32_t)ny;
+  const uint32_t iz = (uint32_t)i / nxy;
+  const uint32_t rem = (uint32_t)i - iz * nxy;
+  const uint32_t iy = rem / (uint32_t)nx, ix = rem - iy * (uint32_t)nx;
+  const int32_t ii = (int32_t)i;
+  int k = 0;
+  if (d3) cl[k++] = iz > 0 ? ii - (int32_t)nxy : -1;
+  cl[k++] = iy > 0 ? ii - nx : -1;
+  cl[k++] = ix > 0 ? ii - 1 : -1;
+  cl[k++] = ix + 1 < (uint32_t)nx ? ii + 1 : -1;
+  cl[k++] = iy + 1 < (uint32_t)ny ? ii + nx : -1;
+  if (d3) cl[k++] = iz + 1 < (uint32_t)nz ? ii + (int32_t)nxy : -1;
+}
+
 __device__ __forceinline__ double warp_tree(double v) {
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) v = v + __shfl_down_sync(0xffffffffu, v, off);

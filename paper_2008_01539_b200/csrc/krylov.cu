@@ -28,11 +28,16 @@ namespace cg = cooperative_groups;
 
 namespace {
 
-constexpr int KT = 1024;  // threads per CTA = 4 chunks per round
+constexpr int KT = 1024;  // threads per CTA
+constexpr int CPR = KT / 256;  // canonical chunks per round
+constexpr int LCPR = CPR == 4 ? 2 : (CPR == 2 ? 1 : 0);
 constexpr int64_t kFuseMaxRows = 1 << 20;  // recompute-fusion only while latency-bound
 
 struct KArgs {
   int32_t nA, nslot, maxit, fixed;
+  int32_t nx, ny, nz;
+  bool d3, implicit;  // implicit: full set, structural ELL columns (not stored)
+  int32_t stage;      // rounds staged per block-level commit (1..RSTAGE)
   int64_t cap;
   bool has_nnc;
   double rtol;
@@ -44,6 +49,8 @@ struct KArgs {
   const double* nnc_val;
   const double* rhs;
   const double* F_raw;
+  const double* part_f2;  // (F,F) chunk partials of the assembly (f2_parts)
+  bool f2_parts;
   double *x, *r, *r0, *p, *v, *s, *t, *p2, *v2, *ph, *sh;
   int32_t neu, fuse;
   double* part;   // [5][pstride]  level-1 partials
@@ -52,11 +59,39 @@ struct KArgs {
   DevScalars* dsc;
 };
 
+#ifndef RSIM_RSTAGE
+#define RSIM_RSTAGE 8
+#endif
+constexpr int RSTAGE = RSIM_RSTAGE;  // rounds whose warp sums are staged before one block-level commit
 struct Red {
-  double ws[5][32];  // warp sums of the current round
+  double ws[5][32];  // warp sums of the current round (level-2 / small reductions)
   double lvl[5][64];
   double res[5];
+  double wsr[RSTAGE][5][32];  // staged warp sums of up to RSTAGE rounds
+  int64_t rid[RSTAGE];        // their round ids
 };
+
+// Stage the warp sums of one round (no block barrier); every RSTAGE rounds,
+// and after the CTA's last round, one barrier pair turns them into level-1
+// chunk partials (8-way trees, canonical).  Warps thus run ahead through up
+// to RSTAGE rounds of loads instead of meeting at two barriers per round.
+__device__ __forceinline__ void stage_round(Red& R, int NQ, const double* val, int slot, int64_t rd, bool flush,
+                                            int nstaged, int64_t nch, double* part, int pstride) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int q = 0; q < NQ; ++q) {
+    double v = warp_tree(val[q]);
+    if (lane == 0) R.wsr[slot][q][w] = v;
+  }
+  if (threadIdx.x == 0) R.rid[slot] = rd;
+  if (!flush) return;
+  __syncthreads();
+  for (int k = threadIdx.x; k < nstaged * CPR * NQ; k += blockDim.x) {
+    const int sl = k / (CPR * NQ), rem = k - sl * CPR * NQ, q = rem >> LCPR, g = rem & (CPR - 1);
+    const int64_t c = R.rid[sl] * CPR + g;
+    if (c < nch) part[q * pstride + c] = tree8(&R.wsr[sl][q][8 * g]);
+  }
+  __syncthreads();
+}
 
 // Per-round commit: warp trees of up to 3 quantities -> 8-way trees -> level-1
 // partials of the 4 chunks of this round.
@@ -68,8 +103,8 @@ __device__ __forceinline__ void commit_round(Red& R, int NQ, const double* val, 
     if (lane == 0) R.ws[q][w] = v;
   }
   __syncthreads();
-  if ((int)threadIdx.x < 4 * NQ) {
-    const int g = threadIdx.x & 3, q = threadIdx.x >> 2;
+  if ((int)threadIdx.x < CPR * NQ) {
+    const int g = threadIdx.x & (CPR - 1), q = threadIdx.x >> LCPR;
     if (chunk0 + g < nch) part[q * pstride + chunk0 + g] = tree8(&R.ws[q][8 * g]);
   }
   __syncthreads();
@@ -85,12 +120,12 @@ __device__ __forceinline__ void reduce_small(Red& R, int q, const double* src, i
     return;
   }
   const int P2 = (P + 255) / 256;
-  for (int c0 = 0; c0 < P2; c0 += 4) {  // 4 chunks of 256 partials per pass
+  for (int c0 = 0; c0 < P2; c0 += CPR) {  // CPR chunks of 256 partials per pass
     const int idx = c0 * 256 + threadIdx.x;
     double v = warp_tree(idx < P ? src[idx] : 0.0);
     if (lane == 0) R.ws[q][w] = v;
     __syncthreads();
-    if (threadIdx.x < 4 && c0 + (int)threadIdx.x < P2) R.lvl[q][c0 + threadIdx.x] = tree8(&R.ws[q][8 * threadIdx.x]);
+    if ((int)threadIdx.x < CPR && c0 + (int)threadIdx.x < P2) R.lvl[q][c0 + threadIdx.x] = tree8(&R.ws[q][8 * threadIdx.x]);
     __syncthreads();
   }
   if (P2 == 1) {
@@ -134,7 +169,14 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
   const double* __restrict__ val = a.ell_val;
   int32_t cl[6];
 #pragma unroll
-  for (int s = 0; s < 6; ++s) cl[s] = (s < a.nslot) ? __ldg(&col[s * a.cap + l]) : -1;
+  for (int s = 0; s < 6; ++s) cl[s] = -1;
+  if (a.implicit) {
+    implicit_cols(a.nx, a.ny, a.nz, a.d3, l, cl);
+  } else {
+#pragma unroll
+    for (int s = 0; s < 6; ++s)
+      if (s < a.nslot) cl[s] = __ldg(&col[s * a.cap + l]);
+  }
   double xv[6][B];
 #pragma unroll
   for (int s = 0; s < 6; ++s)
@@ -158,7 +200,9 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
   }
 }
 
-template <int B>
+// FUSE is a template parameter: the two variants have different live state,
+// and one kernel holding both spills heavily at 64 registers / thread.
+template <int B, bool FUSE>
 __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   __shared__ Red R;
   const bool single = gridDim.x == 1;
@@ -168,52 +212,68 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   };
   const int64_t nr = a.nA;
   const int64_t nch = (nr + 255) / 256;
-  const int64_t nrounds = (nch + 3) / 4;
+  const int64_t nrounds = (nch + CPR - 1) / CPR;
   const int tid = threadIdx.x;
 
-  // global canonical reduction of NQ quantities whose level-1 partials are in a.part
-  auto reduce = [&](int NQ) {
+  // global canonical reduction of NQ quantities whose level-1 partials are in
+  // a.part (quantity 1 of the init may come from the assembly's part_f2)
+  auto reduce = [&](int NQ, const double* src1 = nullptr) {
     sync();
     const int P1 = (int)nch;
+    auto src = [&](int q) { return (q == 1 && src1) ? src1 : a.part + q * a.pstride; };
     if (P1 <= 64 * 256) {
-      for (int q = 0; q < NQ; ++q) reduce_small(R, q, a.part + q * a.pstride, P1);
+      for (int q = 0; q < NQ; ++q) reduce_small(R, q, src(q), P1);
     } else {
       // distributed level 2, one more barrier, then the (small) rest per CTA
       const int P2 = (P1 + 255) / 256;
-      for (int64_t rr = blockIdx.x; rr * 4 < P2; rr += gridDim.x) {
-        const int64_t c2 = rr * 4 + (tid >> 8);
+      for (int64_t rr = blockIdx.x; rr * CPR < P2; rr += gridDim.x) {
+        const int64_t c2 = rr * CPR + (tid >> 8);
         const int64_t idx = c2 * 256 + (tid & 255);
         double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-        for (int q = 0; q < NQ; ++q) v[q] = idx < P1 ? a.part[q * a.pstride + idx] : 0.0;
-        commit_round(R, NQ, v, rr * 4, P2, a.part2, a.pstride2);
+        for (int q = 0; q < NQ; ++q) v[q] = idx < P1 ? src(q)[idx] : 0.0;
+        commit_round(R, NQ, v, rr * CPR, P2, a.part2, a.pstride2);
       }
       sync();
       for (int q = 0; q < NQ; ++q) reduce_small(R, q, a.part2 + q * a.pstride2, P2);
     }
   };
 
-#define ROUNDS_BEGIN                                             \
-  for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) { \
-    const int64_t l = rd * KT + tid;                             \
-    const bool ok = l < nr;                                      \
+#define ROUNDS_BEGIN                                                         \
+  {                                                                          \
+  int rloc = 0;                                                              \
+  for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x, ++rloc) {     \
+    const int64_t l = rd * KT + tid;                                         \
+    const bool ok = l < nr;                                                  \
     double val[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#define ROUNDS_END(NQ)                                           \
-  commit_round(R, NQ, val, rd * 4, nch, a.part, a.pstride);      \
+#define ROUNDS_END(NQ)                                                       \
+    {                                                                        \
+      const int slot = rloc % a.stage;                                       \
+      const bool last = rd + gridDim.x >= nrounds;                           \
+      stage_round(R, NQ, val, slot, rd, slot == a.stage - 1 || last, slot + 1, nch, a.part, a.pstride); \
+    }                                                                        \
+  }                                                                          \
   }
 
-  // ---- init: r = r0 = rhs, x = 0;  (rhs, rhs), (F, F)
+  // ---- init: r = r0 = rhs, x = 0;  (rhs, rhs), (F, F) (the latter from the
+  //      assembly's canonical chunk partials when it left them)
+  const int nq_init = a.f2_parts ? 1 : 2;
   ROUNDS_BEGIN
   if (ok) {
-    double bv[B], fv[B];
+    double bv[B];
 #pragma unroll
-    for (int e = 0; e < B; ++e) { bv[e] = a.rhs[l * B + e]; fv[e] = a.F_raw[l * B + e]; }
+    for (int e = 0; e < B; ++e) bv[e] = a.rhs[l * B + e];
 #pragma unroll
     for (int e = 0; e < B; ++e) { a.r[l * B + e] = bv[e]; a.r0[l * B + e] = bv[e]; a.x[l * B + e] = 0.0; }
     val[0] = rsim::blk::rowdot<B>(bv, bv);
-    val[1] = rsim::blk::rowdot<B>(fv, fv);
+    if (!a.f2_parts) {
+      double fv[B];
+#pragma unroll
+      for (int e = 0; e < B; ++e) fv[e] = a.F_raw[l * B + e];
+      val[1] = rsim::blk::rowdot<B>(fv, fv);
+    }
   }
-  ROUNDS_END(2)
-  reduce(2);
+  ROUNDS_END(nq_init)
+  reduce(2, a.f2_parts ? a.part_f2 : nullptr);
   const double bb = R.res[0];
   if (blockIdx.x == 0 && tid == 0) a.dsc->f2 = sqrt(R.res[1]);
   const double bnorm = sqrt(bb);
@@ -232,7 +292,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   // fuse: neighbours' p and s are recomputed at the gather site (fewer grid
   // barriers, latency regime); !fuse: owners store p and s, then a barrier,
   // then plain gathers (less memory traffic, bandwidth regime).
-  const bool fuse = a.fuse != 0;
+  constexpr bool fuse = FUSE;
   int it_total = 0;
   // attempt 0: as configured; attempt 1 (only after a Neumann-1 breakdown or
   // cap): block-Jacobi only, restarted from x0 = 0 (same rule as the oracle)
@@ -447,12 +507,20 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.nslot = c->nslot;
   a.maxit = o->lin_maxit;
   a.fixed = o->fixed_lin_iters;
+  a.nx = c->nx; a.ny = c->ny; a.nz = c->nz;
+  a.d3 = c->d3;
+  a.implicit = c->cols_implicit;
+  // staging lets warps drift apart by several rounds: good for the regular
+  // full-grid sweep, bad for L1 reuse of scattered gathers on partial sets
+  a.stage = c->cols_implicit ? RSTAGE : 1;
   a.cap = c->n;
   a.has_nnc = c->has_nnc;
   a.rtol = o->lin_rtol;
   a.ell_col = c->ell_col; a.ell_val = c->ell_val;
   a.act = c->act; a.nptr = c->nptr; a.nnc_lcol = c->nnc_lcol; a.nnc_val = c->nnc_val;
   a.rhs = c->rhs; a.F_raw = c->F_raw;
+  a.part_f2 = c->part_f2;
+  a.f2_parts = c->f2_parts;
   a.x = c->x; a.r = c->r; a.r0 = c->r0; a.p = c->p; a.v = c->v; a.s = c->s; a.t = c->t;
   a.p2 = c->p2; a.v2 = c->v2; a.ph = c->ph; a.sh = c->sh;
   a.neu = o->precond == RSIM_PREC_NEUMANN1;
@@ -462,10 +530,13 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.part = c->part;
   a.part2 = c->part + 5 * (int64_t)a.pstride;
   a.dsc = c->dsc;
-  const int64_t nrounds = ((c->nA + 255) / 256 + 3) / 4;
+  const int64_t nrounds = ((c->nA + 255) / 256 + CPR - 1) / CPR;
+  auto kern = a.fuse ? k_bicgstab<B, true> : k_bicgstab<B, false>;
   if (c->max_coop_blocks[B] == 0) {
-    int per_sm = 0;
-    RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bicgstab<B>, KT, 0));
+    int per_sm = 0, per_sm2 = 0;
+    RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bicgstab<B, true>, KT, 0));
+    RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_bicgstab<B, false>, KT, 0));
+    if (per_sm2 < per_sm) per_sm = per_sm2;
     c->max_coop_blocks[B] = per_sm * c->sm_count;
     if (c->max_coop_blocks[B] < 1) c->max_coop_blocks[B] = 1;
   }
@@ -473,9 +544,9 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   if (grid < 1) grid = 1;
   void* args[] = {&a};
   if (grid == 1) {
-    k_bicgstab<B><<<1, KT, 0, c->stream>>>(a);
+    kern<<<1, KT, 0, c->stream>>>(a);
   } else {
-    RSIM_CUDA(cudaLaunchCooperativeKernel((void*)k_bicgstab<B>, grid, KT, args, 0, c->stream));
+    RSIM_CUDA(cudaLaunchCooperativeKernel((void*)kern, grid, KT, args, 0, c->stream));
   }
   c->launches++;
   RSIM_CUDA(cudaGetLastError());

@@ -621,7 +621,7 @@ int dsm_disabled() {
 }  // namespace
 
 int launch_krylov_dsm(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
-  if (dsm_disabled() || c->nA <= 0) return RSIM_ENOTAPPLICABLE;
+  if (dsm_disabled() || c->nA <= 0 || c->cols_implicit || (c->f2_parts && !c->keep_F)) return RSIM_ENOTAPPLICABLE;
   const int nch = (c->nA + RSIM_RED_CHUNK - 1) / RSIM_RED_CHUNK;
   if (nch > 4 * GMAX) return RSIM_ENOTAPPLICABLE;
   DArgs a;
