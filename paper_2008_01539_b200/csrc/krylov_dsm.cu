@@ -43,6 +43,10 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int r) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(o) : "r"(a), "r"(r));
   return o;
 }
+#ifndef RSIM_DSM_TRACE
+#define RSIM_DSM_TRACE 0
+#endif
+constexpr bool kTrace = RSIM_DSM_TRACE != 0;
 constexpr int GMAX = 16;
 constexpr int NNCMAX = 256;             // NNC entries cached in smem per CTA
 constexpr int NNC_GLOBAL = 0x40000000;  // flag in the range end: entries stay in global
@@ -85,15 +89,15 @@ template <int B, int NS, bool MS, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   // Shared layout (identical in every CTA, so a neighbour row's cluster
   // address is mapa(base, owner) + row offset, computed once per solve):
-  //   V[RC][9][BP]: per row r, p0, p1, v0, v1, ph, sh, s, t (p, v
+  //   V[RC][11][BP]: per row r, p0, p1, v0, v1, ph, sh, s, t, r0, x (p, v
   //   double-buffered: neighbours read the previous iterate while the owner
   //   writes the new one; s, t feed the neighbours' recompute of r)
   //   mval[NS][RC][B*B] (MS), NNC ranges, NNC blocks + cluster addresses.
   // Own-row-only vectors r0, x, s, t live in registers.
   constexpr int BP = (B == 3) ? 4 : B;
-  constexpr int ROWD = 9 * BP;
+  constexpr int ROWD = 11 * BP;
   constexpr uint32_t ROWB = ROWD * 8;
-  constexpr int O_R = 0, O_P = 1, O_V = 3, O_PH = 5, O_SH = 6, O_S = 7, O_T = 8;
+  constexpr int O_R = 0, O_P = 1, O_V = 3, O_PH = 5, O_SH = 6, O_S = 7, O_T = 8, O_R0 = 9, O_X = 10;
   extern __shared__ __align__(16) double dyn[];
   const int RC = 1 << a.LRC;
   double* V = dyn;
@@ -136,15 +140,17 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   // cluster.sync() with its MEMBAR.GPU (scripts/micro/xchg.cu).
   __shared__ unsigned long long tc[8];  // RSIM_KTRACE cycle accumulators (rank 0, thread 0)
   __shared__ unsigned long long tcr[8];  // per-CTA: [0,1] csync wait, [2,3] spmv, [4] reduce tail (warp 0 / last warp)
-  const bool tr = a.trace && rank == 0 && tid == 0;
-  const int trw = (a.trace && lane == 0) ? (w == 0 ? 1 : (w == (RC >> 5) - 1 ? 2 : 0)) : 0;
-  if (a.trace && tid < 8) tcr[tid] = 0;
+  // tracing is compiled in only with -DRSIM_DSM_TRACE (its registers cost the
+  // 512-thread variant spills); RSIM_KTRACE=1 then enables it at run time
+  const bool tr = kTrace && a.trace && rank == 0 && tid == 0;
+  const int trw = (kTrace && a.trace && lane == 0) ? (w == 0 ? 1 : (w == (RC >> 5) - 1 ? 2 : 0)) : 0;
+  if (kTrace && a.trace && tid < 8) tcr[tid] = 0;
   auto csync = [&]() {
-    const long long tb = (tr || trw) ? clock64() : 0;
+    const long long tb = (kTrace && (tr || trw)) ? clock64() : 0;
     __syncthreads();
     if (G > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
-    if (tr) tc[6] += (unsigned long long)(clock64() - tb);
-    if (trw) tcr[trw - 1] += (unsigned long long)(clock64() - tb);
+    if (kTrace && tr) tc[6] += (unsigned long long)(clock64() - tb);
+    if (kTrace && trw) tcr[trw - 1] += (unsigned long long)(clock64() - tb);
   };
   // Canonical reduction of NQ per-row values (one per thread): warp trees into
   // shared memory, ONE cluster barrier, then warp q of every CTA gathers the 8
@@ -163,7 +169,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
 #pragma unroll
       for (int q = 0; q < NQ; ++q) ws[wbuf][q][w] = v[q];
     csync();
-    const long long t_tail = trw == 1 ? clock64() : 0;
+    const long long t_tail = (kTrace && trw == 1) ? clock64() : 0;
     for (int q = w; q < NQ; q += (1 << LWPC)) {  // warp w finishes quantities w, w+WPC, ...
       double cp[2] = {0.0, 0.0};
 #pragma unroll
@@ -194,7 +200,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < NQ; ++q) out[q] = res_s[q];
-    if (trw == 1) tcr[4] += (unsigned long long)(clock64() - t_tail);
+    if (kTrace && trw == 1) tcr[4] += (unsigned long long)(clock64() - t_tail);
     wbuf ^= 1;
   };
   auto xbar = [&]() { csync(); };
@@ -240,20 +246,30 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
 
   // y = xown + Σ_slots Â_s x_col (+ NNC), canonical order
   auto spmv = [&](auto MODEc, int offo, const double* xown, double beta, double omega, double alpha, double* y) {
-    const long long t_sp = trw ? clock64() : 0;
-    double xv[NS][B];
-#pragma unroll
-    for (int s = 0; s < NS; ++s)
-      if (nmask & (1u << s)) gather(MODEc, na[s], offo, beta, omega, alpha, xv[s]);
+    const long long t_sp = (kTrace && trw) ? clock64() : 0;
+    // slots in groups of SG (all in flight within a group); the 512/1024-thread
+    // variants (128/64 registers) use SG = 2 so the gathered rows do not spill.
+    // The accumulation order (slots ascending) is unchanged.
+    constexpr int SG = MAXT <= 256 ? NS : 2;
     double acc[B];
 #pragma unroll
     for (int e = 0; e < B; ++e) acc[e] = xown[e];
 #pragma unroll
-    for (int s = 0; s < NS; ++s)
-      if (nmask & (1u << s)) {
-        const double* M = MS ? &mval[((size_t)s * RC + lam) * B * B] : &a.ell_val[((int64_t)s * a.cap + l) * B * B];
-        rsim::blk::gemv_acc_flat<B>(M, xv[s], acc);
+    for (int s0 = 0; s0 < NS; s0 += SG) {
+      double xv[SG][B];
+#pragma unroll
+      for (int k = 0; k < SG; ++k)
+        if (s0 + k < NS && (nmask & (1u << (s0 + k)))) gather(MODEc, na[s0 + k], offo, beta, omega, alpha, xv[k]);
+#pragma unroll
+      for (int k = 0; k < SG; ++k) {
+        const int s = s0 + k;
+        if (s < NS && (nmask & (1u << s))) {
+          const double* M = MS ? &mval[((size_t)s * RC + lam) * B * B] : &a.ell_val[((int64_t)s * a.cap + l) * B * B];
+          rsim::blk::gemv_acc_flat<B>(M, xv[k], acc);
+        }
       }
+      if (SG < NS) asm volatile("" ::: "memory");  // keep the next group's loads after this group's math
+    }
     if (a.has_nnc) {
       const int2 rg = nrng[lam];
       if (rg.y & NNC_GLOBAL) {
@@ -275,13 +291,16 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
     }
 #pragma unroll
     for (int e = 0; e < B; ++e) y[e] = acc[e];
-    if (trw) tcr[1 + trw] += (unsigned long long)(clock64() - t_sp);
+    if (kTrace && trw) tcr[1 + trw] += (unsigned long long)(clock64() - t_sp);
   };
 
-  double r0r[B], xr[B], sr[B], tr_[B];
+  // own-row r0 and x live in shared memory (register pressure of the 512-thread variant)
+  double* r0r = Vo + O_R0 * BP;
+  double* xr = Vo + O_X * BP;
+  double sr[B], tr_[B];
   double res[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-  for (int e = 0; e < B; ++e) { r0r[e] = 0.0; xr[e] = 0.0; sr[e] = 0.0; tr_[e] = 0.0; }
+  for (int e = 0; e < B; ++e) { sr[e] = 0.0; tr_[e] = 0.0; }
   // ---- load: matrix rows (MS), neighbour addresses, rhs -> r, r0; x = 0; (b,b), (F,F)
   if (tid == 0) nnc_cnt = 0;
   __syncthreads();
@@ -328,7 +347,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
         if (cl >= 0) {
           nmask |= 1u << s;
           na[s] = caddr(cl);
-          if (a.trace && (cl >> LSH) != rank) atomicAdd(&tcr[5], 1ull);
+          if (kTrace && a.trace && (cl >> LSH) != rank) atomicAdd(&tcr[5], 1ull);
           if (MS)
 #pragma unroll
             for (int e = 0; e < B * B; ++e)
@@ -353,7 +372,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
     status = RSIM_ENOCONV;
     if (tr)
       for (int k = 0; k < 8; ++k) tc[k] = 0;
-    long long t0 = clock64();
+    long long t0 = kTrace ? clock64() : 0;
 #define KT_MARK(k) do { if (tr) { long long t1 = clock64(); tc[k] += (unsigned long long)(t1 - t0); t0 = t1; } } while (0)
     int it_total = 0;
     // attempt 0: as configured; attempt 1 (only after a Neumann-1 breakdown or
@@ -522,7 +541,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   if (valid)
 #pragma unroll
     for (int e = 0; e < B; ++e) a.x[l * B + e] = xr[e];
-  if (a.trace) {
+  if (kTrace && a.trace) {
     if (valid) atomicAdd(&tcr[6], 1ull);
     __syncthreads();
     if (tid < 8) atomicAdd(&a.trace[8 + rank * 8 + tid], tcr[tid]);
@@ -538,7 +557,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
 size_t smem_bytes(int B, int NS, bool MS, int LRC) {
   const size_t R = (size_t)1 << LRC;
   const size_t BP = (B == 3) ? 4 : B;
-  size_t b = 9 * R * BP * sizeof(double) + R * sizeof(int2) + NNCMAX * (B * B * sizeof(double) + sizeof(const double*));
+  size_t b = 11 * R * BP * sizeof(double) + R * sizeof(int2) + NNCMAX * (B * B * sizeof(double) + sizeof(const double*));
   if (MS) b += NS * R * B * B * sizeof(double);
   return b;
 }
