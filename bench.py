@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import argparse
 import json
+from pathlib import Path
 import os
 import subprocess
 import sys
@@ -418,8 +419,20 @@ def main():
         alg = int(cnt[4]) * bytes_k7(case.n, 0, 2)
         per_launch_units = f"{bytes_k7(case.n, 0, 2)} B per full-grid set update"
     achieved = alg / (phase_ms[dom] / 1e3) / 1e9
+    # measured DRAM traffic per launch of that kernel (ncu --set full, committed
+    # under profiles/): compare with the algorithmic bytes per launch
+    kern = {0: "k_scatter_rg", 1: "k_assemble", 2: "k_krylov_dsm", 3: "k_update"}[dom]
+    traffic = None
+    try:
+        tj = json.load(open(Path(__file__).resolve().parent / "profiles" / "r01_traffic.json"))
+        traffic = tj["dram_bytes_per_launch"].get(kern)
+    except (OSError, ValueError, KeyError):
+        pass
+    launches_dom = solves if dom == 2 else max(1, iters_per_run * args.steps)
     roof = {"kernel": names[dom], "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": None,
+            "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": traffic,
+            "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/r01_ncu_summary.md)",
+            "algorithmic_bytes_per_launch": alg / launches_dom,
             "algorithmic_bytes": per_launch_units,
             "phase_ms_per_step": {k: float(v) / args.steps for k, v in zip(names, phase_ms)},
             "krylov_solves_per_step": solves / args.steps, "krylov_row_iters_per_step": row_iters / args.steps}
