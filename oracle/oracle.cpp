@@ -366,6 +366,106 @@ static int bicgstab_once(const Model& M, const rsim_solver_opts& o, bool neu, do
   return fixed ? RSIM_OK : RSIM_ENOCONV;
 }
 
+// GMRES(m), m = RSIM_GMRES_M, right-preconditioned (block-Jacobi fused into Â:
+// M = I; or the Neumann-1 polynomial), x0 = 0, classical Gram-Schmidt (the
+// j+1 projections (w, v_i) are reduced together, then w -= Σ h_ij v_i in
+// ascending i), Givens rotations on the Hessenberg column, restart from the
+// true residual r = b − Â x.  Convergence on the Givens residual estimate
+// |g_{j+1}| <= rtol·‖b‖ (also a happy breakdown h_{j+1,j} = 0).  Element
+// formulas and reduction order are the contract krylov_gmres.cu follows.
+template <int B>
+static int gmres(const Model& M, const rsim_solver_opts& o, bool neu, double* x, int32_t* iters, double* relres) {
+  constexpr int MM = RSIM_GMRES_M;
+  const int64_t nr = M.nA, N = nr * B;
+  std::vector<double> r(M.rhs), V((int64_t)(MM + 1) * N), z(N), w(N), y(N), u(N);
+  auto prec = [&](const double* in, double* out) {  // out = M^{-1} in
+    if (!neu) {
+      std::copy(in, in + N, out);
+      return;
+    }
+    spmv<B>(M, in, y.data());
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < N; ++e) out[e] = in[e] + (in[e] - y[e]);
+  };
+  std::fill(x, x + N, 0.0);
+  double beta = std::sqrt(dotc<B>(nr, r.data(), r.data()));
+  const double bnorm = beta;
+  *iters = 0;
+  *relres = 0.0;
+  if (bnorm == 0.0) return RSIM_OK;
+  const bool fixed = o.fixed_lin_iters > 0;
+  const int maxit = fixed ? o.fixed_lin_iters : o.lin_maxit;
+  const double tol = o.lin_rtol * bnorm;
+  double H[MM + 1][MM], cs[MM], sn[MM], g[MM + 1], yy[MM];
+  int total = 0;
+  for (;;) {
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < N; ++e) V[e] = r[e] / beta;
+    for (int q = 0; q <= MM; ++q) g[q] = 0.0;
+    g[0] = beta;
+    int k = 0;
+    bool done = false;
+    double resid = beta;
+    for (int j = 0; j < MM; ++j) {
+      const double* vj = &V[(int64_t)j * N];
+      prec(vj, z.data());
+      spmv<B>(M, z.data(), w.data());
+      for (int i = 0; i <= j; ++i) H[i][j] = dotc<B>(nr, w.data(), &V[(int64_t)i * N]);
+#pragma omp parallel for schedule(static)
+      for (int64_t e = 0; e < N; ++e) {
+        double we = w[e];
+        for (int i = 0; i <= j; ++i) we = we - H[i][j] * V[(int64_t)i * N + e];
+        w[e] = we;
+      }
+      const double hn = std::sqrt(dotc<B>(nr, w.data(), w.data()));
+      H[j + 1][j] = hn;
+      for (int i = 0; i < j; ++i) {
+        const double t = cs[i] * H[i][j] + sn[i] * H[i + 1][j];
+        H[i + 1][j] = -sn[i] * H[i][j] + cs[i] * H[i + 1][j];
+        H[i][j] = t;
+      }
+      const double den = std::sqrt(H[j][j] * H[j][j] + hn * hn);
+      if (den == 0.0 || !std::isfinite(den)) { *iters = total + 1; return RSIM_ENUM; }
+      cs[j] = H[j][j] / den;
+      sn[j] = hn / den;
+      H[j][j] = cs[j] * H[j][j] + sn[j] * hn;
+      H[j + 1][j] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      ++total;
+      k = j + 1;
+      resid = std::fabs(g[j + 1]);
+      if (hn == 0.0 || (!fixed && resid <= tol) || total >= maxit) { done = true; break; }
+#pragma omp parallel for schedule(static)
+      for (int64_t e = 0; e < N; ++e) V[(int64_t)(j + 1) * N + e] = w[e] / hn;
+    }
+    for (int i = k - 1; i >= 0; --i) {  // back substitution
+      double t = g[i];
+      for (int l = i + 1; l < k; ++l) t = t - H[i][l] * yy[l];
+      yy[i] = t / H[i][i];
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < N; ++e) {
+      double ue = yy[0] * V[e];
+      for (int i = 1; i < k; ++i) ue = ue + yy[i] * V[(int64_t)i * N + e];
+      u[e] = ue;
+    }
+    prec(u.data(), z.data());
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < N; ++e) x[e] = x[e] + z[e];
+    *iters = total;
+    *relres = resid / bnorm;
+    if (done && (fixed ? total >= maxit : (resid <= tol || resid == 0.0))) return RSIM_OK;
+    if (total >= maxit) return fixed ? RSIM_OK : RSIM_ENOCONV;
+    // restart from the true residual
+    spmv<B>(M, x, y.data());
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < N; ++e) r[e] = M.rhs[e] - y[e];
+    beta = std::sqrt(dotc<B>(nr, r.data(), r.data()));
+    if (beta == 0.0) return RSIM_OK;
+  }
+}
+
 // Neumann-1 preconditioned solve with a deterministic fallback: if it breaks
 // down or hits the cap, the solve restarts from x0 = 0 with block-Jacobi only
 // (the Neumann polynomial is not guaranteed positive on non-M-matrix blocks,
@@ -373,10 +473,14 @@ static int bicgstab_once(const Model& M, const rsim_solver_opts& o, bool neu, do
 template <int B>
 static int bicgstab(const Model& M, const rsim_solver_opts& o, double* x, int32_t* iters, double* relres) {
   const bool neu = o.precond == RSIM_PREC_NEUMANN1;
-  int st = bicgstab_once<B>(M, o, neu, x, iters, relres);
+  const bool gm = o.lin_method == RSIM_LIN_GMRES;
+  auto once = [&](bool n, int32_t* it) {
+    return gm ? gmres<B>(M, o, n, x, it, relres) : bicgstab_once<B>(M, o, n, x, it, relres);
+  };
+  int st = once(neu, iters);
   if (neu && (st == RSIM_ENUM || st == RSIM_ENOCONV)) {
     int32_t it2 = 0;
-    st = bicgstab_once<B>(M, o, false, x, &it2, relres);
+    st = once(false, &it2);
     *iters += it2;
   }
   return st;

@@ -65,6 +65,8 @@ struct rsim_gpu_ctx {
   bool cols_implicit = false;  // last assembly: V_A = all cells, ELL columns not stored (structural)
   bool f2_parts = false;       // last assembly left (F,F) chunk partials in part_f2 (F_raw only if keep_F)
   bool keep_F = false;         // debug: the row kernel also stores the raw residual
+  double* gm_V = nullptr;      // GMRES basis (RSIM_GMRES_M + 1 vectors), allocated on first use
+  double* gm_part = nullptr;   // GMRES reduction partials
   int64_t nnc_total = 0;
   rsim_fluid_params fl{};
   double bhp = 0.0;
@@ -165,6 +167,7 @@ int launch_categories(rsim_gpu_ctx* c, uint8_t* dev_out);
 int launch_seed_support(rsim_gpu_ctx* c, double eps);
 int launch_reset_seed(rsim_gpu_ctx* c, double eps);
 int launch_materialize_cols(rsim_gpu_ctx* c);
+int launch_gmres(rsim_gpu_ctx* c, const rsim_solver_opts* o);
 int launch_state_from_dp(rsim_gpu_ctx* c, double p_hi, double scale);
 
 // ---- device helpers ------------------------------------------------------------

@@ -557,6 +557,7 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
 
 int launch_krylov(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   if (c->nA <= 0) return RSIM_OK;
+  if (o->lin_method == RSIM_LIN_GMRES) return launch_gmres(c, o);
   {  // small systems: one cluster with matrix + vectors in distributed smem
     int r = launch_krylov_dsm(c, o);
     if (r != RSIM_ENOTAPPLICABLE) return r;

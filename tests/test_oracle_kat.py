@@ -553,3 +553,27 @@ def test_mass_balance_closed_system():
     F = o.assemble_raw(np.arange(c.n, dtype=np.int32))[0]
     mass = c.pv.sum() * c.fluid.rho_ref[1]
     assert abs(F.sum()) * DAY <= 1e-10 * mass
+
+
+def test_oracle_gmres_solves_the_system():
+    """GMRES(30) in the oracle: the solution satisfies Â x = rhs to the
+    tolerance (dense check), and agrees with BiCGSTAB's solution."""
+    import scipy.sparse as sp
+    case = pkg.Case(2, nx=24, ny=24, n_dfn=6)
+    orc = Oracle(case)
+    s = case.init_state()
+    s.u[::2] -= np.linspace(0, 2e6, case.n)
+    orc.set_state(s, 86400.0)
+    act = np.arange(case.n, dtype=np.int32)
+    F, rhs, rp, col, val = orc.assemble(act)
+    b = case.b
+    A = (sp.identity(case.n * b) + sp.bsr_matrix((val.reshape(-1, b, b), col, rp),
+                                                 shape=(case.n * b, case.n * b))).tocsr()
+    for pc in (0, 2):
+        o = case.solver_opts(lin_method=1, precond=pc, lin_rtol=1e-11)
+        rc, x, it, rr = orc.linear_solve(case.n, o)
+        assert rc == 0 and it > 0
+        assert np.linalg.norm(A @ x - rhs) <= 1e-9 * np.linalg.norm(rhs)
+        o2 = case.solver_opts(lin_method=0, precond=pc, lin_rtol=1e-11)
+        _, x2, _, _ = orc.linear_solve(case.n, o2)
+        assert np.allclose(x, x2, rtol=1e-6, atol=1e-9 * np.abs(x2).max())
