@@ -236,8 +236,10 @@ def _cpu_model():
     return None
 
 
-def c5_sweep(pkg, fractions, reps, hbm):
-    """Config 5: K7 compaction, K1 assembly, 50 BiCGSTAB iterations per active fraction."""
+def c5_sweep(pkg, fractions, reps, hbm, ilu_fracs=()):
+    """Config 5: K7 compaction, K1 assembly, 50 BiCGSTAB iterations per active fraction
+    (block-Jacobi); the ILU(0) second row at the fractions in ilu_fracs
+    (level-scheduled factorisation + 50 iterations, one timed run)."""
     import ctypes as C
     case = pkg.Case(5)
     sim = pkg.GpuSimulator(case)
@@ -276,6 +278,16 @@ def c5_sweep(pkg, fractions, reps, hbm):
                 L.rsim_gpu_elapsed(ctx, a, bb, C.byref(v))
                 ms[key].append(v.value)
         m = {k: float(np.median(v)) for k, v in ms.items()}
+        ilu = None
+        if any(abs(frac - f) < 1e-9 for f in ilu_fracs):
+            oi = case.solver_opts(fixed_lin_iters=50, lin_maxit=50, precond=pkg.PREC_ILU0)
+            for r in range(2):
+                L.rsim_gpu_mark(ctx, 14)
+                L.rsim_gpu_linear_solve(ctx, C.byref(oi))
+                L.rsim_gpu_mark(ctx, 15)
+            v = C.c_double()
+            L.rsim_gpu_elapsed(ctx, 14, 15, C.byref(v))
+            ilu = v.value
         by7 = bytes_k7(n, nA, 2)
         by1 = nA * bytes_assembly_row(b, 3, s)
         byk = nA * (50 * bytes_krylov_row_iter(b, s) + bytes_krylov_row_init(b))
@@ -288,6 +300,8 @@ def c5_sweep(pkg, fractions, reps, hbm):
             "k7_frac": by7 / m["k7"] / 1e6 / hbm,
             "active_cell_iters_per_s": nA / ((m["k7"] + m["k1"] + m["krylov"]) / 1e3),
         })
+        if ilu is not None:
+            out[-1]["krylov50_ilu0_ms"] = ilu  # includes the per-assembly level schedule + factorisation
     sim.close()
     return out
 
@@ -299,6 +313,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--c5", default="0.05,1.0", help="config-5 active fractions ('' to skip)")
+    ap.add_argument("--c5-ilu", default="0.05", help="fractions that also get the ILU(0) row ('' to skip)")
     ap.add_argument("--c5-reps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--precond", type=int, default=None,
@@ -454,7 +469,8 @@ def main():
     sim.close()
     if rank == 0 and args.c5:
         fr = [float(x) for x in args.c5.split(",") if x]
-        line["c5_sweep"] = c5_sweep(pkg, fr, args.c5_reps, hbm)
+        ilu_fr = [float(x) for x in args.c5_ilu.split(",") if x.strip()]
+        line["c5_sweep"] = c5_sweep(pkg, fr, args.c5_reps, hbm, ilu_fr)
     if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(case, s0, dts, opts)
     barrier(dist)

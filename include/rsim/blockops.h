@@ -81,6 +81,16 @@ RSIM_HD void gemv_acc_flat(const double* M, const double* x, double* y) {
   }
 }
 
+/* y = M x, flat row-major block. */
+template <int B>
+RSIM_HD void gemv_flat(const double* M, const double* x, double* y) {
+  for (int r = 0; r < B; ++r) {
+    double s = M[r * B] * x[0];
+    for (int c = 1; c < B; ++c) s = s + M[r * B + c] * x[c];
+    y[r] = s;
+  }
+}
+
 /* y -= M x, flat row-major block. */
 template <int B>
 RSIM_HD void gemv_sub_flat(const double* M, const double* x, double* y) {

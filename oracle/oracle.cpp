@@ -280,17 +280,105 @@ static double dotc(int64_t nrows, const double* a, const double* b) {
   return canon_reduce(nrows, [a, b](int64_t l) { return blk::rowdot<B>(a + l * B, b + l * B); });
 }
 
+// Block ILU(0) of the unit-block-diagonal Â in the local (natural) ordering
+// (north star "level-scheduled ILU(0)"): rows in ascending
+// order (IKJ); row i: for each lower entry k (ascending column) L_ik = A_ik
+// D_k^{-1}, then A_ij -= L_ik U_kj over row k's upper entries (ascending j) that
+// exist in row i (j == i: the diagonal block).  A GPU level schedule computes
+// each row with exactly these operations in this order, so the factors and the
+// triangular solves are bit-identical whatever the schedule.
+template <int B>
+struct Ilu0 {
+  std::vector<int64_t> ptr;   // rows: entries sorted by column, diagonal excluded
+  std::vector<int32_t> col;
+  std::vector<double> val;    // L (col < row) / U (col > row) blocks
+  std::vector<double> dinv;   // inverse diagonal blocks of U
+  std::vector<double> tmp;
+};
+
+template <int B>
+static bool ilu0_factor(const Model& M, Ilu0<B>& F) {
+  const int32_t n = M.nA;
+  constexpr int BB = B * B;
+  F.ptr.assign(n + 1, 0);
+  F.col.resize(M.col.size());
+  F.val.resize(M.val.size());
+  for (int32_t l = 0; l < n; ++l) {
+    const int64_t a = M.rowptr[l], e = M.rowptr[l + 1];
+    std::vector<std::pair<int32_t, int64_t>> ent;
+    for (int64_t p = a; p < e; ++p) ent.emplace_back(M.col[p], p);
+    std::stable_sort(ent.begin(), ent.end(), [](auto& x, auto& y) { return x.first < y.first; });
+    F.ptr[l + 1] = e;
+    for (int64_t k = 0; k < e - a; ++k) {
+      F.col[a + k] = ent[k].first;
+      for (int q = 0; q < BB; ++q) F.val[(a + k) * BB + q] = M.val[ent[k].second * BB + q];
+    }
+  }
+  F.dinv.assign((int64_t)n * BB, 0.0);
+  std::vector<double> dg(BB);
+  for (int32_t i = 0; i < n; ++i) {
+    for (int q = 0; q < BB; ++q) dg[q] = (q % (B + 1) == 0) ? 1.0 : 0.0;
+    for (int64_t p = F.ptr[i]; p < F.ptr[i + 1] && F.col[p] < i; ++p) {
+      const int32_t k = F.col[p];
+      double L[BB];
+      blk::gemm_flat<B>(&F.val[p * BB], &F.dinv[(int64_t)k * BB], L);
+      for (int q = 0; q < BB; ++q) F.val[p * BB + q] = L[q];
+      for (int64_t r = F.ptr[k]; r < F.ptr[k + 1]; ++r) {
+        const int32_t j = F.col[r];
+        if (j <= k) continue;
+        if (j == i) {
+          blk::gemm_sub_flat<B>(L, &F.val[r * BB], dg.data());
+        } else {
+          for (int64_t t = F.ptr[i]; t < F.ptr[i + 1]; ++t)
+            if (F.col[t] == j) { blk::gemm_sub_flat<B>(L, &F.val[r * BB], &F.val[t * BB]); break; }
+        }
+      }
+    }
+    if (!blk::inv_flat<B>(dg.data(), &F.dinv[(int64_t)i * BB])) return false;
+  }
+  F.tmp.assign((int64_t)n * B, 0.0);
+  return true;
+}
+
+// out = (LU)^{-1} z: forward (unit L) then backward (U) substitution
+template <int B>
+static void ilu0_apply(const Ilu0<B>& F, int32_t n, const double* z, double* out, std::vector<double>& y) {
+  constexpr int BB = B * B;
+  for (int32_t i = 0; i < n; ++i) {
+    double t[B];
+    for (int c = 0; c < B; ++c) t[c] = z[(int64_t)i * B + c];
+    for (int64_t p = F.ptr[i]; p < F.ptr[i + 1] && F.col[p] < i; ++p)
+      blk::gemv_sub_flat<B>(&F.val[p * BB], &y[(int64_t)F.col[p] * B], t);
+    for (int c = 0; c < B; ++c) y[(int64_t)i * B + c] = t[c];
+  }
+  for (int32_t i = n - 1; i >= 0; --i) {
+    double t[B];
+    for (int c = 0; c < B; ++c) t[c] = y[(int64_t)i * B + c];
+    for (int64_t p = F.ptr[i]; p < F.ptr[i + 1]; ++p)
+      if (F.col[p] > i) blk::gemv_sub_flat<B>(&F.val[p * BB], &out[(int64_t)F.col[p] * B], t);
+    blk::gemv_flat<B>(&F.dinv[(int64_t)i * BB], t, &out[(int64_t)i * B]);
+  }
+}
+
 // BiCGSTAB (van der Vorst) on the scaled system  Â x = rhs,  x0 = 0.
 // Element formulas and reduction order are the contract the GPU kernel
 // (csrc/krylov.cu) follows.
 template <int B>
-static int bicgstab_once(const Model& M, const rsim_solver_opts& o, bool neu, double* x, int32_t* iters,
+static int bicgstab_once(const Model& M, const rsim_solver_opts& o, int pk, double* x, int32_t* iters,
                          double* relres) {
   const int64_t nr = M.nA, N = nr * B;
+  const bool neu = pk != RSIM_PREC_BJACOBI;  // a preconditioner on top of the fused block-Jacobi
   std::vector<double> r(M.rhs), r0(M.rhs), p(N, 0.0), v(N, 0.0), s(N), t(N), ph, sh, y;
   if (neu) { ph.assign(N, 0.0); sh.assign(N, 0.0); y.assign(N, 0.0); }
-  // M^{-1} z = z + (z - Â z): first-order Neumann polynomial on the unit-diagonal system
+  Ilu0<B> F;
+  if (pk == RSIM_PREC_ILU0 && !ilu0_factor<B>(M, F)) { *iters = 0; return RSIM_ENUM; }
+  // Neumann-1: M^{-1} z = z + (z - Â z) (first-order polynomial on the unit-diagonal system);
+  // ILU(0): M^{-1} z = (LU)^{-1} z
   auto prec = [&](const std::vector<double>& z, std::vector<double>& out) {
+    if (pk == RSIM_PREC_ILU0) {
+      ilu0_apply<B>(F, M.nA, z.data(), out.data(), y);
+      return;
+    }
     spmv<B>(M, z.data(), y.data());
 #pragma omp parallel for schedule(static)
     for (int64_t e = 0; e < N; ++e) out[e] = z[e] + (z[e] - y[e]);
@@ -374,13 +462,19 @@ static int bicgstab_once(const Model& M, const rsim_solver_opts& o, bool neu, do
 // |g_{j+1}| <= rtol·‖b‖ (also a happy breakdown h_{j+1,j} = 0).  Element
 // formulas and reduction order are the contract krylov_gmres.cu follows.
 template <int B>
-static int gmres(const Model& M, const rsim_solver_opts& o, bool neu, double* x, int32_t* iters, double* relres) {
+static int gmres(const Model& M, const rsim_solver_opts& o, int pk, double* x, int32_t* iters, double* relres) {
   constexpr int MM = RSIM_GMRES_M;
   const int64_t nr = M.nA, N = nr * B;
   std::vector<double> r(M.rhs), V((int64_t)(MM + 1) * N), z(N), w(N), y(N), u(N);
+  Ilu0<B> F;
+  if (pk == RSIM_PREC_ILU0 && !ilu0_factor<B>(M, F)) { *iters = 0; return RSIM_ENUM; }
   auto prec = [&](const double* in, double* out) {  // out = M^{-1} in
-    if (!neu) {
+    if (pk == RSIM_PREC_BJACOBI) {
       std::copy(in, in + N, out);
+      return;
+    }
+    if (pk == RSIM_PREC_ILU0) {
+      ilu0_apply<B>(F, M.nA, in, out, y);
       return;
     }
     spmv<B>(M, in, y.data());
@@ -472,15 +566,15 @@ static int gmres(const Model& M, const rsim_solver_opts& o, bool neu, double* x,
 // e.g. black-oil).  Iterations of both attempts are reported.
 template <int B>
 static int bicgstab(const Model& M, const rsim_solver_opts& o, double* x, int32_t* iters, double* relres) {
-  const bool neu = o.precond == RSIM_PREC_NEUMANN1;
+  const int pk = o.precond;
   const bool gm = o.lin_method == RSIM_LIN_GMRES;
-  auto once = [&](bool n, int32_t* it) {
-    return gm ? gmres<B>(M, o, n, x, it, relres) : bicgstab_once<B>(M, o, n, x, it, relres);
+  auto once = [&](int k, int32_t* it) {
+    return gm ? gmres<B>(M, o, k, x, it, relres) : bicgstab_once<B>(M, o, k, x, it, relres);
   };
-  int st = once(neu, iters);
-  if (neu && (st == RSIM_ENUM || st == RSIM_ENOCONV)) {
+  int st = once(pk, iters);
+  if (pk != RSIM_PREC_BJACOBI && (st == RSIM_ENUM || st == RSIM_ENOCONV)) {
     int32_t it2 = 0;
-    st = once(false, &it2);
+    st = once(RSIM_PREC_BJACOBI, &it2);
     *iters += it2;
   }
   return st;

@@ -272,6 +272,7 @@ int rsim_gpu_destroy(rsim_gpu_ctx* c) {
                   c->gm_V, c->gm_part};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  ilu_free(c);
   if (c->hsc) cudaFreeHost(c->hsc);
   for (auto& e : c->marks)
     if (e) cudaEventDestroy(e);

@@ -43,7 +43,7 @@ struct DevScalars {
   unsigned long long maxB;
   unsigned long long halo;
   int32_t part_count;       // number of K1 F-norm partials
-  int32_t pad1;
+  int32_t ilu_bad;          // ILU(0) factorisation hit a singular pivot (=> block-Jacobi fallback)
 };
 
 struct DDLists {
@@ -67,6 +67,13 @@ struct rsim_gpu_ctx {
   bool keep_F = false;         // debug: the row kernel also stores the raw residual
   double* gm_V = nullptr;      // GMRES basis (RSIM_GMRES_M + 1 vectors), allocated on first use
   double* gm_part = nullptr;   // GMRES reduction partials
+  struct Ilu {                 // level-scheduled block ILU(0) (ilu.cu)
+    int32_t *ptr = nullptr, *col = nullptr, *src = nullptr, *frows = nullptr, *foff = nullptr, *brows = nullptr,
+            *boff = nullptr;
+    double *val = nullptr, *dinv = nullptr, *y = nullptr;
+    int64_t cap[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // element capacities, one per buffer
+    int32_t nnz = 0, nf = 0, nb = 0, maxw = 0;
+  } ilu;
   int64_t nnc_total = 0;
   rsim_fluid_params fl{};
   double bhp = 0.0;
@@ -134,6 +141,11 @@ struct rsim_gpu_ctx {
 // ---- error plumbing (abi.cu) -------------------------------------------------
 void rsim_set_error(const std::string& msg);
 int rsim_cuda_fail(cudaError_t e, const char* what);
+#define RSIM_TRY(x)                    \
+  do {                                 \
+    const int rsim_r_ = (x);           \
+    if (rsim_r_ != RSIM_OK) return rsim_r_; \
+  } while (0)
 #define RSIM_CUDA(call)                                   \
   do {                                                    \
     cudaError_t _e = (call);                              \
@@ -168,6 +180,8 @@ int launch_seed_support(rsim_gpu_ctx* c, double eps);
 int launch_reset_seed(rsim_gpu_ctx* c, double eps);
 int launch_materialize_cols(rsim_gpu_ctx* c);
 int launch_gmres(rsim_gpu_ctx* c, const rsim_solver_opts* o);
+int ilu_prepare(rsim_gpu_ctx* c);  // pattern, level schedules, factorisation (precond == ILU0)
+void ilu_free(rsim_gpu_ctx* c);
 int launch_state_from_dp(rsim_gpu_ctx* c, double p_hi, double scale);
 
 // ---- device helpers ------------------------------------------------------------

@@ -23,6 +23,7 @@
 #include <cstdlib>
 
 #include "ctx.cuh"
+#include "ilu.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -52,7 +53,8 @@ struct KArgs {
   const double* part_f2;  // (F,F) chunk partials of the assembly (f2_parts)
   bool f2_parts;
   double *x, *r, *r0, *p, *v, *s, *t, *p2, *v2, *ph, *sh;
-  int32_t neu, fuse;
+  int32_t neu, fuse, ilu;  // neu: Neumann-1; ilu: level-scheduled ILU(0) (never fused)
+  IluArgs fa;
   double* part;   // [5][pstride]  level-1 partials
   double* part2;  // [5][pstride2] level-2 partials (very large systems)
   int32_t pstride, pstride2;
@@ -202,7 +204,7 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
 
 // FUSE is a template parameter: the two variants have different live state,
 // and one kernel holding both spills heavily at 64 registers / thread.
-template <int B, bool FUSE>
+template <int B, bool FUSE, bool ILU>
 __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   __shared__ Red R;
   const bool single = gridDim.x == 1;
@@ -296,8 +298,14 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   int it_total = 0;
   // attempt 0: as configured; attempt 1 (only after a Neumann-1 breakdown or
   // cap): block-Jacobi only, restarted from x0 = 0 (same rule as the oracle)
-  for (int attempt = 0; attempt < (a.neu ? 2 : 1); ++attempt) {
+  // ILU is a template parameter: the level-scheduled solves would otherwise
+  // change the register allocation (and speed) of the common variants
+  const bool ilu_bad = ILU && a.dsc->ilu_bad;
+  for (int attempt = 0; attempt < ((a.neu || ILU) ? 2 : 1); ++attempt) {
   const bool neu = a.neu && attempt == 0;
+  const bool ilu = ILU && attempt == 0;
+  const bool prec = neu || ilu;  // ph = M^{-1} p, sh = M^{-1} s are stored
+  if (ilu && ilu_bad) { status = RSIM_ENUM; it = 0; continue; }  // singular pivot: block-Jacobi only
   if (attempt) {
     for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
       const int64_t l = rd * KT + tid;
@@ -354,11 +362,12 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       }
       sync();
     }
-    // ---- v = Â p (BJ) or v = Â ph (Neumann-1); (r0, v) and the lagged (r, r)
+    if (ilu) ilu_apply<B>(a.fa, pc, a.ph, sync);  // ph = (LU)^{-1} p (p stored: unfused)
+    // ---- v = Â p (BJ) or v = Â ph (Neumann-1, ILU(0)); (r0, v) and the lagged (r, r)
     ROUNDS_BEGIN
     if (ok) {
       double y[B];
-      if (neu) {
+      if (prec) {
         spmv_row<B>(a, l, 3, Vecs{a.r, a.ph, vo, a.s, a.t}, 0.0, 0.0, 0.0, &a.ph[l * B], y);
       } else if (fuse) {
         double pown[B];
@@ -414,11 +423,12 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       }
       sync();
     }
-    // ---- t = Â s (BJ) or t = Â sh (Neumann-1); (s,s), (t,s), (t,t), (r0,s), (r0,t)
+    if (ilu) ilu_apply<B>(a.fa, a.s, a.sh, sync);  // sh = (LU)^{-1} s
+    // ---- t = Â s (BJ) or t = Â sh (Neumann-1, ILU(0)); (s,s), (t,s), (t,t), (r0,s), (r0,t)
     ROUNDS_BEGIN
     if (ok) {
       double sv[B], y[B];
-      if (neu) {
+      if (prec) {
         if (fuse) nbr_val<B>(2, V2, l, 0.0, 0.0, alpha, sv);
         else
 #pragma unroll
@@ -446,8 +456,8 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     ROUNDS_END(5)
     reduce(5);
     const double ss = R.res[0], ts = R.res[1], tt = R.res[2], r0s = R.res[3], r0t = R.res[4];
-    const double* phv = neu ? a.ph : pc;
-    const double* shv = neu ? a.sh : a.s;
+    const double* phv = prec ? a.ph : pc;
+    const double* shv = prec ? a.sh : a.s;
     if (!fixed && sqrt(ss) <= tol) {
       for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
         const int64_t l = rd * KT + tid;
@@ -488,7 +498,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     status = (fixed || sqrt(R.res[0]) <= tol) ? RSIM_OK : RSIM_ENOCONV;
   }
   it_total += it;
-  if (!(neu && (status == RSIM_ENUM || status == RSIM_ENOCONV))) break;
+  if (!(prec && (status == RSIM_ENUM || status == RSIM_ENOCONV))) break;
   }
   it = it_total;
   if (blockIdx.x == 0 && tid == 0) {
@@ -524,19 +534,23 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.x = c->x; a.r = c->r; a.r0 = c->r0; a.p = c->p; a.v = c->v; a.s = c->s; a.t = c->t;
   a.p2 = c->p2; a.v2 = c->v2; a.ph = c->ph; a.sh = c->sh;
   a.neu = o->precond == RSIM_PREC_NEUMANN1;
-  a.fuse = c->nA <= kFuseMaxRows ? 1 : 0;
+  a.ilu = o->precond == RSIM_PREC_ILU0;
+  a.fa = ilu_args(c);
+  a.fuse = (c->nA <= kFuseMaxRows && !a.ilu) ? 1 : 0;
   a.pstride = (int32_t)((c->n + 255) / 256);
   a.pstride2 = (a.pstride + 255) / 256;
   a.part = c->part;
   a.part2 = c->part + 5 * (int64_t)a.pstride;
   a.dsc = c->dsc;
   const int64_t nrounds = ((c->nA + 255) / 256 + CPR - 1) / CPR;
-  auto kern = a.fuse ? k_bicgstab<B, true> : k_bicgstab<B, false>;
+  auto kern = a.ilu ? k_bicgstab<B, false, true> : (a.fuse ? k_bicgstab<B, true, false> : k_bicgstab<B, false, false>);
   if (c->max_coop_blocks[B] == 0) {
-    int per_sm = 0, per_sm2 = 0;
-    RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bicgstab<B, true>, KT, 0));
-    RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_bicgstab<B, false>, KT, 0));
+    int per_sm = 0, per_sm2 = 0, per_sm3 = 0;
+    RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bicgstab<B, true, false>, KT, 0));
+    RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_bicgstab<B, false, false>, KT, 0));
+    RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, k_bicgstab<B, false, true>, KT, 0));
     if (per_sm2 < per_sm) per_sm = per_sm2;
+    if (per_sm3 < per_sm) per_sm = per_sm3;
     c->max_coop_blocks[B] = per_sm * c->sm_count;
     if (c->max_coop_blocks[B] < 1) c->max_coop_blocks[B] = 1;
   }
@@ -557,8 +571,10 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
 
 int launch_krylov(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   if (c->nA <= 0) return RSIM_OK;
+  const bool ilu = o->precond == RSIM_PREC_ILU0;
+  if (ilu) RSIM_TRY(ilu_prepare(c));
   if (o->lin_method == RSIM_LIN_GMRES) return launch_gmres(c, o);
-  {  // small systems: one cluster with matrix + vectors in distributed smem
+  if (!ilu) {  // small systems: one cluster with matrix + vectors in distributed smem
     int r = launch_krylov_dsm(c, o);
     if (r != RSIM_ENOTAPPLICABLE) return r;
   }

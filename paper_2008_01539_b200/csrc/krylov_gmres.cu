@@ -13,6 +13,7 @@
 #include <cooperative_groups.h>
 
 #include "ctx.cuh"
+#include "ilu.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -24,7 +25,8 @@ constexpr int MM = RSIM_GMRES_M;   // restart length
 constexpr int NQMAX = MM + 1;      // quantities of one reduction (projections)
 
 struct GArgs {
-  int32_t nA, nslot, maxit, fixed, neu;
+  int32_t nA, nslot, maxit, fixed, neu, ilu;
+  IluArgs fa;
   int64_t cap;
   int32_t nx, ny, nz;
   bool d3, has_nnc, implicit, f2_parts;
@@ -197,8 +199,12 @@ __global__ void __launch_bounds__(GT, 1) k_gmres(const GArgs a) {
   int status = RSIM_OK, total_all = 0;
   double relres = 0.0;
   if (bnorm != 0.0) {
-    for (int attempt = 0; attempt < (a.neu ? 2 : 1); ++attempt) {
+    const bool ilu_bad = a.ilu && a.dsc->ilu_bad;
+    for (int attempt = 0; attempt < ((a.neu || a.ilu) ? 2 : 1); ++attempt) {
       const bool neu = a.neu && attempt == 0;
+      const bool ilu = a.ilu && attempt == 0;
+      const bool prec = neu || ilu;
+      if (ilu && ilu_bad) { status = RSIM_ENUM; continue; }  // singular pivot: block-Jacobi only
       if (attempt) {  // block-Jacobi only, from x0 = 0
         GPASS_BEGIN
 #pragma unroll
@@ -234,6 +240,9 @@ __global__ void __launch_bounds__(GT, 1) k_gmres(const GArgs a) {
             for (int e = 0; e < B; ++e) a.z[l * B + e] = vj[l * B + e] + (vj[l * B + e] - y[e]);
             GPASS_END
             sync();
+            zsrc = a.z;
+          } else if (ilu) {  // z = (LU)^{-1} v_j
+            ilu_apply<B>(a.fa, vj, a.z, sync);
             zsrc = a.z;
           }
           // ---- w = Â z;  (w, v_i), i <= j
@@ -314,7 +323,7 @@ __global__ void __launch_bounds__(GT, 1) k_gmres(const GArgs a) {
         for (int e = 0; e < B; ++e) {
           double ue = R.yy[0] * a.V[l * B + e];
           for (int i = 1; i < k; ++i) ue = ue + R.yy[i] * a.V[((int64_t)i * a.cap + l) * B + e];
-          if (neu) a.u[l * B + e] = ue;
+          if (prec) a.u[l * B + e] = ue;
           else a.x[l * B + e] = a.x[l * B + e] + ue;
         }
         GPASS_END
@@ -328,6 +337,13 @@ __global__ void __launch_bounds__(GT, 1) k_gmres(const GArgs a) {
             const double ue = a.u[l * B + e];
             a.x[l * B + e] = a.x[l * B + e] + (ue + (ue - y[e]));
           }
+          GPASS_END
+        } else if (ilu) {
+          sync();
+          ilu_apply<B>(a.fa, a.u, a.z, sync);
+          GPASS_BEGIN
+#pragma unroll
+          for (int e = 0; e < B; ++e) a.x[l * B + e] = a.x[l * B + e] + a.z[l * B + e];
           GPASS_END
         }
         relres = resid / bnorm;
@@ -349,7 +365,7 @@ __global__ void __launch_bounds__(GT, 1) k_gmres(const GArgs a) {
         if (beta == 0.0) { status = RSIM_OK; break; }
       }
       total_all += total;
-      if (!(neu && (status == RSIM_ENUM || status == RSIM_ENOCONV))) break;
+      if (!(prec && (status == RSIM_ENUM || status == RSIM_ENOCONV))) break;
       sync();
     }
   }
@@ -375,6 +391,8 @@ int launch_g(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   GArgs a;
   a.nA = c->nA; a.nslot = c->nslot; a.maxit = o->lin_maxit; a.fixed = o->fixed_lin_iters;
   a.neu = o->precond == RSIM_PREC_NEUMANN1;
+  a.ilu = o->precond == RSIM_PREC_ILU0;
+  a.fa = ilu_args(c);
   a.cap = c->n;
   a.nx = c->nx; a.ny = c->ny; a.nz = c->nz; a.d3 = c->d3;
   a.has_nnc = c->has_nnc; a.implicit = c->cols_implicit; a.f2_parts = c->f2_parts;

@@ -1,7 +1,8 @@
-"""GMRES(30) (north star alternative to BiCGSTAB): GPU
-kernel vs oracle, bit-exact — solution, iteration count, residual estimate —
-on every Krylov layout (small / grid / full-set implicit columns, b = 1, 2, 3,
-NNC), with block-Jacobi and Neumann-1, and whole localized runs."""
+"""GMRES(30) and level-scheduled ILU(0) (north star alternatives to BiCGSTAB /
+block-Jacobi): GPU kernels vs oracle, bit-exact — solution,
+iteration count, residual — on every Krylov layout (small / grid / full-set
+implicit columns, b = 1, 2, 3, NNC), with block-Jacobi, Neumann-1 and ILU(0),
+and whole localized runs."""
 import numpy as np
 import pytest
 
@@ -20,7 +21,7 @@ def _state(case, seed):
     return s
 
 
-def _check(case, act, precond, its=None, seed=3):
+def _check(case, act, precond, its=None, seed=3, method=None):
     if act is not None:
         act = np.union1d(act, np.flatnonzero(case.pinned())).astype(np.int32)
     s = _state(case, seed)
@@ -31,7 +32,7 @@ def _check(case, act, precond, its=None, seed=3):
     sim.set_state(s, 86400.0)
     st = sim.set_active(act)
     sim.assemble()
-    opts = case.solver_opts(precond=precond, lin_method=pkg.LIN_GMRES)
+    opts = case.solver_opts(precond=precond, lin_method=pkg.LIN_GMRES if method is None else method)
     if its:
         opts.fixed_lin_iters = its
         opts.lin_maxit = its
@@ -47,7 +48,10 @@ def _check(case, act, precond, its=None, seed=3):
     return it_o
 
 
-@pytest.mark.parametrize("precond", [pkg.PREC_BJACOBI, pkg.PREC_NEUMANN1])
+PRECS = [pkg.PREC_BJACOBI, pkg.PREC_NEUMANN1, pkg.PREC_ILU0]
+
+
+@pytest.mark.parametrize("precond", PRECS)
 @pytest.mark.parametrize("cfg,nA", [(dict(config=1), 400), (dict(config=2, nx=96, ny=96, n_dfn=20), 2500),
                                     (dict(config=4, nx=40, ny=40, nz=4, n_dfn=6), 3000),
                                     (dict(config=5, nx=160, ny=160, nz=1), 20000)])
@@ -58,13 +62,13 @@ def test_gmres_partial_sets(cfg, nA, precond):
     _check(case, act, precond)
 
 
-@pytest.mark.parametrize("precond", [pkg.PREC_BJACOBI, pkg.PREC_NEUMANN1])
+@pytest.mark.parametrize("precond", PRECS)
 def test_gmres_full_set_grid(precond):
     case = pkg.Case(2, nx=200, ny=200, n_dfn=40)
     _check(case, None, precond)
 
 
-@pytest.mark.parametrize("precond", [pkg.PREC_BJACOBI, pkg.PREC_NEUMANN1])
+@pytest.mark.parametrize("precond", PRECS)
 def test_gmres_full_set_implicit_columns_restart(precond):
     # 1.2 M rows, V_A = all cells (structural columns), 45 iterations = one restart
     case = pkg.Case(3, nx=160, ny=128, nz=60)
@@ -72,11 +76,13 @@ def test_gmres_full_set_implicit_columns_restart(precond):
     _check(case, None, precond, its=45)
 
 
+@pytest.mark.parametrize("method,precond", [(pkg.LIN_GMRES, pkg.PREC_NEUMANN1), (pkg.LIN_GMRES, pkg.PREC_ILU0),
+                                            (pkg.LIN_BICGSTAB, pkg.PREC_ILU0)])
 @pytest.mark.parametrize("name,kw", [("c1", dict(config=1)), ("c2s", dict(config=2, nx=64, ny=64, n_dfn=20)),
                                      ("c4s", dict(config=4, nx=32, ny=32, nz=4, n_dfn=10))])
-def test_gmres_localized_run_bit_exact(name, kw):
+def test_localized_run_bit_exact(name, kw, method, precond):
     case = pkg.Case(**kw)
-    opts = case.solver_opts(lin_method=pkg.LIN_GMRES)
+    opts = case.solver_opts(lin_method=method, precond=precond)
     dts = case.schedule()[:8]
     ro = Oracle(case).run_case(1, case.init_state(), dts, opts)
     sim = pkg.GpuSimulator(case)
@@ -85,3 +91,19 @@ def test_gmres_localized_run_bit_exact(name, kw):
         assert rg[k] == ro[k], (k, rg[k], ro[k])
     assert np.array_equal(rg["states"].u, ro["states"].u)
     sim.close()
+
+
+# ---- BiCGSTAB with ILU(0): level-scheduled triangular solves inside the grid kernel
+@pytest.mark.parametrize("cfg,nA", [(dict(config=1), 400), (dict(config=2, nx=96, ny=96, n_dfn=20), 2500),
+                                    (dict(config=4, nx=40, ny=40, nz=4, n_dfn=6), 3000),
+                                    (dict(config=3, nx=48, ny=48, nz=8), 9000)])
+def test_bicgstab_ilu0_partial_sets(cfg, nA):
+    case = pkg.Case(**cfg)
+    rng = np.random.default_rng(nA)
+    act = np.sort(rng.choice(case.n, min(nA, case.n), replace=False)).astype(np.int32)
+    _check(case, act, pkg.PREC_ILU0, method=pkg.LIN_BICGSTAB)
+
+
+def test_bicgstab_ilu0_full_set():
+    case = pkg.Case(2, nx=200, ny=200, n_dfn=40)
+    _check(case, None, pkg.PREC_ILU0, method=pkg.LIN_BICGSTAB)
