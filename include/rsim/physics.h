@@ -10,6 +10,10 @@
  * device with --fmad=false so no side contracts a*b+c into an FMA, and the
  * only transcendental (exp) is implemented here (rexp) instead of libm.
  *
+ * Divisions by model constants (μ, Δt, the Corey denominators, p_bub, p_gas)
+ * are written as multiplications by the reciprocal, (1.0 / c), which the
+ * compiler evaluates once per thread; both sides use the same expression.
+ *
  * These functions are pure: no traversal, no set logic, no linear algebra.
  * The oracle (oracle/) shares ONLY this header and blockops.h with the
  * product; its assembly loop, set logic, Krylov solver and Newton control are
@@ -85,10 +89,10 @@ RSIM_HD double rexp(double x) {
 /* Quadratic Corey curve on the normalised saturation (s − s_r)/den,
  * clamped to [0,1].  dkr is d kr / d s. */
 RSIM_HD void corey2(double s, double s_r, double den, double& kr, double& dkr) {
-  double se = (s - s_r) / den;
+  double se = (s - s_r) * (1.0 / den);
   if (!(se > 0.0)) { kr = 0.0; dkr = 0.0; }
   else if (!(se < 1.0)) { kr = 1.0; dkr = 0.0; }
-  else { kr = se * se; dkr = (2.0 * se) / den; }
+  else { kr = se * se; dkr = (2.0 * se) * (1.0 / den); }
 }
 
 /* Per-cell property block.
@@ -110,8 +114,8 @@ RSIM_HD void props(const rsim_fluid_params& f, const double* u, uint8_t /*st*/, 
   double drho = f.c_f[1] * rho;
   P.A[0] = rho;
   P.dA[0][0] = drho;
-  P.L[0] = rho / f.mu[1];
-  P.dL[0][0] = drho / f.mu[1];
+  P.L[0] = rho * (1.0 / f.mu[1]);
+  P.dL[0][0] = drho * (1.0 / f.mu[1]);
 }
 
 /* ---- Model 2: oil-water, u = (p, S_w); equations (water, oil) --------- */
@@ -132,12 +136,12 @@ RSIM_HD void props(const rsim_fluid_params& f, const double* u, uint8_t /*st*/, 
   double krw, dkrw, kro, dkro;
   corey2(sw, f.swc, den, krw, dkrw);
   corey2(so, f.sor, den, kro, dkro); /* d/dso; d so/d sw = -1 */
-  P.L[0] = (rw * krw) / f.mu[0];
-  P.dL[0][0] = (drw * krw) / f.mu[0];
-  P.dL[0][1] = (rw * dkrw) / f.mu[0];
-  P.L[1] = (ro * kro) / f.mu[1];
-  P.dL[1][0] = (dro * kro) / f.mu[1];
-  P.dL[1][1] = -((ro * dkro) / f.mu[1]);
+  P.L[0] = (rw * krw) * (1.0 / f.mu[0]);
+  P.dL[0][0] = (drw * krw) * (1.0 / f.mu[0]);
+  P.dL[0][1] = (rw * dkrw) * (1.0 / f.mu[0]);
+  P.L[1] = (ro * kro) * (1.0 / f.mu[1]);
+  P.dL[1][0] = (dro * kro) * (1.0 / f.mu[1]);
+  P.dL[1][1] = -((ro * dkro) * (1.0 / f.mu[1]));
 }
 
 /* ---- Model 3: black-oil, u = (p, S_w, X); equations (water, oil, gas) --
@@ -151,7 +155,7 @@ RSIM_HD void props(const rsim_fluid_params& f, const double* u, uint8_t st, Prop
   double eo = rexp(f.c_f[1] * (p - f.p_ref));
   double rs, drs_dp, drs_dx, sg, dsg_dx;
   if (st == RSIM_BO_SAT) {
-    rs = (f.rs_b * p) / f.p_bub; drs_dp = f.rs_b / f.p_bub; drs_dx = 0.0;
+    rs = (f.rs_b * p) * (1.0 / f.p_bub); drs_dp = f.rs_b * (1.0 / f.p_bub); drs_dx = 0.0;
     sg = X; dsg_dx = 1.0;
   } else {
     rs = X; drs_dp = 0.0; drs_dx = 1.0;
@@ -164,7 +168,7 @@ RSIM_HD void props(const rsim_fluid_params& f, const double* u, uint8_t st, Prop
   double dbo_drs = -((f.bo_alpha * bo) / q);
   double dbo_dp = f.c_f[1] * bo + dbo_drs * drs_dp;
   double dbo_dx = dbo_drs * drs_dx;
-  double bg = p / f.p_gas;
+  double bg = p * (1.0 / f.p_gas);
   double dbg = 1.0 / f.p_gas;
 
   P.A[0] = sw * bw;
@@ -186,23 +190,23 @@ RSIM_HD void props(const rsim_fluid_params& f, const double* u, uint8_t st, Prop
   corey2(sw, f.swc, den, krw, dkrw);
   corey2(so, f.sor, den, kro, dkro);
   corey2(sg, f.sgc, den, krg, dkrg);
-  double lo = (bo * kro) / f.mu[1];
-  double dlo_dp = (dbo_dp * kro) / f.mu[1];
-  double dlo_dsw = -((bo * dkro) / f.mu[1]);
-  double dlo_dx = (dbo_dx * kro + bo * (dkro * dso_dx)) / f.mu[1];
-  P.L[0] = (bw * krw) / f.mu[0];
-  P.dL[0][0] = (dbw * krw) / f.mu[0];
-  P.dL[0][1] = (bw * dkrw) / f.mu[0];
+  double lo = (bo * kro) * (1.0 / f.mu[1]);
+  double dlo_dp = (dbo_dp * kro) * (1.0 / f.mu[1]);
+  double dlo_dsw = -((bo * dkro) * (1.0 / f.mu[1]));
+  double dlo_dx = (dbo_dx * kro + bo * (dkro * dso_dx)) * (1.0 / f.mu[1]);
+  P.L[0] = (bw * krw) * (1.0 / f.mu[0]);
+  P.dL[0][0] = (dbw * krw) * (1.0 / f.mu[0]);
+  P.dL[0][1] = (bw * dkrw) * (1.0 / f.mu[0]);
   P.dL[0][2] = 0.0;
   P.L[1] = lo;
   P.dL[1][0] = dlo_dp;
   P.dL[1][1] = dlo_dsw;
   P.dL[1][2] = dlo_dx;
-  double lg = (bg * krg) / f.mu[2];
+  double lg = (bg * krg) * (1.0 / f.mu[2]);
   P.L[2] = lg + rs * lo;
-  P.dL[2][0] = ((dbg * krg) / f.mu[2] + drs_dp * lo) + rs * dlo_dp;
+  P.dL[2][0] = ((dbg * krg) * (1.0 / f.mu[2]) + drs_dp * lo) + rs * dlo_dp;
   P.dL[2][1] = rs * dlo_dsw;
-  P.dL[2][2] = ((bg * (dkrg * dsg_dx)) / f.mu[2] + drs_dx * lo) + rs * dlo_dx;
+  P.dL[2][2] = ((bg * (dkrg * dsg_dx)) * (1.0 / f.mu[2]) + drs_dx * lo) + rs * dlo_dx;
 }
 
 /* Mass in place M_e = pv φ(p) A_e (used for the old-time accumulation). */
@@ -219,9 +223,9 @@ RSIM_HD void accum_row(const rsim_fluid_params& f, double pv, double p, const Pr
   double pvp = pv * (1.0 + f.c_r * (p - f.p_ref));
   double pvc = pv * f.c_r;
   for (int e = 0; e < B; ++e) {
-    R[e] = (pvp * P.A[e] - Mold[e]) / dt;
-    D[e][0] = (pvp * P.dA[e][0] + pvc * P.A[e]) / dt;
-    for (int v = 1; v < B; ++v) D[e][v] = (pvp * P.dA[e][v]) / dt;
+    R[e] = (pvp * P.A[e] - Mold[e]) * (1.0 / dt);
+    D[e][0] = (pvp * P.dA[e][0] + pvc * P.A[e]) * (1.0 / dt);
+    for (int v = 1; v < B; ++v) D[e][v] = (pvp * P.dA[e][v]) * (1.0 / dt);
   }
 }
 
@@ -292,7 +296,7 @@ template <int B>
 RSIM_HD void substitute(const rsim_fluid_params& f, double* u, uint8_t& st) {
   if (B >= 2) u[1] = clamp01(u[1]);
   if (B == 3) {
-    double rs_sat = (f.rs_b * u[0]) / f.p_bub;
+    double rs_sat = (f.rs_b * u[0]) * (1.0 / f.p_bub);
     if (st == RSIM_BO_UNDERSAT) {
       if (u[2] > rs_sat) { st = RSIM_BO_SAT; u[2] = 0.0; }
     } else {
