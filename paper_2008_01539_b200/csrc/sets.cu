@@ -12,7 +12,13 @@
 //   Alg. 2 phase-1 labels, V_T
 // The expand/shrink decision is taken ON THE DEVICE from ‖δp_B‖∞ (each K7
 // kernel evaluates it), so K6 -> K7 -> compaction runs without a host round trip.
+#include <cooperative_groups.h>
+
+#include <cstdlib>
+
 #include "ctx.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -198,17 +204,16 @@ struct Pos4 {
   int64_t t;                // vec4: word index
   bool ok;
 };
-__device__ __forceinline__ Pos4 pos4(const Geo4& g) {
+__device__ __forceinline__ Pos4 pos4(const Geo4& g, int32_t row, int32_t seg) {
   Pos4 p;
-  p.row = blockIdx.x;
+  p.row = row;
   p.iz = p.row / g.ny;
   p.iy = p.row - p.iz * g.ny;
-  p.xw = blockIdx.y * g.bs + threadIdx.x;
+  p.xw = seg * g.bs + threadIdx.x;
   p.ok = p.xw < g.wrow;
   p.t = (int64_t)p.row * g.wrow + p.xw;
   return p;
 }
-__device__ __forceinline__ int32_t tile_id(const Geo4& g) { return blockIdx.x * g.nseg + blockIdx.y; }
 
 // Combine over the graph neighbours of the 4 cells of group p of per-byte
 // bit-0 lanes produced by `L(word index)`; `edge` is the lane value of a
@@ -258,13 +263,10 @@ __device__ __forceinline__ int block_sum(int v, int* sh8) {
 // device decided to shrink).  With COUNT the same pass also counts A_new per
 // tile (compaction pass 1), which needs only the cell's own bits.
 template <bool COUNT>
-__global__ void __launch_bounds__(256) k_dilate(Geo4 g, uint8_t* __restrict__ flags, uint8_t bit_in, uint8_t bit_out,
-                                                const DevScalars* __restrict__ dsc, SetMode M, int do_dilate,
-                                                int32_t* __restrict__ tile_cnt) {
-  __shared__ int sh8[8];
-  const bool ex = decide_expand(M, dsc);
-  const bool dil = do_dilate && ((M.mode == MODE_DEVICE || M.mode == MODE_DD) ? ex : true);
-  const Pos4 p = pos4(g);
+__device__ __forceinline__ void dilate_tile(const Geo4& g, uint8_t* __restrict__ flags, uint8_t bit_in, uint8_t bit_out,
+                                            bool ex, bool dil, const SetMode& M, int32_t row, int32_t seg,
+                                            int32_t* __restrict__ tile_cnt, int* sh8) {
+  const Pos4 p = pos4(g, row, seg);
   int cnt = 0;
   if (p.ok) {
     if (g.vec4) {
@@ -308,22 +310,34 @@ __global__ void __launch_bounds__(256) k_dilate(Geo4 g, uint8_t* __restrict__ fl
   }
   if (COUNT) {
     const int s = block_sum(cnt, sh8);
-    if (threadIdx.x == 0) tile_cnt[tile_id(g)] = s;
+    if (threadIdx.x == 0) tile_cnt[row * g.nseg + seg] = s;
+    __syncthreads();  // sh8 is reused by the next tile
   }
+}
+
+template <bool COUNT>
+__global__ void __launch_bounds__(256) k_dilate(Geo4 g, uint8_t* __restrict__ flags, uint8_t bit_in, uint8_t bit_out,
+                                                const DevScalars* __restrict__ dsc, SetMode M, int do_dilate,
+                                                int32_t* __restrict__ tile_cnt) {
+  __shared__ int sh8[8];
+  const bool ex = decide_expand(M, dsc);
+  const bool dil = do_dilate && ((M.mode == MODE_DEVICE || M.mode == MODE_DD) ? ex : true);
+  dilate_tile<COUNT>(g, flags, bit_in, bit_out, ex, dil, M, blockIdx.x, blockIdx.y, tile_cnt, sh8);
 }
 
 // Compaction pass 2: exclusive scan of the tile counts (one block; counts
 // staged through shared memory, strips of consecutive tiles per thread).
 // Also publishes the decision + n_A and resets the counters of pass 3.
-__global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t* __restrict__ cnt, int32_t* __restrict__ off,
-                                                      int32_t ntiles, DevScalars* dsc, SetMode M) {
-  extern __shared__ int32_t scnt[];  // padded: entry i at i + i/32 (conflict-free strips)
-  __shared__ int32_t wsum[32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+// Block-wide exclusive scan of the tile counts (any blockDim, multiple of 32);
+// scnt: shared staging of ntiles + ntiles/32 + 1 ints.
+__device__ __forceinline__ void scan_tiles_dev(const int32_t* __restrict__ cnt, int32_t* __restrict__ off,
+                                               int32_t ntiles, DevScalars* dsc, const SetMode& M, int32_t* scnt,
+                                               int32_t* wsum) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nth = blockDim.x, nw = nth >> 5;
   auto P = [](int32_t i) { return i + (i >> 5); };
-  for (int32_t k = threadIdx.x; k < ntiles; k += 1024) scnt[P(k)] = cnt[k];
+  for (int32_t k = threadIdx.x; k < ntiles; k += nth) scnt[P(k)] = cnt[k];
   __syncthreads();
-  const int32_t per = (ntiles + 1023) / 1024;
+  const int32_t per = (ntiles + nth - 1) / nth;
   const int32_t b0 = threadIdx.x * per;
   int32_t tot = 0;
   for (int32_t k = 0; k < per; ++k)
@@ -337,7 +351,7 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t* __restrict__
   if (lane == 31) wsum[w] = x;
   __syncthreads();
   if (w == 0) {
-    int32_t z = wsum[lane];
+    int32_t z = lane < nw ? wsum[lane] : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       int32_t y = __shfl_up_sync(0xffffffffu, z, o);
@@ -354,25 +368,30 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t* __restrict__
       run += c;
     }
   __syncthreads();
-  for (int32_t k = threadIdx.x; k < ntiles; k += 1024) off[k] = scnt[P(k)];
-  if (threadIdx.x == 1023) {
-    dsc->nA = wsum[31];
+  for (int32_t k = threadIdx.x; k < ntiles; k += nth) off[k] = scnt[P(k)];
+  if (threadIdx.x == nth - 1) {
+    dsc->nA = wsum[nw - 1];
     dsc->expand = decide_expand(M, dsc) ? 1 : 0;
     dsc->nB = 0;
     dsc->n_new = 0;
   }
 }
 
+__global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t* __restrict__ cnt, int32_t* __restrict__ off,
+                                                      int32_t ntiles, DevScalars* dsc, SetMode M) {
+  extern __shared__ int32_t scnt[];  // padded: entry i at i + i/32 (conflict-free strips)
+  __shared__ int32_t wsum[32];
+  scan_tiles_dev(cnt, off, ntiles, dsc, M, scnt, wsum);
+}
+
 // Compaction pass 3 (same tiles): A_new, V_B, V_T/labels, g2l, sorted
 // active list (block scan of the per-thread counts 0..4).
-__global__ void __launch_bounds__(256) k_scatter(Geo4 g, const uint8_t* __restrict__ fin, uint8_t* __restrict__ fout,
-                                                 SetMode M, int32_t round, DevScalars* dsc,
-                                                 const int32_t* __restrict__ tile_off, int32_t* __restrict__ act,
-                                                 int32_t* __restrict__ g2l, int32_t* __restrict__ label) {
-  __shared__ int32_t wpre[8];
-  __shared__ int sh8[8];
-  const bool ex = decide_expand(M, dsc);
-  const Pos4 p = pos4(g);
+__device__ __forceinline__ void scatter_tile(const Geo4& g, const uint8_t* __restrict__ fin, uint8_t* __restrict__ fout,
+                                             const SetMode& M, bool ex, int32_t round, DevScalars* dsc,
+                                             const int32_t* __restrict__ tile_off, int32_t* __restrict__ act,
+                                             int32_t* __restrict__ g2l, int32_t* __restrict__ label, int32_t row,
+                                             int32_t seg, int32_t* wpre, int* sh8) {
+  const Pos4 p = pos4(g, row, seg);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t keep = 0, bnd = 0, f4 = 0;
   const int64_t rb = (int64_t)p.row * g.nx;
@@ -424,7 +443,7 @@ __global__ void __launch_bounds__(256) k_scatter(Geo4 g, const uint8_t* __restri
   __syncthreads();
   int pre = x - c;
   for (int k = 0; k < w; ++k) pre += wpre[k];
-  int32_t pos = tile_off[tile_id(g)] + pre;
+  int32_t pos = tile_off[row * g.nseg + seg] + pre;
   int nnew = 0;
   const int64_t i0 = rb + 4 * (int64_t)p.xw;
   int32_t gl[4];
@@ -465,6 +484,61 @@ __global__ void __launch_bounds__(256) k_scatter(Geo4 g, const uint8_t* __restri
   if (threadIdx.x == 0) {
     if (nb) atomicAdd(&dsc->nB, nb);
     if (nn) atomicAdd(&dsc->n_new, nn);
+  }
+  __syncthreads();  // wpre / sh8 are reused by the next tile
+}
+
+__global__ void __launch_bounds__(256) k_scatter(Geo4 g, const uint8_t* __restrict__ fin, uint8_t* __restrict__ fout,
+                                                 SetMode M, int32_t round, DevScalars* dsc,
+                                                 const int32_t* __restrict__ tile_off, int32_t* __restrict__ act,
+                                                 int32_t* __restrict__ g2l, int32_t* __restrict__ label) {
+  __shared__ int32_t wpre[8];
+  __shared__ int sh8[8];
+  const bool ex = decide_expand(M, dsc);
+  scatter_tile(g, fin, fout, M, ex, round, dsc, tile_off, act, g2l, label, blockIdx.x, blockIdx.y, wpre, sh8);
+}
+
+// Whole set update in ONE cooperative kernel for small grids (the localized
+// solver's common case: every pass is latency-bound, so four dependent launches
+// cost more than the work).  Blocks loop over the same tiles as the separate
+// kernels; grid barriers separate the dilation rounds, the count, the scan
+// (block 0) and the scatter, so the results are those of the multi-kernel path.
+constexpr int kCoopMaxTiles = 4096;
+__global__ void __launch_bounds__(256) k_set_update_coop(Geo4 g, uint8_t* __restrict__ flags,
+                                                         uint8_t* __restrict__ flags_alt, SetMode M, int rounds,
+                                                         int32_t round, DevScalars* dsc, int32_t* __restrict__ tile_cnt,
+                                                         int32_t* __restrict__ tile_off, int32_t* __restrict__ act,
+                                                         int32_t* __restrict__ g2l, int32_t* __restrict__ label) {
+  __shared__ int sh8[8];
+  __shared__ int32_t wpre[8];
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t scnt[kCoopMaxTiles + kCoopMaxTiles / 32 + 1];
+  auto grid = cg::this_grid();
+  const int32_t ntiles = g.ny * g.nz * g.nseg;
+  const bool ex = decide_expand(M, dsc);
+  const bool dil = (M.mode == MODE_DEVICE || M.mode == MODE_DD) ? ex : true;
+  for (int r = 0; r < rounds; ++r) {
+    const uint8_t bin = (r % 2 == 0) ? F_D0 : F_D1, bout = (r % 2 == 0) ? F_D1 : F_D0;
+    const bool last = r + 1 == rounds;
+    for (int32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+      const int32_t row = tl / g.nseg, seg = tl - row * g.nseg;
+      if (last) dilate_tile<true>(g, flags, bin, bout, ex, dil, M, row, seg, tile_cnt, sh8);
+      else dilate_tile<false>(g, flags, bin, bout, ex, dil, M, row, seg, tile_cnt, sh8);
+    }
+    grid.sync();
+  }
+  if (rounds == 0) {
+    for (int32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+      const int32_t row = tl / g.nseg, seg = tl - row * g.nseg;
+      dilate_tile<true>(g, flags, F_D0, F_D1, ex, false, M, row, seg, tile_cnt, sh8);
+    }
+    grid.sync();
+  }
+  if (blockIdx.x == 0) scan_tiles_dev(tile_cnt, tile_off, ntiles, dsc, M, scnt, wsum);
+  grid.sync();
+  for (int32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+    const int32_t row = tl / g.nseg, seg = tl - row * g.nseg;
+    scatter_tile(g, flags, flags_alt, M, ex, round, dsc, tile_off, act, g2l, label, row, seg, wpre, sh8);
   }
 }
 
@@ -897,6 +971,15 @@ int launch_threshold(rsim_gpu_ctx* c, double eps) {
 
 // Full set update: [m-1 dilation rounds] + [round m fused with the tile count]
 // + scan + scatter.  4 launches for m = 2, no host round trip.
+static bool coop_set_update_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("RSIM_NO_COOP_K7");
+    v = (e && *e == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // single-block tile scan (counts staged in dynamic shared memory)
 static int launch_scan_tiles(rsim_gpu_ctx* c, int64_t ntiles, const SetMode& M) {
   const size_t smem = (size_t)(ntiles + ntiles / 32 + 1) * sizeof(int32_t);
@@ -930,6 +1013,34 @@ int launch_set_update(rsim_gpu_ctx* c, int mode, int round, double eps, int m, i
   // row groups reuse the ±y words RG-fold but give RG-fold fewer blocks: only
   // for grids large enough to fill the GPU many times over
   const bool use_rg = g.vec4 && (int64_t)grg.x * grg.y >= 16 * 148;
+  if (!use_rg && ntiles <= kCoopMaxTiles && coop_set_update_enabled()) {
+    static int per_sm = 0;
+    if (per_sm == 0) {
+      RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_set_update_coop, g.bs, 0));
+      if (per_sm < 1) per_sm = 1;
+    }
+    const int64_t maxb = (int64_t)per_sm * c->sm_count;
+    int grid = (int)(ntiles < maxb ? ntiles : maxb);
+    int32_t* tc = c->tile_cnt;
+    int32_t* to = c->tile_off;
+    int32_t* ab = c->act_buf;
+    int32_t* gl = c->g2l;
+    int32_t* lb = c->label;
+    uint8_t* f0 = c->flags;
+    uint8_t* f1 = c->flags_alt;
+    DevScalars* ds = c->dsc;
+    Geo4 gg = g;
+    SetMode MM = M;
+    int rr = rounds;
+    int32_t rd = round;
+    void* args[] = {&gg, &f0, &f1, &MM, &rr, &rd, &ds, &tc, &to, &ab, &gl, &lb};
+    RSIM_CUDA(cudaLaunchCooperativeKernel((void*)k_set_update_coop, grid, g.bs, args, 0, c->stream));
+    c->launches++;
+    RSIM_CUDA(cudaGetLastError());
+    std::swap(c->flags, c->flags_alt);
+    c->act = c->act_buf;
+    return RSIM_OK;
+  }
   for (int r = 0; r + 1 < rounds; ++r) {
     uint8_t bin = (r % 2 == 0) ? F_D0 : F_D1, bout = (r % 2 == 0) ? F_D1 : F_D0;
     if (use_rg) k_dilate_rg<false><<<grg, g.bs, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, 1, c->tile_cnt);
