@@ -466,6 +466,18 @@ def main():
         "roofline": roof,
         "clocks": clk.summary(),
     }
+    if rank == 0:  # the paper's comparison on the same workload (one timed run each, after the timed region)
+        cmp = {}
+        for sv, nm in ((0, "standard"), (1, "localized"), (2, "adaptive_dd")):
+            sim.run_case(sv, s0, dts, opts)
+            sim.L.rsim_gpu_mark(sim._ctx, 20)
+            r = sim.run_case(sv, s0, dts, opts)
+            sim.L.rsim_gpu_mark(sim._ctx, 21)
+            ms = C.c_double()
+            sim.L.rsim_gpu_elapsed(sim._ctx, 20, 21, C.byref(ms))
+            cmp[nm] = {"ms_per_run": ms.value, "newton_iters": r["iterations"], "krylov_iters": r["lin_iters"],
+                       "sum_nA": r["sum_na"], "total_MA": r["total_ma"], "status": r["status"]}
+        line["solver_comparison"] = cmp
     sim.close()
     if rank == 0 and args.c5:
         fr = [float(x) for x in args.c5.split(",") if x]
