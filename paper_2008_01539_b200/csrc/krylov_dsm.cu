@@ -43,6 +43,9 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int r) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(o) : "r"(a), "r"(r));
   return o;
 }
+#ifndef RSIM_DSM_PUSH
+#define RSIM_DSM_PUSH 1
+#endif
 #ifndef RSIM_DSM_TRACE
 #define RSIM_DSM_TRACE 0
 #endif
@@ -70,6 +73,30 @@ struct DArgs {
 };
 
 // Cluster loads of a row's B components (shared::cluster address; B = 3 is padded to 4).
+__device__ __forceinline__ void mb_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// 8-byte store into a peer CTA's shared memory that completes bytes on the
+// peer's transaction mbarrier (the completion has release semantics at
+// cluster scope: the issuing warp's earlier shared-memory writes, ordered by
+// __syncwarp / __syncthreads, are visible to the peer after its wait)
+__device__ __forceinline__ void st_async_f64(uint32_t remote_addr, double v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(remote_addr),
+               "l"(__double_as_longlong(v)), "r"(remote_bar)
+               : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nLAB_WAIT:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\nbra LAB_WAIT;\nDONE:\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
 // Row loads of B components through a generic pointer into this CTA's or a
 // peer CTA's shared memory (the hardware routes a peer window to DSMEM).
 // B = 3 rows are padded to 4 doubles, so every row starts 16-byte aligned.
@@ -108,6 +135,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   __shared__ int nnc_cnt;
   __shared__ double ws[2][5][32];  // [buf][q][warp]: canonical warp sums of this CTA
   __shared__ double res_s[5];
+#if RSIM_DSM_PUSH
+  __shared__ double tab[2][5][64];            // [buf][q][chunk | warp] pushed by every CTA (st.async)
+  __shared__ __align__(8) uint64_t mbar[2];   // one transaction barrier per tab buffer
+#endif
 
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
@@ -152,6 +183,93 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
     if (kTrace && tr) tc[6] += (unsigned long long)(clock64() - tb);
     if (kTrace && trw) tcr[trw - 1] += (unsigned long long)(clock64() - tb);
   };
+#if RSIM_DSM_PUSH
+  // Canonical reduction by PUSH: warp trees; with RC >= 256 (a CTA owns whole
+  // 256-row chunks) warp 0 forms this CTA's chunk partials, otherwise every
+  // warp ships its canonical warp sum; the values go with st.async straight
+  // into every CTA's table, completing bytes on that CTA's transaction
+  // mbarrier, so after its own wait a CTA reads everything from LOCAL shared
+  // memory (no cluster barrier, no remote loads); warp q finishes quantity q,
+  // one __syncthreads broadcasts.  Tables alternate; a CTA can run at most one
+  // reduction ahead (its next contribution needs everyone's previous one).
+  const bool chunk_mode = a.LRC >= 8;
+  const int CPC = chunk_mode ? (1 << (a.LRC - 8)) : 0;  // chunks per CTA
+  const int WPC = 1 << LWPC;
+  const uint32_t tab_u32 = smem_u32(&tab[0][0][0]), bar_u32 = smem_u32(&mbar[0]);
+  const uint32_t my_tab = mapa_u32(tab_u32, lane < G ? lane : 0);  // lane k talks to CTA k
+  const uint32_t my_bar = mapa_u32(bar_u32, lane < G ? lane : 0);
+  int kx = 0;
+  auto reduce = [&](auto NQc, const double* val, double* out) {
+    constexpr int NQ = decltype(NQc)::value;
+    double v[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) v[q] = val[q];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) v[q] = v[q] + __shfl_down_sync(0xffffffffu, v[q], off);
+    const int X = kx & 1;
+    const uint32_t par = (uint32_t)(kx >> 1) & 1u;
+    ++kx;
+    if (tid == 0) mb_arrive_expect_tx(bar_u32 + X * 8, chunk_mode ? (uint32_t)(nch * NQ * 8) : (uint32_t)(G * WPC * NQ * 8));
+    if (chunk_mode) {
+      if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) ws[wbuf][q][w] = v[q];
+      __syncthreads();
+      if (w == 0)
+        for (int pi = lane; pi < CPC * G; pi += 32) {
+          const int j = pi / G, dst = pi - j * G;
+          const int c = rank * CPC + j;
+          if (c < nch) {
+            const uint32_t rt = mapa_u32(tab_u32, dst), rb = mapa_u32(bar_u32, dst) + X * 8;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+              st_async_f64(rt + (uint32_t)(((X * 5 + q) * 64 + c) * 8), tree8(&ws[wbuf][q][8 * j]), rb);
+          }
+        }
+    } else {
+      __syncwarp();
+      double bq[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) bq[q] = __shfl_sync(0xffffffffu, v[q], 0);
+      if (lane < G)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) st_async_f64(my_tab + (uint32_t)(((X * 5 + q) * 64 + rank * WPC + w) * 8), bq[q], my_bar + X * 8);
+    }
+    const long long tb = (kTrace && trw) ? clock64() : 0;
+    mb_wait(bar_u32 + X * 8, par);
+    if (kTrace && trw) tcr[trw - 1] += (unsigned long long)(clock64() - tb);
+    for (int q = w; q < NQ; q += WPC) {  // warp q finishes quantity q from local shared memory
+      double cp0 = 0.0, cp1 = 0.0;
+      if (chunk_mode) {
+        if (lane < nch) cp0 = tab[X][q][lane];
+        if (lane + 32 < nch) cp1 = tab[X][q][lane + 32];
+      } else if (lane < nch) {  // nch <= 8 here
+        double w8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int gw = 8 * lane + k;
+          w8[k] = (gw < G * WPC && ((int64_t)gw << 5) < nr) ? tab[X][q][gw] : 0.0;  // structural zero
+        }
+        cp0 = tree8(w8);
+      }
+      double r;
+      if (nch == 1) {
+        r = cp0;
+      } else {
+        // lanes >= n hold +0.0, so the shuffle tree of warp_tree_n is bit-identical
+        double W[8] = {warp_tree_n(cp0, nch), nch > 32 ? warp_tree_n(cp1, nch - 32) : 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        r = tree8(W);
+      }
+      if (lane == 0) res_s[q] = r;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) out[q] = res_s[q];
+    wbuf ^= 1;
+  };
+#else
   // Canonical reduction of NQ per-row values (one per thread): warp trees into
   // shared memory, ONE cluster barrier, then warp q of every CTA gathers the 8
   // warp sums of each chunk via DSMEM and finishes the canonical tree (8-way
@@ -203,6 +321,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
     if (kTrace && trw == 1) tcr[4] += (unsigned long long)(clock64() - t_tail);
     wbuf ^= 1;
   };
+#endif
   auto xbar = [&]() { csync(); };
 
   // neighbour rows: cluster address per Cartesian slot (bit s of nmask = present)
@@ -303,7 +422,16 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   for (int e = 0; e < B; ++e) { sr[e] = 0.0; tr_[e] = 0.0; }
   // ---- load: matrix rows (MS), neighbour addresses, rhs -> r, r0; x = 0; (b,b), (F,F)
   if (tid == 0) nnc_cnt = 0;
+#if RSIM_DSM_PUSH
+  if (tid == 0) {
+    mb_init(bar_u32, 1);
+    mb_init(bar_u32 + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster.sync();  // every CTA's barriers initialised before the first st.async
+#else
   __syncthreads();
+#endif
   {
     double val[3] = {0.0, 0.0, 0.0};
     if (valid) {
