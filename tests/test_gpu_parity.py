@@ -26,6 +26,7 @@ CASES = {
     "c5rg": dict(config=5, nx=256, ny=256, nz=40),
     "c4rg": dict(config=4, nx=256, ny=256, nz=40, n_dfn=20),
     "c1x": dict(config=1, nx=102, ny=50),
+    "c5mid": dict(config=5, nx=64, ny=128, nz=40),  # > 4096 row tiles, < 16*148 row groups: separate row kernels
 }
 
 
@@ -53,7 +54,7 @@ def random_active(case, seed, frac=0.3):
     return np.union1d(a, pin).astype(np.int32)
 
 
-@pytest.mark.parametrize("name", [k for k in CASES if not k.endswith("rg")])
+@pytest.mark.parametrize("name", [k for k in CASES if not k.endswith("rg") and k != "c5mid"])
 def test_assemble_and_solve_bit_exact(name):
     case = pkg.Case(**CASES[name])
     s = perturbed_state(case, 7)
@@ -87,7 +88,7 @@ def test_assemble_and_solve_bit_exact(name):
     sim.close()
 
 
-@pytest.mark.parametrize("name", ["c1", "c2s", "c3s", "c5rg", "c4rg", "c1x"])
+@pytest.mark.parametrize("name", ["c1", "c2s", "c3s", "c5rg", "c4rg", "c1x", "c5mid"])
 @pytest.mark.parametrize("m", [1, 2, 4])
 @pytest.mark.parametrize("shrink_locked", [False, True])
 def test_estimate_active_flags_bit_exact(name, m, shrink_locked):
@@ -174,3 +175,30 @@ def test_run_case_bit_exact(name, solver, precond):
     assert rg["total_ma"] == ro["total_ma"]
     assert np.array_equal(rg["states"].u, ro["states"].u)
     sim.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2s", "c5mid"])
+def test_set_update_paths_agree(name, monkeypatch):
+    """The single-kernel cooperative K7 (small grids) and the multi-kernel path
+    give identical sets: run the same estimate with RSIM_NO_COOP_K7 in a child."""
+    import subprocess, sys, json, os
+    code = f"""
+import json, numpy as np, paper_2008_01539_b200 as pkg
+from tests.test_gpu_parity import CASES, random_active
+case = pkg.Case(**CASES[{name!r}])
+sim = pkg.GpuSimulator(case)
+rng = np.random.default_rng(5)
+va = random_active(case, 11, 0.05)
+dp = np.zeros(case.n); dp[va] = rng.lognormal(-2.0, 2.0, len(va))
+sim.set_active(va); sim.upload_dp(dp); sim.threshold(0.2)
+st = sim.estimate_active(0.2, 2, False)
+print(json.dumps({{"a": sim.active().tolist(), "b": sim.boundary().tolist(), "ex": int(st.expand)}}))
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ({}, {"RSIM_NO_COOP_K7": "1"}):
+        e = dict(os.environ, **env, PYTHONPATH=root)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=e, cwd=root, timeout=600)
+        assert r.returncode == 0, r.stderr
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1]
