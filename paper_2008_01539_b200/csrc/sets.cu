@@ -1019,7 +1019,12 @@ int launch_set_update(rsim_gpu_ctx* c, int mode, int round, double eps, int m, i
       RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_set_update_coop, g.bs, 0));
       if (per_sm < 1) per_sm = 1;
     }
-    const int64_t maxb = (int64_t)per_sm * c->sm_count;
+    static const int gmax = [] {
+      const char* e = std::getenv("RSIM_K7_COOP_GRID");
+      return (e && *e) ? std::atoi(e) : 1 << 30;
+    }();
+    int64_t maxb = (int64_t)per_sm * c->sm_count;
+    if (maxb > gmax) maxb = gmax;
     int grid = (int)(ntiles < maxb ? ntiles : maxb);
     int32_t* tc = c->tile_cnt;
     int32_t* to = c->tile_off;
