@@ -9,7 +9,13 @@ import numpy as np
 import paper_2008_01539_b200 as pkg
 
 which = sys.argv[1] if len(sys.argv) > 1 else "c2"
-if which == "c2":
+if which == "c2dd":  # adaptive nonlinear DD on the bench workload
+    case = pkg.Case(2)
+    sim = pkg.GpuSimulator(case)
+    dts = case.schedule()[:int(sys.argv[2]) if len(sys.argv) > 2 else 30]
+    r = sim.run_case(2, case.init_state(), dts, case.solver_opts())
+    print("c2dd", {k: v for k, v in r.items() if k != "states"})
+elif which == "c2":
     case = pkg.Case(2)
     sim = pkg.GpuSimulator(case)
     dts = case.schedule()[:int(sys.argv[2]) if len(sys.argv) > 2 else 8]
