@@ -52,6 +52,8 @@ struct DDLists {
   int32_t* sub_cells = nullptr;            // device, concatenated sorted lists
   int32_t* halo_cells = nullptr;
   int64_t sub_cap = 0, halo_cap = 0;
+  int32_t* hist = nullptr;                 // device [2][n_sub] list sizes
+  int64_t hist_cap = 0;
   int32_t selected = -1;
 };
 

@@ -845,6 +845,40 @@ __device__ __forceinline__ bool dd_pred(const Geo& g, const int32_t* __restrict_
   return h;
 }
 
+// Sizes of every subdomain list and halo list in one pass: cell i counts for
+// its own label (sub) and once for every distinct neighbour label k != label(i)
+// (halo of k) — integer sums, order-independent.  hist: [2][n_sub] in global.
+__global__ void __launch_bounds__(256) k_dd_hist(Geo g, const int32_t* __restrict__ label, int n_sub,
+                                                 int32_t* __restrict__ hist) {
+  extern __shared__ int32_t sh[];  // [2][n_sub]
+  for (int k = threadIdx.x; k < 2 * n_sub; k += blockDim.x) sh[k] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x * 8;
+  for (int q = 0; q < 8; ++q) {
+    const int64_t i = base + q;
+    if (i >= g.n) break;
+    const int32_t li = label[i];
+    if (li >= 0 && li < n_sub) atomicAdd(&sh[li], 1);
+    // each distinct neighbour label counts once: the j-th neighbour counts
+    // unless an earlier neighbour (enumeration order) carries the same label
+    int idx = 0;
+    each_nbr(g, i, [&](int64_t j) {
+      const int32_t lj = label[j];
+      const int me = idx++;
+      if (lj < 0 || lj >= n_sub || lj == li) return;
+      int k2 = 0;
+      bool dup = false;
+      each_nbr(g, i, [&](int64_t j2) {
+        if (k2++ < me && label[j2] == lj) dup = true;
+      });
+      if (!dup) atomicAdd(&sh[n_sub + lj], 1);
+    });
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 2 * n_sub; k += blockDim.x)
+    if (sh[k]) atomicAdd(&hist[k], sh[k]);
+}
+
 __global__ void __launch_bounds__(256) k_dd_count(Geo g, const int32_t* __restrict__ label, int k, int sel,
                                                   int32_t* __restrict__ tile_cnt) {
   __shared__ int32_t wsum[8];
@@ -1139,16 +1173,21 @@ int launch_dd_partition(rsim_gpu_ctx* c, int32_t n_sub, int32_t* sizes) {
   d.halo_off.assign(n_sub + 1, 0);
   d.selected = -1;
   std::vector<int32_t> cnt_sub(n_sub), cnt_halo(n_sub);
-  // counts (two syncs per subdomain; Phase-2 setup happens once per timestep)
-  for (int sel = 0; sel < 2; ++sel) {
-    for (int k = 0; k < n_sub; ++k) {
-      k_dd_count<<<ntiles, 256, 0, c->stream>>>(g, c->label, k, sel, c->tile_cnt);
-      { const int r = launch_scan_tiles(c, ntiles, SetMode{MODE_KEEP, 0, 0.0, 1, 0}); if (r != RSIM_OK) return r; }
-      c->launches += 1;
-      RSIM_CUDA(cudaMemcpyAsync(&(sel ? cnt_halo : cnt_sub)[k], &c->dsc->nA, sizeof(int32_t),
-                                cudaMemcpyDeviceToHost, c->stream));
-      RSIM_CUDA(cudaStreamSynchronize(c->stream));
+  // all list sizes in one pass and one sync (Phase-2 setup happens once per timestep)
+  {
+    std::vector<int32_t> h(2 * (size_t)n_sub, 0);
+    if (2 * (int64_t)n_sub > d.hist_cap) {
+      if (d.hist) cudaFree(d.hist);
+      d.hist_cap = 2 * (int64_t)n_sub + 64;
+      RSIM_CUDA(cudaMalloc(&d.hist, sizeof(int32_t) * d.hist_cap));
     }
+    int32_t* dh = d.hist;
+    RSIM_CUDA(cudaMemsetAsync(dh, 0, sizeof(int32_t) * 2 * n_sub, c->stream));
+    k_dd_hist<<<ntiles, 256, sizeof(int32_t) * 2 * n_sub, c->stream>>>(g, c->label, n_sub, dh);
+    c->launches++;
+    RSIM_CUDA(cudaMemcpyAsync(h.data(), dh, sizeof(int32_t) * 2 * n_sub, cudaMemcpyDeviceToHost, c->stream));
+    RSIM_CUDA(cudaStreamSynchronize(c->stream));
+    for (int k = 0; k < n_sub; ++k) { cnt_sub[k] = h[k]; cnt_halo[k] = h[n_sub + k]; }
   }
   for (int k = 0; k < n_sub; ++k) {
     d.sub_off[k + 1] = d.sub_off[k] + cnt_sub[k];
