@@ -97,6 +97,8 @@ __global__ void k_reset_scalars(DevScalars* d) {
   d->lin_relres = 0.0;
   d->f2 = 0.0;
   d->finf = 0ull;
+  d->maxA = 0ull;  // ‖δp‖∞ of the coming update (a fused update has no memset of its own)
+  d->maxB = 0ull;
 }
 
 // p component of the interleaved state: dst[i] = u[i*b]
@@ -381,10 +383,26 @@ int rsim_gpu_linear_solve(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
 
 int rsim_gpu_update(rsim_gpu_ctx* c, double eps) {
   c->last_eps = eps;
+  if (c->update_applied) {  // fused into the preceding cluster Krylov launch (Newton loops only)
+    c->update_applied = false;
+    return RSIM_OK;
+  }
   rsim_phase_begin(c, 3);
   TRY(launch_update(c, eps));
   rsim_phase_end(c);
   return RSIM_OK;
+}
+
+// Newton loops: solve + update, with the update fused into the Krylov kernel
+// when the cluster path runs (the public linear_solve never fuses).
+int rsim_internal_solve_update(rsim_gpu_ctx* c, const rsim_solver_opts* o, double eps) {
+  c->fuse_update = true;
+  c->fuse_eps = eps;
+  c->update_applied = false;
+  const int r = rsim_gpu_linear_solve(c, o);
+  c->fuse_update = false;
+  if (r != RSIM_OK) return r;
+  return rsim_gpu_update(c, eps);
 }
 
 int rsim_gpu_threshold(rsim_gpu_ctx* c, double eps) {

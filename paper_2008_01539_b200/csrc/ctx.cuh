@@ -67,6 +67,9 @@ struct rsim_gpu_ctx {
   bool cols_implicit = false;  // last assembly: V_A = all cells, ELL columns not stored (structural)
   bool f2_parts = false;       // last assembly left (F,F) chunk partials in part_f2 (F_raw only if keep_F)
   bool keep_F = false;         // debug: the row kernel also stores the raw residual
+  bool fuse_update = false;    // Newton loops: the cluster Krylov kernel also applies K6 (eps below)
+  double fuse_eps = 0.0;
+  bool update_applied = false; // the last Krylov launch already applied the update
   double* gm_V = nullptr;      // GMRES basis (RSIM_GMRES_M + 1 vectors), allocated on first use
   double* gm_part = nullptr;   // GMRES reduction partials
   struct Ilu {                 // level-scheduled block ILU(0) (ilu.cu)

@@ -70,6 +70,12 @@ struct DArgs {
   double* x;
   DevScalars* dsc;
   unsigned long long* trace;  // optional [8] cycle accumulators (RSIM_KTRACE)
+  // fused Newton update (K6, sets.cu k_update) in the epilogue, Newton loops only
+  int32_t upd;
+  double eps;
+  rsim_fluid_params fl;
+  double *u, *dp, *last_dp;
+  uint8_t *st, *flags;
 };
 
 // Cluster loads of a row's B components (shared::cluster address; B = 3 is padded to 4).
@@ -669,6 +675,40 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   if (valid)
 #pragma unroll
     for (int e = 0; e < B; ++e) a.x[l * B + e] = xr[e];
+  if (a.upd) {  // K6 in the epilogue (same operations as k_update): u += δu, substitution, flags, ‖δp‖∞
+    double aA = 0.0, aB = 0.0;
+    bool bad = false;
+    if (valid) {
+      const int64_t i = a.act[l];
+      double ui[B];
+#pragma unroll
+      for (int c = 0; c < B; ++c) ui[c] = a.u[i * B + c] + xr[c];
+      uint8_t stv = a.st[i];
+      rsim::phys::substitute<B>(a.fl, ui, stv);
+#pragma unroll
+      for (int c = 0; c < B; ++c) a.u[i * B + c] = ui[c];
+      a.st[i] = stv;
+      const double d = xr[0];
+      const double ad = fabs(d);
+      bad = !isfinite(d);
+      a.dp[i] = d;
+      a.last_dp[i] = ad;
+      uint8_t f = a.flags[i];
+      if (ad >= a.eps) {
+        f |= F_FLAG;
+        if (f & F_B) f |= F_D0;
+      }
+      a.flags[i] = f;
+      aA = ad;
+      aB = (f & F_B) ? ad : 0.0;
+    }
+    if (bad) a.dsc->status = RSIM_ENUM;
+    const double wa = warp_max(aA), wb = warp_max(aB);
+    if (lane == 0) {
+      if (wa > 0.0) atomic_max_bits(&a.dsc->maxA, wa);
+      if (wb > 0.0) atomic_max_bits(&a.dsc->maxB, wb);
+    }
+  }
   if (kTrace && a.trace) {
     if (valid) atomicAdd(&tcr[6], 1ull);
     __syncthreads();
@@ -791,6 +831,10 @@ int launch_krylov_dsm(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.F_raw = c->F_raw;
   a.x = c->x;
   a.trace = c->ktrace;
+  a.upd = c->fuse_update ? 1 : 0;
+  a.eps = c->fuse_eps;
+  a.fl = c->fl;
+  a.u = c->u; a.dp = c->dp; a.last_dp = c->last_dp; a.st = c->st; a.flags = c->flags;
   a.dsc = c->dsc;
   // one chunk per CTA when possible (G = nch <= 16), else 2 or 4 chunks per CTA
   // (powers of two, so the owner of a row is a shift)
@@ -820,6 +864,7 @@ int launch_krylov_dsm(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
     if (r != RSIM_OK) return r;
     if (ok) {
       c->launches++;
+      c->update_applied = c->fuse_update;
       RSIM_CUDA(cudaGetLastError());
       return RSIM_OK;
     }

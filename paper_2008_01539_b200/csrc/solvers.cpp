@@ -25,6 +25,7 @@ int64_t rsim_internal_n(const rsim_gpu_ctx* c);
 int rsim_internal_b(const rsim_gpu_ctx* c);
 int32_t rsim_internal_nA(const rsim_gpu_ctx* c);
 extern "C" int rsim_internal_add_row_iters(rsim_gpu_ctx* c, int64_t v);
+extern "C" int rsim_internal_solve_update(rsim_gpu_ctx* c, const rsim_solver_opts* o, double eps);
 
 namespace {
 
@@ -47,8 +48,7 @@ void rep_push(rsim_newton_report* rep, const rsim_iter_record& r, int64_t n) {
 // assemble -> Krylov -> update over the current device active list.
 int local_step(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   TRY(rsim_gpu_assemble(c));
-  TRY(rsim_gpu_linear_solve(c, o));
-  TRY(rsim_gpu_update(c, o->eps_set));
+  TRY(rsim_internal_solve_update(c, o, o->eps_set));
   return RSIM_OK;
 }
 
