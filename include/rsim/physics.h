@@ -88,11 +88,11 @@ RSIM_HD double rexp(double x) {
 
 /* Quadratic Corey curve on the normalised saturation (s − s_r)/den,
  * clamped to [0,1].  dkr is d kr / d s. */
-RSIM_HD void corey2(double s, double s_r, double den, double& kr, double& dkr) {
-  double se = (s - s_r) * (1.0 / den);
+RSIM_HD void corey2(double s, double s_r, double inv_den, double& kr, double& dkr) {
+  double se = (s - s_r) * inv_den;
   if (!(se > 0.0)) { kr = 0.0; dkr = 0.0; }
   else if (!(se < 1.0)) { kr = 1.0; dkr = 0.0; }
-  else { kr = se * se; dkr = (2.0 * se) * (1.0 / den); }
+  else { kr = se * se; dkr = (2.0 * se) * inv_den; }
 }
 
 /* Per-cell property block.
@@ -107,19 +107,38 @@ struct Props {
   double dL[B][B];
 };
 
+/* Model constants plus the reciprocals the formulas use, formed ONCE per
+ * context (host) and shipped to the kernels as a by-value argument: every
+ * formula multiplies by these, so host and device use the same bits without
+ * a division per evaluation. */
+struct Fluid : rsim_fluid_params {
+  double inv_mu[3];
+  double inv_pbub, inv_pgas;
+  double inv_den2;  /* 1 / (1 − swc − sor)        oil-water Corey  */
+  double inv_den3;  /* 1 / (1 − swc − sor − sgc)  black-oil Corey  */
+  RSIM_HD Fluid() : rsim_fluid_params(), inv_mu{0.0, 0.0, 0.0}, inv_pbub(0.0), inv_pgas(0.0), inv_den2(0.0), inv_den3(0.0) {}
+  RSIM_HD explicit Fluid(const rsim_fluid_params& f) : rsim_fluid_params(f) {
+    for (int k = 0; k < 3; ++k) inv_mu[k] = 1.0 / f.mu[k];
+    inv_pbub = 1.0 / f.p_bub;
+    inv_pgas = 1.0 / f.p_gas;
+    inv_den2 = 1.0 / ((1.0 - f.swc) - f.sor);
+    inv_den3 = 1.0 / (((1.0 - f.swc) - f.sor) - f.sgc);
+  }
+};
+
 /* ---- Model 1: single phase slightly compressible, u = (p) ------------ */
-RSIM_HD void props(const rsim_fluid_params& f, const double* u, uint8_t /*st*/, Props<1>& P) {
+RSIM_HD void props(const Fluid& f, const double* u, uint8_t /*st*/, Props<1>& P) {
   double p = u[0];
   double rho = f.rho_ref[1] * rexp(f.c_f[1] * (p - f.p_ref));
   double drho = f.c_f[1] * rho;
   P.A[0] = rho;
   P.dA[0][0] = drho;
-  P.L[0] = rho * (1.0 / f.mu[1]);
-  P.dL[0][0] = drho * (1.0 / f.mu[1]);
+  P.L[0] = rho * f.inv_mu[1];
+  P.dL[0][0] = drho * f.inv_mu[1];
 }
 
 /* ---- Model 2: oil-water, u = (p, S_w); equations (water, oil) --------- */
-RSIM_HD void props(const rsim_fluid_params& f, const double* u, uint8_t /*st*/, Props<2>& P) {
+RSIM_HD void props(const Fluid& f, const double* u, uint8_t /*st*/, Props<2>& P) {
   double p = u[0], sw = u[1];
   double rw = f.rho_ref[0] * rexp(f.c_f[0] * (p - f.p_ref));
   double drw = f.c_f[0] * rw;
@@ -132,30 +151,29 @@ RSIM_HD void props(const rsim_fluid_params& f, const double* u, uint8_t /*st*/, 
   P.A[1] = ro * so;
   P.dA[1][0] = dro * so;
   P.dA[1][1] = -ro;
-  double den = 1.0 - f.swc - f.sor;
   double krw, dkrw, kro, dkro;
-  corey2(sw, f.swc, den, krw, dkrw);
-  corey2(so, f.sor, den, kro, dkro); /* d/dso; d so/d sw = -1 */
-  P.L[0] = (rw * krw) * (1.0 / f.mu[0]);
-  P.dL[0][0] = (drw * krw) * (1.0 / f.mu[0]);
-  P.dL[0][1] = (rw * dkrw) * (1.0 / f.mu[0]);
-  P.L[1] = (ro * kro) * (1.0 / f.mu[1]);
-  P.dL[1][0] = (dro * kro) * (1.0 / f.mu[1]);
-  P.dL[1][1] = -((ro * dkro) * (1.0 / f.mu[1]));
+  corey2(sw, f.swc, f.inv_den2, krw, dkrw);
+  corey2(so, f.sor, f.inv_den2, kro, dkro); /* d/dso; d so/d sw = -1 */
+  P.L[0] = (rw * krw) * f.inv_mu[0];
+  P.dL[0][0] = (drw * krw) * f.inv_mu[0];
+  P.dL[0][1] = (rw * dkrw) * f.inv_mu[0];
+  P.L[1] = (ro * kro) * f.inv_mu[1];
+  P.dL[1][0] = (dro * kro) * f.inv_mu[1];
+  P.dL[1][1] = -((ro * dkro) * f.inv_mu[1]);
 }
 
 /* ---- Model 3: black-oil, u = (p, S_w, X); equations (water, oil, gas) --
  * status SAT: X = S_g, R_s = R_s,sat(p);  UNDERSAT: X = R_s, S_g = 0.
  * Surface-volume conservation:  water φ S_w b_w;  oil φ S_o b_o;
  * gas φ (S_g b_g + R_s S_o b_o); b_l reciprocal formation volume factors.  */
-RSIM_HD void props(const rsim_fluid_params& f, const double* u, uint8_t st, Props<3>& P) {
+RSIM_HD void props(const Fluid& f, const double* u, uint8_t st, Props<3>& P) {
   double p = u[0], sw = u[1], X = u[2];
   double bw = rexp(f.c_f[0] * (p - f.p_ref));
   double dbw = f.c_f[0] * bw;
   double eo = rexp(f.c_f[1] * (p - f.p_ref));
   double rs, drs_dp, drs_dx, sg, dsg_dx;
   if (st == RSIM_BO_SAT) {
-    rs = (f.rs_b * p) * (1.0 / f.p_bub); drs_dp = f.rs_b * (1.0 / f.p_bub); drs_dx = 0.0;
+    rs = (f.rs_b * p) * f.inv_pbub; drs_dp = f.rs_b * f.inv_pbub; drs_dx = 0.0;
     sg = X; dsg_dx = 1.0;
   } else {
     rs = X; drs_dp = 0.0; drs_dx = 1.0;
@@ -168,8 +186,8 @@ RSIM_HD void props(const rsim_fluid_params& f, const double* u, uint8_t st, Prop
   double dbo_drs = -((f.bo_alpha * bo) / q);
   double dbo_dp = f.c_f[1] * bo + dbo_drs * drs_dp;
   double dbo_dx = dbo_drs * drs_dx;
-  double bg = p * (1.0 / f.p_gas);
-  double dbg = 1.0 / f.p_gas;
+  double bg = p * f.inv_pgas;
+  double dbg = f.inv_pgas;
 
   P.A[0] = sw * bw;
   P.dA[0][0] = sw * dbw;
@@ -185,47 +203,46 @@ RSIM_HD void props(const rsim_fluid_params& f, const double* u, uint8_t st, Prop
   P.dA[2][1] = -(rs * bo);
   P.dA[2][2] = (dsg_dx * bg + drs_dx * sobo) + rs * P.dA[1][2];
 
-  double den = ((1.0 - f.swc) - f.sor) - f.sgc;
   double krw, dkrw, kro, dkro, krg, dkrg;
-  corey2(sw, f.swc, den, krw, dkrw);
-  corey2(so, f.sor, den, kro, dkro);
-  corey2(sg, f.sgc, den, krg, dkrg);
-  double lo = (bo * kro) * (1.0 / f.mu[1]);
-  double dlo_dp = (dbo_dp * kro) * (1.0 / f.mu[1]);
-  double dlo_dsw = -((bo * dkro) * (1.0 / f.mu[1]));
-  double dlo_dx = (dbo_dx * kro + bo * (dkro * dso_dx)) * (1.0 / f.mu[1]);
-  P.L[0] = (bw * krw) * (1.0 / f.mu[0]);
-  P.dL[0][0] = (dbw * krw) * (1.0 / f.mu[0]);
-  P.dL[0][1] = (bw * dkrw) * (1.0 / f.mu[0]);
+  corey2(sw, f.swc, f.inv_den3, krw, dkrw);
+  corey2(so, f.sor, f.inv_den3, kro, dkro);
+  corey2(sg, f.sgc, f.inv_den3, krg, dkrg);
+  double lo = (bo * kro) * f.inv_mu[1];
+  double dlo_dp = (dbo_dp * kro) * f.inv_mu[1];
+  double dlo_dsw = -((bo * dkro) * f.inv_mu[1]);
+  double dlo_dx = (dbo_dx * kro + bo * (dkro * dso_dx)) * f.inv_mu[1];
+  P.L[0] = (bw * krw) * f.inv_mu[0];
+  P.dL[0][0] = (dbw * krw) * f.inv_mu[0];
+  P.dL[0][1] = (bw * dkrw) * f.inv_mu[0];
   P.dL[0][2] = 0.0;
   P.L[1] = lo;
   P.dL[1][0] = dlo_dp;
   P.dL[1][1] = dlo_dsw;
   P.dL[1][2] = dlo_dx;
-  double lg = (bg * krg) * (1.0 / f.mu[2]);
+  double lg = (bg * krg) * f.inv_mu[2];
   P.L[2] = lg + rs * lo;
-  P.dL[2][0] = ((dbg * krg) * (1.0 / f.mu[2]) + drs_dp * lo) + rs * dlo_dp;
+  P.dL[2][0] = ((dbg * krg) * f.inv_mu[2] + drs_dp * lo) + rs * dlo_dp;
   P.dL[2][1] = rs * dlo_dsw;
-  P.dL[2][2] = ((bg * (dkrg * dsg_dx)) * (1.0 / f.mu[2]) + drs_dx * lo) + rs * dlo_dx;
+  P.dL[2][2] = ((bg * (dkrg * dsg_dx)) * f.inv_mu[2] + drs_dx * lo) + rs * dlo_dx;
 }
 
 /* Mass in place M_e = pv φ(p) A_e (used for the old-time accumulation). */
 template <int B>
-RSIM_HD void mass(const rsim_fluid_params& f, double pv, double p, const Props<B>& P, double* M) {
+RSIM_HD void mass(const Fluid& f, double pv, double p, const Props<B>& P, double* M) {
   double pvp = pv * (1.0 + f.c_r * (p - f.p_ref));
   for (int e = 0; e < B; ++e) M[e] = pvp * P.A[e];
 }
 
 /* Accumulation: initialises the row residual R and diagonal block D. */
 template <int B>
-RSIM_HD void accum_row(const rsim_fluid_params& f, double pv, double p, const Props<B>& P,
-                       const double* Mold, double dt, double* R, double (*D)[B]) {
+RSIM_HD void accum_row(const Fluid& f, double pv, double p, const Props<B>& P,
+                       const double* Mold, double inv_dt, double* R, double (*D)[B]) {
   double pvp = pv * (1.0 + f.c_r * (p - f.p_ref));
   double pvc = pv * f.c_r;
   for (int e = 0; e < B; ++e) {
-    R[e] = (pvp * P.A[e] - Mold[e]) * (1.0 / dt);
-    D[e][0] = (pvp * P.dA[e][0] + pvc * P.A[e]) * (1.0 / dt);
-    for (int v = 1; v < B; ++v) D[e][v] = (pvp * P.dA[e][v]) * (1.0 / dt);
+    R[e] = (pvp * P.A[e] - Mold[e]) * inv_dt;
+    D[e][0] = (pvp * P.dA[e][0] + pvc * P.A[e]) * inv_dt;
+    for (int v = 1; v < B; ++v) D[e][v] = (pvp * P.dA[e][v]) * inv_dt;
   }
 }
 
@@ -293,10 +310,10 @@ RSIM_HD void well_rate(double wi, double p, double bhp, const Props<B>& P, doubl
 RSIM_HD double clamp01(double s) { return s < 0.0 ? 0.0 : (s > 1.0 ? 1.0 : s); }
 
 template <int B>
-RSIM_HD void substitute(const rsim_fluid_params& f, double* u, uint8_t& st) {
+RSIM_HD void substitute(const Fluid& f, double* u, uint8_t& st) {
   if (B >= 2) u[1] = clamp01(u[1]);
   if (B == 3) {
-    double rs_sat = (f.rs_b * u[0]) * (1.0 / f.p_bub);
+    double rs_sat = (f.rs_b * u[0]) * f.inv_pbub;
     if (st == RSIM_BO_UNDERSAT) {
       if (u[2] > rs_sat) { st = RSIM_BO_SAT; u[2] = 0.0; }
     } else {

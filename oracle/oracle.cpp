@@ -73,7 +73,7 @@ struct Graph {
 
 struct Model {
   Graph g;
-  rsim_fluid_params fl{};
+  phys::Fluid fl;  // params + reciprocals (physics.h)
   int b = 1;
   std::vector<double> u, mold, dp;
   std::vector<uint8_t> st;
@@ -173,7 +173,7 @@ static bool assemble_row(Model& M, int32_t l) {
   phys::Props<B> Pi;
   phys::props(M.fl, ui, M.st[i], Pi);
   double R[B], D[B][B], O[B][B];
-  phys::accum_row<B>(M.fl, g.pv[i], ui[0], Pi, &M.mold[i * B], M.dt, R, D);
+  phys::accum_row<B>(M.fl, g.pv[i], ui[0], Pi, &M.mold[i * B], 1.0 / M.dt, R, D);
   int64_t pos = M.rowptr[l];
   g.each(i, [&](int64_t j, double T) {
     const double* uj = &M.u[j * B];
@@ -917,7 +917,7 @@ void* orc_create(const rsim_graph_desc* gd, const rsim_fluid_params* f) {
   }
   g.pinned.resize(g.n);
   for (int64_t i = 0; i < g.n; ++i) g.pinned[i] = (uint8_t)(g.kind[i] == RSIM_KIND_FRACTURE || g.wi[i] > 0.0);
-  M->fl = *f;
+  M->fl = phys::Fluid(*f);
   M->b = f->kind;
   M->u.assign(g.n * M->b, 0.0);
   M->mold.assign(g.n * M->b, 0.0);
@@ -1105,7 +1105,7 @@ int orc_run_case(void* h, int32_t solver, const double* dts, int32_t nsteps, con
 
 double orc_rexp(double x) { return phys::rexp(x); }
 
-void orc_corey(double s, double s_r, double den, double* kr, double* dkr) { phys::corey2(s, s_r, den, *kr, *dkr); }
+void orc_corey(double s, double s_r, double den, double* kr, double* dkr) { phys::corey2(s, s_r, 1.0 / den, *kr, *dkr); }
 
 }  // extern "C"
 
@@ -1113,7 +1113,7 @@ template <int B>
 static void props_out(const rsim_fluid_params* f, const double* u, uint8_t st, double* A, double* dA, double* L,
                       double* dL) {
   phys::Props<B> P;
-  phys::props(*f, u, st, P);
+  phys::props(phys::Fluid(*f), u, st, P);
   for (int e = 0; e < B; ++e) {
     A[e] = P.A[e];
     L[e] = P.L[e];

@@ -19,8 +19,8 @@
 namespace {
 
 struct AsmArgs {
-  rsim_fluid_params fl;
-  double dt, bhp;
+  rsim::phys::Fluid fl;
+  double dt, inv_dt, bhp;
   int32_t nx, ny, nz, nslot, nA;
   int64_t cap;
   bool d3, has_nnc;
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
     double R[B], D[B][B], Mo[B];
 #pragma unroll
     for (int c = 0; c < B; ++c) Mo[c] = __ldg(&a.mold[i * B + c]);
-    rsim::phys::accum_row<B>(a.fl, __ldg(&a.pv[i]), ui[0], Pi, Mo, a.dt, R, D);
+    rsim::phys::accum_row<B>(a.fl, __ldg(&a.pv[i]), ui[0], Pi, Mo, a.inv_dt, R, D);
     for (int s = 0; s < a.nslot; ++s)
       if (sHas[rg][s]) {
 #pragma unroll
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(256) k_assemble_row(const AsmArgs a) {
     rsim::phys::Props<B> Pi;
     rsim::phys::props(a.fl, ui, sti, Pi);
     double R[B], D[B][B];
-    rsim::phys::accum_row<B>(a.fl, pv, ui[0], Pi, Mo, a.dt, R, D);
+    rsim::phys::accum_row<B>(a.fl, pv, ui[0], Pi, Mo, a.inv_dt, R, D);
     double Okeep[6][B][B];
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(256) k_assemble_row(const AsmArgs a) {
 
 // Old-time accumulation M^n = pv φ(p) A(u) for every cell (set_state / Δt change).
 template <int B>
-__global__ void k_mold(rsim_fluid_params fl, int64_t n, const double* __restrict__ u, const uint8_t* __restrict__ st,
+__global__ void k_mold(rsim::phys::Fluid fl, int64_t n, const double* __restrict__ u, const uint8_t* __restrict__ st,
                        const double* __restrict__ pv, double* __restrict__ mold) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -446,8 +446,9 @@ int launch_materialize_cols(rsim_gpu_ctx* c) {
 int launch_assemble(rsim_gpu_ctx* c) {
   if (c->nA <= 0) return RSIM_OK;
   AsmArgs a;
-  a.fl = c->fl;
+  a.fl = rsim::phys::Fluid(c->fl);
   a.dt = c->dt;
+  a.inv_dt = 1.0 / c->dt;
   a.bhp = c->bhp;
   a.nx = c->nx; a.ny = c->ny; a.nz = c->nz;
   a.nslot = c->nslot;
@@ -496,9 +497,9 @@ int launch_mold(rsim_gpu_ctx* c) {
   const int th = 256;
   const int64_t blocks = (c->n + th - 1) / th;
   switch (c->b) {
-    case 1: k_mold<1><<<blocks, th, 0, c->stream>>>(c->fl, c->n, c->u, c->st, c->pv, c->mold); break;
-    case 2: k_mold<2><<<blocks, th, 0, c->stream>>>(c->fl, c->n, c->u, c->st, c->pv, c->mold); break;
-    default: k_mold<3><<<blocks, th, 0, c->stream>>>(c->fl, c->n, c->u, c->st, c->pv, c->mold); break;
+    case 1: k_mold<1><<<blocks, th, 0, c->stream>>>(rsim::phys::Fluid(c->fl), c->n, c->u, c->st, c->pv, c->mold); break;
+    case 2: k_mold<2><<<blocks, th, 0, c->stream>>>(rsim::phys::Fluid(c->fl), c->n, c->u, c->st, c->pv, c->mold); break;
+    default: k_mold<3><<<blocks, th, 0, c->stream>>>(rsim::phys::Fluid(c->fl), c->n, c->u, c->st, c->pv, c->mold); break;
   }
   c->launches++;
   RSIM_CUDA(cudaGetLastError());

@@ -73,7 +73,7 @@ struct DArgs {
   // fused Newton update (K6, sets.cu k_update) in the epilogue, Newton loops only
   int32_t upd;
   double eps;
-  rsim_fluid_params fl;
+  rsim::phys::Fluid fl;
   double *u, *dp, *last_dp;
   uint8_t *st, *flags;
 };
@@ -833,7 +833,7 @@ int launch_krylov_dsm(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.trace = c->ktrace;
   a.upd = c->fuse_update ? 1 : 0;
   a.eps = c->fuse_eps;
-  a.fl = c->fl;
+  a.fl = rsim::phys::Fluid(c->fl);
   a.u = c->u; a.dp = c->dp; a.last_dp = c->last_dp; a.st = c->st; a.flags = c->flags;
   a.dsc = c->dsc;
   // one chunk per CTA when possible (G = nch <= 16), else 2 or 4 chunks per CTA

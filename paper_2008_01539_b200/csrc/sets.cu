@@ -54,7 +54,7 @@ __device__ __forceinline__ void each_nbr(const Geo& g, int64_t i, F&& f) {
 
 // ---------------------------------------------------------------- K6 update
 template <int B>
-__global__ void __launch_bounds__(256) k_update(rsim_fluid_params fl, int32_t nA, const int32_t* __restrict__ act,
+__global__ void __launch_bounds__(256) k_update(rsim::phys::Fluid fl, int32_t nA, const int32_t* __restrict__ act,
                                                  const double* __restrict__ x, double* __restrict__ u,
                                                  uint8_t* __restrict__ st, uint8_t* __restrict__ flags,
                                                  double* __restrict__ dp, double* __restrict__ last_dp, double eps,
@@ -984,9 +984,9 @@ int launch_update(rsim_gpu_ctx* c, double eps) {
   RSIM_CUDA(cudaMemsetAsync(&c->dsc->maxA, 0, 2 * sizeof(unsigned long long), c->stream));
   const int64_t g = nblk(c->nA, 256);
   switch (c->b) {
-    case 1: k_update<1><<<g, 256, 0, c->stream>>>(c->fl, c->nA, c->act, c->x, c->u, c->st, c->flags, c->dp, c->last_dp, eps, c->dsc); break;
-    case 2: k_update<2><<<g, 256, 0, c->stream>>>(c->fl, c->nA, c->act, c->x, c->u, c->st, c->flags, c->dp, c->last_dp, eps, c->dsc); break;
-    default: k_update<3><<<g, 256, 0, c->stream>>>(c->fl, c->nA, c->act, c->x, c->u, c->st, c->flags, c->dp, c->last_dp, eps, c->dsc); break;
+    case 1: k_update<1><<<g, 256, 0, c->stream>>>(rsim::phys::Fluid(c->fl), c->nA, c->act, c->x, c->u, c->st, c->flags, c->dp, c->last_dp, eps, c->dsc); break;
+    case 2: k_update<2><<<g, 256, 0, c->stream>>>(rsim::phys::Fluid(c->fl), c->nA, c->act, c->x, c->u, c->st, c->flags, c->dp, c->last_dp, eps, c->dsc); break;
+    default: k_update<3><<<g, 256, 0, c->stream>>>(rsim::phys::Fluid(c->fl), c->nA, c->act, c->x, c->u, c->st, c->flags, c->dp, c->last_dp, eps, c->dsc); break;
   }
   c->launches++;
   RSIM_CUDA(cudaGetLastError());
