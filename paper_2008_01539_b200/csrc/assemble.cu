@@ -14,6 +14,8 @@
 //   no atomics except the ‖F‖∞ / singular-cell reductions.
 // Block-Jacobi scaling is fused: the row is multiplied by D_ii^{-1} before it
 // is stored, so the Krylov kernel sees a unit block diagonal (never stored).
+#include <cstdlib>
+
 #include "ctx.cuh"
 
 namespace {
@@ -404,6 +406,125 @@ __global__ void __launch_bounds__(256) k_assemble_row(const AsmArgs a) {
   if (threadIdx.x == 0) a.part_f2[blockIdx.x] = tree8(wsf);
 }
 
+// FULL set, b = 1, no NNC, nx % 256 == 0, ny % FRY == 0 (config 5, standard
+// Newton on single-phase grids): one 256-thread block per tile of 256 (x) ×
+// FRY (y) cells of one plane.  The properties of every tile cell and of a
+// one-cell halo are evaluated ONCE into shared memory (each needs an exp),
+// instead of once per referencing row as in the row kernel (up to 7 per row,
+// and warps pay for divergent upwind choices); the ±z neighbours are
+// evaluated as in the row kernel.  Same physics.h calls and the same
+// canonical order per row => the same bits.  Each tile row is one canonical
+// 256-row chunk, so the (F,F) chunk partials come out as in the row kernel.
+constexpr int FRY = 4;
+__global__ void __launch_bounds__(256) k_assemble_full1(const AsmArgs a) {
+  // p, ρ, dρ/dp per tile/halo cell; λρ = ρ·(1/μ) and its derivative are re-formed
+  // with the same multiplication props<1> uses (same bits)
+  __shared__ double su[FRY + 2][258], sA[FRY + 2][258], sdA[FRY + 2][258];
+  __shared__ double wsf[FRY][8];
+  using rsim::phys::Props;
+  const int t = threadIdx.x;
+  const int x0 = blockIdx.x * 256, y0 = blockIdx.y * FRY, z = blockIdx.z;
+  const int64_t nxy = (int64_t)a.nx * a.ny;
+  auto put = [&](int r, int c, int64_t i) {
+    double ui[1] = {__ldg(&a.u[i])};
+    Props<1> P;
+    rsim::phys::props(a.fl, ui, (uint8_t)0, P);
+    su[r][c] = ui[0];
+    sA[r][c] = P.A[0]; sdA[r][c] = P.dA[0][0];
+  };
+  const double imu = a.fl.inv_mu[1];
+  for (int r = 0; r < FRY + 2; ++r) {  // tile rows + halo rows, thread t = column x0 + t
+    const int y = y0 - 1 + r;
+    if (y >= 0 && y < a.ny) put(r, t + 1, (int64_t)z * nxy + (int64_t)y * a.nx + x0 + t);
+  }
+  if (t < 2 * (FRY + 2)) {  // x halo columns x0-1 / x0+256
+    const int r = t >> 1, y = y0 - 1 + r, x = (t & 1) ? x0 + 256 : x0 - 1;
+    if (y >= 0 && y < a.ny && x >= 0 && x < a.nx) put(r, (t & 1) ? 257 : 0, (int64_t)z * nxy + (int64_t)y * a.nx + x);
+  }
+  __syncthreads();
+  const int x = x0 + t;
+  double finf = 0.0;
+  for (int ry = 0; ry < FRY; ++ry) {
+    const int y = y0 + ry, r = ry + 1, c = t + 1;
+    const int64_t i = (int64_t)z * nxy + (int64_t)y * a.nx + x;  // = local row l (full set)
+    Props<1> Pi;
+    Pi.A[0] = sA[r][c]; Pi.dA[0][0] = sdA[r][c]; Pi.L[0] = sA[r][c] * imu; Pi.dL[0][0] = sdA[r][c] * imu;
+    const double pi = su[r][c];
+    double R[1], D[1][1], Mo[1] = {__ldg(&a.mold[i])};
+    rsim::phys::accum_row<1>(a.fl, __ldg(&a.pv[i]), pi, Pi, Mo, a.inv_dt, R, D);
+    double O[6];
+    bool has[6];
+    auto conn_s = [&](int s, double T, double pj, double Aj, double dAj) {  // in-plane neighbour from smem
+      double Oo[1][1];
+      const double dp = pi - pj;
+      if (!(dp < 0.0)) {
+        rsim::phys::flux_conn<1>(T, dp, true, Pi, R, D, Oo);
+      } else {
+        Props<1> Pj;
+        Pj.A[0] = Aj; Pj.dA[0][0] = dAj; Pj.L[0] = Aj * imu; Pj.dL[0][0] = dAj * imu;
+        rsim::phys::flux_conn<1>(T, dp, false, Pj, R, D, Oo);
+      }
+      O[s] = Oo[0][0];
+      has[s] = true;
+    };
+    auto conn_g = [&](int s, double T, int64_t j) {  // ±z neighbour: evaluated here, as in the row kernel
+      double Oo[1][1];
+      double uj[1] = {__ldg(&a.u[j])};
+      const double dp = pi - uj[0];
+      if (!(dp < 0.0)) {
+        rsim::phys::flux_conn<1>(T, dp, true, Pi, R, D, Oo);
+      } else {
+        Props<1> Pj;
+        rsim::phys::props(a.fl, uj, (uint8_t)0, Pj);
+        rsim::phys::flux_conn<1>(T, dp, false, Pj, R, D, Oo);
+      }
+      O[s] = Oo[0][0];
+      has[s] = true;
+    };
+#pragma unroll
+    for (int s = 0; s < 6; ++s) has[s] = false;
+    int s = 0;  // slots -z, -y, -x, +x, +y, +z (2D: no z slots)
+    if (a.d3) { if (z > 0) conn_g(s, __ldg(&a.tz[i - nxy]), i - nxy); ++s; }
+    if (y > 0) conn_s(s, __ldg(&a.ty[i - a.nx]), su[r - 1][c], sA[r - 1][c], sdA[r - 1][c]);
+    ++s;
+    if (x > 0) conn_s(s, __ldg(&a.tx[i - 1]), su[r][c - 1], sA[r][c - 1], sdA[r][c - 1]);
+    ++s;
+    if (x < a.nx - 1) conn_s(s, __ldg(&a.tx[i]), su[r][c + 1], sA[r][c + 1], sdA[r][c + 1]);
+    ++s;
+    if (y < a.ny - 1) conn_s(s, __ldg(&a.ty[i]), su[r + 1][c], sA[r + 1][c], sdA[r + 1][c]);
+    ++s;
+    if (a.d3) { if (z < a.nz - 1) conn_g(s, __ldg(&a.tz[i]), i + nxy); ++s; }
+    rsim::phys::well_row<1>(__ldg(&a.wi[i]), pi, a.bhp, Pi, R, D);
+    double Di[1][1];
+    if (!rsim::blk::inv(D, Di)) {
+      atomicMin(&a.dsc->bad_cell, (int32_t)i);
+      a.dsc->status = RSIM_ENUM;
+      Di[0][0] = 0.0;
+    }
+    double yv[1];
+    rsim::blk::gemv<1>(Di, R, yv);
+    if (a.keep_F) __stcs(&a.F_raw[i], R[0]);
+    __stcs(&a.rhs[i], -yv[0]);
+    finf = fmax(finf, fabs(R[0]));
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+      if (q < a.nslot && has[q]) {
+        double Oq[1][1] = {{O[q]}}, S[1][1];
+        rsim::blk::gemm<1>(Di, Oq, S);
+        __stcs(&a.ell_val[(int64_t)q * a.cap + i], S[0][0]);
+      }
+    const double ws = warp_tree(rsim::blk::rowdot<1>(R, R));
+    if ((t & 31) == 0) wsf[ry][t >> 5] = ws;
+  }
+  const double wm = warp_max(finf);
+  if ((t & 31) == 0 && wm > 0.0) atomic_max_bits(&a.dsc->finf, wm);
+  __syncthreads();
+  if (t < FRY) {  // canonical chunk partial of each tile row (256 consecutive rows)
+    const int64_t row0 = (int64_t)z * nxy + (int64_t)(y0 + t) * a.nx + x0;
+    a.part_f2[row0 >> 8] = tree8(wsf[t]);
+  }
+}
+
 // Old-time accumulation M^n = pv φ(p) A(u) for every cell (set_state / Δt change).
 template <int B>
 __global__ void k_mold(rsim::phys::Fluid fl, int64_t n, const double* __restrict__ u, const uint8_t* __restrict__ st,
@@ -443,6 +564,15 @@ int launch_materialize_cols(rsim_gpu_ctx* c) {
   return RSIM_OK;
 }
 
+static bool tile_full1_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("RSIM_NO_TILE_K1");
+    v = (e && *e == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int launch_assemble(rsim_gpu_ctx* c) {
   if (c->nA <= 0) return RSIM_OK;
   AsmArgs a;
@@ -479,6 +609,12 @@ int launch_assemble(rsim_gpu_ctx* c) {
     const int64_t nblocks = (c->nA + 255) / 256;
     const bool full = c->nA == c->n;
     c->cols_implicit = full;
+    if (full && c->b == 1 && !c->has_nnc && c->nx % 256 == 0 && c->ny % FRY == 0 && tile_full1_enabled()) {
+      k_assemble_full1<<<dim3(c->nx / 256, c->ny / FRY, c->nz), 256, 0, c->stream>>>(a);
+      c->launches++;
+      RSIM_CUDA(cudaGetLastError());
+      return RSIM_OK;
+    }
     switch (c->b * 2 + (full ? 1 : 0)) {
       case 2: k_assemble_row<1, false><<<nblocks, 256, 0, c->stream>>>(a); break;
       case 3: k_assemble_row<1, true><<<nblocks, 256, 0, c->stream>>>(a); break;
