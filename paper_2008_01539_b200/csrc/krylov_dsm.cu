@@ -43,6 +43,9 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int r) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(o) : "r"(a), "r"(r));
   return o;
 }
+#ifndef RSIM_DSM_SG512
+#define RSIM_DSM_SG512 1
+#endif
 #ifndef RSIM_DSM_PUSH
 #define RSIM_DSM_PUSH 1
 #endif
@@ -375,7 +378,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
     // slots in groups of SG (all in flight within a group); the 512/1024-thread
     // variants (128/64 registers) use SG = 2 so the gathered rows do not spill.
     // The accumulation order (slots ascending) is unchanged.
-    constexpr int SG = MAXT <= 256 ? NS : 2;
+    constexpr int SG = MAXT <= 256 ? NS : RSIM_DSM_SG512;
     double acc[B];
 #pragma unroll
     for (int e = 0; e < B; ++e) acc[e] = xown[e];
