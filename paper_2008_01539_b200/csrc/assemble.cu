@@ -416,84 +416,100 @@ __global__ void __launch_bounds__(256) k_assemble_row(const AsmArgs a) {
 // canonical order per row => the same bits.  Each tile row is one canonical
 // 256-row chunk, so the (F,F) chunk partials come out as in the row kernel.
 constexpr int FRY = 4;
+template <bool D3>
 __global__ void __launch_bounds__(256) k_assemble_full1(const AsmArgs a) {
-  // p, ρ, dρ/dp per tile/halo cell; λρ = ρ·(1/μ) and its derivative are re-formed
-  // with the same multiplication props<1> uses (same bits)
-  __shared__ double su[FRY + 2][258], sA[FRY + 2][258], sdA[FRY + 2][258];
+  // p and ρ per tile/halo cell; dρ/dp = c·ρ and λρ = ρ·(1/μ) are re-formed
+  // with the same multiplications props<1> uses (same bits).  Slots are
+  // compile-time (no dynamically indexed arrays: nothing goes to local memory).
+  __shared__ double su[FRY + 2][258], sA[FRY + 2][258];
   __shared__ double wsf[FRY][8];
   using rsim::phys::Props;
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31;
   const int x0 = blockIdx.x * 256, y0 = blockIdx.y * FRY, z = blockIdx.z;
   const int64_t nxy = (int64_t)a.nx * a.ny;
-  auto put = [&](int r, int c, int64_t i) {
-    double ui[1] = {__ldg(&a.u[i])};
+  const double cf = a.fl.c_f[1], imu = a.fl.inv_mu[1];
+  auto rho_of = [&](double p) {
+    double ui[1] = {p};
     Props<1> P;
     rsim::phys::props(a.fl, ui, (uint8_t)0, P);
-    su[r][c] = ui[0];
-    sA[r][c] = P.A[0]; sdA[r][c] = P.dA[0][0];
+    return P.A[0];
   };
-  const double imu = a.fl.inv_mu[1];
-  for (int r = 0; r < FRY + 2; ++r) {  // tile rows + halo rows, thread t = column x0 + t
-    const int y = y0 - 1 + r;
-    if (y >= 0 && y < a.ny) put(r, t + 1, (int64_t)z * nxy + (int64_t)y * a.nx + x0 + t);
-  }
-  if (t < 2 * (FRY + 2)) {  // x halo columns x0-1 / x0+256
-    const int r = t >> 1, y = y0 - 1 + r, x = (t & 1) ? x0 + 256 : x0 - 1;
-    if (y >= 0 && y < a.ny && x >= 0 && x < a.nx) put(r, (t & 1) ? 257 : 0, (int64_t)z * nxy + (int64_t)y * a.nx + x);
+  {
+    double pr[FRY + 2];
+#pragma unroll
+    for (int r = 0; r < FRY + 2; ++r) {  // tile rows + halo rows, thread t = column x0 + t
+      const int y = y0 - 1 + r;
+      pr[r] = (y >= 0 && y < a.ny) ? __ldg(&a.u[(int64_t)z * nxy + (int64_t)y * a.nx + x0 + t]) : 0.0;
+    }
+    double ph = 0.0;
+    int hr = -1, hc = 0;
+    if (t < 2 * (FRY + 2)) {  // x halo columns x0-1 / x0+256
+      const int r = t >> 1, y = y0 - 1 + r, x = (t & 1) ? x0 + 256 : x0 - 1;
+      if (y >= 0 && y < a.ny && x >= 0 && x < a.nx) {
+        hr = r; hc = (t & 1) ? 257 : 0;
+        ph = __ldg(&a.u[(int64_t)z * nxy + (int64_t)y * a.nx + x]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < FRY + 2; ++r) {
+      const int y = y0 - 1 + r;
+      if (y >= 0 && y < a.ny) { su[r][t + 1] = pr[r]; sA[r][t + 1] = rho_of(pr[r]); }
+    }
+    if (hr >= 0) { su[hr][hc] = ph; sA[hr][hc] = rho_of(ph); }
   }
   __syncthreads();
-  const int x = x0 + t;
+  const int x = x0 + t, c = t + 1;
   double finf = 0.0;
+  double ty_prev = (y0 > 0) ? __ldg(&a.ty[(int64_t)z * nxy + (int64_t)(y0 - 1) * a.nx + x]) : 0.0;
+#pragma unroll 1
   for (int ry = 0; ry < FRY; ++ry) {
-    const int y = y0 + ry, r = ry + 1, c = t + 1;
+    const int y = y0 + ry, r = ry + 1;
     const int64_t i = (int64_t)z * nxy + (int64_t)y * a.nx + x;  // = local row l (full set)
+    const bool h0 = D3 && z > 0, h5 = D3 && z < a.nz - 1;
+    const double txi = __ldg(&a.tx[i]), tyi = __ldg(&a.ty[i]);
+    const double tzi = h5 ? __ldg(&a.tz[i]) : 0.0, tzm = h0 ? __ldg(&a.tz[i - nxy]) : 0.0;
+    const double pzm = h0 ? __ldg(&a.u[i - nxy]) : 0.0, pzp = h5 ? __ldg(&a.u[i + nxy]) : 0.0;
+    double txl = __shfl_up_sync(0xffffffffu, txi, 1);
+    if (lane == 0) txl = x > 0 ? __ldg(&a.tx[i - 1]) : 0.0;
+    const double pi = su[r][c], Ai = sA[r][c];
     Props<1> Pi;
-    Pi.A[0] = sA[r][c]; Pi.dA[0][0] = sdA[r][c]; Pi.L[0] = sA[r][c] * imu; Pi.dL[0][0] = sdA[r][c] * imu;
-    const double pi = su[r][c];
+    Pi.A[0] = Ai; Pi.dA[0][0] = cf * Ai; Pi.L[0] = Ai * imu; Pi.dL[0][0] = (cf * Ai) * imu;
     double R[1], D[1][1], Mo[1] = {__ldg(&a.mold[i])};
     rsim::phys::accum_row<1>(a.fl, __ldg(&a.pv[i]), pi, Pi, Mo, a.inv_dt, R, D);
-    double O[6];
-    bool has[6];
-    auto conn_s = [&](int s, double T, double pj, double Aj, double dAj) {  // in-plane neighbour from smem
+    auto cn = [&](double T, double pj, double Aj) -> double {  // neighbour with known ρ
       double Oo[1][1];
       const double dp = pi - pj;
       if (!(dp < 0.0)) {
         rsim::phys::flux_conn<1>(T, dp, true, Pi, R, D, Oo);
       } else {
         Props<1> Pj;
-        Pj.A[0] = Aj; Pj.dA[0][0] = dAj; Pj.L[0] = Aj * imu; Pj.dL[0][0] = dAj * imu;
+        Pj.A[0] = Aj; Pj.dA[0][0] = cf * Aj; Pj.L[0] = Aj * imu; Pj.dL[0][0] = (cf * Aj) * imu;
         rsim::phys::flux_conn<1>(T, dp, false, Pj, R, D, Oo);
       }
-      O[s] = Oo[0][0];
-      has[s] = true;
+      return Oo[0][0];
     };
-    auto conn_g = [&](int s, double T, int64_t j) {  // ±z neighbour: evaluated here, as in the row kernel
+    auto cz = [&](double T, double pj) -> double {  // ±z neighbour: ρ evaluated only when it is upwind
       double Oo[1][1];
-      double uj[1] = {__ldg(&a.u[j])};
-      const double dp = pi - uj[0];
+      const double dp = pi - pj;
       if (!(dp < 0.0)) {
         rsim::phys::flux_conn<1>(T, dp, true, Pi, R, D, Oo);
       } else {
+        double uj[1] = {pj};
         Props<1> Pj;
         rsim::phys::props(a.fl, uj, (uint8_t)0, Pj);
         rsim::phys::flux_conn<1>(T, dp, false, Pj, R, D, Oo);
       }
-      O[s] = Oo[0][0];
-      has[s] = true;
+      return Oo[0][0];
     };
-#pragma unroll
-    for (int s = 0; s < 6; ++s) has[s] = false;
-    int s = 0;  // slots -z, -y, -x, +x, +y, +z (2D: no z slots)
-    if (a.d3) { if (z > 0) conn_g(s, __ldg(&a.tz[i - nxy]), i - nxy); ++s; }
-    if (y > 0) conn_s(s, __ldg(&a.ty[i - a.nx]), su[r - 1][c], sA[r - 1][c], sdA[r - 1][c]);
-    ++s;
-    if (x > 0) conn_s(s, __ldg(&a.tx[i - 1]), su[r][c - 1], sA[r][c - 1], sdA[r][c - 1]);
-    ++s;
-    if (x < a.nx - 1) conn_s(s, __ldg(&a.tx[i]), su[r][c + 1], sA[r][c + 1], sdA[r][c + 1]);
-    ++s;
-    if (y < a.ny - 1) conn_s(s, __ldg(&a.ty[i]), su[r + 1][c], sA[r + 1][c], sdA[r + 1][c]);
-    ++s;
-    if (a.d3) { if (z < a.nz - 1) conn_g(s, __ldg(&a.tz[i]), i + nxy); ++s; }
+    // canonical slot order -z, -y, -x, +x, +y, +z (2D: no z slots)
+    double O0 = 0.0, O1 = 0.0, O2 = 0.0, O3 = 0.0, O4 = 0.0, O5 = 0.0;
+    const bool h1 = y > 0, h2 = x > 0, h3 = x < a.nx - 1, h4 = y < a.ny - 1;
+    if (h0) O0 = cz(tzm, pzm);
+    if (h1) O1 = cn(ty_prev, su[r - 1][c], sA[r - 1][c]);
+    if (h2) O2 = cn(txl, su[r][c - 1], sA[r][c - 1]);
+    if (h3) O3 = cn(txi, su[r][c + 1], sA[r][c + 1]);
+    if (h4) O4 = cn(tyi, su[r + 1][c], sA[r + 1][c]);
+    if (h5) O5 = cz(tzi, pzp);
     rsim::phys::well_row<1>(__ldg(&a.wi[i]), pi, a.bhp, Pi, R, D);
     double Di[1][1];
     if (!rsim::blk::inv(D, Di)) {
@@ -506,18 +522,23 @@ __global__ void __launch_bounds__(256) k_assemble_full1(const AsmArgs a) {
     if (a.keep_F) __stcs(&a.F_raw[i], R[0]);
     __stcs(&a.rhs[i], -yv[0]);
     finf = fmax(finf, fabs(R[0]));
-#pragma unroll
-    for (int q = 0; q < 6; ++q)
-      if (q < a.nslot && has[q]) {
-        double Oq[1][1] = {{O[q]}}, S[1][1];
-        rsim::blk::gemm<1>(Di, Oq, S);
-        __stcs(&a.ell_val[(int64_t)q * a.cap + i], S[0][0]);
-      }
+    auto st = [&](int q, bool h, double O) {
+      if (!h) return;
+      double Oq[1][1] = {{O}}, S[1][1];
+      rsim::blk::gemm<1>(Di, Oq, S);
+      __stcs(&a.ell_val[(int64_t)q * a.cap + i], S[0][0]);
+    };
+    if (D3) {
+      st(0, h0, O0); st(1, h1, O1); st(2, h2, O2); st(3, h3, O3); st(4, h4, O4); st(5, h5, O5);
+    } else {
+      st(0, h1, O1); st(1, h2, O2); st(2, h3, O3); st(3, h4, O4);
+    }
     const double ws = warp_tree(rsim::blk::rowdot<1>(R, R));
-    if ((t & 31) == 0) wsf[ry][t >> 5] = ws;
+    if (lane == 0) wsf[ry][t >> 5] = ws;
+    ty_prev = tyi;
   }
   const double wm = warp_max(finf);
-  if ((t & 31) == 0 && wm > 0.0) atomic_max_bits(&a.dsc->finf, wm);
+  if (lane == 0 && wm > 0.0) atomic_max_bits(&a.dsc->finf, wm);
   __syncthreads();
   if (t < FRY) {  // canonical chunk partial of each tile row (256 consecutive rows)
     const int64_t row0 = (int64_t)z * nxy + (int64_t)(y0 + t) * a.nx + x0;
@@ -610,7 +631,8 @@ int launch_assemble(rsim_gpu_ctx* c) {
     const bool full = c->nA == c->n;
     c->cols_implicit = full;
     if (full && c->b == 1 && !c->has_nnc && c->nx % 256 == 0 && c->ny % FRY == 0 && tile_full1_enabled()) {
-      k_assemble_full1<<<dim3(c->nx / 256, c->ny / FRY, c->nz), 256, 0, c->stream>>>(a);
+      if (c->d3) k_assemble_full1<true><<<dim3(c->nx / 256, c->ny / FRY, c->nz), 256, 0, c->stream>>>(a);
+      else k_assemble_full1<false><<<dim3(c->nx / 256, c->ny / FRY, c->nz), 256, 0, c->stream>>>(a);
       c->launches++;
       RSIM_CUDA(cudaGetLastError());
       return RSIM_OK;

@@ -207,13 +207,17 @@ __device__ __forceinline__ void implicit_cols(int32_t nx, int32_t ny, int32_t nz
   const uint32_t rem = (uint32_t)i - iz * nxy;
   const uint32_t iy = rem / (uint32_t)nx, ix = rem - iy * (uint32_t)nx;
   const int32_t ii = (int32_t)i;
-  int k = 0;
-  if (d3) cl[k++] = iz > 0 ? ii - (int32_t)nxy : -1;
-  cl[k++] = iy > 0 ? ii - nx : -1;
-  cl[k++] = ix > 0 ? ii - 1 : -1;
-  cl[k++] = ix + 1 < (uint32_t)nx ? ii + 1 : -1;
-  cl[k++] = iy + 1 < (uint32_t)ny ? ii + nx : -1;
-  if (d3) cl[k++] = iz + 1 < (uint32_t)nz ? ii + (int32_t)nxy : -1;
+  // constant indices only: a runtime slot counter would force cl[] (and the
+  // caller's gathers) into local memory
+  const int32_t ym = iy > 0 ? ii - nx : -1, xm = ix > 0 ? ii - 1 : -1;
+  const int32_t xp = ix + 1 < (uint32_t)nx ? ii + 1 : -1, yp = iy + 1 < (uint32_t)ny ? ii + nx : -1;
+  if (d3) {
+    cl[0] = iz > 0 ? ii - (int32_t)nxy : -1;
+    cl[1] = ym; cl[2] = xm; cl[3] = xp; cl[4] = yp;
+    cl[5] = iz + 1 < (uint32_t)nz ? ii + (int32_t)nxy : -1;
+  } else {
+    cl[0] = ym; cl[1] = xm; cl[2] = xp; cl[3] = yp;
+  }
 }
 
 __device__ __forceinline__ double warp_tree(double v) {

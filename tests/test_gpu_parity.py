@@ -202,3 +202,41 @@ print(json.dumps({{"a": sim.active().tolist(), "b": sim.boundary().tolist(), "ex
         assert r.returncode == 0, r.stderr
         outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
     assert outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("dims", [(1024, 304, 1),   # 2D full set: 256x4 tile kernel
+                                  (256, 64, 19),    # 3D full set: z-marching tile kernel, partial last z-chunk
+                                  (512, 32, 24)])
+def test_full_set_tile_assembly_bit_exact(dims):
+    """Full-set b=1 assembly above the row-kernel threshold runs the tile kernels
+    (k_assemble_full1 in 2D, k_assemble_full1z in 3D): F, rhs, the scaled
+    blocks and the canonical (F,F) partials must equal the oracle's."""
+    nx, ny, nz = dims
+    case = pkg.Case(5, nx=nx, ny=ny, nz=nz)
+    assert case.n >= 148 * 2048
+    s = perturbed_state(case, 5)
+    dt = 86400.0
+    orc = Oracle(case)
+    orc.set_state(s, dt)
+    Fo, ro, rpo, co, vo = orc.assemble(np.arange(case.n, dtype=np.int32))
+    sim = pkg.GpuSimulator(case)
+    assert sim.L.rsim_gpu_set_debug(sim._ctx, 1) == 0  # keep the raw residual for the download
+    sim.set_state(s, dt)
+    sim.set_active(None)
+    sim.assemble()
+    Fg, rg, rpg, cg, vg = sim.system(case.n)
+    assert np.array_equal(rpg, rpo) and np.array_equal(cg, co)
+    assert np.array_equal(Fg, Fo), np.abs(Fg - Fo).max()
+    assert np.array_equal(rg, ro)
+    assert np.array_equal(vg, vo), np.abs(vg - vo).max()
+    # ‖F‖₂ from the kernel's canonical chunk partials (no raw-F re-read) must be the oracle's bits
+    sim.L.rsim_gpu_set_debug(sim._ctx, 0)
+    sim.assemble()
+    opts = case.solver_opts(precond=pkg.PREC_BJACOBI, fixed_lin_iters=2, lin_maxit=2)
+    rc_o, xo, it_o, rr_o = orc.linear_solve(case.n, opts)
+    sim.linear_solve(opts)
+    g = sim.stats()
+    assert g.lin_iters == it_o
+    assert np.array_equal(sim.solution(case.n), xo)
+    assert g.lin_relres == rr_o
+    sim.close()
