@@ -205,6 +205,7 @@ int rsim_gpu_create(rsim_gpu_ctx** out, const rsim_graph_desc* g, const rsim_flu
   TRY(dalloc(&c->act_buf, n)); TRY(dalloc(&c->g2l, n)); TRY(dalloc(&c->label, n));
   TRY(dalloc(&c->list_buf, n));
   TRY(dalloc(&c->dp, n)); TRY(dalloc(&c->last_dp, n));
+  if (g->nx % 32 == 0) { TRY(dalloc(&c->bits[0], n / 32 + 1)); TRY(dalloc(&c->bits[1], n / 32 + 1)); }
   {  // compaction tiles: K7 uses one tile per (x-row, 1024-cell segment), K8 one per 2048 cells
     const int64_t wrow = (g->nx + 3) / 4, bs = wrow >= 256 ? 256 : ((wrow + 31) / 32) * 32;
     const int64_t k7 = (int64_t)g->ny * g->nz * ((wrow + bs - 1) / bs);
@@ -271,7 +272,7 @@ int rsim_gpu_destroy(rsim_gpu_ctx* c) {
                   c->list_buf, c->dp, c->last_dp, c->tile_cnt, c->tile_off, c->ell_col, c->ell_val, c->nnc_lcol,
                   c->nnc_val, c->F_raw, c->rhs, c->part_f2, c->x, c->r, c->r0, c->p, c->v, c->s, c->t, c->p2, c->v2, c->ph, c->sh, c->part,
                   c->dsc, c->dd.sub_cells, c->dd.halo_cells, c->u_ckpt, c->st_ckpt, c->l2_scratch, c->pin0, c->ktrace,
-                  c->gm_V, c->gm_part, c->dd.hist};
+                  c->gm_V, c->gm_part, c->dd.hist, c->bits[0], c->bits[1]};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   ilu_free(c);

@@ -782,10 +782,30 @@ __global__ void k_set_reset(int64_t n, const uint8_t* __restrict__ pin0, uint8_t
 // Support-set seed for an externally given δp (config 5):
 // flags = pinned set | D0 where |δp| >= ε  (reset + seed in one pass, 4 cells
 // per thread: one flag word, two double2 loads).
+// With `bits` (n % 32 == 0) the seed is also written as a bitmap (bit i%32 of
+// word i/32), the input of the bitmap dilation: 8 lanes' nibbles per word.
 __global__ void k_reset_seed(int64_t n, const uint8_t* __restrict__ pin0, const double* __restrict__ dp, double eps,
-                             uint8_t* __restrict__ flags) {
+                             uint8_t* __restrict__ flags, uint32_t* __restrict__ bits) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n4 = n / 4;
+  if (bits) {  // n % 32 == 0: whole 8-lane groups are in range together
+    uint32_t nib = 0;
+    if (t < n4) {
+      uint32_t w = reinterpret_cast<const uint32_t*>(pin0)[t];
+      const double2 a = __ldcs(reinterpret_cast<const double2*>(dp) + 2 * t);
+      const double2 b = __ldcs(reinterpret_cast<const double2*>(dp) + 2 * t + 1);
+      nib = (fabs(a.x) >= eps ? 1u : 0u) | (fabs(a.y) >= eps ? 2u : 0u) | (fabs(b.x) >= eps ? 4u : 0u) |
+            (fabs(b.y) >= eps ? 8u : 0u);
+      w |= ((nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21)) * (uint32_t)F_D0;
+      reinterpret_cast<uint32_t*>(flags)[t] = w;
+    }
+    uint32_t x = nib << (4 * (threadIdx.x & 7));
+    x |= __shfl_xor_sync(0xffffffffu, x, 1);
+    x |= __shfl_xor_sync(0xffffffffu, x, 2);
+    x |= __shfl_xor_sync(0xffffffffu, x, 4);
+    if ((threadIdx.x & 7) == 0 && t < n4) bits[t >> 3] = x;
+    return;
+  }
   if (t < n4) {
     uint32_t w = reinterpret_cast<const uint32_t*>(pin0)[t];
     const double2 a = reinterpret_cast<const double2*>(dp)[2 * t];
@@ -978,6 +998,109 @@ inline int64_t nblk(int64_t n, int th) { return (n + th - 1) / th; }
 
 }  // namespace
 
+// ---- bitmap dilation (large vec4 grids with nx % 32 == 0 and no NNC): the
+// m hop rounds run on a 1-bit-per-cell map (n/8 bytes, L2-resident) with 32
+// cells per thread instead of on the flag bytes; the count pass merges the
+// final map into the flag byte's D bit, so the count / scan / scatter passes
+// and their results are those of the byte path.
+struct GeoB {
+  int64_t nbw;      // bit words
+  int32_t brow;     // bit words per x-row
+  int64_t bplane;   // bit words per plane
+  int32_t ny, nz;
+  bool d3;
+};
+__host__ GeoB geob(const rsim_gpu_ctx* c) {
+  GeoB g;
+  g.nbw = c->n / 32;
+  g.brow = c->nx / 32;
+  g.bplane = (int64_t)g.brow * c->ny;
+  g.ny = c->ny; g.nz = c->nz;
+  g.d3 = c->d3;
+  return g;
+}
+
+// bitmap of flag bit `bit` (32 cells per thread: two 16-byte loads)
+__global__ void k_pack_bits(int64_t nbw, const uint8_t* __restrict__ flags, uint8_t bit, uint32_t* __restrict__ bits) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nbw) return;
+  const uint4* f = reinterpret_cast<const uint4*>(flags) + 2 * t;
+  const uint4 a = f[0], b = f[1];
+  const uint32_t ws[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  const uint32_t sh = bitpos(bit);
+  uint32_t x = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t l = (ws[k] >> sh) & 0x01010101u;  // byte lanes -> 4 bits
+    x |= ((l & 1u) | ((l >> 7) & 2u) | ((l >> 14) & 4u) | ((l >> 21) & 8u)) << (4 * k);
+  }
+  bits[t] = x;
+}
+
+// one hop: out(i) = in(i) | OR over the 6 Cartesian neighbours
+__global__ void k_dilate_bits(GeoB g, const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                              const DevScalars* __restrict__ dsc, SetMode M) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= g.nbw) return;
+  const bool ex = decide_expand(M, dsc);
+  if ((M.mode == MODE_DEVICE || M.mode == MODE_DD) && !ex) return;  // no dilation this update
+  const int64_t row = t / g.brow;
+  const int32_t xw = (int32_t)(t - row * g.brow);
+  const int32_t iz = (int32_t)(row / g.ny), iy = (int32_t)(row - (int64_t)iz * g.ny);
+  const uint32_t v = in[t];
+  uint32_t o = v | (v << 1) | (v >> 1);
+  if (xw > 0) o |= in[t - 1] >> 31;
+  if (xw < g.brow - 1) o |= in[t + 1] << 31;
+  if (iy > 0) o |= in[t - g.brow];
+  if (iy < g.ny - 1) o |= in[t + g.brow];
+  if (g.d3) {
+    if (iz > 0) o |= in[t - g.bplane];
+    if (iz < g.nz - 1) o |= in[t + g.bplane];
+  }
+  out[t] = o;
+}
+
+// count pass of the bitmap path (row groups as k_dilate_rg<true>): the final
+// map goes into the D bit of the flag words, then A_new is counted per tile
+__global__ void __launch_bounds__(256) k_count_merge_rg(Geo4 g, uint8_t* __restrict__ flags,
+                                                         const uint32_t* __restrict__ bits,
+                                                         const DevScalars* __restrict__ dsc, SetMode M,
+                                                         int32_t* __restrict__ tile_cnt) {
+  __shared__ int sh[8][RG];
+  const bool ex = decide_expand(M, dsc);
+  const bool dil = (M.mode == MODE_DEVICE || M.mode == MODE_DD) ? ex : true;
+  const PosRG p = pos_rg(g);
+  uint32_t* fw = reinterpret_cast<uint32_t*>(flags);
+  int cnt[RG];
+#pragma unroll
+  for (int k = 0; k < RG; ++k) {
+    cnt[k] = 0;
+    if (!(p.ok && k < p.nrow)) continue;
+    const int64_t t = p.t0 + (int64_t)k * g.wrow;
+    uint32_t w = fw[t];
+    if (dil) {
+      const uint32_t nib = (__ldg(&bits[t >> 3]) >> (4 * (t & 7))) & 0xFu;
+      const uint32_t l = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+      w = (w & ~(0x01010101u * M.dbit)) | (l * M.dbit);
+      fw[t] = w;
+    }
+    cnt[k] = __popc(a_new4(w, M.mode, ex, M.dbit));
+  }
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < RG; ++k) {
+    const int v = __reduce_add_sync(0xffffffffu, cnt[k]);
+    if (lane == 0) sh[wi][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < p.nrow) {
+    int s = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) s += sh[q][threadIdx.x];
+    const int32_t row = p.iz * g.ny + p.iy0 + threadIdx.x;
+    tile_cnt[row * g.nseg + blockIdx.y] = s;
+  }
+}
+
 // ============================================================== launchers
 int launch_update(rsim_gpu_ctx* c, double eps) {
   if (c->nA <= 0) return RSIM_OK;
@@ -1005,6 +1128,19 @@ int launch_threshold(rsim_gpu_ctx* c, double eps) {
 
 // Full set update: [m-1 dilation rounds] + [round m fused with the tile count]
 // + scan + scatter.  4 launches for m = 2, no host round trip.
+// bitmap dilation: large grids (row-group path), whole bit words per x-row, no NNC
+static bool bits_path_possible(const rsim_gpu_ctx* c) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("RSIM_NO_BITS_K7");
+    v = (e && *e == '1') ? 0 : 1;
+  }
+  if (!v || c->has_nnc || c->nx % 32 != 0 || !c->bits[0]) return false;
+  const Geo4 g = geo4(c);
+  const dim3 grg = rg_grid(g);
+  return g.vec4 && (int64_t)grg.x * grg.y >= 16 * 148;
+}
+
 static bool coop_set_update_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -1080,6 +1216,22 @@ int launch_set_update(rsim_gpu_ctx* c, int mode, int round, double eps, int m, i
     c->act = c->act_buf;
     return RSIM_OK;
   }
+  const bool seeded = c->seed_bits_ready;
+  c->seed_bits_ready = false;
+  if (use_rg && rounds > 0 && bits_path_possible(c)) {
+    const GeoB gb = geob(c);
+    const int64_t nb = nblk(gb.nbw, 256);
+    if (!seeded) {
+      k_pack_bits<<<nb, 256, 0, c->stream>>>(gb.nbw, c->flags, F_D0, c->bits[0]);
+      c->launches++;
+    }
+    for (int r = 0; r < rounds; ++r) {
+      k_dilate_bits<<<nb, 256, 0, c->stream>>>(gb, c->bits[r & 1], c->bits[(r + 1) & 1], c->dsc, M);
+      c->launches++;
+    }
+    k_count_merge_rg<<<grg, g.bs, 0, c->stream>>>(g, c->flags, c->bits[rounds & 1], c->dsc, M, c->tile_cnt);
+    c->launches++;
+  } else {
   for (int r = 0; r + 1 < rounds; ++r) {
     uint8_t bin = (r % 2 == 0) ? F_D0 : F_D1, bout = (r % 2 == 0) ? F_D1 : F_D0;
     if (use_rg) k_dilate_rg<false><<<grg, g.bs, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, 1, c->tile_cnt);
@@ -1096,6 +1248,7 @@ int launch_set_update(rsim_gpu_ctx* c, int mode, int round, double eps, int m, i
       k_dilate<true><<<grid, g.bs, 0, c->stream>>>(g, c->flags, bin, bout, c->dsc, M, rounds > 0 ? 1 : 0,
                                                    c->tile_cnt);
     c->launches++;
+  }
   }
   { const int r = launch_scan_tiles(c, ntiles, M); if (r != RSIM_OK) return r; }
   if (use_rg)
@@ -1260,7 +1413,9 @@ int launch_dd_skip(rsim_gpu_ctx* c, int32_t k) {
 // flags := pinned | D0 where |δp| >= ε  (set reset + support seed, one pass)
 int launch_reset_seed(rsim_gpu_ctx* c, double eps) {
   TRY_K7(ensure_pin0(c));
-  k_reset_seed<<<nblk(c->n / 4 + 1, 256), 256, 0, c->stream>>>(c->n, c->pin0, c->dp, eps, c->flags);
+  uint32_t* bits = bits_path_possible(c) ? c->bits[0] : nullptr;
+  k_reset_seed<<<nblk(c->n / 4 + 1, 256), 256, 0, c->stream>>>(c->n, c->pin0, c->dp, eps, c->flags, bits);
+  c->seed_bits_ready = bits != nullptr;  // consumed by the next set update
   c->launches++;
   RSIM_CUDA(cudaGetLastError());
   return RSIM_OK;

@@ -240,3 +240,43 @@ def test_full_set_tile_assembly_bit_exact(dims):
     assert np.array_equal(sim.solution(case.n), xo)
     assert g.lin_relres == rr_o
     sim.close()
+
+
+def _dilate_np(mask, m):
+    """m hops of 6-neighbour (4 in 2D) dilation on a (nz, ny, nx) boolean grid."""
+    out = mask.copy()
+    for _ in range(m):
+        cur = out.copy()
+        for ax in range(3):
+            if cur.shape[ax] > 1:
+                sl_a = [slice(None)] * 3
+                sl_b = [slice(None)] * 3
+                sl_a[ax], sl_b[ax] = slice(1, None), slice(None, -1)
+                out[tuple(sl_a)] |= cur[tuple(sl_b)]
+                out[tuple(sl_b)] |= cur[tuple(sl_a)]
+    return out
+
+
+@pytest.mark.parametrize("frac,m", [(0.05, 2), (0.2, 1), (0.5, 3), (1.0, 2)])
+def test_support_active_c5_field(frac, m):
+    """Config-5 set update (fused reset + seed, bitmap dilation on large grids,
+    count / scan / scatter): V_A = m-hop dilation of {|δp| >= ε} and its
+    boundary layer, against a numpy restatement."""
+    import ctypes as C
+    case = pkg.Case(5, nx=256, ny=256, nz=40)
+    eps = 1e-3
+    dp, _, _ = case.c5_field(frac, m, eps)
+    sim = pkg.GpuSimulator(case)
+    sim.upload_dp(dp)
+    st = pkg.GpuStats()
+    assert sim.L.rsim_gpu_support_active(sim._ctx, eps, m, C.byref(st)) == 0
+    shape = (case.nz, case.ny, case.nx)
+    a = _dilate_np((np.abs(dp) >= eps).reshape(shape), m)
+    act = np.flatnonzero(a.ravel()).astype(np.int32)
+    ga = sim.active()
+    assert st.n_active == len(act)
+    assert np.array_equal(ga, act)
+    inner = ~_dilate_np(~a, 1)  # active cells whose every neighbour is active
+    bnd = np.flatnonzero((a & ~inner).ravel()).astype(np.int32)
+    assert np.array_equal(sim.boundary(), bnd)
+    sim.close()
