@@ -650,6 +650,9 @@ __global__ void __launch_bounds__(256) k_dilate_rg(Geo4 g, uint8_t* __restrict__
   }
 }
 
+// BT (block tiles, one segment per x-row): the offsets are per block (its RG
+// rows), the rows' offsets inside the block come from the block's own counts.
+template <bool BT>
 __global__ void __launch_bounds__(256) k_scatter_rg(Geo4 g, const uint8_t* __restrict__ fin,
                                                     uint8_t* __restrict__ fout, SetMode M, int32_t round,
                                                     DevScalars* dsc, const int32_t* __restrict__ tile_off,
@@ -712,13 +715,24 @@ __global__ void __launch_bounds__(256) k_scatter_rg(Geo4 g, const uint8_t* __res
   __syncthreads();
   unsigned long long pre = x - packed;
   for (int q = 0; q < wi; ++q) pre += wpre[q];
+  unsigned long long rowoff = 0;  // BT: exclusive prefix of the row totals inside the block
+  int32_t boff = 0;
+  if (BT) {
+    unsigned long long tot = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) tot += wpre[q];
+#pragma unroll
+    for (int k = 1; k < RG; ++k) rowoff += ((tot >> (16 * (k - 1))) & 0xFFFFu) << (16 * k);
+    rowoff += (rowoff << 16) + (rowoff << 32) + (rowoff << 48);  // running sums (fields < 2^16)
+    boff = tile_off[blockIdx.x];
+  }
   int nb = 0, nnew = 0;
 #pragma unroll
   for (int k = 0; k < RG; ++k) {
     if (!(p.ok && k < p.nrow)) continue;
     const int64_t t = p.t0 + (int64_t)k * g.wrow;
     const int32_t row = p.iz * g.ny + p.iy0 + k;
-    int32_t pos = tile_off[row * g.nseg + blockIdx.y] + (int32_t)((pre >> (16 * k)) & 0xFFFFu);
+    int32_t pos = (BT ? boff + (int32_t)((rowoff >> (16 * k)) & 0xFFFFu) : tile_off[row * g.nseg + blockIdx.y]) +
+                  (int32_t)((pre >> (16 * k)) & 0xFFFFu);
     const int64_t i0 = 4 * t;
     int32_t gl[4];
     uint32_t out = 0;
@@ -1065,7 +1079,7 @@ __global__ void k_dilate_bits(GeoB g, const uint32_t* __restrict__ in, uint32_t*
 __global__ void __launch_bounds__(256) k_count_merge_rg(Geo4 g, uint8_t* __restrict__ flags,
                                                          const uint32_t* __restrict__ bits,
                                                          const DevScalars* __restrict__ dsc, SetMode M,
-                                                         int32_t* __restrict__ tile_cnt) {
+                                                         int32_t* __restrict__ tile_cnt, bool bt) {
   __shared__ int sh[8][RG];
   const bool ex = decide_expand(M, dsc);
   const bool dil = (M.mode == MODE_DEVICE || M.mode == MODE_DD) ? ex : true;
@@ -1093,7 +1107,14 @@ __global__ void __launch_bounds__(256) k_count_merge_rg(Geo4 g, uint8_t* __restr
     if (lane == 0) sh[wi][k] = v;
   }
   __syncthreads();
-  if (threadIdx.x < p.nrow) {
+  if (bt) {  // one count per block (its RG rows)
+    if (threadIdx.x == 0) {
+      int s = 0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q)
+        for (int k = 0; k < RG; ++k) s += sh[q][k];
+      tile_cnt[blockIdx.x] = s;
+    }
+  } else if (threadIdx.x < p.nrow) {
     int s = 0;
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) s += sh[q][threadIdx.x];
     const int32_t row = p.iz * g.ny + p.iy0 + threadIdx.x;
@@ -1216,6 +1237,7 @@ int launch_set_update(rsim_gpu_ctx* c, int mode, int round, double eps, int m, i
     c->act = c->act_buf;
     return RSIM_OK;
   }
+  bool bt = false;
   const bool seeded = c->seed_bits_ready;
   c->seed_bits_ready = false;
   if (use_rg && rounds > 0 && bits_path_possible(c)) {
@@ -1229,7 +1251,8 @@ int launch_set_update(rsim_gpu_ctx* c, int mode, int round, double eps, int m, i
       k_dilate_bits<<<nb, 256, 0, c->stream>>>(gb, c->bits[r & 1], c->bits[(r + 1) & 1], c->dsc, M);
       c->launches++;
     }
-    k_count_merge_rg<<<grg, g.bs, 0, c->stream>>>(g, c->flags, c->bits[rounds & 1], c->dsc, M, c->tile_cnt);
+    bt = g.nseg == 1;  // block tiles: RG-fold fewer offsets to scan
+    k_count_merge_rg<<<grg, g.bs, 0, c->stream>>>(g, c->flags, c->bits[rounds & 1], c->dsc, M, c->tile_cnt, bt);
     c->launches++;
   } else {
   for (int r = 0; r + 1 < rounds; ++r) {
@@ -1250,9 +1273,12 @@ int launch_set_update(rsim_gpu_ctx* c, int mode, int round, double eps, int m, i
     c->launches++;
   }
   }
-  { const int r = launch_scan_tiles(c, ntiles, M); if (r != RSIM_OK) return r; }
-  if (use_rg)
-    k_scatter_rg<<<grg, g.bs, 0, c->stream>>>(g, c->flags, c->flags_alt, M, round, c->dsc, c->tile_off, c->act_buf,
+  { const int r = launch_scan_tiles(c, bt ? (int64_t)grg.x : ntiles, M); if (r != RSIM_OK) return r; }
+  if (use_rg && bt)
+    k_scatter_rg<true><<<grg, g.bs, 0, c->stream>>>(g, c->flags, c->flags_alt, M, round, c->dsc, c->tile_off,
+                                                    c->act_buf, c->g2l, c->label);
+  else if (use_rg)
+    k_scatter_rg<false><<<grg, g.bs, 0, c->stream>>>(g, c->flags, c->flags_alt, M, round, c->dsc, c->tile_off, c->act_buf,
                                               c->g2l, c->label);
   else
     k_scatter<<<grid, g.bs, 0, c->stream>>>(g, c->flags, c->flags_alt, M, round, c->dsc, c->tile_off, c->act_buf,
