@@ -1122,6 +1122,164 @@ __global__ void __launch_bounds__(256) k_count_merge_rg(Geo4 g, uint8_t* __restr
   }
 }
 
+// Keep pass of the bitmap path with block tiles (one x-row segment): A_new of
+// every cell from its flag byte with the final dilation bit merged in, as a
+// keep bitmap (1 bit per cell) + one count per block.  The flag bytes are not
+// rewritten: the scatter takes A_new of a cell and of its neighbours from the
+// keep bitmap (L1/L2-resident) and only the cell's own byte from the flags.
+__device__ __forceinline__ uint32_t nib_to_lanes(uint32_t nib) {
+  return (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+}
+__device__ __forceinline__ uint32_t lanes_to_nib(uint32_t l) {
+  return (l & 1u) | ((l >> 7) & 2u) | ((l >> 14) & 4u) | ((l >> 21) & 8u);
+}
+__global__ void __launch_bounds__(256) k_keep_rg(Geo4 g, const uint8_t* __restrict__ flags,
+                                                 const uint32_t* __restrict__ bits, uint32_t* __restrict__ keepbits,
+                                                 const DevScalars* __restrict__ dsc, SetMode M,
+                                                 int32_t* __restrict__ blk_cnt) {
+  // the block's cells (RG consecutive x-rows of one plane, as in the scatter)
+  // are the contiguous flag words [w0, w0 + nrow·wrow): 4 words (16 cells,
+  // one uint4) per thread, half a keep-bitmap word
+  __shared__ int sh[8];
+  const bool ex = decide_expand(M, dsc);
+  const bool dil = (M.mode == MODE_DEVICE || M.mode == MODE_DD) ? ex : true;
+  const int32_t gpp = (g.ny + RG - 1) / RG;
+  const int32_t iz = blockIdx.x / gpp, iy0 = (blockIdx.x - iz * gpp) * RG;
+  const int32_t nrow = g.ny - iy0 < RG ? g.ny - iy0 : RG;
+  const int64_t w0 = ((int64_t)iz * g.ny + iy0) * g.wrow;
+  const int64_t nq = (int64_t)nrow * g.wrow / 4;
+  const int lane = threadIdx.x & 31;
+  const uint4* f4 = reinterpret_cast<const uint4*>(flags) + w0 / 4;
+  int cnt = 0;
+  for (int64_t q0 = 0; q0 < nq; q0 += blockDim.x) {  // warp-uniform trip count
+    const int64_t q = q0 + threadIdx.x;
+    uint32_t nib16 = 0;
+    if (q < nq) {
+      const uint4 v = __ldcs(&f4[q]);
+      uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+      uint32_t dm = 0;
+      if (dil) dm = (__ldg(&bits[(w0 + 4 * q) >> 3]) >> (16 * (q & 1))) & 0xFFFFu;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        uint32_t w = ws[e];
+        if (dil) w = (w & ~(0x01010101u * M.dbit)) | (nib_to_lanes((dm >> (4 * e)) & 0xFu) * M.dbit);
+        nib16 |= lanes_to_nib(a_new4(w, M.mode, ex, M.dbit)) << (4 * e);
+      }
+      cnt += __popc(nib16);
+    }
+    const uint32_t other = __shfl_xor_sync(0xffffffffu, nib16, 1);
+    if (q < nq && (q & 1) == 0) keepbits[(w0 + 4 * q) >> 3] = nib16 | (other << 16);
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if (lane == 0) sh[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) s += sh[q];
+    blk_cnt[blockIdx.x] = s;
+  }
+}
+
+// Scatter of the bitmap path (block tiles): A_new lanes of a word and of its
+// neighbours from the keep bitmap, the cell's own byte for PIN / T.
+__global__ void __launch_bounds__(256) k_scatter_kb(Geo4 g, const uint8_t* __restrict__ fin,
+                                                    const uint32_t* __restrict__ keepbits,
+                                                    uint8_t* __restrict__ fout, SetMode M, int32_t round,
+                                                    DevScalars* dsc, const int32_t* __restrict__ blk_off,
+                                                    int32_t* __restrict__ act, int32_t* __restrict__ g2l,
+                                                    int32_t* __restrict__ label) {
+  __shared__ unsigned long long wpre[8];
+  __shared__ int sh8[8];
+  const PosRG p = pos_rg(g);
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const uint32_t* fw = reinterpret_cast<const uint32_t*>(fin);
+  const int32_t boff = blk_off[blockIdx.x];
+  auto K = [&](int64_t u) { return nib_to_lanes((__ldg(&keepbits[u >> 3]) >> (4 * (u & 7))) & 0xFu); };
+  uint32_t kc[RG + 2], own[RG];
+#pragma unroll
+  for (int j = 0; j < RG + 2; ++j) {
+    const int32_t iy = p.iy0 - 1 + j;
+    const bool row_ok = iy >= 0 && iy < g.ny && (j == 0 || j == RG + 1 || j - 1 < p.nrow);
+    const int64_t t = p.t0 + (int64_t)(j - 1) * g.wrow;
+    if (j >= 1 && j <= RG) own[j - 1] = (p.ok && row_ok) ? __ldcs(&fw[t]) : 0u;
+    // off-grid rows count as "keep" for the boundary test (no neighbour there)
+    kc[j] = (iy >= 0 && iy < g.ny) ? ((p.ok && row_ok) ? K(t) : 0u) : 0x01010101u;
+  }
+  uint32_t keep[RG], bnd[RG];
+  unsigned long long packed = 0;  // 16-bit per-row counts
+#pragma unroll
+  for (int k = 0; k < RG; ++k) {
+    const int64_t t = p.t0 + (int64_t)k * g.wrow;
+    const bool rok = p.ok && k < p.nrow;
+    keep[k] = rok ? kc[k + 1] : 0u;
+    const uint32_t xa = xnbr_lanes(g, p, t, rok, keep[k], 0x01010101u, false, K);
+    bnd[k] = 0;
+    if (keep[k]) {
+      uint32_t all = xa & kc[k] & kc[k + 2];
+      if (g.d3) {
+        all &= p.iz > 0 ? K(t - g.wplane) : 0x01010101u;
+        all &= p.iz < g.nz - 1 ? K(t + g.wplane) : 0x01010101u;
+      }
+      bnd[k] = keep[k] & ~all & 0x01010101u;
+    }
+    packed |= (unsigned long long)__popc(keep[k]) << (16 * k);
+  }
+  unsigned long long x = packed;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wpre[wi] = x;
+  __syncthreads();
+  unsigned long long pre = x - packed, tot = 0;
+  for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+    if (q < wi) pre += wpre[q];
+    tot += wpre[q];
+  }
+  unsigned long long rowoff = 0;  // exclusive prefix of the row totals inside the block
+#pragma unroll
+  for (int k = 1; k < RG; ++k) rowoff += ((tot >> (16 * (k - 1))) & 0xFFFFu) << (16 * k);
+  rowoff += (rowoff << 16) + (rowoff << 32) + (rowoff << 48);  // running sums (fields < 2^16)
+  int nb = 0, nnew = 0;
+#pragma unroll
+  for (int k = 0; k < RG; ++k) {
+    if (!(p.ok && k < p.nrow)) continue;
+    const int64_t t = p.t0 + (int64_t)k * g.wrow;
+    int32_t pos = boff + (int32_t)((rowoff >> (16 * k)) & 0xFFFFu) + (int32_t)((pre >> (16 * k)) & 0xFFFFu);
+    const int64_t i0 = 4 * t;
+    int32_t gl[4];
+    uint32_t out = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t f = (own[k] >> (8 * e)) & 0xFFu;
+      uint32_t o = f & (F_PIN | F_T);
+      gl[e] = -1;
+      if ((keep[k] >> (8 * e)) & 1u) {
+        o |= F_A;
+        if ((bnd[k] >> (8 * e)) & 1u) o |= F_B;
+        if (M.mode == MODE_DD) {
+          if (!(f & F_T)) { label[i0 + e] = round; ++nnew; }
+          o |= F_T;
+        }
+        act[pos] = (int32_t)(i0 + e);
+        gl[e] = pos++;
+      }
+      out |= o << (8 * e);
+    }
+    reinterpret_cast<uint32_t*>(fout)[t] = out;
+    reinterpret_cast<int4*>(g2l)[t] = make_int4(gl[0], gl[1], gl[2], gl[3]);
+    nb += __popc(bnd[k]);
+  }
+  const int nbs = block_sum(nb, sh8);
+  __syncthreads();
+  const int nns = block_sum(nnew, sh8);
+  if (threadIdx.x == 0) {
+    if (nbs) atomicAdd(&dsc->nB, nbs);
+    if (nns) atomicAdd(&dsc->n_new, nns);
+  }
+}
+
 // ============================================================== launchers
 int launch_update(rsim_gpu_ctx* c, double eps) {
   if (c->nA <= 0) return RSIM_OK;
@@ -1160,6 +1318,15 @@ static bool bits_path_possible(const rsim_gpu_ctx* c) {
   const Geo4 g = geo4(c);
   const dim3 grg = rg_grid(g);
   return g.vec4 && (int64_t)grg.x * grg.y >= 16 * 148;
+}
+
+static bool keepbits_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("RSIM_NO_KEEPBITS_K7");
+    v = (e && *e == '1') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 static bool coop_set_update_enabled() {
@@ -1252,6 +1419,19 @@ int launch_set_update(rsim_gpu_ctx* c, int mode, int round, double eps, int m, i
       c->launches++;
     }
     bt = g.nseg == 1;  // block tiles: RG-fold fewer offsets to scan
+    if (bt && keepbits_enabled()) {
+      uint32_t* kb = c->bits[(rounds + 1) & 1];  // the buffer the final map is not in
+      k_keep_rg<<<grg, g.bs, 0, c->stream>>>(g, c->flags, c->bits[rounds & 1], kb, c->dsc, M, c->tile_cnt);
+      c->launches++;
+      { const int r = launch_scan_tiles(c, (int64_t)grg.x, M); if (r != RSIM_OK) return r; }
+      k_scatter_kb<<<grg, g.bs, 0, c->stream>>>(g, c->flags, kb, c->flags_alt, M, round, c->dsc, c->tile_off,
+                                                c->act_buf, c->g2l, c->label);
+      c->launches++;
+      RSIM_CUDA(cudaGetLastError());
+      std::swap(c->flags, c->flags_alt);
+      c->act = c->act_buf;
+      return RSIM_OK;
+    }
     k_count_merge_rg<<<grg, g.bs, 0, c->stream>>>(g, c->flags, c->bits[rounds & 1], c->dsc, M, c->tile_cnt, bt);
     c->launches++;
   } else {
