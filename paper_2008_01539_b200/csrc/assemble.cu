@@ -96,6 +96,9 @@ __device__ __forceinline__ void store_scaled(double* dst, const double (*Di)[B],
 // NNC connections, the well, D^{-1}; then every lane stores its scaled block.
 // The terms are computed by physics.h flux_terms() and added in the same order
 // as flux_conn() in the oracle, so rows are bit-identical.
+#ifndef RSIM_K1ROW_MINB
+#define RSIM_K1ROW_MINB 4  // b = 1 row kernel: blocks per SM (register cap 64)
+#endif
 constexpr int LPR = 8;
 constexpr int RPB = 256 / LPR;
 constexpr int64_t kRowKernelMin = 148 * 2048;  // rows: switch to one thread per row
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
 // active with local index = global index, so neither act / g2l are read nor
 // the structural ELL columns stored (consumers use implicit_col()).
 template <int B, bool FULL>
-__global__ void __launch_bounds__(256) k_assemble_row(const AsmArgs a) {
+__global__ void __launch_bounds__(256, B == 1 ? RSIM_K1ROW_MINB : 1) k_assemble_row(const AsmArgs a) {
   constexpr bool KEEP = (B == 1);
   __shared__ double wsf[8];
   double finf = 0.0, ff = 0.0;

@@ -112,31 +112,50 @@ __device__ __forceinline__ void commit_round(Red& R, int NQ, const double* val, 
   __syncthreads();
 }
 
-// Canonical reduction of P partials src[0..P) held in global memory, done by
-// ONE CTA (all 1024 threads call it); requires P <= 64*256.  Result in R.res[q].
-__device__ __forceinline__ void reduce_small(Red& R, int q, const double* src, int P) {
+// Canonical reduction of P partials (P <= 64*256) held in global memory, done
+// by ONE CTA (all 1024 threads call it), for NQ quantities at once: one pass
+// over the partials per 4 chunks for all of them (NQ-fold fewer dependent
+// load + barrier steps).  src(q) gives quantity q's partials; results in
+// R.res[q].  Per quantity: warp trees + 8-way trees over chunks of 256
+// partials, then the same over the chunk results (blockops.h canonical tree).
+template <class SF>
+__device__ __forceinline__ void reduce_small_multi(Red& R, int NQ, SF&& src, int P) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (P == 1) {
-    if (threadIdx.x == 0) R.res[q] = src[0];
+    if ((int)threadIdx.x < NQ) R.res[threadIdx.x] = src(threadIdx.x)[0];
     __syncthreads();
     return;
   }
   const int P2 = (P + 255) / 256;
-  for (int c0 = 0; c0 < P2; c0 += CPR) {  // CPR chunks of 256 partials per pass
+  for (int c0 = 0; c0 < P2; c0 += CPR) {
     const int idx = c0 * 256 + threadIdx.x;
-    double v = warp_tree(idx < P ? src[idx] : 0.0);
-    if (lane == 0) R.ws[q][w] = v;
+    double v[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) v[q] = (q < NQ && idx < P) ? src(q)[idx] : 0.0;  // all loads in flight
+#pragma unroll
+    for (int q = 0; q < 5; ++q)
+      if (q < NQ) {
+        const double t = warp_tree(v[q]);
+        if (lane == 0) R.ws[q][w] = t;
+      }
     __syncthreads();
-    if ((int)threadIdx.x < CPR && c0 + (int)threadIdx.x < P2) R.lvl[q][c0 + threadIdx.x] = tree8(&R.ws[q][8 * threadIdx.x]);
+    if ((int)threadIdx.x < CPR * NQ) {
+      const int g = threadIdx.x & (CPR - 1), q = threadIdx.x >> LCPR;
+      if (c0 + g < P2) R.lvl[q][c0 + g] = tree8(&R.ws[q][8 * g]);
+    }
     __syncthreads();
   }
   if (P2 == 1) {
-    if (threadIdx.x == 0) R.res[q] = R.lvl[q][0];
+    if ((int)threadIdx.x < NQ) R.res[threadIdx.x] = R.lvl[threadIdx.x][0];
   } else {
-    double v = warp_tree(threadIdx.x < (unsigned)P2 ? R.lvl[q][threadIdx.x] : 0.0);
-    if (lane == 0 && w < 8) R.ws[q][w] = v;
+#pragma unroll
+    for (int q = 0; q < 5; ++q)
+      if (q < NQ) {
+        const double t = warp_tree(threadIdx.x < (unsigned)P2 ? R.lvl[q][threadIdx.x] : 0.0);
+        if (lane == 0 && w < 8) R.ws[q][w] = t;
+      }
     __syncthreads();
-    if (threadIdx.x == 0) R.res[q] = tree8(&R.ws[q][0]);
+    if ((int)threadIdx.x < NQ) R.res[threadIdx.x] = tree8(&R.ws[threadIdx.x][0]);
   }
   __syncthreads();
 }
@@ -224,7 +243,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     const int P1 = (int)nch;
     auto src = [&](int q) { return (q == 1 && src1) ? src1 : a.part + q * a.pstride; };
     if (P1 <= 64 * 256) {
-      for (int q = 0; q < NQ; ++q) reduce_small(R, q, src(q), P1);
+      reduce_small_multi(R, NQ, src, P1);
     } else {
       // distributed level 2, one more barrier, then the (small) rest per CTA
       const int P2 = (P1 + 255) / 256;
@@ -236,7 +255,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
         commit_round(R, NQ, v, rr * CPR, P2, a.part2, a.pstride2);
       }
       sync();
-      for (int q = 0; q < NQ; ++q) reduce_small(R, q, a.part2 + q * a.pstride2, P2);
+      reduce_small_multi(R, NQ, [&](int q) { return (const double*)(a.part2 + q * a.pstride2); }, P2);
     }
   };
 
@@ -536,7 +555,11 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.neu = o->precond == RSIM_PREC_NEUMANN1;
   a.ilu = o->precond == RSIM_PREC_ILU0;
   a.fa = ilu_args(c);
-  a.fuse = (c->nA <= kFuseMaxRows && !a.ilu) ? 1 : 0;
+  static const int64_t fuse_max = [] {  // env override: tuning only
+    const char* e = std::getenv("RSIM_FUSE_MAX_ROWS");
+    return (e && *e) ? (int64_t)std::atoll(e) : kFuseMaxRows;
+  }();
+  a.fuse = (c->nA <= fuse_max && !a.ilu) ? 1 : 0;
   a.pstride = (int32_t)((c->n + 255) / 256);
   a.pstride2 = (a.pstride + 255) / 256;
   a.part = c->part;
