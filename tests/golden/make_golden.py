@@ -1,0 +1,93 @@
+"""Generate the committed golden fixtures under tests/golden/ from the CPU oracle.
+
+The reference (arXiv 2008.01539, /root/reference) ships no code, case files or
+golden vectors, so these fixtures are produced by the oracle
+(`oracle/oracle.cpp`, itself pinned by the SPEC known-answer tests in
+tests/test_oracle_kat.py) on seeded small cases.  They freeze the oracle's
+bits: `tests/test_golden.py` checks that the oracle still reproduces them
+(CPU) and that the sm_100a path through the C-ABI reproduces them (GPU) —
+without re-running the oracle on the GPU box.
+
+    python tests/golden/make_golden.py      # rewrites tests/golden/*.npz
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+import paper_2008_01539_b200 as pkg  # noqa: E402  (case generation + option structs only)
+from oracle import Oracle  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+# name -> (Case kwargs, solver (0 standard, 1 localized, 2 DD), number of timesteps, precond or None)
+GOLDEN = {
+    "c1_standard": (dict(config=1), 0, 6, None),
+    "c1_localized": (dict(config=1), 1, 20, None),
+    "c1_dd": (dict(config=1), 2, 8, None),
+    "c2s_localized": (dict(config=2, nx=48, ny=48, n_dfn=12), 1, 10, None),
+    "c2s_dd": (dict(config=2, nx=48, ny=48, n_dfn=12), 2, 6, None),
+    "c3s_localized": (dict(config=3, nx=24, ny=24, nz=4), 1, 5, None),
+    "c4s_localized": (dict(config=4, nx=24, ny=24, nz=4, n_dfn=8), 1, 5, None),
+    "c2s_localized_bj": (dict(config=2, nx=48, ny=48, n_dfn=12), 1, 6, 0),
+}
+
+REC_FIELDS = ["n_active", "lin_iters", "subdomain", "mode_expand", "dp_inf_A", "dp_inf_B", "f_norm2",
+              "f_norminf", "lin_res"]
+
+
+def opts_for(case, solver, precond):
+    opts = case.solver_opts() if precond is None else case.solver_opts(precond=precond)
+    if solver == 2:
+        opts.m = 4
+    return opts
+
+
+def first_step_report(orc, case, solver, opts):
+    """Newton report of the first timestep through the SPEC entry point of `solver`."""
+    s0 = case.init_state()
+    dt = float(case.schedule()[0])
+    if solver == 0:
+        _, rep, rc = orc.newton_standard(s0, dt, opts)
+        labels = va = None
+    else:
+        va = orc.initial_active(None, opts.eps_set, opts.m)
+        labels = None
+        if solver == 1:
+            _, rep, rc = orc.newton_localized(s0, dt, va, opts.m, opts.eps_set, opts)
+        else:
+            _, rep, rc, labels = orc.adaptive_nonlinear_dd(s0, dt, va, opts.m, opts.eps_set, opts)
+    recs = rep.records()
+    out = {f"rec_{f}": np.array([r[f] for r in recs]) for f in REC_FIELDS}
+    out.update(step0_rc=rc, step0_iterations=rep.iterations, step0_outer=rep.outer_iterations,
+               step0_nsub=rep.n_subdomains, step0_lin_total=rep.lin_iters_total, step0_sum_na=rep.sum_na)
+    if solver != 0:
+        out["step0_va"] = va
+    if labels is not None:
+        out["step0_labels"] = labels
+    return out
+
+
+def make(name):
+    kw, solver, nsteps, precond = GOLDEN[name]
+    case = pkg.Case(**kw)
+    opts = opts_for(case, solver, precond)
+    orc = Oracle(case)
+    d = first_step_report(orc, case, solver, opts)
+    dts = case.schedule()[:nsteps]
+    r = orc.run_case(solver, case.init_state(), dts, opts)
+    d.update(solver=solver, dts=np.asarray(dts, np.float64), status=r["status"], iterations=r["iterations"],
+             sum_na=r["sum_na"], lin_iters=r["lin_iters"], cuts=r["cuts"], total_ma=r["total_ma"],
+             u=r["states"].u, st=r["states"].status)
+    return d
+
+
+if __name__ == "__main__":
+    for name in (sys.argv[1:] or GOLDEN):
+        d = make(name)
+        np.savez_compressed(os.path.join(HERE, name + ".npz"), **d)
+        print(name, "iters", int(d["iterations"]), "lin", int(d["lin_iters"]), "sum_na", int(d["sum_na"]),
+              "status", int(d["status"]))
