@@ -97,6 +97,13 @@ class Case:
         self.b = int(self.fluid.kind)
         self.n_nnc = int(L.rsim_case_n_nnc(self._h))
 
+    def well_rates(self, states: "CellStates") -> np.ndarray:
+        """Surface production rates (water, oil, gas) in m^3/s at `states`."""
+        q = np.zeros(3)
+        _check(A.lib().rsim_well_rates(self._h, A.ptr(states.u, C.c_double), A.ptr(states.status, C.c_uint8),
+                                       A.ptr(q, C.c_double)), "well_rates")
+        return q
+
     def __del__(self):
         if getattr(self, "_h", None):
             A.lib().rsim_case_destroy(self._h)
@@ -349,3 +356,20 @@ def device_info() -> dict:
     sm, ma, mi = C.c_int32(), C.c_int32(), C.c_int32()
     _check(A.lib().rsim_gpu_device_info(name, 256, C.byref(sm), C.byref(ma), C.byref(mi)), "device_info")
     return {"name": name.value.decode(), "sm_count": sm.value, "cc": (ma.value, mi.value)}
+
+
+SOLVERS = {"standard": 0, "localized": 1, "adaptive_dd": 2}
+
+
+def simulate(config: int, solver: str = "localized", out_dir: str | None = None, *, nx: int = 0, ny: int = 0,
+             nz: int = 0, seed: int = 0, n_dfn: int = -1, m: int = 0, eps_p: float = 0.0, n_steps: int = 0,
+             precond: int = -1, report_every_days: float = 0.0, write_fields: bool = True) -> dict:
+    """Case runner (SPEC.md sim_driver_cli run_case, include/rsim/simulate.h): run a seeded
+    config on the GPU with the named solver; writes rates.csv / metrics.csv / summary.txt
+    (+ field dumps) into out_dir when given.  eps_p in Pa (0 -> case default)."""
+    co = A.CaseOpts(config, nx, ny, nz, seed, n_dfn, -1)
+    so = A.SimOpts(SOLVERS[solver], m, eps_p, n_steps, precond, report_every_days, int(write_fields))
+    mt = A.RunMetrics()
+    rc = A.lib().rsim_simulate(C.byref(co), C.byref(so), (out_dir or "").encode(), C.byref(mt))
+    _check(rc, "simulate")
+    return {f: getattr(mt, f) for f, _ in A.RunMetrics._fields_ if f != "pad"}

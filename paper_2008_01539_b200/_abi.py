@@ -93,6 +93,22 @@ class CaseOpts(C.Structure):
     ]
 
 
+class SimOpts(C.Structure):
+    _fields_ = [
+        ("solver", C.c_int32), ("m", C.c_int32), ("eps_p", C.c_double), ("n_steps", C.c_int32),
+        ("precond", C.c_int32), ("report_every_days", C.c_double), ("write_fields", C.c_int32),
+    ]
+
+
+class RunMetrics(C.Structure):
+    _fields_ = [
+        ("status", C.c_int32), ("timesteps", C.c_int32), ("total_iters", C.c_int32), ("total_lin", C.c_int32),
+        ("cuts", C.c_int32), ("pad", C.c_int32), ("sum_na", C.c_int64), ("total_ma", C.c_double),
+        ("avg_ma", C.c_double), ("sim_days", C.c_double), ("cum_oil_m3", C.c_double),
+        ("cum_water_m3", C.c_double), ("cum_gas_m3", C.c_double), ("wall_s", C.c_double),
+    ]
+
+
 # name -> (restype, argtypes); every symbol declared in include/rsim/*.h
 P = C.c_void_p
 PROTOS: dict[str, tuple] = {
@@ -108,6 +124,9 @@ PROTOS: dict[str, tuple] = {
     "rsim_case_schedule": (C.c_int32, [P, dptr, C.c_int32]),
     "rsim_case_solver_opts": (C.c_int, [P, C.POINTER(SolverOpts)]),
     "rsim_case_n_nnc": (C.c_int64, [P]),
+    # simulate.h (case runner, SPEC.md sim_driver_cli)
+    "rsim_well_rates": (C.c_int, [P, dptr, u8ptr, dptr]),
+    "rsim_simulate": (C.c_int, [C.POINTER(CaseOpts), C.POINTER(SimOpts), C.c_char_p, C.POINTER(RunMetrics)]),
     "rsim_case_c5_field": (C.c_double, [P, C.c_double, C.c_int32, C.c_double, dptr, dptr]),
     # gpu_abi.h
     "rsim_gpu_set_device": (C.c_int, [C.c_int32]),

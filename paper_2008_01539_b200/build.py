@@ -33,7 +33,8 @@ NVFLAGS = ARCH + [
     "-Xptxas", "-v" if os.environ.get("RSIM_PTXAS_V") else "-O3",
     "-I", str(ROOT / "include"), "-I", str(CSRC),
 ]
-SOURCES = ["abi.cu", "assemble.cu", "krylov.cu", "krylov_dsm.cu", "krylov_gmres.cu", "ilu.cu", "sets.cu", "solvers.cpp", "cases.cpp"]
+SOURCES = ["abi.cu", "assemble.cu", "krylov.cu", "krylov_dsm.cu", "krylov_gmres.cu", "ilu.cu", "sets.cu", "solvers.cpp", "cases.cpp", "simulate.cpp"]
+CLI = PKG / "lib" / "simulate"
 
 
 def _run(cmd: list[str]) -> str:
@@ -71,6 +72,10 @@ def build_product(force: bool = False, verbose: bool = False) -> Path:
         objs = list(ex.map(one, SOURCES))
     if force or _stale(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-ccbin", HOSTCXX, *map(str, objs), "-o", str(LIB), "-lgomp"])
+    main = CSRC / "simulate_main.cpp"
+    if force or _stale(CLI, [main, LIB] + hdrs):  # the case-runner CLI (SPEC.md sim_driver_cli)
+        _run([HOSTCXX, "-O2", "-std=c++17", "-I", str(ROOT / "include"), str(main), "-o", str(CLI),
+              "-L", str(LIB.parent), "-lrsim", "-Wl,-rpath,$ORIGIN"])
     return LIB
 
 

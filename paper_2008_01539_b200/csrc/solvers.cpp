@@ -26,6 +26,11 @@ int rsim_internal_b(const rsim_gpu_ctx* c);
 int32_t rsim_internal_nA(const rsim_gpu_ctx* c);
 extern "C" int rsim_internal_add_row_iters(rsim_gpu_ctx* c, int64_t v);
 extern "C" int rsim_internal_solve_update(rsim_gpu_ctx* c, const rsim_solver_opts* o, double eps);
+typedef int (*rsim_step_cb)(void* user, double dt, const rsim_newton_report* rep);
+extern "C" int rsim_internal_run_case_cb(rsim_gpu_ctx* c, int32_t solver, const double* dts, int32_t nsteps,
+                                         const rsim_solver_opts* o, int32_t* total_iters, double* total_ma,
+                                         int64_t* total_na, int32_t* total_lin, int32_t* n_cuts, rsim_step_cb cb,
+                                         void* user);
 
 namespace {
 
@@ -226,6 +231,15 @@ int rsim_adaptive_nonlinear_dd(rsim_gpu_ctx* c, double* u, uint8_t* status, doub
 int rsim_run_case_dev(rsim_gpu_ctx* c, int32_t solver, const double* dts, int32_t nsteps, const rsim_solver_opts* o,
                       int32_t* total_iters, double* total_ma, int64_t* total_na, int32_t* total_lin,
                       int32_t* n_cuts) {
+  return rsim_internal_run_case_cb(c, solver, dts, nsteps, o, total_iters, total_ma, total_na, total_lin, n_cuts,
+                                   nullptr, nullptr);
+}
+
+// run_case with a hook called after every committed timestep (the case
+// runner's per-step outputs, simulate.cpp); cb returning non-zero aborts.
+int rsim_internal_run_case_cb(rsim_gpu_ctx* c, int32_t solver, const double* dts, int32_t nsteps,
+                              const rsim_solver_opts* o, int32_t* total_iters, double* total_ma, int64_t* total_na,
+                              int32_t* total_lin, int32_t* n_cuts, rsim_step_cb cb, void* user) {
   if (!c || !dts || !o || nsteps < 1) return RSIM_EARG;
   *total_iters = 0; *total_ma = 0.0; *total_na = 0; *total_lin = 0; *n_cuts = 0;
   rsim_newton_report* rep = new rsim_newton_report;
@@ -262,6 +276,7 @@ int rsim_run_case_dev(rsim_gpu_ctx* c, int32_t solver, const double* dts, int32_
     }
     r = rsim_internal_commit_step(c);
     first = false;
+    if (r == RSIM_OK && cb) r = cb(user, dt, rep);
   }
   delete rep;
   if (r != RSIM_OK) return r;
