@@ -541,7 +541,11 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.implicit = c->cols_implicit;
   // staging lets warps drift apart by several rounds: good for the regular
   // full-grid sweep, bad for L1 reuse of scattered gathers on partial sets
-  a.stage = c->cols_implicit ? RSTAGE : 1;
+  static const int stage_env = [] {  // env override: tuning only
+    const char* e = std::getenv("RSIM_KSTAGE");
+    return (e && *e) ? std::atoi(e) : 0;
+  }();
+  a.stage = stage_env > 0 ? (stage_env < RSTAGE ? stage_env : RSTAGE) : (c->cols_implicit ? RSTAGE : 1);
   a.cap = c->n;
   a.has_nnc = c->has_nnc;
   a.rtol = o->lin_rtol;
