@@ -306,6 +306,62 @@ def c5_sweep(pkg, fractions, reps, hbm, ilu_fracs=()):
     return out
 
 
+def eos_flash_line(pkg, n, reps, no_cpu):
+    """Peng-Robinson flash throughput (paper Case 3 fluid C1/C10
+    at 340 K): n cells with seeded pressures 14.7-3500 psi and overall compositions,
+    device-resident (rsim_eos_flash_dev on the torch stream, CUDA events), plus the
+    oracle on the host cores over a bounded sample.  Compute-bound (rlog / rexp per
+    stability and successive-substitution step), so no HBM roofline."""
+    import ctypes as C
+    import torch
+    e = pkg.eos_case3()
+    rng = np.random.default_rng(2008015393)
+    p = rng.uniform(14.7, 3500.0, n) * 6894.757293168361
+    z1 = rng.uniform(0.2, 0.8, n)
+    z = np.stack([z1, 1.0 - z1], axis=1).reshape(-1)
+    dev = torch.device("cuda")
+    tp, tz = torch.from_numpy(p).to(dev), torch.from_numpy(z).to(dev)
+    st = torch.empty(n, dtype=torch.uint8, device=dev)
+    nu = torch.empty(n, dtype=torch.float64, device=dev)
+    tx, ty = torch.empty(2 * n, dtype=torch.float64, device=dev), torch.empty(2 * n, dtype=torch.float64, device=dev)
+    zf = torch.empty(2 * n, dtype=torch.float64, device=dev)
+    it = torch.empty(n, dtype=torch.int32, device=dev)
+    L = pkg._abi.lib()
+    stream = torch.cuda.current_stream()
+
+    def run():
+        rc = L.rsim_eos_flash_dev(C.byref(e), 340.0, n, tp.data_ptr(), tz.data_ptr(), st.data_ptr(), nu.data_ptr(),
+                                  tx.data_ptr(), ty.data_ptr(), zf.data_ptr(), it.data_ptr(), stream.cuda_stream)
+        assert rc == 0, rc
+
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(reps):
+        run()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / reps
+    stc = st.cpu().numpy()
+    out = {"cells": n, "ms": ms, "cells_per_s": n / (ms / 1e3), "two_phase_fraction": float((stc == 2).mean()),
+           "mean_iters": float(it.double().mean().item()), "gpu_launches_per_flash": 1,
+           "fluid": "C1/C10 (paper Case 3), 340 K, p 14.7-3500 psi, z_C1 0.2-0.8"}
+    if not no_cpu:
+        import oracle
+        cores = len(os.sched_getaffinity(0))
+        oracle.set_threads(cores)
+        m = min(n, 1 << 17)
+        t0 = time.perf_counter()
+        o = oracle.eos_flash(e, 340.0, p[:m], z[:2 * m])
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": m / dt, "unit": "cells/s", "cores": cores, "kind": "port",
+                               "sample": f"first {m} cells ({dt:.2f} s, oracle/ OpenMP {cores} threads)"}
+        out["bit_exact_vs_oracle_sample"] = bool(np.array_equal(o["nu_g"], nu[:m].cpu().numpy()))
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -316,6 +372,7 @@ def main():
     ap.add_argument("--c5-ilu", default="0.05", help="fractions that also get the ILU(0) row ('' to skip)")
     ap.add_argument("--c5-reps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--flash-cells", type=int, default=1 << 22, help="PR flash bench cells (0 to skip)")
     ap.add_argument("--precond", type=int, default=None,
                     help="0 block-Jacobi, 2 block-Jacobi + first-order Neumann polynomial (default: case default)")
     args = ap.parse_args()
@@ -483,6 +540,8 @@ def main():
         fr = [float(x) for x in args.c5.split(",") if x]
         ilu_fr = [float(x) for x in args.c5_ilu.split(",") if x.strip()]
         line["c5_sweep"] = c5_sweep(pkg, fr, args.c5_reps, hbm, ilu_fr)
+    if rank == 0 and args.flash_cells > 0:
+        line["eos_flash"] = eos_flash_line(pkg, args.flash_cells, 5, args.no_cpu)
     if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(case, s0, dts, opts)
     barrier(dist)

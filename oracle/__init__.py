@@ -52,6 +52,12 @@ PROTOS = {
     "orc_props": (C.c_int, [C.POINTER(A.FluidParams), d, C.c_uint8, d, d, d, d]),
     "orc_set_u": (C.c_int, [P, d, u8]),
     "orc_assemble_raw": (C.c_int64, [P, i32, C.c_int32, d, d, i32, i32, d, C.c_int64]),
+    "orc_eos_rlog": (C.c_double, [C.c_double]),
+    "orc_eos_cubic_roots": (C.c_int, [C.c_double, C.c_double, d]),
+    "orc_eos_phase": (C.c_int, [C.POINTER(A.EosParams), C.c_double, C.c_double, d, C.c_int32, C.c_int32, d, d]),
+    "orc_eos_rachford_rice": (C.c_int, [C.c_int32, d, d, d]),
+    "orc_eos_stability": (C.c_int, [C.POINTER(A.EosParams), C.c_double, C.c_double, d, d, i32]),
+    "orc_eos_flash": (C.c_int, [C.POINTER(A.EosParams), C.c_double, C.c_int64, d, d, u8, d, d, d, d, i32]),
 }
 
 _lib = None
@@ -250,3 +256,18 @@ class Oracle:
         F = np.zeros(self.n * self.b)
         self.L.orc_full_residual(self._h, A.ptr(F, C.c_double))
         return F
+
+
+def eos_flash(e, T: float, p: np.ndarray, z: np.ndarray) -> dict:
+    """CPU flash of every cell (oracle, OpenMP): same outputs as pkg.eos_flash."""
+    n, nc = len(p), e.nc
+    p = np.ascontiguousarray(p, np.float64)
+    z = np.ascontiguousarray(z, np.float64).reshape(n * nc)
+    out = dict(status=np.zeros(n, np.uint8), nu_g=np.zeros(n), x=np.zeros(n * nc), y=np.zeros(n * nc),
+               zfac=np.zeros(2 * n), iters=np.zeros(n, np.int32))
+    rc = lib().orc_eos_flash(C.byref(e), T, n, A.ptr(p, C.c_double), A.ptr(z, C.c_double),
+                             A.ptr(out["status"], C.c_uint8), A.ptr(out["nu_g"], C.c_double),
+                             A.ptr(out["x"], C.c_double), A.ptr(out["y"], C.c_double),
+                             A.ptr(out["zfac"], C.c_double), A.ptr(out["iters"], C.c_int32))
+    assert rc == 0, rc
+    return out

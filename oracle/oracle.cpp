@@ -20,7 +20,7 @@
 //                            decisions SPEC.md:444, :456
 //   timestep cut / run_case
 //
-// Shared with the product: ONLY include/rsim/physics.h (cell-local
+// Shared with the product: ONLY include/rsim/physics.h, include/rsim/eos.h (cell-local
 // constitutive relations) and include/rsim/blockops.h (b×b block arithmetic
 // and the canonical reduction order).  Traversal, set logic, Krylov and
 // Newton control below are written independently of the CUDA code.
@@ -1166,6 +1166,83 @@ int orc_full_residual(void* h, double* F_raw) {
   if (st < 0) return RSIM_ENUM;
   std::memcpy(F_raw, M.Fraw.data(), sizeof(double) * M.Fraw.size());
   return RSIM_OK;
+}
+
+}  // extern "C"
+
+// ---- Peng-Robinson property functions and flash (
+//      SPEC.md:135-177).  The cell-local arithmetic is include/rsim/eos.h,
+//      shared with csrc/eos.cu (bit-identical results); these wrappers are the
+//      CPU checker and the CPU baseline of the flash bench line.
+#include "rsim/eos.h"
+
+namespace {
+template <class F>
+int eos_dispatch(int nc, F&& f) {
+  switch (nc) {
+    case 1: return f(std::integral_constant<int, 1>{});
+    case 2: return f(std::integral_constant<int, 2>{});
+    case 3: return f(std::integral_constant<int, 3>{});
+    case 4: return f(std::integral_constant<int, 4>{});
+    default: return RSIM_EARG;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+double orc_eos_rlog(double x) { return rsim::eos::rlog(x); }
+
+int orc_eos_cubic_roots(double A, double B, double* r3) { return rsim::eos::cubic_roots(A, B, r3); }
+
+int orc_eos_phase(const rsim_eos_params* e, double T, double p, const double* x, int32_t sel, int32_t min_g,
+                  double* Z, double* lnphi) {
+  const rsim::eos::Terms t = rsim::eos::terms(*e, T);
+  return eos_dispatch(e->nc, [&](auto NCc) {
+    constexpr int NC = decltype(NCc)::value;
+    return rsim::eos::phase_props<NC>(t, p, x, sel, min_g != 0, *Z, lnphi) ? RSIM_OK : RSIM_ENUM;
+  });
+}
+
+int orc_eos_rachford_rice(int32_t nc, const double* z, const double* K, double* nu) {
+  return eos_dispatch(nc, [&](auto NCc) {
+    constexpr int NC = decltype(NCc)::value;
+    return rsim::eos::rachford_rice<NC>(z, K, *nu) ? RSIM_OK : RSIM_EARG;
+  });
+}
+
+int orc_eos_stability(const rsim_eos_params* e, double T, double p, const double* z, double* K, int32_t* stable) {
+  const rsim::eos::Terms t = rsim::eos::terms(*e, T);
+  return eos_dispatch(e->nc, [&](auto NCc) {
+    constexpr int NC = decltype(NCc)::value;
+    int its = 0;
+    *stable = rsim::eos::stability<NC>(t, p, z, K, &its) ? 1 : 0;
+    return RSIM_OK;
+  });
+}
+
+int orc_eos_flash(const rsim_eos_params* e, double T, int64_t n, const double* p, const double* z, uint8_t* status,
+                  double* nu_g, double* x, double* y, double* zfac, int32_t* iters) {
+  if (!e || e->nc < 1 || e->nc > RSIM_EOS_NCMAX) return RSIM_EARG;
+  const rsim::eos::Terms t = rsim::eos::terms(*e, T);
+  return eos_dispatch(e->nc, [&](auto NCc) {
+    constexpr int NC = decltype(NCc)::value;
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t i = 0; i < n; ++i) {
+      rsim::eos::Flash<NC> R;
+      rsim::eos::flash<NC>(t, p[i], &z[i * NC], R);
+      status[i] = (uint8_t)R.status;
+      nu_g[i] = R.nu_g;
+      for (int c = 0; c < NC; ++c) {
+        x[i * NC + c] = R.x[c];
+        y[i * NC + c] = R.y[c];
+      }
+      zfac[2 * i] = R.Zo;
+      zfac[2 * i + 1] = R.Zg;
+      if (iters) iters[i] = R.iters;
+    }
+    return RSIM_OK;
+  });
 }
 
 }  // extern "C"

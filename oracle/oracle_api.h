@@ -15,6 +15,7 @@
 #ifndef RSIM_ORACLE_API_H
 #define RSIM_ORACLE_API_H
 
+#include "rsim/eos.h"
 #include <stdint.h>
 #include "rsim/types.h"
 
@@ -96,6 +97,16 @@ int64_t orc_assemble_raw(void* h, const int32_t* act, int32_t nA, double* F_raw,
 /* Residual of the current state on the FULL cell set (for mass balance /
  * restriction tests); F_raw has n*b entries. */
 int orc_full_residual(void* h, double* F_raw);
+
+/* Peng-Robinson EoS (arithmetic in include/rsim/eos.h). */
+double orc_eos_rlog(double x);
+int orc_eos_cubic_roots(double A, double B, double* r3);
+int orc_eos_phase(const rsim_eos_params* e, double T, double p, const double* x, int32_t sel, int32_t min_g,
+                  double* Z, double* lnphi);
+int orc_eos_rachford_rice(int32_t nc, const double* z, const double* K, double* nu);
+int orc_eos_stability(const rsim_eos_params* e, double T, double p, const double* z, double* K, int32_t* stable);
+int orc_eos_flash(const rsim_eos_params* e, double T, int64_t n, const double* p, const double* z, uint8_t* status,
+                  double* nu_g, double* x, double* y, double* zfac, int32_t* iters);
 
 #ifdef __cplusplus
 }

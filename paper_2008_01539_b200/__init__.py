@@ -373,3 +373,27 @@ def simulate(config: int, solver: str = "localized", out_dir: str | None = None,
     rc = A.lib().rsim_simulate(C.byref(co), C.byref(so), (out_dir or "").encode(), C.byref(mt))
     _check(rc, "simulate")
     return {f: getattr(mt, f) for f, _ in A.RunMetrics._fields_ if f != "pad"}
+
+
+def eos_case3() -> A.EosParams:
+    """Paper Case 3 fluid: C1 / C10 Peng-Robinson components (include/rsim/eos.h)."""
+    e = A.EosParams()
+    _check(A.lib().rsim_eos_case3(C.byref(e)), "eos_case3")
+    return e
+
+
+def eos_flash(e: A.EosParams, T: float, p: np.ndarray, z: np.ndarray) -> dict:
+    """Peng-Robinson flash of every cell on the GPU: two-sided
+    Michelsen stability test, then successive substitution.  p[n] in Pa,
+    z[n, nc] overall mole fractions.  Returns status (RSIM_PH_*: 0 oil, 1 gas,
+    2 two-phase), nu_g, x, y ([n*nc]), zfac ([2n]: Z_o, Z_g), iters."""
+    n, nc = len(p), e.nc
+    p = np.ascontiguousarray(p, np.float64)
+    z = np.ascontiguousarray(z, np.float64).reshape(n * nc)
+    out = dict(status=np.zeros(n, np.uint8), nu_g=np.zeros(n), x=np.zeros(n * nc), y=np.zeros(n * nc),
+               zfac=np.zeros(2 * n), iters=np.zeros(n, np.int32))
+    _check(A.lib().rsim_eos_flash(C.byref(e), T, n, A.ptr(p, C.c_double), A.ptr(z, C.c_double),
+                                  A.ptr(out["status"], C.c_uint8), A.ptr(out["nu_g"], C.c_double),
+                                  A.ptr(out["x"], C.c_double), A.ptr(out["y"], C.c_double),
+                                  A.ptr(out["zfac"], C.c_double), A.ptr(out["iters"], C.c_int32)), "eos_flash")
+    return out

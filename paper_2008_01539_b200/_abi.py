@@ -109,6 +109,18 @@ class RunMetrics(C.Structure):
     ]
 
 
+EOS_NCMAX = 4
+
+
+class EosParams(C.Structure):
+    _fields_ = [
+        ("nc", C.c_int32), ("tc", C.c_double * EOS_NCMAX), ("pc", C.c_double * EOS_NCMAX),
+        ("omega", C.c_double * EOS_NCMAX), ("mw", C.c_double * EOS_NCMAX),
+        ("kij", (C.c_double * EOS_NCMAX) * EOS_NCMAX), ("flash_tol", C.c_double), ("flash_maxit", C.c_int32),
+        ("stab_maxit", C.c_int32),
+    ]
+
+
 # name -> (restype, argtypes); every symbol declared in include/rsim/*.h
 P = C.c_void_p
 PROTOS: dict[str, tuple] = {
@@ -127,6 +139,13 @@ PROTOS: dict[str, tuple] = {
     # simulate.h (case runner, SPEC.md sim_driver_cli)
     "rsim_well_rates": (C.c_int, [P, dptr, u8ptr, dptr]),
     "rsim_simulate": (C.c_int, [C.POINTER(CaseOpts), C.POINTER(SimOpts), C.c_char_p, C.POINTER(RunMetrics)]),
+    # eos.h (Peng-Robinson flash)
+    "rsim_eos_case3": (C.c_int, [C.POINTER(EosParams)]),
+    "rsim_eos_flash": (C.c_int, [C.POINTER(EosParams), C.c_double, C.c_int64, dptr, dptr, u8ptr, dptr, dptr, dptr,
+                                 dptr, i32ptr]),
+    "rsim_eos_flash_dev": (C.c_int, [C.POINTER(EosParams), C.c_double, C.c_int64, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p]),
     "rsim_case_c5_field": (C.c_double, [P, C.c_double, C.c_int32, C.c_double, dptr, dptr]),
     # gpu_abi.h
     "rsim_gpu_set_device": (C.c_int, [C.c_int32]),
