@@ -58,6 +58,7 @@ struct KArgs {
   double* part;   // [5][pstride]  level-1 partials
   double* part2;  // [5][pstride2] level-2 partials (very large systems)
   int32_t pstride, pstride2;
+  int32_t red_small_max;  // chunk partials reduced redundantly by every CTA up to this count
   DevScalars* dsc;
 };
 
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     sync();
     const int P1 = (int)nch;
     auto src = [&](int q) { return (q == 1 && src1) ? src1 : a.part + q * a.pstride; };
-    if (P1 <= 64 * 256) {
+    if (P1 <= a.red_small_max) {
       reduce_small_multi(R, NQ, src, P1);
     } else {
       // distributed level 2, one more barrier, then the (small) rest per CTA
@@ -564,6 +565,11 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
     return (e && *e) ? (int64_t)std::atoll(e) : kFuseMaxRows;
   }();
   a.fuse = (c->nA <= fuse_max && !a.ilu) ? 1 : 0;
+  static const int32_t red_small = [] {  // env override: tuning only
+    const char* e = std::getenv("RSIM_RED_SMALL_MAX");
+    return (e && *e) ? (int32_t)std::atoi(e) : 64 * 256;
+  }();
+  a.red_small_max = red_small < 64 * 256 ? red_small : 64 * 256;
   a.pstride = (int32_t)((c->n + 255) / 256);
   a.pstride2 = (a.pstride + 255) / 256;
   a.part = c->part;
