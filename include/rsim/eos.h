@@ -335,7 +335,11 @@ template <int NC>
 RSIM_HD bool stability(const Terms& t, double p, const double* z, double* Kout, int* iters) {
   double Zz, lz[NC], d[NC];
   if (!phase_props<NC>(t, p, z, RSIM_ROOT_LIQUID, true, Zz, lz)) return true;
-  for (int i = 0; i < NC; ++i) d[i] = z[i] > 0.0 ? rlog(z[i]) + lz[i] : 0.0;
+  double lzc[NC];
+  for (int i = 0; i < NC; ++i) {
+    lzc[i] = z[i] > 0.0 ? rlog(z[i]) : 0.0;
+    d[i] = z[i] > 0.0 ? lzc[i] + lz[i] : 0.0;
+  }
   bool stable = true;
   double best = 1.0 + 1e-10;  // ΣY > 1 <=> TPD < 0
   int its = 0;
@@ -353,16 +357,18 @@ RSIM_HD bool stability(const Terms& t, double p, const double* z, double* Kout, 
       for (int i = 0; i < NC; ++i) sY = sY + Y[i];
       double y[NC], ly[NC], Zy;
       for (int i = 0; i < NC; ++i) y[i] = Y[i] / sY;
-      if (!phase_props<NC>(t, p, y, trial == 0 ? RSIM_ROOT_VAPOR : RSIM_ROOT_LIQUID, true, Zy, ly)) {
+      // trial phase root by the trial's side (vapour-like: largest, liquid-like: smallest)
+      if (!phase_props<NC>(t, p, y, trial == 0 ? RSIM_ROOT_VAPOR : RSIM_ROOT_LIQUID, false, Zy, ly)) {
         trivial = true;
         break;
       }
       double err = 0.0, triv = 0.0;
       for (int i = 0; i < NC; ++i) {
         if (!(z[i] > 0.0)) continue;
-        const double Yn = rexp(d[i] - ly[i]);
+        const double lY = d[i] - ly[i];  // ln Y_new
+        const double Yn = rexp(lY);
         err = fmax(err, fabs(Yn / Y[i] - 1.0));
-        const double lk = rlog(Yn) - rlog(z[i]);
+        const double lk = lY - lzc[i];     // ln(Y_new / z)
         triv = triv + lk * lk;
         Y[i] = Yn;
       }
