@@ -306,6 +306,23 @@ def c5_sweep(pkg, fractions, reps, hbm, ilu_fracs=()):
     return out
 
 
+def flash_field(n):
+    """Cells of a square 2D grid in natural order: a smooth depletion field (pressure
+    drawn down from 3500 psi towards 14.7 psi around 64 seeded producers, the C1
+    fraction varying smoothly 0.2-0.8), as a simulator hands cells to the flash.
+    Returns p [Pa], z [n*2] and the generator."""
+    rng = np.random.default_rng(2008015393)
+    side = int(np.sqrt(n))
+    n = side * side
+    yy, xx = np.meshgrid(np.arange(side), np.arange(side), indexing="ij")
+    sx, sy = rng.uniform(0, side, 64), rng.uniform(0, side, 64)
+    d2 = np.minimum.reduce([(xx.ravel() - a) ** 2.0 + (yy.ravel() - b) ** 2.0 for a, b in zip(sx, sy)])
+    rr = 0.08 * side
+    p = (14.7 + (3500.0 - 14.7) * (1.0 - np.exp(-d2 / (2 * rr * rr)))) * 6894.757293168361
+    z1 = 0.5 + 0.3 * np.sin(2 * np.pi * xx.ravel() / side) * np.cos(2 * np.pi * yy.ravel() / side)
+    return p, np.stack([z1, 1.0 - z1], axis=1).reshape(-1), rng
+
+
 def eos_flash_line(pkg, n, reps, no_cpu):
     """Peng-Robinson flash throughput (paper Case 3 fluid C1/C10
     at 340 K): n cells with seeded pressures 14.7-3500 psi and overall compositions,
@@ -315,10 +332,8 @@ def eos_flash_line(pkg, n, reps, no_cpu):
     import ctypes as C
     import torch
     e = pkg.eos_case3()
-    rng = np.random.default_rng(2008015393)
-    p = rng.uniform(14.7, 3500.0, n) * 6894.757293168361
-    z1 = rng.uniform(0.2, 0.8, n)
-    z = np.stack([z1, 1.0 - z1], axis=1).reshape(-1)
+    p, z, rng = flash_field(n)
+    n = len(p)
     dev = torch.device("cuda")
     tp, tz = torch.from_numpy(p).to(dev), torch.from_numpy(z).to(dev)
     st = torch.empty(n, dtype=torch.uint8, device=dev)
@@ -334,20 +349,32 @@ def eos_flash_line(pkg, n, reps, no_cpu):
                                   tx.data_ptr(), ty.data_ptr(), zf.data_ptr(), it.data_ptr(), stream.cuda_stream)
         assert rc == 0, rc
 
-    for _ in range(3):
-        run()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(reps):
-        run()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1) / reps
+    def timed():
+        for _ in range(3):
+            run()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(reps):
+            run()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1) / reps
+
+    ms = timed()
     stc = st.cpu().numpy()
     out = {"cells": n, "ms": ms, "cells_per_s": n / (ms / 1e3), "two_phase_fraction": float((stc == 2).mean()),
            "mean_iters": float(it.double().mean().item()), "gpu_launches_per_flash": 1,
-           "fluid": "C1/C10 (paper Case 3), 340 K, p 14.7-3500 psi, z_C1 0.2-0.8"}
+           "fluid": "C1/C10 (paper Case 3), 340 K",
+           "field": "2D grid order, smooth depletion field 14.7-3500 psi around 64 seeded producers, z_C1 0.2-0.8"}
+    perm = torch.from_numpy(rng.permutation(n)).to(dev)  # same cells, random order: worst-case warp divergence
+    tp.copy_(tp[perm])
+    tz.copy_(tz.view(n, 2)[perm].reshape(-1))
+    ms_s = timed()
+    out["cells_per_s_shuffled"] = n / (ms_s / 1e3)
+    tp.copy_(torch.from_numpy(p).to(dev))
+    tz.copy_(torch.from_numpy(z).to(dev))
+    run()
     if not no_cpu:
         import oracle
         cores = len(os.sched_getaffinity(0))

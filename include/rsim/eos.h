@@ -259,8 +259,16 @@ RSIM_HD void lnphi(const Terms& t, double Z, double A, double B, double am, doub
 /* Z and ln φ of composition x at p with the given root selector; MIN_G picks
  * the root of lowest Gibbs energy Σ x_i ln φ_i instead.  Returns false when
  * no root exceeds B. */
+/* Out of line on the device (RSIM_EOS_NI): it is called from six sites, and
+ * inlining all of them overflows the instruction cache (ncu: "no_instructions"
+ * was the top stall of the fully inlined kernel). */
+#if defined(__CUDACC__)
+#define RSIM_EOS_NI __host__ __device__ __noinline__
+#else
+#define RSIM_EOS_NI inline
+#endif
 template <int NC>
-RSIM_HD bool phase_props(const Terms& t, double p, const double* x, int sel, bool min_g, double& Z, double* lp) {
+RSIM_EOS_NI bool phase_props(const Terms& t, double p, const double* x, int sel, bool min_g, double& Z, double* lp) {
   double A, B, am, bm, sa[NC];
   mix<NC>(t, p, x, A, B, am, bm, sa);
   double r[3];
