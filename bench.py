@@ -149,8 +149,11 @@ def barrier(dist):
 # --------------------------------------------------------------------------
 # algorithmic bytes: b unknowns/cell, s Cartesian slots
 def bytes_krylov_row_iter(b, s):
+    # 2 SpMVs (s column indices + s blocks + x_l + y write) + 14 vector passes:
+    # (r0,v),(r,r) 2, s update 3, (r0,s),(r0,t) 1, x/r/next-p update 8 (x, p,
+    # s, t, v read; x, r, p written -- the next p is formed in the x/r pass)
     spmv = s * (8 * b * b + 4) + 16 * b
-    return 2 * spmv + 120 * b
+    return 2 * spmv + 112 * b
 
 
 def bytes_krylov_row_init(b):
@@ -395,7 +398,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--c5", default="0.05,1.0", help="config-5 active fractions ('' to skip)")
+    ap.add_argument("--c5", default="0.01,0.05,0.2,0.5,1.0", help="config-5 active fractions ('' to skip)")
     ap.add_argument("--c5-ilu", default="0.05", help="fractions that also get the ILU(0) row ('' to skip)")
     ap.add_argument("--c5-reps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")

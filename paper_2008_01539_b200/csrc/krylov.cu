@@ -311,6 +311,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   int it = 0;
   double relres = 0.0;
   int cur = 0;  // which (p, v) buffer pair holds the current iterate
+  bool p_ready = false;  // unfused: the next p was stored by the x/r update pass
   // fuse: neighbours' p and s are recomputed at the gather site (fewer grid
   // barriers, latency regime); !fuse: owners store p and s, then a barrier,
   // then plain gathers (less memory traffic, bandwidth regime).
@@ -338,6 +339,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     }
     rho = 1.0; alpha = 1.0; omega = 1.0; rho_new = bb;
     cur = 0;
+    p_ready = false;
     status = RSIM_ENOCONV;
     sync();
   }
@@ -350,6 +352,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     const int pmode = it == 1 ? 1 : 0;
     const Vecs V0{a.r, po, vo, a.s, a.t};  // p_j = (s_j − ω t_j) + β (p_old_j − ω v_old_j)
     if (!fuse) {  // p = r + β (p − ω v), stored, then visible to all
+      if (!p_ready)  // (else already stored by the previous x/r update pass)
       for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
         const int64_t l = rd * KT + tid;
         if (l < nr) {
@@ -492,7 +495,16 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     if (tt == 0.0 || !isfinite(tt)) { status = RSIM_ENUM; break; }
     omega = ts / tt;
     // ---- x, r update (own rows, no barrier: neighbours recompute r from s, t
-    //      until the next reduction, and the next p-pass reads only its own r)
+    //      until the next reduction, and the next p-pass reads only its own r).
+    //      Unfused: the next iterate's p = r + β' (p − ω v) is formed here from
+    //      the same registers (own row only; β' needs only this iteration's
+    //      reductions), so the separate p pass and its re-read of s, t, p
+    //      disappear.  Same expressions as nbr_val mode 0 -> same bits.
+    const double rho_next = r0s - omega * r0t;
+    const bool more = !(omega == 0.0 || rho_next == 0.0 || !isfinite(rho_next)) && it < maxit;
+    const bool pfuse = !fuse && more;
+    const double beta_next = pfuse ? (rho_next / rho_new) * (alpha / omega) : 0.0;
+    double* pn = cur ? a.p : a.p2;  // the next iterate's p buffer
     for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
       const int64_t l = rd * KT + tid;
       if (l < nr)
@@ -500,11 +512,14 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
         for (int e = 0; e < B; ++e) {
           const int64_t q = l * B + e;
           a.x[q] = (a.x[q] + alpha * phv[q]) + omega * shv[q];
-          a.r[q] = a.s[q] - omega * a.t[q];
+          const double rq = a.s[q] - omega * a.t[q];
+          a.r[q] = rq;
+          if (pfuse) pn[q] = rq + beta_next * (pc[q] - omega * vc[q]);
         }
     }
+    p_ready = pfuse;
     rho = rho_new;
-    rho_new = r0s - omega * r0t;
+    rho_new = rho_next;
     if (omega == 0.0 || rho_new == 0.0 || !isfinite(rho_new)) { status = RSIM_ENUM; break; }
     cur ^= 1;
   }
