@@ -54,6 +54,7 @@ struct KArgs {
   bool f2_parts;
   double *x, *r, *r0, *p, *v, *s, *t, *p2, *v2, *ph, *sh;
   int32_t neu, fuse, ilu;  // neu: Neumann-1; ilu: level-scheduled ILU(0) (never fused)
+  int32_t fuse_s;          // unfused, block-Jacobi: s recomputed at the t-SpMV gather sites (no s pass)
   IluArgs fa;
   double* part;   // [5][pstride]  level-1 partials
   double* part2;  // [5][pstride2] level-2 partials (very large systems)
@@ -418,7 +419,8 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     if (r0v == 0.0 || !isfinite(r0v)) { status = RSIM_ENUM; break; }
     alpha = rho_new / r0v;
     const Vecs V2{a.r, po, vc, a.s, a.t};  // s_j = r_j − α v_j
-    if (!fuse) {  // s = r − α v, stored, barrier
+    const bool fs = fuse || (!prec && a.fuse_s);  // s recomputed where gathered, stored by its owner
+    if (!fs) {  // s = r − α v, stored, barrier
       for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
         const int64_t l = rd * KT + tid;
         if (l < nr)
@@ -457,7 +459,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
 #pragma unroll
           for (int e = 0; e < B; ++e) sv[e] = a.s[l * B + e];
         spmv_row<B>(a, l, 3, Vecs{a.r, a.sh, vc, a.s, a.t}, 0.0, 0.0, 0.0, &a.sh[l * B], y);
-      } else if (fuse) {
+      } else if (fs) {
         nbr_val<B>(2, V2, l, 0.0, 0.0, alpha, sv);
         spmv_row<B>(a, l, 2, V2, 0.0, 0.0, alpha, sv, y);
       } else {
@@ -465,7 +467,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
         for (int e = 0; e < B; ++e) sv[e] = a.s[l * B + e];
         spmv_row<B>(a, l, 3, Vecs{a.r, a.s, vc, a.s, a.t}, 0.0, 0.0, 0.0, sv, y);
       }
-      if (fuse)
+      if (fs)
 #pragma unroll
         for (int e = 0; e < B; ++e) a.s[l * B + e] = sv[e];
 #pragma unroll
@@ -580,6 +582,13 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
     return (e && *e) ? (int64_t)std::atoll(e) : kFuseMaxRows;
   }();
   a.fuse = (c->nA <= fuse_max && !a.ilu) ? 1 : 0;
+  // s recompute at the gather sites: measured on config 5 (50 iterations),
+  // 9.50 -> 9.35 ms at 5 % (1.7 M rows), even at 20 %, 114.5 -> 119.1 ms at 100 %
+  static const int64_t fuse_s_max = [] {  // env override: tuning only
+    const char* e = std::getenv("RSIM_FUSE_S_MAX_ROWS");
+    return (e && *e) ? (int64_t)std::atoll(e) : (int64_t)1 << 22;
+  }();
+  a.fuse_s = c->nA <= fuse_s_max ? 1 : 0;
   static const int32_t red_small = [] {  // env override: tuning only
     const char* e = std::getenv("RSIM_RED_SMALL_MAX");
     // measured on config 5 at 5 % (6 559 chunks): every CTA scanning all chunk

@@ -1,7 +1,7 @@
 #!/bin/bash
-# c2 headline under several cluster-kernel environment settings
+# A/B of one tuning env variable on config-5 phases: ab_env.sh VAR "v1 v2 ..." [fractions]
 mkdir -p gpurun_out/ab
-for cfg in "default:" "lrc7:RSIM_DSM_MINLRC=7" "lrc8:RSIM_DSM_MINLRC=8" "lrc9:RSIM_DSM_MINLRC=9"; do
-  name=${cfg%%:*}; envs=${cfg#*:}
-  env $envs timeout 600 python bench.py --no-cpu --steps 3 --warmup 3 --c5 "" > gpurun_out/ab/env_$name.json 2>&1
+VAR=$1; VALS=$2; FR=${3:-0.05,0.2,1.0}
+for v in $VALS; do
+  env $VAR=$v timeout 600 python scripts/c5_phases.py $FR 3 > gpurun_out/ab/env_${VAR}_$v.json 2>&1
 done
