@@ -557,13 +557,14 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.nx = c->nx; a.ny = c->ny; a.nz = c->nz;
   a.d3 = c->d3;
   a.implicit = c->cols_implicit;
-  // staging lets warps drift apart by several rounds: good for the regular
-  // full-grid sweep, bad for L1 reuse of scattered gathers on partial sets
+  // staging lets warps drift apart by several rounds (more loads in flight):
+  // best for the regular full-grid sweep and long passes; short passes over
+  // scattered partial sets prefer warps kept close (L1 reuse of the gathers)
   static const int stage_env = [] {  // env override: tuning only
     const char* e = std::getenv("RSIM_KSTAGE");
     return (e && *e) ? std::atoi(e) : 0;
   }();
-  a.stage = stage_env > 0 ? (stage_env < RSTAGE ? stage_env : RSTAGE) : (c->cols_implicit ? RSTAGE : 1);
+  a.stage = 1;  // set below from the rounds per CTA
   a.cap = c->n;
   a.has_nnc = c->has_nnc;
   a.rtol = o->lin_rtol;
@@ -616,6 +617,15 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   }
   int grid = nrounds < c->max_coop_blocks[B] ? (int)nrounds : c->max_coop_blocks[B];
   if (grid < 1) grid = 1;
+  {
+    // measured on config 5 (50 iterations, rounds per CTA at 5 / 20 / 50 % =
+    // 11 / 44 / 110): stage 1 -> 2 -> 4 -> 8 gives 9.35 / 9.15 / 9.31 / 10.07 ms
+    // at 5 %, 30.7 / 29.1 / 28.4 / 28.4 at 20 %, 72.3 / 68.2 / 65.8 / 64.9 at 50 %
+    const int64_t rpc = (nrounds + grid - 1) / grid;
+    const int st = c->cols_implicit ? RSTAGE : (rpc < 24 ? 2 : (rpc < 96 ? 4 : 8));
+    a.stage = stage_env > 0 ? stage_env : st;
+    if (a.stage > RSTAGE) a.stage = RSTAGE;
+  }
   void* args[] = {&a};
   if (grid == 1) {
     kern<<<1, KT, 0, c->stream>>>(a);
