@@ -8,10 +8,11 @@ lines = [l for l in open(sys.argv[1]) if l.startswith('"')]
 rows = list(csv.reader(lines))
 h = rows[0]
 ik, iv, iu = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+im = h.index("Metric Name")
 scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
 agg = collections.defaultdict(list)
 for r in rows[1:]:
-    if len(r) == len(h) and r[iv]:
+    if len(r) == len(h) and r[iv] and r[im] == "gpu__time_duration.sum":
         agg[r[ik].split("(")[0]].append(float(r[iv].replace(",", "")) * scale.get(r[iu], 1e-3))
 tot = sum(sum(v) for v in agg.values())
 print(f"total {tot / 1e3:.3f} ms over {sum(len(v) for v in agg.values())} launches")
