@@ -35,7 +35,10 @@ enum { RSIM_BO_UNDERSAT = 0, RSIM_BO_SAT = 1 };
 enum { RSIM_KIND_MATRIX = 0, RSIM_KIND_FRACTURE = 1 };
 
 /* Linear solver selectors. */
-enum { RSIM_LIN_BICGSTAB = 0, RSIM_LIN_GMRES = 1 };
+enum { RSIM_LIN_BICGSTAB = 0, RSIM_LIN_GMRES = 1, RSIM_LIN_DIRECT = 2 };
+/* Exact (direct) solve of small active systems:
+ * dense LU with partial pivoting, n_A*b unknowns at most. */
+#define RSIM_DIRECT_MAX 4096
 #define RSIM_GMRES_M 30 /* GMRES restart length (SPEC-free choice: GMRES(30)) */
 enum { RSIM_PREC_BJACOBI = 0, RSIM_PREC_ILU0 = 1, RSIM_PREC_NEUMANN1 = 2 };
 

@@ -580,7 +580,78 @@ static int bicgstab(const Model& M, const rsim_solver_opts& o, double* x, int32_
   return st;
 }
 
+// Exact solve of the assembled system (SPEC.md:311-325:
+// solve(J, F) "exact" for small active systems, the Krylov cross-check).
+// Dense LU with partial pivoting of Â = D⁻¹J (unit block diagonal + the scaled
+// off-diagonal blocks; entries of one row block added in CSR order), column-
+// major, right-looking, k ascending:
+//   pivot  = the first row i ≥ k of maximal |w_ik| (any non-finite entry in the
+//            column, or a zero pivot => RSIM_ENUM);
+//   swap rows k and piv across ALL columns (multipliers included);
+//   l_ik   = w_ik / w_kk  (a division, stored in place);
+//   w_ij   = w_ij − l_ik·w_kj for j > k, i > k (one product, one subtraction).
+// Solve: b ← P b (the swaps in k order); forward, column-oriented:
+// b_i −= l_ik·b_k (k ascending); backward: b_k /= u_kk, then b_i −= u_ik·b_k for
+// i < k (k descending).  Every w_ij sees its updates in k order, so any
+// schedule that keeps that order (the GPU: one column owner per CTA, one grid
+// barrier per k) reproduces these bits.  iters = 1, relres = 0 (not formed).
+template <int B>
+static int direct_solve(const Model& M, double* x, int32_t* iters, double* relres) {
+  *iters = 1;
+  *relres = 0.0;
+  const int64_t N = (int64_t)M.nA * B;
+  if (N > RSIM_DIRECT_MAX) return RSIM_EARG;
+  if (N == 0) return RSIM_OK;
+  std::vector<double> W((size_t)(N * N), 0.0);
+  for (int64_t e = 0; e < N; ++e) W[e * N + e] = 1.0;
+  for (int32_t l = 0; l < M.nA; ++l)
+    for (int64_t p = M.rowptr[l]; p < M.rowptr[l + 1]; ++p)
+      for (int r = 0; r < B; ++r)
+        for (int c = 0; c < B; ++c) {
+          double& w = W[((int64_t)M.col[p] * B + c) * N + (int64_t)l * B + r];
+          w = w + M.val[p * B * B + r * B + c];
+        }
+  std::vector<int32_t> piv((size_t)N);
+  for (int64_t k = 0; k < N; ++k) {
+    double* ck = &W[k * N];
+    int64_t pv = k;
+    double best = -1.0;
+    for (int64_t i = k; i < N; ++i) {
+      if (!std::isfinite(ck[i])) return RSIM_ENUM;
+      if (std::fabs(ck[i]) > best) { best = std::fabs(ck[i]); pv = i; }
+    }
+    if (best == 0.0) return RSIM_ENUM;
+    piv[k] = (int32_t)pv;
+    if (pv != k)
+      for (int64_t j = 0; j < N; ++j) std::swap(W[j * N + k], W[j * N + pv]);
+    const double d = ck[k];
+    for (int64_t i = k + 1; i < N; ++i) ck[i] = ck[i] / d;
+    for (int64_t j = k + 1; j < N; ++j) {
+      double* cj = &W[j * N];
+      const double ukj = cj[k];
+      for (int64_t i = k + 1; i < N; ++i) cj[i] = cj[i] - ck[i] * ukj;
+    }
+  }
+  for (int64_t e = 0; e < N; ++e) x[e] = M.rhs[e];
+  for (int64_t k = 0; k < N; ++k)
+    if (piv[k] != k) std::swap(x[k], x[piv[k]]);
+  for (int64_t k = 0; k < N; ++k)
+    for (int64_t i = k + 1; i < N; ++i) x[i] = x[i] - W[k * N + i] * x[k];
+  for (int64_t k = N - 1; k >= 0; --k) {
+    x[k] = x[k] / W[k * N + k];
+    for (int64_t i = 0; i < k; ++i) x[i] = x[i] - W[k * N + i] * x[k];
+  }
+  return RSIM_OK;
+}
+
 static int linsolve_any(const Model& M, const rsim_solver_opts& o, double* x, int32_t* it, double* rr) {
+  if (o.lin_method == RSIM_LIN_DIRECT) {
+    switch (M.b) {
+      case 1: return direct_solve<1>(M, x, it, rr);
+      case 2: return direct_solve<2>(M, x, it, rr);
+      default: return direct_solve<3>(M, x, it, rr);
+    }
+  }
   switch (M.b) {
     case 1: return bicgstab<1>(M, o, x, it, rr);
     case 2: return bicgstab<2>(M, o, x, it, rr);

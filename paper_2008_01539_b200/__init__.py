@@ -22,7 +22,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _abi as A
-from ._abi import (FLUID_BLACKOIL, FLUID_OILWATER, FLUID_SINGLE, LIN_BICGSTAB, LIN_GMRES, PREC_BJACOBI, PREC_ILU0,
+from ._abi import (DIRECT_MAX, FLUID_BLACKOIL, FLUID_OILWATER, FLUID_SINGLE, LIN_BICGSTAB, LIN_DIRECT, LIN_GMRES, PREC_BJACOBI, PREC_ILU0,
                    PREC_NEUMANN1, RSIM_EARG, RSIM_ECUDA,
                    RSIM_ENOCONV, RSIM_ENUM, RSIM_OK, FluidParams, GpuStats, GraphDesc, NewtonReport, SolverOpts)
 
@@ -30,7 +30,7 @@ __all__ = [
     "Case", "CellStates", "GpuSimulator", "RsimError", "compute_ma", "timestep_schedule", "SolverOpts",
     "NewtonReport", "FluidParams", "GraphDesc", "RSIM_OK", "RSIM_EARG", "RSIM_ECUDA", "RSIM_ENUM", "RSIM_ENOCONV",
     "FLUID_SINGLE", "FLUID_OILWATER", "FLUID_BLACKOIL", "PREC_BJACOBI", "PREC_ILU0", "PREC_NEUMANN1", "DAY",
-    "LIN_BICGSTAB", "LIN_GMRES",
+    "LIN_BICGSTAB", "LIN_GMRES", "LIN_DIRECT", "DIRECT_MAX",
 ]
 
 DAY = 86400.0

@@ -17,7 +17,8 @@ LIB_PATH = Path(os.environ.get("RSIM_LIB") or (Path(__file__).resolve().parent /
 
 RSIM_OK, RSIM_EARG, RSIM_ECUDA, RSIM_ENUM, RSIM_ENOCONV = 0, 1, 2, 3, 4
 FLUID_SINGLE, FLUID_OILWATER, FLUID_BLACKOIL = 1, 2, 3
-LIN_BICGSTAB, LIN_GMRES = 0, 1
+LIN_BICGSTAB, LIN_GMRES, LIN_DIRECT = 0, 1, 2
+DIRECT_MAX = 4096  # RSIM_DIRECT_MAX (include/rsim/types.h)
 PREC_BJACOBI, PREC_ILU0, PREC_NEUMANN1 = 0, 1, 2
 MAX_ITER_RECORDS = 4096
 

@@ -33,7 +33,7 @@ NVFLAGS = ARCH + [
     "-Xptxas", "-v" if os.environ.get("RSIM_PTXAS_V") else "-O3",
     "-I", str(ROOT / "include"), "-I", str(CSRC),
 ]
-SOURCES = ["abi.cu", "assemble.cu", "krylov.cu", "krylov_dsm.cu", "krylov_gmres.cu", "ilu.cu", "sets.cu", "solvers.cpp", "cases.cpp", "simulate.cpp", "eos.cu"]
+SOURCES = ["abi.cu", "assemble.cu", "krylov.cu", "krylov_dsm.cu", "krylov_gmres.cu", "ilu.cu", "sets.cu", "solvers.cpp", "cases.cpp", "simulate.cpp", "eos.cu", "direct.cu"]
 CLI = PKG / "lib" / "simulate"
 
 

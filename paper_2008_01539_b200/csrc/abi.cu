@@ -272,7 +272,7 @@ int rsim_gpu_destroy(rsim_gpu_ctx* c) {
                   c->list_buf, c->dp, c->last_dp, c->tile_cnt, c->tile_off, c->ell_col, c->ell_val, c->nnc_lcol,
                   c->nnc_val, c->F_raw, c->rhs, c->part_f2, c->x, c->r, c->r0, c->p, c->v, c->s, c->t, c->p2, c->v2, c->ph, c->sh, c->part,
                   c->dsc, c->dd.sub_cells, c->dd.halo_cells, c->u_ckpt, c->st_ckpt, c->l2_scratch, c->pin0, c->ktrace,
-                  c->gm_V, c->gm_part, c->dd.hist, c->bits[0], c->bits[1]};
+                  c->gm_V, c->gm_part, c->dd.hist, c->bits[0], c->bits[1], c->dn_W, c->dn_colbuf, c->dn_piv};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   ilu_free(c);

@@ -72,6 +72,9 @@ struct rsim_gpu_ctx {
   bool update_applied = false; // the last Krylov launch already applied the update
   double* gm_V = nullptr;      // GMRES basis (RSIM_GMRES_M + 1 vectors), allocated on first use
   double* gm_part = nullptr;   // GMRES reduction partials
+  double* dn_W = nullptr;      // direct solve: dense N×N (RSIM_DIRECT_MAX²), allocated on first use
+  double* dn_colbuf = nullptr; // direct solve: double-buffered pivot column
+  int32_t* dn_piv = nullptr;   // direct solve: row interchanges
   struct Ilu {                 // level-scheduled block ILU(0) (ilu.cu)
     int32_t *ptr = nullptr, *col = nullptr, *src = nullptr, *frows = nullptr, *foff = nullptr, *brows = nullptr,
             *boff = nullptr;
@@ -187,6 +190,7 @@ int launch_seed_support(rsim_gpu_ctx* c, double eps);
 int launch_reset_seed(rsim_gpu_ctx* c, double eps);
 int launch_materialize_cols(rsim_gpu_ctx* c);
 int launch_gmres(rsim_gpu_ctx* c, const rsim_solver_opts* o);
+int launch_direct(rsim_gpu_ctx* c, const rsim_solver_opts* o);
 int ilu_prepare(rsim_gpu_ctx* c);  // pattern, level schedules, factorisation (precond == ILU0)
 void ilu_free(rsim_gpu_ctx* c);
 int launch_state_from_dp(rsim_gpu_ctx* c, double p_hi, double scale);

@@ -641,6 +641,7 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
 
 int launch_krylov(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   if (c->nA <= 0) return RSIM_OK;
+  if (o->lin_method == RSIM_LIN_DIRECT) return launch_direct(c, o);  // exact dense LU (direct.cu)
   const bool ilu = o->precond == RSIM_PREC_ILU0;
   if (ilu) RSIM_TRY(ilu_prepare(c));
   if (o->lin_method == RSIM_LIN_GMRES) return launch_gmres(c, o);
