@@ -309,6 +309,50 @@ def c5_sweep(pkg, fractions, reps, hbm, ilu_fracs=()):
     return out
 
 
+def direct_line(pkg, no_cpu, reps=3):
+    """Exact dense-LU solve (lin_method = LIN_DIRECT): config 5
+    full sets of 2048 and 4096 (the maximum) unknowns; GPU time per solve (build +
+    factorisation + triangular solves) and, at 2048, the oracle's on one host core."""
+    import ctypes as C
+    from oracle import Oracle
+    out = []
+    for nx, ny in ((32, 64), (64, 64)):
+        case = pkg.Case(5, nx=nx, ny=ny, nz=1)
+        sim = pkg.GpuSimulator(case)
+        L, ctx = sim.L, sim._ctx
+        s0 = case.init_state()
+        s0.u[::case.b] -= np.random.default_rng(7).uniform(0, 3e6, case.n)
+        sim.set_state(s0, 86400.0)
+        sim.set_active(None)
+        sim.assemble()
+        opts = case.solver_opts(lin_method=pkg.LIN_DIRECT)
+        ms = []
+        for r in range(reps + 1):
+            L.rsim_gpu_mark(ctx, 16)
+            L.rsim_gpu_linear_solve(ctx, C.byref(opts))
+            L.rsim_gpu_mark(ctx, 17)
+            v = C.c_double()
+            L.rsim_gpu_elapsed(ctx, 16, 17, C.byref(v))
+            if r:
+                ms.append(v.value)
+        st = sim.stats()
+        xg = sim.solution(case.n)
+        sim.close()
+        row = {"n_unknowns": case.n * case.b, "ms": float(np.median(ms)), "status": st.status,
+               "gpu_launches_per_solve": 3}
+        if not no_cpu and case.n <= 2048:
+            o = Oracle(case)
+            o.set_state(s0, 86400.0)
+            o.assemble(np.arange(case.n, dtype=np.int32))
+            t0 = time.perf_counter()
+            rc, xo, _, _ = o.linear_solve(case.n, opts)
+            row["cpu_oracle_ms"] = (time.perf_counter() - t0) * 1e3
+            row["cpu_oracle_cores"] = 1
+            row["bit_exact_vs_oracle"] = bool(rc == st.status and np.array_equal(xg, xo))
+        out.append(row)
+    return out
+
+
 def flash_field(n):
     """Cells of a square 2D grid in natural order: a smooth depletion field (pressure
     drawn down from 3500 psi towards 14.7 psi around 64 seeded producers, the C1
@@ -402,6 +446,7 @@ def main():
     ap.add_argument("--c5-ilu", default="0.05", help="fractions that also get the ILU(0) row ('' to skip)")
     ap.add_argument("--c5-reps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--direct", type=int, default=1, help="time the exact dense-LU solve at N = 2048 / 4096 (0 to skip)")
     ap.add_argument("--flash-cells", type=int, default=1 << 22, help="PR flash bench cells (0 to skip)")
     ap.add_argument("--precond", type=int, default=None,
                     help="0 block-Jacobi, 2 block-Jacobi + first-order Neumann polynomial (default: case default)")
@@ -572,6 +617,8 @@ def main():
         line["c5_sweep"] = c5_sweep(pkg, fr, args.c5_reps, hbm, ilu_fr)
     if rank == 0 and args.flash_cells > 0:
         line["eos_flash"] = eos_flash_line(pkg, args.flash_cells, 5, args.no_cpu)
+    if rank == 0 and args.direct:
+        line["direct_solve"] = direct_line(pkg, args.no_cpu)
     if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(case, s0, dts, opts)
     barrier(dist)
