@@ -26,6 +26,7 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int DT = 256;  // threads per CTA
+constexpr int kMaxOwn = 64;  // columns per CTA at most (G >= N / 64)
 
 struct DArgs {
   int32_t nA, nslot, b;
@@ -96,6 +97,7 @@ __global__ void __launch_bounds__(DT) k_direct_lu(const DArgs a) {
   extern __shared__ double sc[];  // column k (rows k..N-1), then the multipliers
   __shared__ Piv sp[DT / 32];
   __shared__ int s_fail;
+  __shared__ double s_wk[kMaxOwn], s_wp[kMaxOwn];  // w_kj, w_pj of the own columns (step k)
   auto grid = cg::this_grid();
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int64_t N = a.N;
@@ -145,31 +147,52 @@ __global__ void __launch_bounds__(DT) k_direct_lu(const DArgs a) {
     for (int64_t i = k + 1 + t; i < N; i += DT) sc[i - k] = sc[i - k] / d;
     __syncthreads();
     if (blockIdx.x == 0 && t == 0) a.piv[k] = (int32_t)pv;
-    // ---- own columns: swap rows k / pv (all columns), update j > k
-    for (int64_t j = blockIdx.x; j < N; j += G) {
+    // ---- own columns: swap rows k / pv (all columns), update j > k.
+    // Phase 1 reads w_kj / w_pj of every own column into shared memory (one
+    // barrier), so phase 2 writes without any per-column barrier: the owner
+    // of row pv uses the old row-k value, thread 0 writes the swapped row k
+    // (and row pv of the L columns, j < k), which nobody reads in phase 2.
+    if (t < kMaxOwn) {  // own column c = blockIdx.x + c·G
+      const int64_t j = blockIdx.x + (int64_t)t * G;
+      if (j < N) { s_wk[t] = a.W[j * N + k]; s_wp[t] = a.W[j * N + pv]; }
+    }
+    __syncthreads();
+    int c = 0;
+    for (int64_t j = blockIdx.x; j < N; j += G, ++c) {
       double* cj = a.W + j * N;
       if (j == k) {  // column k: pivot and multipliers from the (swapped) shared copy
         for (int64_t i = k + t; i < N; i += DT) cj[i] = sc[i - k];
         continue;
       }
-      // row swap k <-> pv (all columns), then for j > k the update; the
-      // thread owning row pv uses the old row-k value (no write/read race)
-      const double wk = cj[k], wp = cj[pv];
-      __syncthreads();  // every thread has read w_kj / w_pj before any write
-      if (t == 0) cj[k] = wp;
+      const double wk = s_wk[c], wp = s_wp[c];
+      if (t == 0) {
+        cj[k] = wp;
+        if (j < k && pv != k) cj[pv] = wk;
+      }
       if (j > k) {
-        for (int64_t i = k + 1 + t; i < N; i += DT) {
+        int64_t i = k + 1 + t;
+        for (; i + 3 * DT < N; i += 4 * DT) {  // 4 independent rows in flight per thread
+          double w0 = cj[i], w1 = cj[i + DT], w2 = cj[i + 2 * DT], w3 = cj[i + 3 * DT];
+          if (i == pv) w0 = wk;
+          if (i + DT == pv) w1 = wk;
+          if (i + 2 * DT == pv) w2 = wk;
+          if (i + 3 * DT == pv) w3 = wk;
+          cj[i] = w0 - sc[i - k] * wp;
+          cj[i + DT] = w1 - sc[i + DT - k] * wp;
+          cj[i + 2 * DT] = w2 - sc[i + 2 * DT - k] * wp;
+          cj[i + 3 * DT] = w3 - sc[i + 3 * DT - k] * wp;
+        }
+        for (; i < N; i += DT) {
           const double wi = (i == pv) ? wk : cj[i];
           cj[i] = wi - sc[i - k] * wp;
         }
-      } else if (t == 0 && pv != k) {
-        cj[pv] = wk;
       }
-      if (j == k + 1) {  // the next step's column copy (after its swap and update)
-        __syncthreads();
-        double* nb = a.colbuf + ((k + 1) & 1) * N;
-        for (int64_t i = k + 1 + t; i < N; i += DT) nb[i] = cj[i];
-      }
+    }
+    if (k + 1 < N && (int)((k + 1) % G) == (int)blockIdx.x) {  // the next step's column copy
+      __syncthreads();
+      const double* cn = a.W + (k + 1) * N;
+      double* nb = a.colbuf + ((k + 1) & 1) * N;
+      for (int64_t i = k + 1 + t; i < N; i += DT) nb[i] = cn[i];
     }
     grid.sync();
   }
@@ -277,6 +300,7 @@ int launch_b(rsim_gpu_ctx* c) {
   if (g > gmax) g = gmax;
   if (g > c->sm_count) g = c->sm_count;
   if (g < 1) g = 1;
+  if ((N + g - 1) / g > kMaxOwn) return RSIM_EARG;  // (never at N <= RSIM_DIRECT_MAX on 148 SMs)
   void* args[] = {&a};
   RSIM_CUDA(cudaLaunchCooperativeKernel((void*)k_direct_lu<B>, g, DT, args, smem, c->stream));
   c->launches++;
