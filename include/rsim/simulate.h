@@ -45,6 +45,7 @@ typedef struct {
   int32_t precond;           /* -1 -> case default (RSIM_PREC_*)                 */
   double report_every_days;  /* field dumps every this many days; 0 -> end only */
   int32_t write_fields;      /* 0: no field dumps at all                         */
+  int32_t lin_method;        /* -1 -> case default (RSIM_LIN_*; DIRECT: n_A·b <= RSIM_DIRECT_MAX) */
 } rsim_sim_opts;
 
 typedef struct {

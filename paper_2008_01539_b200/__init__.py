@@ -363,12 +363,13 @@ SOLVERS = {"standard": 0, "localized": 1, "adaptive_dd": 2}
 
 def simulate(config: int, solver: str = "localized", out_dir: str | None = None, *, nx: int = 0, ny: int = 0,
              nz: int = 0, seed: int = 0, n_dfn: int = -1, m: int = 0, eps_p: float = 0.0, n_steps: int = 0,
-             precond: int = -1, report_every_days: float = 0.0, write_fields: bool = True) -> dict:
+             precond: int = -1, report_every_days: float = 0.0, write_fields: bool = True,
+             lin_method: int = -1) -> dict:
     """Case runner (SPEC.md sim_driver_cli run_case, include/rsim/simulate.h): run a seeded
     config on the GPU with the named solver; writes rates.csv / metrics.csv / summary.txt
     (+ field dumps) into out_dir when given.  eps_p in Pa (0 -> case default)."""
     co = A.CaseOpts(config, nx, ny, nz, seed, n_dfn, -1)
-    so = A.SimOpts(SOLVERS[solver], m, eps_p, n_steps, precond, report_every_days, int(write_fields))
+    so = A.SimOpts(SOLVERS[solver], m, eps_p, n_steps, precond, report_every_days, int(write_fields), lin_method)
     mt = A.RunMetrics()
     rc = A.lib().rsim_simulate(C.byref(co), C.byref(so), (out_dir or "").encode(), C.byref(mt))
     _check(rc, "simulate")

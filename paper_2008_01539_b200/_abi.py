@@ -98,6 +98,7 @@ class SimOpts(C.Structure):
     _fields_ = [
         ("solver", C.c_int32), ("m", C.c_int32), ("eps_p", C.c_double), ("n_steps", C.c_int32),
         ("precond", C.c_int32), ("report_every_days", C.c_double), ("write_fields", C.c_int32),
+        ("lin_method", C.c_int32),
     ]
 
 

@@ -197,6 +197,7 @@ int rsim_simulate(const rsim_case_opts* co, const rsim_sim_opts* so, const char*
   if (so->eps_p > 0.0) o.eps_p = o.eps_set = so->eps_p;
   o.m = so->m > 0 ? so->m : (so->solver == 2 ? 4 : o.m);
   if (so->precond >= 0) o.precond = so->precond;
+  if (so->lin_method >= 0) o.lin_method = so->lin_method;
   int r = RSIM_OK;
   const bool files = out_dir && *out_dir;
   if (files) {

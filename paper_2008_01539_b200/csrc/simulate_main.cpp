@@ -3,7 +3,7 @@
 //
 //   simulate --config N [--nx X --ny Y --nz Z --seed S --n-dfn K]
 //            [--solver standard|localized|adaptive_dd] [--m N] [--eps-p PSI]
-//            [--steps K] [--precond bj|neumann1|ilu0] [--out DIR]
+//            [--steps K] [--precond bj|neumann1|ilu0] [--lin bicgstab|gmres|direct] [--out DIR]
 //            [--report-every DAYS] [--no-fields]
 //
 // The reference's case-file grammar was never written (geometry
@@ -22,7 +22,7 @@ static int usage(const char* msg) {
   std::fprintf(stderr,
                "usage: simulate --config N [--nx X --ny Y --nz Z --seed S --n-dfn K] "
                "[--solver standard|localized|adaptive_dd] [--m N] [--eps-p PSI] [--steps K] "
-               "[--precond bj|neumann1|ilu0] [--out DIR] [--report-every DAYS] [--no-fields]\n");
+               "[--precond bj|neumann1|ilu0] [--lin bicgstab|gmres|direct] [--out DIR] [--report-every DAYS] [--no-fields]\n");
   return 2;
 }
 
@@ -35,6 +35,7 @@ int main(int argc, char** argv) {
   std::memset(&so, 0, sizeof(so));
   so.solver = 1;
   so.precond = -1;
+  so.lin_method = -1;
   so.write_fields = 1;
   std::string out;
   for (int k = 1; k < argc; ++k) {
@@ -69,6 +70,13 @@ int main(int argc, char** argv) {
       else if (s == "neumann1") so.precond = RSIM_PREC_NEUMANN1;
       else if (s == "ilu0") so.precond = RSIM_PREC_ILU0;
       else return usage(("unknown preconditioner " + s).c_str());
+      continue;
+    } else if (a == "--lin") {
+      const std::string s = v;
+      if (s == "bicgstab") so.lin_method = RSIM_LIN_BICGSTAB;
+      else if (s == "gmres") so.lin_method = RSIM_LIN_GMRES;
+      else if (s == "direct") so.lin_method = RSIM_LIN_DIRECT;
+      else return usage(("unknown linear solver " + s).c_str());
       continue;
     } else {
       return usage(("unknown option " + a).c_str());

@@ -141,3 +141,31 @@ def test_simulate_c1_outputs_parity_and_acceptance(tmp_path):
         assert res[solver]["total_ratio_MA"] <= std["total_ratio_MA"] / 6
         assert res[solver]["average_ratio_MA_per_iteration"] <= 0.15
     assert res["localized"]["total_iterations"] <= 1.25 * std["total_iterations"]
+
+
+@pytest.mark.gpu
+def test_simulate_direct_solve_cli_matches_oracle(tmp_path):
+    # the case runner with the exact dense-LU solve (--lin direct, SURVEY.md §8f
+    # row 4) on a config-1 grid small enough for every active set (n·b = 900)
+    from oracle import Oracle
+    case = pkg.Case(1, nx=30, ny=30)
+    d = tmp_path / "direct"
+    r = _cli("--config", "1", "--nx", "30", "--ny", "30", "--solver", "localized", "--lin", "direct",
+             "--out", str(d))
+    assert r.returncode == 0, r.stderr
+    summ = _summary(d / "summary.txt")
+    assert summ["status"] == 0 and summ["cuts"] == 0
+    opts = case.solver_opts(lin_method=pkg.LIN_DIRECT)
+    ro = Oracle(case).run_case(1, case.init_state(), case.schedule(), opts)
+    assert ro["iterations"] == summ["total_iterations"] and ro["sum_na"] == summ["sum_nA"]
+    assert ro["lin_iters"] == summ["total_linear_iterations"] == summ["total_iterations"]
+    final_p = np.loadtxt(d / f"pressure_t{summ['simulated_days']:.6g}.txt").ravel()
+    assert np.array_equal(final_p, ro["states"].u / PSI)
+    # and against the default Krylov run: the same states within the Newton tolerance
+    rk = Oracle(case).run_case(1, case.init_state(), case.schedule(), case.solver_opts())
+    assert np.abs(final_p - rk["states"].u / PSI).max() <= 2 * case.solver_opts().eps_p / PSI
+
+
+def test_cli_rejects_unknown_linear_solver():
+    r = _cli("--config", "1", "--lin", "cholesky")
+    assert r.returncode == 2 and "unknown linear solver" in r.stderr
