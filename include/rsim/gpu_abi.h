@@ -80,7 +80,9 @@ int rsim_gpu_estimate_active(rsim_gpu_ctx* ctx, double eps, int32_t m, int32_t s
 
 /* ---- one Newton iteration's kernels ------------------------------------ */
 int rsim_gpu_assemble(rsim_gpu_ctx* ctx);                                   /* K1 (+K2 pattern)  */
-int rsim_gpu_linear_solve(rsim_gpu_ctx* ctx, const rsim_solver_opts* o);    /* K3/K4/K5 persistent */
+/* solve: o->lin_method BICGSTAB / GMRES (persistent Krylov kernels, K3/K4/K5) or
+ * DIRECT (exact dense LU with partial pivoting, n_A*b <= RSIM_DIRECT_MAX, else RSIM_EARG). */
+int rsim_gpu_linear_solve(rsim_gpu_ctx* ctx, const rsim_solver_opts* o);
 int rsim_gpu_update(rsim_gpu_ctx* ctx, double eps);                         /* K6                */
 int rsim_gpu_stats_get(rsim_gpu_ctx* ctx, rsim_gpu_stats* st);              /* sync + D2H scalars */
 
