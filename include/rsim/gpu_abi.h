@@ -1,7 +1,7 @@
 /*
  * rsim/gpu_abi.h — the thin extern "C" boundary between host solver control
  * (C++ rsim::Simulator, include/rsim/simulator.hpp) and the hand-written
- * sm_100a fp64 kernels (paper_2008_01539_b200/csrc/*.cu).
+ * sm_100a fp64 kernels (paper_2008_01539_b200/csrc/ *.cu files).
  *
  * The reference has no FFI: its interface is the SPEC
  * operation list.  Each call below replaces the SPEC operation cited beside

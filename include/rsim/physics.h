@@ -323,6 +323,37 @@ RSIM_HD void substitute(const Fluid& f, double* u, uint8_t& st) {
   }
 }
 
+/* Newton update of one cell: u += w·δu, then variable substitution; returns
+ * the applied pressure change w·δp (the value the support set, the flags and
+ * ‖δp‖∞ see).  w is the per-cell Appleyard chop (DESIGN.md §5 item 11):
+ *   w = min(1, dp_max_rel·|p| / |δp|, ds_max / max(|δS_w|, |δS_g|, |δS_o|))
+ * with δS_g counted only in the saturated state (X = S_g) and δS_o = −(δS_w + δS_g).
+ * Off (w = 1 exactly, so u + 1·δu == u + δu bit for bit) when both limits are 0,
+ * which is every config but the black-oil one. */
+template <int B>
+RSIM_HD double apply_update(const Fluid& f, double* u, uint8_t& st, const double* x) {
+  double w = 1.0;
+  if (f.dp_max_rel > 0.0) {
+    const double a = fabs(x[0]), lim = f.dp_max_rel * fabs(u[0]);
+    if (a > lim) w = lim / a;
+  }
+  if (B >= 2 && f.ds_max > 0.0) {
+    double a = fabs(x[1]);
+    double so = x[1];
+    if (B == 3 && st == RSIM_BO_SAT) {
+      const double g = fabs(x[2]);
+      if (g > a) a = g;
+      so = so + x[2];
+    }
+    so = fabs(so);
+    if (so > a) a = so;
+    if (w * a > f.ds_max) w = f.ds_max / a;
+  }
+  for (int c = 0; c < B; ++c) u[c] = u[c] + w * x[c];
+  substitute<B>(f, u, st);
+  return w * x[0];
+}
+
 }  // namespace phys
 }  // namespace rsim
 

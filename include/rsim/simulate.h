@@ -12,6 +12,11 @@
  *                (surface m^3/day; bhp in psi; one row per committed timestep)
  *   metrics.csv  step, time_days, dt_days, iterations, sum_nA_over_n, sum_nA,
  *                lin_iters, n_subdomains
+ *   iterations.csv  step, attempt, committed, dt_days, iter, n_active,
+ *                active_fraction, lin_iters, subdomain, mode_expand, dp_inf_A,
+ *                dp_inf_B, f_norm2, f_norminf, lin_relres — one row per Newton
+ *                iteration (DD: per local solve) of every attempt, cut ones
+ *                included (committed = 0): the per-iteration active fraction
  *   summary.txt  Tables-2..6-style totals (timesteps, total iterations,
  *                total M_A, average M_A per iteration, cuts, cumulative oil)
  *   pressure_t<days>.txt / satwater_t / satgas_t / phasestatus_t

@@ -65,6 +65,10 @@ typedef struct {
   double rs_b;         /* sm3/sm3, Rs at p_bub;  Rs_sat(p) = rs_b * p / p_bub     */
   double bo_alpha;     /* 1/(sm3/sm3): b_o = exp(c_o (p-p_ref)) / (1 + alpha Rs) */
   double p_gas;        /* Pa: b_g = p / p_gas                                     */
+  /* Newton update limiter (Appleyard chop per cell, DESIGN.md §5 item 11); 0 = off.
+   * The cell's update δu is scaled by w = min(1, dp_max_rel·|p|/|δp|, ds_max/max|δS|). */
+  double dp_max_rel;   /* max |δp| per iteration relative to the cell pressure   */
+  double ds_max;       /* max |δS_w|, |δS_g| per iteration                       */
 } rsim_fluid_params;
 
 /* The immutable connection graph, Cartesian part as face

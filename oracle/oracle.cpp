@@ -596,7 +596,7 @@ static int bicgstab(const Model& M, const rsim_solver_opts& o, double* x, int32_
 // schedule that keeps that order (the GPU: one column owner per CTA, one grid
 // barrier per k) reproduces these bits.  iters = 1, relres = 0 (not formed).
 template <int B>
-static int direct_solve(const Model& M, double* x, int32_t* iters, double* relres) {
+static int direct_solve(Model& M, double* x, int32_t* iters, double* relres) {
   *iters = 1;
   *relres = 0.0;
   const int64_t N = (int64_t)M.nA * B;
@@ -616,11 +616,15 @@ static int direct_solve(const Model& M, double* x, int32_t* iters, double* relre
     double* ck = &W[k * N];
     int64_t pv = k;
     double best = -1.0;
+    bool bad = false;
     for (int64_t i = k; i < N; ++i) {
-      if (!std::isfinite(ck[i])) return RSIM_ENUM;
-      if (std::fabs(ck[i]) > best) { best = std::fabs(ck[i]); pv = i; }
+      if (!std::isfinite(ck[i])) bad = true;
+      else if (std::fabs(ck[i]) > best) { best = std::fabs(ck[i]); pv = i; }
     }
-    if (best == 0.0) return RSIM_ENUM;
+    if (bad || best == 0.0) {  // singular / non-finite pivot column: name its cell
+      M.bad_cell = M.act[k / B];
+      return RSIM_ENUM;
+    }
     piv[k] = (int32_t)pv;
     if (pv != k)
       for (int64_t j = 0; j < N; ++j) std::swap(W[j * N + k], W[j * N + pv]);
@@ -644,8 +648,10 @@ static int direct_solve(const Model& M, double* x, int32_t* iters, double* relre
   return RSIM_OK;
 }
 
-static int linsolve_any(const Model& M, const rsim_solver_opts& o, double* x, int32_t* it, double* rr) {
-  if (o.lin_method == RSIM_LIN_DIRECT) {
+static int linsolve_any(Model& M, const rsim_solver_opts& o, double* x, int32_t* it, double* rr) {
+  // the exact solve covers n_A·b <= RSIM_DIRECT_MAX; larger active sets fall
+  // back to BiCGSTAB (same rule as krylov.cu launch_krylov)
+  if (o.lin_method == RSIM_LIN_DIRECT && (int64_t)M.nA * M.b <= RSIM_DIRECT_MAX) {
     switch (M.b) {
       case 1: return direct_solve<1>(M, x, it, rr);
       case 2: return direct_solve<2>(M, x, it, rr);
@@ -667,10 +673,7 @@ static void update(Model& M, const double* x) {
 #pragma omp parallel for schedule(static)
   for (int32_t l = 0; l < M.nA; ++l) {
     int64_t i = M.act[l];
-    double* ui = &M.u[i * B];
-    for (int c = 0; c < B; ++c) ui[c] = ui[c] + x[(int64_t)l * B + c];
-    phys::substitute<B>(M.fl, ui, M.st[i]);
-    M.dp[i] = x[(int64_t)l * B];
+    M.dp[i] = phys::apply_update<B>(M.fl, &M.u[i * B], M.st[i], &x[(int64_t)l * B]);
   }
 }
 static void update_any(Model& M, const double* x) {
@@ -1129,12 +1132,14 @@ int32_t orc_initial_active(void* h, const double* p_prev, double eps, int32_t m,
   return (int32_t)l.size();
 }
 
-int orc_run_case(void* h, int32_t solver, const double* dts, int32_t nsteps, const rsim_solver_opts* o,
-                 int32_t* total_iters, double* total_ma, int64_t* total_na, int32_t* total_lin, int32_t* n_cuts) {
-  Model& M = *static_cast<Model*>(h);
+// The driver loop over dts from the model's current state;
+// p_prev = pressure at the start of the previous committed step (empty: the
+// first-step rule of initial_active), updated in place.
+static int run_steps(Model& M, int32_t solver, const double* dts, int32_t nsteps, const rsim_solver_opts* o,
+                     std::vector<double>& p_prev, int32_t* total_iters, double* total_ma, int64_t* total_na,
+                     int32_t* total_lin, int32_t* n_cuts) {
   const int B = M.b;
   const int64_t n = M.g.n;
-  std::vector<double> p_prev;  // pressure at the start of the previous step
   std::deque<double> q(dts, dts + nsteps);
   *total_iters = 0; *total_ma = 0.0; *total_na = 0; *total_lin = 0; *n_cuts = 0;
   std::vector<double> u_save;
@@ -1172,6 +1177,31 @@ int orc_run_case(void* h, int32_t solver, const double* dts, int32_t nsteps, con
   }
   delete rep;
   return status;
+}
+
+int orc_run_case(void* h, int32_t solver, const double* dts, int32_t nsteps, const rsim_solver_opts* o,
+                 int32_t* total_iters, double* total_ma, int64_t* total_na, int32_t* total_lin, int32_t* n_cuts) {
+  std::vector<double> p_prev;
+  return run_steps(*static_cast<Model*>(h), solver, dts, nsteps, o, p_prev, total_iters, total_ma, total_na,
+                   total_lin, n_cuts);
+}
+
+// Continue a run one or more timesteps at a time (the bench's reference arm
+// times single timesteps of the workload in sequence).  p_prev_io[n]: in, the
+// pressure at the start of the previous committed step; out, updated.  *has_prev
+// = 0 selects the first-step rule and is set to 1 after a committed step.
+int orc_run_steps(void* h, int32_t solver, const double* dts, int32_t nsteps, const rsim_solver_opts* o,
+                  double* p_prev_io, int32_t* has_prev, int32_t* total_iters, double* total_ma, int64_t* total_na,
+                  int32_t* total_lin, int32_t* n_cuts) {
+  Model& M = *static_cast<Model*>(h);
+  std::vector<double> p_prev;
+  if (*has_prev) p_prev.assign(p_prev_io, p_prev_io + M.g.n);
+  const int r = run_steps(M, solver, dts, nsteps, o, p_prev, total_iters, total_ma, total_na, total_lin, n_cuts);
+  if (!p_prev.empty()) {
+    std::copy(p_prev.begin(), p_prev.end(), p_prev_io);
+    *has_prev = 1;
+  }
+  return r;
 }
 
 double orc_rexp(double x) { return phys::rexp(x); }

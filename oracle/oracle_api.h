@@ -81,6 +81,9 @@ int32_t orc_initial_active(void* h, const double* p_prev, double eps, int32_t m,
 int orc_run_case(void* h, int32_t solver, const double* dts, int32_t nsteps,
                  const rsim_solver_opts* o, int32_t* total_iters, double* total_ma,
                  int64_t* total_na, int32_t* total_lin, int32_t* n_cuts);
+int orc_run_steps(void* h, int32_t solver, const double* dts, int32_t nsteps, const rsim_solver_opts* o,
+                  double* p_prev_io, int32_t* has_prev, int32_t* total_iters, double* total_ma, int64_t* total_na,
+                  int32_t* total_lin, int32_t* n_cuts);
 
 /* Property-suite hooks. */
 double orc_rexp(double x);

@@ -77,8 +77,12 @@ class Case:
     """Seeded synthetic input for one BASELINE.json config (include/rsim/cases.h)."""
 
     def __init__(self, config: int, nx: int = 0, ny: int = 0, nz: int = 0, seed: int = 0, n_dfn: int = -1,
-                 n_steps: int = -1):
-        L = A.lib()
+                 n_steps: int = -1, lib=None):
+        # lib: any library exporting include/rsim/cases.h (librsim.so by default; the
+        # oracle's own liborsim.so links the same host-only generator, so the CPU
+        # reference arm builds its inputs without loading the product library)
+        L = lib if lib is not None else A.lib()
+        self._L = L
         o = A.CaseOpts(config, nx, ny, nz, seed, n_dfn, n_steps)
         self._h = L.rsim_case_create(C.byref(o))
         if not self._h:
@@ -106,7 +110,7 @@ class Case:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            A.lib().rsim_case_destroy(self._h)
+            self._L.rsim_case_destroy(self._h)
             self._h = None
 
     # borrowed arrays (copies, so they outlive nothing)
@@ -136,7 +140,7 @@ class Case:
         return ptr_, self._arr(self.graph.nnc_nbr, m, np.int32), self._arr(self.graph.nnc_t, m, np.float64)
 
     def perm(self, axis: int) -> np.ndarray:
-        return self._arr(A.lib().rsim_case_perm(self._h, axis), self.n, np.float64)
+        return self._arr(self._L.rsim_case_perm(self._h, axis), self.n, np.float64)
 
     def pinned(self) -> np.ndarray:
         return (self.kind == 1) | (self.well_wi > 0)
@@ -144,17 +148,17 @@ class Case:
     def init_state(self) -> CellStates:
         u = np.zeros(self.n * self.b, np.float64)
         st = np.zeros(self.n, np.uint8)
-        A.lib().rsim_case_init_state(self._h, A.ptr(u, C.c_double), A.ptr(st, C.c_uint8))
+        self._L.rsim_case_init_state(self._h, A.ptr(u, C.c_double), A.ptr(st, C.c_uint8))
         return CellStates(u, st)
 
     def schedule(self) -> np.ndarray:
         buf = np.zeros(4096, np.float64)
-        k = A.lib().rsim_case_schedule(self._h, A.ptr(buf, C.c_double), 4096)
+        k = self._L.rsim_case_schedule(self._h, A.ptr(buf, C.c_double), 4096)
         return buf[:k].copy()
 
     def solver_opts(self, **kw) -> SolverOpts:
         o = SolverOpts()
-        A.lib().rsim_case_solver_opts(self._h, C.byref(o))
+        self._L.rsim_case_solver_opts(self._h, C.byref(o))
         for k, v in kw.items():
             setattr(o, k, v)
         return o
@@ -162,7 +166,7 @@ class Case:
     def c5_field(self, target: float, m: int = 2, eps: float = 1e-3):
         dp = np.zeros(self.n, np.float64)
         R = C.c_double(0.0)
-        f = A.lib().rsim_case_c5_field(self._h, target, m, eps, A.ptr(dp, C.c_double), C.byref(R))
+        f = self._L.rsim_case_c5_field(self._h, target, m, eps, A.ptr(dp, C.c_double), C.byref(R))
         return dp, float(f), float(R.value)
 
 

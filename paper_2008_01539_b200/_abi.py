@@ -34,6 +34,7 @@ class FluidParams(C.Structure):
         ("rho_ref", C.c_double * 3), ("c_f", C.c_double * 3), ("mu", C.c_double * 3),
         ("swc", C.c_double), ("sor", C.c_double), ("sgc", C.c_double),
         ("p_bub", C.c_double), ("rs_b", C.c_double), ("bo_alpha", C.c_double), ("p_gas", C.c_double),
+        ("dp_max_rel", C.c_double), ("ds_max", C.c_double),
     ]
 
 

@@ -80,12 +80,14 @@ def build_product(force: bool = False, verbose: bool = False) -> Path:
 
 
 def build_oracle(force: bool = False) -> Path:
+    # the oracle links its own copy of the host-only case generator (csrc/cases.cpp,
+    # include/rsim/cases.h) so the CPU reference arm never loads librsim.so
     out = ORACLE / "_build" / "liborsim.so"
-    deps = [ORACLE / "oracle.cpp", ORACLE / "oracle_api.h"] + _headers()
+    deps = [ORACLE / "oracle.cpp", ORACLE / "oracle_api.h", CSRC / "cases.cpp"] + _headers()
     if force or _stale(out, deps):
         out.parent.mkdir(parents=True, exist_ok=True)
         _run([HOSTCXX, "-O3", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off", "-shared",
-              "-I", str(ROOT / "include"), str(ORACLE / "oracle.cpp"), "-o", str(out)])
+              "-I", str(ROOT / "include"), str(ORACLE / "oracle.cpp"), str(CSRC / "cases.cpp"), "-o", str(out)])
     return out
 
 

@@ -372,8 +372,16 @@ int rsim_gpu_assemble(rsim_gpu_ctx* c) {
   return RSIM_OK;
 }
 
+// C-linkage setter for the host-only translation units (simulate.cpp)
+void rsim_set_error_c(const char* msg) { rsim_set_error(msg); }
+
 int rsim_gpu_linear_solve(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
-  if (!o) return RSIM_EARG;
+  if (!c || !o) return RSIM_EARG;
+  if (o->lin_method < RSIM_LIN_BICGSTAB || o->lin_method > RSIM_LIN_DIRECT || o->precond < RSIM_PREC_BJACOBI ||
+      o->precond > RSIM_PREC_NEUMANN1) {
+    rsim_set_error("rsim_gpu_linear_solve: lin_method / precond out of range");
+    return RSIM_EARG;
+  }
   rsim_phase_begin(c, 2);
   c->counters[2] += 1;
   c->counters[3] += c->nA;

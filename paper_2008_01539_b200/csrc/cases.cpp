@@ -14,6 +14,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <utility>
@@ -317,6 +319,10 @@ void build_c4(rsim_case& c, int n_dfn) {  // 3D black-oil, DFN + stage fractures
   c.p_init = 21e6; c.bhp = 8e6; c.sw_init = 0.2;
   set_fluid_blackoil(c);
   c.fl.p_ref = c.p_init;
+  // Newton update limiter (DESIGN.md §5 item 11); RSIM_C4_LIMITER="dp_rel,ds" overrides (tuning only)
+  c.fl.dp_max_rel = 0.5;
+  c.fl.ds_max = 0.2;
+  if (const char* e = std::getenv("RSIM_C4_LIMITER")) std::sscanf(e, "%lf,%lf", &c.fl.dp_max_rel, &c.fl.ds_max);
   c.n_steps = 20;
   c.eps = 1e-8 * (c.p_init - c.bhp);
   finish(c);

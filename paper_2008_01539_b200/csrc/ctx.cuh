@@ -72,7 +72,8 @@ struct rsim_gpu_ctx {
   bool update_applied = false; // the last Krylov launch already applied the update
   double* gm_V = nullptr;      // GMRES basis (RSIM_GMRES_M + 1 vectors), allocated on first use
   double* gm_part = nullptr;   // GMRES reduction partials
-  double* dn_W = nullptr;      // direct solve: dense N×N (RSIM_DIRECT_MAX²), allocated on first use
+  double* dn_W = nullptr;      // direct solve: dense N×N (N ≤ RSIM_DIRECT_MAX), grown on demand
+  int64_t dn_cap = 0;          // direct solve: N the three dn_* buffers are sized for
   double* dn_colbuf = nullptr; // direct solve: double-buffered pivot column
   int32_t* dn_piv = nullptr;   // direct solve: row interchanges
   struct Ilu {                 // level-scheduled block ILU(0) (ilu.cu)

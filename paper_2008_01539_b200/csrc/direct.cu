@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(DT) k_direct_lu(const DArgs a) {
       for (int q = 1; q < DT / 32; ++q) r = piv_max(r, sp[q]);
       sp[0] = r;
       s_fail = (r.bad || r.v == 0.0) ? 1 : 0;
+      if (s_fail && blockIdx.x == 0) atomicMin(&a.dsc->bad_cell, a.act[k / B]);  // the pivot column's cell
     }
     __syncthreads();
     if (s_fail) { fail = 1; break; }  // every CTA takes the same branch
@@ -271,11 +272,25 @@ template <int B>
 int launch_b(rsim_gpu_ctx* c) {
   const int64_t N = (int64_t)c->nA * B;
   if (N > RSIM_DIRECT_MAX) return RSIM_EARG;
-  if (!c->dn_W) {
-    const int64_t M = RSIM_DIRECT_MAX;
-    RSIM_CUDA(cudaMalloc(&c->dn_W, sizeof(double) * M * M));
-    RSIM_CUDA(cudaMalloc(&c->dn_colbuf, sizeof(double) * 2 * M));
-    RSIM_CUDA(cudaMalloc(&c->dn_piv, sizeof(int32_t) * M));
+  if (N > c->dn_cap) {  // grow on demand, all three buffers or none
+    if (c->dn_W) cudaFree(c->dn_W);
+    if (c->dn_colbuf) cudaFree(c->dn_colbuf);
+    if (c->dn_piv) cudaFree(c->dn_piv);
+    c->dn_W = nullptr; c->dn_colbuf = nullptr; c->dn_piv = nullptr; c->dn_cap = 0;
+    const int64_t M = N < 512 ? 512 : N;
+    cudaError_t e1 = cudaMalloc(&c->dn_W, sizeof(double) * M * M);
+    cudaError_t e2 = cudaMalloc(&c->dn_colbuf, sizeof(double) * 2 * M);
+    cudaError_t e3 = cudaMalloc(&c->dn_piv, sizeof(int32_t) * M);
+    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+      if (c->dn_W) cudaFree(c->dn_W);
+      if (c->dn_colbuf) cudaFree(c->dn_colbuf);
+      if (c->dn_piv) cudaFree(c->dn_piv);
+      c->dn_W = nullptr; c->dn_colbuf = nullptr; c->dn_piv = nullptr;
+      cudaGetLastError();
+      rsim_set_error("direct solve: workspace allocation failed");
+      return RSIM_ECUDA;
+    }
+    c->dn_cap = M;
   }
   DArgs a;
   a.nA = c->nA; a.nslot = c->nslot; a.b = B;

@@ -641,7 +641,9 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
 
 int launch_krylov(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   if (c->nA <= 0) return RSIM_OK;
-  if (o->lin_method == RSIM_LIN_DIRECT) return launch_direct(c, o);  // exact dense LU (direct.cu)
+  // exact dense LU (direct.cu) up to RSIM_DIRECT_MAX unknowns; larger active
+  // sets fall back to BiCGSTAB (the oracle applies the same rule)
+  if (o->lin_method == RSIM_LIN_DIRECT && (int64_t)c->nA * c->b <= RSIM_DIRECT_MAX) return launch_direct(c, o);
   const bool ilu = o->precond == RSIM_PREC_ILU0;
   if (ilu) RSIM_TRY(ilu_prepare(c));
   if (o->lin_method == RSIM_LIN_GMRES) return launch_gmres(c, o);

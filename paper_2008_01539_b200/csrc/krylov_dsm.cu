@@ -685,13 +685,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
       const int64_t i = a.act[l];
       double ui[B];
 #pragma unroll
-      for (int c = 0; c < B; ++c) ui[c] = a.u[i * B + c] + xr[c];
+      for (int c = 0; c < B; ++c) ui[c] = a.u[i * B + c];
       uint8_t stv = a.st[i];
-      rsim::phys::substitute<B>(a.fl, ui, stv);
+      const double d = rsim::phys::apply_update<B>(a.fl, ui, stv, xr);
 #pragma unroll
       for (int c = 0; c < B; ++c) a.u[i * B + c] = ui[c];
       a.st[i] = stv;
-      const double d = xr[0];
       const double ad = fabs(d);
       bad = !isfinite(d);
       a.dp[i] = d;

@@ -64,15 +64,14 @@ __global__ void __launch_bounds__(256) k_update(rsim::phys::Fluid fl, int32_t nA
   bool bad = false;
   if (l < nA) {
     const int64_t i = act[l];
-    double ui[B];
+    double ui[B], xi[B];
 #pragma unroll
-    for (int c = 0; c < B; ++c) ui[c] = u[i * B + c] + x[l * B + c];
+    for (int c = 0; c < B; ++c) { ui[c] = u[i * B + c]; xi[c] = x[l * B + c]; }
     uint8_t s = st[i];
-    rsim::phys::substitute<B>(fl, ui, s);
+    const double d = rsim::phys::apply_update<B>(fl, ui, s, xi);
 #pragma unroll
     for (int c = 0; c < B; ++c) u[i * B + c] = ui[c];
     st[i] = s;
-    const double d = x[l * B];
     const double a = fabs(d);
     bad = !isfinite(d);
     dp[i] = d;

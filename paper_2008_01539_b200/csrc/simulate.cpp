@@ -17,7 +17,9 @@
 #include "rsim/physics.h"
 #include "rsim/simulate.h"
 
-typedef int (*rsim_step_cb)(void* user, double dt, const rsim_newton_report* rep);
+// hook after every timestep attempt: committed = 1 (accepted) or 0 (failed, about to be cut)
+typedef int (*rsim_step_cb)(void* user, double dt, const rsim_newton_report* rep, int committed);
+extern "C" void rsim_set_error_c(const char* msg);
 extern "C" int rsim_internal_run_case_cb(rsim_gpu_ctx* c, int32_t solver, const double* dts, int32_t nsteps,
                                          const rsim_solver_opts* o, int32_t* total_iters, double* total_ma,
                                          int64_t* total_na, int32_t* total_lin, int32_t* n_cuts, rsim_step_cb cb,
@@ -72,6 +74,8 @@ struct Run {
   std::vector<uint8_t> st;
   FILE* rates = nullptr;
   FILE* metrics = nullptr;
+  FILE* iters = nullptr;
+  int attempt = 0;
   rsim_run_metrics* m = nullptr;
 };
 
@@ -124,8 +128,23 @@ int dump_fields(const Run& R) {
   return r;
 }
 
-int on_step(void* user, double dt, const rsim_newton_report* rep) {
+// iterations.csv: one row per Newton iteration / local solve of every attempt
+void log_iterations(Run& R, double dt, const rsim_newton_report* rep, int committed) {
+  if (!R.iters) return;
+  ++R.attempt;
+  for (int32_t k = 0; k < rep->n_records; ++k) {
+    const rsim_iter_record& q = rep->rec[k];
+    std::fprintf(R.iters, "%d,%d,%d,%.10g,%d,%d,%.8g,%d,%d,%d,%.10g,%.10g,%.10g,%.10g,%.6g\n", R.step + 1, R.attempt,
+                 committed, dt / kDay, k, q.n_active, (double)q.n_active / (double)R.n, q.lin_iters, q.subdomain,
+                 q.mode_expand, q.dp_inf_A, q.dp_inf_B, q.f_norm2, q.f_norminf, q.lin_res);
+  }
+}
+
+int on_step(void* user, double dt, const rsim_newton_report* rep, int committed) {
   Run& R = *static_cast<Run*>(user);
+  log_iterations(R, dt, rep, committed);
+  if (!committed) return RSIM_OK;
+  R.attempt = 0;
   R.t += dt;
   ++R.step;
   int r = rsim_gpu_get_state(R.ctx, R.u.data(), R.st.data());
@@ -172,6 +191,10 @@ int rsim_well_rates(const rsim_case* c, const double* u, const uint8_t* st, doub
 
 int rsim_simulate(const rsim_case_opts* co, const rsim_sim_opts* so, const char* out_dir, rsim_run_metrics* out) {
   if (!co || !so || !out || so->solver < 0 || so->solver > 2) return RSIM_EARG;
+  if (so->precond < -1 || so->precond > RSIM_PREC_NEUMANN1 || so->lin_method < -1 || so->lin_method > RSIM_LIN_DIRECT) {
+    rsim_set_error_c("rsim_simulate: precond / lin_method out of range");
+    return RSIM_EARG;
+  }
   std::memset(out, 0, sizeof(*out));
   rsim_case* cs = rsim_case_create(co);
   if (!cs) return RSIM_EARG;
@@ -209,8 +232,12 @@ int rsim_simulate(const rsim_case_opts* co, const rsim_sim_opts* so, const char*
     if (r == RSIM_OK) {
       R.rates = std::fopen((R.dir + "/rates.csv").c_str(), "w");
       R.metrics = std::fopen((R.dir + "/metrics.csv").c_str(), "w");
-      if (!R.rates || !R.metrics) r = RSIM_EARG;
+      R.iters = std::fopen((R.dir + "/iterations.csv").c_str(), "w");
+      if (!R.rates || !R.metrics || !R.iters) r = RSIM_EARG;
     }
+    if (R.iters)
+      std::fprintf(R.iters, "step,attempt,committed,dt_days,iter,n_active,active_fraction,lin_iters,subdomain,"
+                            "mode_expand,dp_inf_A,dp_inf_B,f_norm2,f_norminf,lin_relres\n");
     if (R.rates) std::fprintf(R.rates, "time_days,oil_rate,gas_rate,bhp,water_rate,oil_rate_bbl\n");
     if (R.metrics) std::fprintf(R.metrics, "step,time_days,dt_days,iterations,sum_nA_over_n,sum_nA,lin_iters,n_subdomains\n");
   }
@@ -246,6 +273,7 @@ int rsim_simulate(const rsim_case_opts* co, const rsim_sim_opts* so, const char*
   }
   if (R.rates) std::fclose(R.rates);
   if (R.metrics) std::fclose(R.metrics);
+  if (R.iters) std::fclose(R.iters);
   if (R.ctx) rsim_gpu_destroy(R.ctx);
   rsim_case_destroy(cs);
   return r;

@@ -26,7 +26,8 @@ int rsim_internal_b(const rsim_gpu_ctx* c);
 int32_t rsim_internal_nA(const rsim_gpu_ctx* c);
 extern "C" int rsim_internal_add_row_iters(rsim_gpu_ctx* c, int64_t v);
 extern "C" int rsim_internal_solve_update(rsim_gpu_ctx* c, const rsim_solver_opts* o, double eps);
-typedef int (*rsim_step_cb)(void* user, double dt, const rsim_newton_report* rep);
+// hook after every timestep attempt: committed = 1 (accepted) or 0 (failed, about to be cut)
+typedef int (*rsim_step_cb)(void* user, double dt, const rsim_newton_report* rep, int committed);
 extern "C" int rsim_internal_run_case_cb(rsim_gpu_ctx* c, int32_t solver, const double* dts, int32_t nsteps,
                                          const rsim_solver_opts* o, int32_t* total_iters, double* total_ma,
                                          int64_t* total_na, int32_t* total_lin, int32_t* n_cuts, rsim_step_cb cb,
@@ -267,6 +268,10 @@ int rsim_internal_run_case_cb(rsim_gpu_ctx* c, int32_t solver, const double* dts
     *total_lin += rep->lin_iters_total;
     if (st == RSIM_ECUDA || st == RSIM_EARG) { status_out = st; break; }
     if (st != RSIM_OK) {
+      if (cb) {
+        r = cb(user, dt, rep, 0);
+        if (r != RSIM_OK) break;
+      }
       r = rsim_gpu_restore_state(c);
       if (dt * 0.5 < 1e-4 * 86400.0) { status_out = st; break; }
       ++*n_cuts;
@@ -276,7 +281,7 @@ int rsim_internal_run_case_cb(rsim_gpu_ctx* c, int32_t solver, const double* dts
     }
     r = rsim_internal_commit_step(c);
     first = false;
-    if (r == RSIM_OK && cb) r = cb(user, dt, rep);
+    if (r == RSIM_OK && cb) r = cb(user, dt, rep, 1);
   }
   delete rep;
   if (r != RSIM_OK) return r;

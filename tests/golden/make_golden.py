@@ -18,7 +18,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
-import paper_2008_01539_b200 as pkg  # noqa: E402  (case generation + option structs only)
+import oracle  # noqa: E402  (oracle.Case: the oracle library's own case generator)
 from oracle import Oracle  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -34,6 +34,19 @@ GOLDEN = {
     "c4s_localized": (dict(config=4, nx=24, ny=24, nz=4, n_dfn=8), 1, 5, None),
     "c2s_localized_bj": (dict(config=2, nx=48, ny=48, n_dfn=12), 1, 6, 0),
 }
+
+# Full-size BASELINE configs (the bench workload and the first timesteps of configs 3 and 4):
+# the final state is stored as a digest (sha256 of the u / status bytes) plus every
+# SUBSAMPLE-th cell's unknowns, so the fixture stays small.  Generation takes minutes
+# (config 4: ~20 min on 8 host threads), so only c2 is re-checked on the CPU suite.
+FULL = {
+    "c2_bench_localized": (dict(config=2), 1, 30, None),
+    "c2_bench_dd": (dict(config=2), 2, 30, None),
+    "c3_full_localized": (dict(config=3), 1, 20, None),
+    "c4_full_localized": (dict(config=4), 1, 2, None),
+}
+SUBSAMPLE = 101
+CPU_RECHECK = ("c2_bench_localized", "c2_bench_dd")
 
 REC_FIELDS = ["n_active", "lin_iters", "subdomain", "mode_expand", "dp_inf_A", "dp_inf_B", "f_norm2",
               "f_norminf", "lin_res"]
@@ -71,21 +84,38 @@ def first_step_report(orc, case, solver, opts):
     return out
 
 
+def digest(u: np.ndarray, st: np.ndarray) -> dict:
+    import hashlib
+    b = u.size // st.size
+    idx = np.arange(0, st.size, SUBSAMPLE)
+    return dict(u_sha256=hashlib.sha256(np.ascontiguousarray(u, np.float64).tobytes()).hexdigest(),
+                st_sha256=hashlib.sha256(np.ascontiguousarray(st, np.uint8).tobytes()).hexdigest(),
+                sub_idx=idx, u_sub=u.reshape(-1, b)[idx].copy(), st_sub=st[idx].copy(),
+                p_sum=float(np.sum(u[::b])), n_sat=int(np.sum(st == 1)))
+
+
 def make(name):
-    kw, solver, nsteps, precond = GOLDEN[name]
-    case = pkg.Case(**kw)
+    full = name in FULL
+    kw, solver, nsteps, precond = (FULL if full else GOLDEN)[name]
+    case = oracle.Case(**kw)
     opts = opts_for(case, solver, precond)
     orc = Oracle(case)
     d = first_step_report(orc, case, solver, opts)
     dts = case.schedule()[:nsteps]
     r = orc.run_case(solver, case.init_state(), dts, opts)
     d.update(solver=solver, dts=np.asarray(dts, np.float64), status=r["status"], iterations=r["iterations"],
-             sum_na=r["sum_na"], lin_iters=r["lin_iters"], cuts=r["cuts"], total_ma=r["total_ma"],
-             u=r["states"].u, st=r["states"].status)
+             sum_na=r["sum_na"], lin_iters=r["lin_iters"], cuts=r["cuts"], total_ma=r["total_ma"])
+    if full:
+        d.update(digest(r["states"].u, r["states"].status))
+        if "step0_va" in d:  # the initial active set is re-derived from the case on the GPU side
+            d["step0_va_sha256"] = __import__("hashlib").sha256(d.pop("step0_va").astype(np.int32).tobytes()).hexdigest()
+    else:
+        d.update(u=r["states"].u, st=r["states"].status)
     return d
 
 
 if __name__ == "__main__":
+    oracle.set_threads(len(os.sched_getaffinity(0)))
     for name in (sys.argv[1:] or GOLDEN):
         d = make(name)
         np.savez_compressed(os.path.join(HERE, name + ".npz"), **d)

@@ -104,14 +104,26 @@ def test_oracle_direct_isolated_cells_elementwise():
     assert rc == 0 and np.array_equal(x, rhs)
 
 
-def test_oracle_direct_oversize_is_argument_error():
+def test_oracle_direct_oversize_falls_back_to_bicgstab():
+    # n_A·b > DIRECT_MAX: the exact solve does not apply, BiCGSTAB runs instead (same
+    # rule on the GPU, krylov.cu launch_krylov), so a growing active set never aborts a run
     c = pkg.Case(5, nx=64, ny=66, nz=1)
     assert c.n > pkg.DIRECT_MAX
     o = Oracle(c)
     o.set_state(_state(c, 1), DAY)
     o.assemble(np.arange(c.n, dtype=np.int32))
-    rc, _, _, _ = o.linear_solve(c.n, c.solver_opts(lin_method=pkg.LIN_DIRECT))
-    assert rc == pkg.RSIM_EARG
+    rc, x, it, rr = o.linear_solve(c.n, c.solver_opts(lin_method=pkg.LIN_DIRECT))
+    rc2, x2, it2, rr2 = o.linear_solve(c.n, c.solver_opts(lin_method=pkg.LIN_BICGSTAB))
+    assert rc == rc2 == 0 and it == it2 > 1 and rr == rr2
+    assert np.array_equal(x, x2)
+
+
+def test_runner_rejects_out_of_range_solver_options():
+    # lin_method / precond are range-checked before any GPU work (RSIM_EARG)
+    for kw in (dict(lin_method=3), dict(precond=7)):
+        with pytest.raises(pkg.RsimError) as e:
+            pkg.simulate(1, "localized", nx=20, ny=20, n_steps=1, **kw)
+        assert e.value.code == pkg.RSIM_EARG
 
 
 def test_oracle_localized_newton_with_direct_solve():
@@ -171,6 +183,26 @@ def test_gpu_direct_partial_sets(cfg, nA):
                                  dict(config=2, nx=40, ny=40, n_dfn=6)])
 def test_gpu_direct_full_sets(cfg):
     _gpu_check(pkg.Case(**cfg), None)
+
+
+@pytest.mark.gpu
+def test_gpu_direct_oversize_falls_back_like_the_oracle():
+    case = pkg.Case(5, nx=64, ny=66, nz=1)  # N = 4224 > DIRECT_MAX
+    s = _state(case, 4)
+    orc = Oracle(case)
+    orc.set_state(s, DAY)
+    orc.assemble(np.arange(case.n, dtype=np.int32))
+    opts = case.solver_opts(lin_method=pkg.LIN_DIRECT)
+    rc_o, xo, it_o, _ = orc.linear_solve(case.n, opts)
+    sim = pkg.GpuSimulator(case)
+    sim.set_state(s, DAY)
+    sim.set_active(None)
+    sim.assemble()
+    sim.linear_solve(opts)
+    g = sim.stats()
+    assert rc_o == g.status == 0 and g.lin_iters == it_o > 1
+    assert np.array_equal(sim.solution(case.n), xo)
+    sim.close()
 
 
 @pytest.mark.gpu
