@@ -1,26 +1,32 @@
 #!/usr/bin/env python
-"""bench.py — active-cell Newton iterations/s of the localized FIM solver.
+"""bench.py — active-cell Newton iterations/s of the localized FIM solver on one B200.
 
-Contract (see DESIGN.md §Measurement):
+Contract (see DESIGN.md §7):
   python bench.py --gpus N --steps K --warmup W [--impl reference]
 One JSON line on rank 0.
 
-Workload (config.workload): BASELINE.json configs[1] — 2D two-phase
-oil-water, 256x256, 40-line DFN, 30 backward-Euler timesteps, solved with the
-adaptive-localized Newton (Algorithm 1).  One bench "step" = one full run of
-that case (all 30 timesteps, Newton + Krylov + set estimation) from the same
-seeded initial state.  metric = Σ n_A over all Newton iterations / time.
+Headline workload (config.workload): BASELINE.json configs[3] — config 4, the
+3D three-phase black-oil model with gas liberation, 512x512x16 = 4.2 M cells,
+400 DFN planes + 20 stage fractures, the whole 20-step schedule, adaptive-
+localized Newton (Algorithm 1).  It is the largest full-Newton config that fits
+one GPU (config 5 is a kernel sweep).  One bench "step" = one whole run from the
+seeded initial state.  metric = Σ n_A over every Newton iteration / time.
 
-  value : device-resident run (state already in HBM), CUDA events on the
+  value : device-resident runs (state already in HBM), CUDA events on the
           context stream, L2 flushed (512 MB write) before every step.
   e2e   : the same run through the public C-ABI entry point rsim_run_case
           with pinned host buffers (H2D of the initial state + D2H of the
           final state inside the timed region).
-  roofline : dominant kernel of the workload (per-phase CUDA-event time).
-  c5_sweep : config 5 (1024x1024x32) kernel throughput at several active
-          fractions — compaction (K7), assembly (K1), 50 BiCGSTAB iterations.
-  cpu_baseline : the CPU oracle (oracle/, C++ restatement) on this box's
-          host cores, same workload, bounded sample.
+  roofline : dominant phase of the workload (per-phase CUDA events).
+  parity_vs_oracle : the timed run's totals and final-state sha256 against the
+          oracle fixture of the same run (tests/golden/, make_golden.py), plus a
+          live bit-exact check against the oracle's CPU sample in this run.
+  cpu_baseline : the CPU oracle (oracle/, C++ restatement, OpenMP on every
+          host core) on a bounded sample of the same workload, with the GPU's
+          rate on exactly that sample beside it.
+  per_config : configs 1-3 with the same fields (c3 logs the active fraction
+          of every Newton iteration); c5_sweep : config 5 kernel throughput
+          (K7 / K1 / 50 BiCGSTAB) at 1-100 % active; eos_flash; direct_solve.
 Multi-GPU: the path does not shard across GPUs in this tier (one GPU per
 case) => N independent replicas, max time over ranks.
 """
@@ -147,13 +153,18 @@ def barrier(dist):
 
 
 # --------------------------------------------------------------------------
-# algorithmic bytes: b unknowns/cell, s Cartesian slots
-def bytes_krylov_row_iter(b, s):
-    # 2 SpMVs (s column indices + s blocks + x_l + y write) + 14 vector passes:
-    # (r0,v),(r,r) 2, s update 3, (r0,s),(r0,t) 1, x/r/next-p update 8 (x, p,
-    # s, t, v read; x, r, p written -- the next p is formed in the x/r pass)
-    spmv = s * (8 * b * b + 4) + 16 * b
-    return 2 * spmv + 112 * b
+# algorithmic bytes: b unknowns/cell, s Cartesian slots, nnc NNC entries per row
+def bytes_spmv_row(b, s, nnc=0.0, cols=True):
+    # per row: (s + NNC) column indices (4 B, absent when the columns are structural)
+    # and b×b blocks, own x read + y write (unit diagonal implicit)
+    return (s + nnc) * (8 * b * b + (4 if cols else 0)) + 16 * b
+
+
+def bytes_krylov_row_iter(b, s, nnc=0.0, neumann=False, cols=True):
+    # one BiCGSTAB iteration: 2 SpMVs (4 with the first-order Neumann polynomial:
+    # M⁻¹z = 2z − Âz before each product) + 14 vector passes: (r0,v),(r,r) 2,
+    # s update 3, (r0,s),(r0,t) 1, x/r/next-p update 8 (x, p, s, t, v read; x, r, p written)
+    return (4 if neumann else 2) * bytes_spmv_row(b, s, nnc, cols) + 112 * b
 
 
 def bytes_krylov_row_init(b):
@@ -169,63 +180,317 @@ def bytes_k7(n, nA, m):
     return (19 + 2 * m) * n + 4 * nA
 
 
-WORKLOAD = {"config": 2, "solver": 1, "name": "c2_oilwater_256x256_dfn40_localized_newton_30steps"}
+# The named synthetic grids (BASELINE.json configs[0..3]).  The
+# first solver is the config's measured line; the others are the paper's comparison.
+# Fixtures: tests/golden/<name>.npz, made by tests/golden/make_golden.py from the CPU
+# oracle on exactly these runs (whole schedule, seeded initial state).
+CONFIGS = {
+    1: dict(key="c1", workload="c1_singlephase_100x100_fracture_20steps", solvers=("localized", "standard"),
+            fixtures={"localized": "c1_localized", "standard": "c1_bench_standard"}, cpu="full"),
+    2: dict(key="c2", workload="c2_oilwater_256x256_dfn40_30steps", solvers=("localized", "adaptive_dd", "standard"),
+            fixtures={"localized": "c2_bench_localized", "adaptive_dd": "c2_bench_dd"}, cpu="full"),
+    3: dict(key="c3", workload="c3_hydrofrac_256x256x32_12stages_20steps",
+            solvers=("localized", "adaptive_dd", "standard"),
+            fixtures={"localized": "c3_full_localized", "adaptive_dd": "c3_full_dd"}, cpu="step1"),
+    4: dict(key="c4", workload="c4_blackoil_512x512x16_dfn400_20stages_20steps", solvers=("localized", "adaptive_dd"),
+            fixtures={"localized": "c4_full_localized", "adaptive_dd": "c4_full_dd"}, cpu="newton1"),
+}
+HEADLINE = 4  # the largest full-Newton config that fits one GPU (c5 is a kernel sweep)
+SOLVER_ID = {"standard": 0, "localized": 1, "adaptive_dd": 2}
+GOLDEN = Path(ROOT) / "tests" / "golden"
+CPU_SAMPLES = {
+    "full": "whole runs of the workload (every timestep)",
+    "step1": "the first timestep of the workload (run_case over dts[:1])",
+    "newton1": "the first Newton iteration of the first timestep (newton_localized, max_newton = 1, "
+               "from the seeded state and V_A^init)",
+}
 
 
-def run_reference(args, rank, ws):  # noqa: C901
-    """--impl reference: the CPU oracle (port of SPEC + Algorithms 1-2) on all host threads."""
-    if rank != 0:
-        return
-    import paper_2008_01539_b200 as pkg
+def opts_for(case, solver: str, precond=None):
+    """Solver options of a config (tests/golden/make_golden.py opts_for: m = 4 for DD, App. A)."""
+    o = case.solver_opts()
+    if precond is not None:
+        o.precond = precond
+    if solver == "adaptive_dd":
+        o.m = 4
+    return o
+
+
+def state_digest(u, st) -> dict:
+    import hashlib
+    return {"u_sha256": hashlib.sha256(np.ascontiguousarray(u, np.float64).tobytes()).hexdigest(),
+            "st_sha256": hashlib.sha256(np.ascontiguousarray(st, np.uint8).tobytes()).hexdigest()}
+
+
+def fixture_check(name: str, r: dict, u, st) -> dict:
+    """GPU run totals + final-state digest against the oracle fixture of the same run."""
+    p = GOLDEN / f"{name}.npz"
+    if not p.exists():
+        return {"fixture": name, "match": None, "why": "fixture missing"}
+    g = np.load(p)
+    dg = state_digest(u, st)
+    ref = ({"u_sha256": str(g["u_sha256"]), "st_sha256": str(g["st_sha256"])} if "u_sha256" in g
+           else state_digest(g["u"], g["st"]))
+    bad = [k for k in ("status", "iterations", "sum_na", "lin_iters", "cuts") if int(r[k]) != int(g[k])]
+    if float(r["total_ma"]) != float(g["total_ma"]):
+        bad.append("total_ma")
+    bad += [k for k in ("u_sha256", "st_sha256") if dg[k] != ref[k]]
+    return {"fixture": name, "match": not bad, "mismatch": bad,
+            "checked": "status, Newton/Krylov iterations, Σn_A, cuts, M_A, sha256 of final u and status"}
+
+
+class GpuRun:
+    """One config on one GPU context: device-resident run_case with checkpoint restore."""
+
+    def __init__(self, pkg, cfg: int, solver: str, precond=None):
+        import ctypes as C
+        self.C, self.pkg = C, pkg
+        self.case = pkg.Case(cfg)
+        self.s0 = self.case.init_state()
+        self.dts = np.ascontiguousarray(self.case.schedule(), np.float64)
+        self.solver = solver
+        self.opts = opts_for(self.case, solver, precond)
+        self.sim = pkg.GpuSimulator(self.case)
+        self.L, self.ctx = self.sim.L, self.sim._ctx
+        self.sim.set_state(self.s0, float(self.dts[0]))
+        self.L.rsim_gpu_checkpoint(self.ctx, 0)
+        self.it, self.lin, self.cuts = C.c_int32(), C.c_int32(), C.c_int32()
+        self.ma, self.na = C.c_double(), C.c_int64()
+
+    def totals(self, rc):
+        return {"status": rc, "iterations": self.it.value, "sum_na": self.na.value, "lin_iters": self.lin.value,
+                "cuts": self.cuts.value, "total_ma": self.ma.value}
+
+    def run_dev(self, solver=None, restore=True):
+        from paper_2008_01539_b200 import _abi as A
+        C = self.C
+        sid = SOLVER_ID[solver or self.solver]
+        opts = self.opts if solver in (None, self.solver) else opts_for(self.case, solver)
+        if restore:
+            self.L.rsim_gpu_checkpoint(self.ctx, 1)
+        rc = self.L.rsim_run_case_dev(self.ctx, sid, A.ptr(self.dts, C.c_double), len(self.dts), C.byref(opts),
+                                      C.byref(self.it), C.byref(self.ma), C.byref(self.na), C.byref(self.lin),
+                                      C.byref(self.cuts))
+        if rc != 0:
+            raise RuntimeError(f"run_case_dev failed rc={rc}: {self.L.rsim_gpu_last_error()}")
+        return self.totals(rc)
+
+    def timed_dev(self, solver=None):
+        """One device-resident run, L2 flushed first, CUDA events on the context stream."""
+        C = self.C
+        self.L.rsim_gpu_checkpoint(self.ctx, 1)  # seeded initial state (outside the timed region)
+        self.L.rsim_gpu_flush_l2(self.ctx)
+        self.L.rsim_gpu_mark(self.ctx, 0)
+        r = self.run_dev(solver, restore=False)
+        self.L.rsim_gpu_mark(self.ctx, 1)
+        v = C.c_double()
+        self.L.rsim_gpu_elapsed(self.ctx, 0, 1, C.byref(v))
+        return v.value, r
+
+    def state(self):
+        s = self.sim.get_state()
+        return s.u, s.status
+
+    def close(self):
+        self.sim.close()
+
+
+def measure_config(pkg, cfg: int, steps: int, warmup: int, hbm: float, peak_kind: str, dist=None, lr=0,
+                   e2e_runs: int | None = None, compare: bool = True) -> dict:
+    """value / e2e / roofline / launches / clocks / parity of one config's main solver;
+    the paper's solver comparison on the same workload."""
+    from paper_2008_01539_b200 import _abi as A
+    import ctypes as C
+    spec = CONFIGS[cfg]
+    main = spec["solvers"][0]
+    R = GpuRun(pkg, cfg, main)
+    L, ctx, case = R.L, R.ctx, R.case
+    b, D = case.b, (3 if case.nz > 1 else 2)
+    s = 2 * D
+    for _ in range(warmup):
+        R.run_dev()
+    # ---- device-resident timed region (phase timers off: no extra events)
+    L.rsim_gpu_timers(ctx, 0, None, None)
+    cnt = np.zeros(5, np.int64)
+    barrier(dist)
+    tot_ms, tot_na = 0.0, 0
+    l0, l1 = C.c_int32(), C.c_int32()
+    with Clocks(lr) as clk:
+        L.rsim_gpu_timers(ctx, -1, None, C.byref(l0))
+        for _ in range(steps):
+            ms, r = R.timed_dev()
+            tot_ms += ms
+            tot_na += r["sum_na"]
+        L.rsim_gpu_timers(ctx, -1, None, C.byref(l1))
+    barrier(dist)
+    u_end, st_end = R.state()
+    t_max = dist_max(dist, tot_ms)
+    value = dist_sum(dist, float(tot_na)) / (t_max / 1e3)
+    out = {"workload": spec["workload"], "solver": main, "n_cells": case.n, "b": b, "timesteps": len(R.dts),
+           "value": value, "unit": "active-cell iters/s", "ms_per_step": t_max / steps, "steps": steps,
+           "warmup": warmup, "gpu_launches": int(l1.value - l0.value), "clocks": clk.summary(),
+           "run": dict(r),
+           "active_fraction_mean": r["total_ma"] / max(1, r["iterations"])}
+    parity = {main: fixture_check(spec["fixtures"][main], r, u_end, st_end)}
+    # ---- phase breakdown (separate run with per-phase CUDA events; not part of `value`)
+    L.rsim_gpu_timers(ctx, 1, None, None)
+    L.rsim_gpu_checkpoint(ctx, 1)
+    L.rsim_gpu_flush_l2(ctx)
+    L.rsim_gpu_counters(ctx, None, 1)
+    R.run_dev(restore=False)
+    phase_ms = np.zeros(4)
+    L.rsim_gpu_timers(ctx, 0, A.ptr(phase_ms, C.c_double), None)
+    L.rsim_gpu_counters(ctx, A.ptr(cnt, C.c_int64), 1)  # work counters of this one run
+    # ---- e2e through the public C-ABI entry point with pinned host buffers
+    import torch
+    u_pin = torch.empty(len(R.s0.u), dtype=torch.float64, pin_memory=True).numpy()
+    st_pin = torch.empty(len(R.s0.status), dtype=torch.uint8, pin_memory=True).numpy()
+    ne = steps if e2e_runs is None else max(1, min(steps, e2e_runs))
+    e2e_t, e2e_na = 0.0, 0
+    for k in range(ne + 1):
+        u_pin[:] = R.s0.u
+        st_pin[:] = R.s0.status
+        L.rsim_gpu_flush_l2(ctx)
+        L.rsim_gpu_stats_get(ctx, C.byref(pkg.GpuStats()))
+        t0 = time.perf_counter()
+        rc = L.rsim_run_case(ctx, SOLVER_ID[main], A.ptr(u_pin, C.c_double), A.ptr(st_pin, C.c_uint8),
+                             A.ptr(R.dts, C.c_double), len(R.dts), C.byref(R.opts), C.byref(R.it), C.byref(R.ma),
+                             C.byref(R.na), C.byref(R.lin), C.byref(R.cuts))
+        dt_ = time.perf_counter() - t0
+        if rc != 0:
+            raise RuntimeError("rsim_run_case failed")
+        if k > 0:
+            e2e_t += dt_
+            e2e_na += R.na.value
+    e2e_t = dist_max(dist, e2e_t)
+    out["e2e"] = {"value": dist_sum(dist, float(e2e_na)) / e2e_t, "unit": "active-cell iters/s",
+                  "h2d_bytes_per_step": int(R.s0.u.nbytes + R.s0.status.nbytes + R.dts.nbytes),
+                  "d2h_bytes_per_step": int(R.s0.u.nbytes + R.s0.status.nbytes), "runs": ne,
+                  "api": "rsim_run_case (C-ABI), pinned host buffers"}
+    parity[main]["e2e_state_match"] = state_digest(u_pin, st_pin) == state_digest(u_end, st_end)
+    # ---- roofline of the dominant phase (per-phase CUDA-event time, algorithmic bytes)
+    names = ["set_estimation_K7", "assembly_K1", "krylov_bicgstab_K3K5", "update_K6"]
+    dom = int(np.argmax(phase_ms))
+    asm_rows, row_iters, solves, krylov_rows, k7_updates = (int(x) for x in cnt)
+    nnc = case.n_nnc * 2 / case.n  # NNC entries per row (each NNC is stored in both rows)
+    neu = R.opts.precond == pkg.PREC_NEUMANN1
+    if dom == 2:
+        per = bytes_krylov_row_iter(b, s, nnc, neu)
+        alg = row_iters * per + krylov_rows * bytes_krylov_row_init(b)
+        units = f"{per:.1f} B per row-iteration ({'Neumann-1: 4' if neu else '2'} SpMVs) + " \
+                f"{bytes_krylov_row_init(b)} B per row init"
+        launches_dom = solves
+    elif dom == 1:
+        per = bytes_assembly_row(b, D, s, nnc)
+        alg, units, launches_dom = asm_rows * per, f"{per:.1f} B per active row", max(1, r["iterations"])
+    else:
+        alg = k7_updates * bytes_k7(case.n, 0, R.opts.m)
+        units, launches_dom = f"{bytes_k7(case.n, 0, R.opts.m)} B per full-grid set update", max(1, k7_updates)
+    achieved = alg / (phase_ms[dom] / 1e3) / 1e9
+    out["roofline"] = {"kernel": names[dom], "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                       "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": None,
+                       "traffic_note": "ncu DRAM bytes of this kernel: profiles/ (not measurable inside this run)",
+                       "algorithmic_bytes_per_launch": alg / max(1, launches_dom), "algorithmic_bytes": units,
+                       "phase_ms_per_run": {k: float(v) for k, v in zip(names, phase_ms)},
+                       "krylov_solves_per_run": solves, "krylov_row_iters_per_run": row_iters}
+    # ---- the paper's comparison on the same workload (one timed device-resident run each)
+    if compare:
+        cmp = {main: {"ms_per_run": t_max / steps, **out["run"]}}
+        for sv in spec["solvers"][1:]:
+            if case.n <= 1 << 20:
+                R.run_dev(sv)  # warm (small configs; the big ones are warm from the main solver)
+            ms, rr = R.timed_dev(sv)
+            cmp[sv] = {"ms_per_run": ms, **rr}
+            if sv in spec["fixtures"]:
+                u2, st2 = R.state()
+                parity[sv] = fixture_check(spec["fixtures"][sv], rr, u2, st2)
+        out["solver_comparison"] = cmp
+    out["parity_vs_oracle"] = parity
+    out["_R"] = R
+    out["_final"] = (u_end, st_end)
+    return out
+
+
+def cpu_sample(cfg: int, threads: int, budget_s: float = 10.0, max_runs: int = 30) -> dict:
+    """The CPU oracle (oracle/, OpenMP) on a bounded sample of config cfg's workload.
+    Returns the rate and the sample's result (for the live GPU-vs-oracle check)."""
     import oracle
     from oracle import Oracle
-    cores = len(os.sched_getaffinity(0))
-    oracle.set_threads(cores)
-    case = pkg.Case(WORKLOAD["config"])
-    s0 = case.init_state()
-    dts = case.schedule()
-    opts = case.solver_opts()
-    if args.precond is not None:
-        opts.precond = args.precond
+    oracle.set_threads(threads)
+    spec = CONFIGS[cfg]
+    main = spec["solvers"][0]
+    case = oracle.Case(cfg)
+    s0, dts = case.init_state(), case.schedule()
+    opts = opts_for(case, main)
     orc = Oracle(case)
-    for _ in range(args.warmup):
-        orc.run_case(WORKLOAD["solver"], s0, dts, opts)
-    tot_na, tot_t = 0, 0.0
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        r = orc.run_case(WORKLOAD["solver"], s0, dts, opts)
-        tot_t += time.perf_counter() - t0
-        tot_na += r["sum_na"]
-    v = tot_na / tot_t
-    line = {
-        "metric": "active-cell Newton iters/s", "value": v, "unit": "active-cell iters/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "impl": "reference",
-        "config": {"workload": WORKLOAD["name"], "n_cells": case.n, "timesteps": len(dts), "parallelism": "replicas"},
-        "cpu_baseline": {"value": v, "unit": "active-cell iters/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} full runs of the workload (oracle/, OpenMP {cores} threads)"},
-        "e2e": {"value": v, "unit": "active-cell iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+    kind = spec["cpu"]
+    tot_na, tot_t, runs, last = 0, 0.0, 0, None
+    while runs < 1 or (tot_t < budget_s and runs < max_runs):
+        if kind == "newton1":
+            opts.max_newton = 1
+            va = orc.initial_active(None, opts.eps_set, opts.m)
+            t0 = time.perf_counter()
+            _, rep, rc = orc.newton_localized(s0, float(dts[0]), va, opts.m, opts.eps_set, opts)
+            dt = time.perf_counter() - t0
+            na = rep.sum_na
+            last = {"records": rep.records(), "rc": rc}
+        else:
+            d = dts if kind == "full" else dts[:1]
+            t0 = time.perf_counter()
+            r = orc.run_case(SOLVER_ID[main], s0, d, opts)
+            dt = time.perf_counter() - t0
+            na = r["sum_na"]
+            last = r
+        tot_na, tot_t, runs = tot_na + na, tot_t + dt, runs + 1
+        if kind != "full":
+            break
+    return {"value": tot_na / tot_t, "unit": "active-cell iters/s", "cores": threads, "kind": "port",
+            "sample": f"{runs} x {CPU_SAMPLES[kind]} ({tot_t:.1f} s, oracle/ OpenMP {threads} threads)",
+            "model": _cpu_model(), "_last": last, "_kind": kind, "_seconds": tot_t}
 
 
-def cpu_baseline(case, s0, dts, opts):
-    import oracle
-    from oracle import Oracle
-    cores = len(os.sched_getaffinity(0))
-    oracle.set_threads(cores)
-    orc = Oracle(case)
-    tot_na, tot_t, runs = 0, 0.0, 0
-    while tot_t < 10.0 and runs < 30:
-        t0 = time.perf_counter()
-        r = orc.run_case(WORKLOAD["solver"], s0, dts, opts)
-        tot_t += time.perf_counter() - t0
-        tot_na += r["sum_na"]
-        runs += 1
-    return {"value": tot_na / tot_t, "unit": "active-cell iters/s", "cores": cores, "kind": "port",
-            "sample": f"{runs} full runs of the workload ({tot_t:.1f} s, oracle/ OpenMP {cores} threads)",
-            "model": _cpu_model()}
+def gpu_same_sample(R: GpuRun, kind: str, cpu_last, final=None) -> dict:
+    """The GPU on exactly the CPU sample (rate like for like) + live bit-exact check."""
+    C = R.C
+    if kind == "full":
+        u, st = final  # final state of the timed runs (the whole workload)
+        ok = state_digest(u, st) == state_digest(cpu_last["states"].u, cpu_last["states"].status)
+        return {"live_oracle_match": bool(ok), "checked": "sha256 of the final u / status after the whole run"}
+    if kind == "step1":
+        R.L.rsim_gpu_checkpoint(R.ctx, 1)
+        s0 = R.s0
+        R.L.rsim_gpu_mark(R.ctx, 2)
+        r = R.sim.run_case(SOLVER_ID[R.solver], s0, R.dts[:1], R.opts)
+        R.L.rsim_gpu_mark(R.ctx, 3)
+        v = C.c_double()
+        R.L.rsim_gpu_elapsed(R.ctx, 2, 3, C.byref(v))
+        ok = all(r[k] == cpu_last[k] for k in ("status", "iterations", "sum_na", "lin_iters", "cuts")) and \
+            np.array_equal(r["states"].u, cpu_last["states"].u)
+        return {"value": r["sum_na"] / (v.value / 1e3), "ms": v.value, "live_oracle_match": bool(ok),
+                "checked": "totals and final u of the first timestep, bit for bit"}
+    # newton1: the first Newton iteration from the seeded state
+    opts = opts_for(R.case, R.solver)
+    opts.max_newton = 1
+    R.sim.set_state(R.s0, float(R.dts[0]))
+    R.sim.initial_active(True, opts.eps_set, opts.m)
+    va = R.sim.active()
+    R.L.rsim_gpu_mark(R.ctx, 2)
+    _, rep = R.sim.newton_localized(R.s0, float(R.dts[0]), va, opts.m, opts.eps_set, opts)
+    R.L.rsim_gpu_mark(R.ctx, 3)
+    v = C.c_double()
+    R.L.rsim_gpu_elapsed(R.ctx, 2, 3, C.byref(v))
+    g, o = rep.records(), cpu_last["records"]
+    ok = len(g) == len(o) and all(a == b for a, b in zip(g, o))
+    return {"value": rep.sum_na / (v.value / 1e3), "ms": v.value, "live_oracle_match": bool(ok),
+            "checked": "per-iteration records (n_A, Krylov iterations, ‖δp‖∞, ‖F‖₂, ‖F‖∞, Krylov residual), bit for bit"}
+
+
+def cpu_serial(cfg: int) -> dict | None:
+    """One thread (the SPEC's serial oracle) on one whole run: c1, c2 only."""
+    if CONFIGS[cfg]["cpu"] != "full":
+        return None
+    r = cpu_sample(cfg, 1, budget_s=0.0, max_runs=1)
+    return {"value": r["value"], "unit": r["unit"], "cores": 1, "sample": r["sample"]}
 
 
 def _cpu_model():
@@ -234,9 +499,55 @@ def _cpu_model():
             for line in f:
                 if line.startswith("model name"):
                     return line.split(":", 1)[1].strip()
-    except Exception:
+    except OSError:
         pass
     return None
+
+
+def strip(d: dict) -> dict:
+    return {k: v for k, v in d.items() if not k.startswith("_")}
+
+
+def run_reference(args, rank, ws):
+    """--impl reference: the CPU oracle (port of SPEC + Algorithms 1-2, oracle/) on all host
+    threads, on the headline config's bounded sample; never loads the product library."""
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0))
+    spec = CONFIGS[HEADLINE]
+    vals, secs, sample = [], 0.0, ""
+    for k in range(args.warmup + args.steps):
+        r = cpu_sample(HEADLINE, cores, budget_s=0.0, max_runs=1)
+        if k >= args.warmup:
+            vals.append(r["value"])
+            secs += r["_seconds"]
+            sample = r["sample"]
+    v = len(vals) / sum(1.0 / x for x in vals)  # Σ n_A / Σ t over the timed samples (equal n_A per sample)
+    loaded = sorted({ln.split()[-1] for ln in open("/proc/self/maps") if "rsim" in ln and ".so" in ln})
+    c = cpu_case(HEADLINE)
+    line = {
+        "metric": "active-cell Newton iters/s", "value": v, "unit": "active-cell iters/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, SURVEY.md App. A)", "impl": "reference",
+        "config": config_key(HEADLINE, c.n, len(c.schedule()), ws),
+        "cpu_baseline": {"value": v, "unit": "active-cell iters/s", "cores": cores, "kind": "port",
+                         "sample": f"each step: {sample}"},
+        "e2e": {"value": v, "unit": "active-cell iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "native_libs_loaded": loaded,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_case(cfg: int):
+    import oracle  # the oracle library's own linked case generator (no product library)
+    return oracle.Case(cfg)
+
+
+def config_key(cfg: int, n: int, nsteps: int, ws: int) -> dict:
+    """The `config` object: identical in both arms (workload identity only)."""
+    return {"workload": CONFIGS[cfg]["workload"], "n_cells": n, "timesteps": nsteps,
+            "solver": CONFIGS[cfg]["solvers"][0], "parallelism": f"replicas x{ws}"}
 
 
 def c5_sweep(pkg, fractions, reps, hbm, ilu_fracs=()):
@@ -293,7 +604,8 @@ def c5_sweep(pkg, fractions, reps, hbm, ilu_fracs=()):
             ilu = v.value
         by7 = bytes_k7(n, nA, 2)
         by1 = nA * bytes_assembly_row(b, 3, s)
-        byk = nA * (50 * bytes_krylov_row_iter(b, s) + bytes_krylov_row_init(b))
+        # full set: the ELL columns are structural (computed from the cell coordinates, not loaded)
+        byk = nA * (50 * bytes_krylov_row_iter(b, s, cols=nA < n) + bytes_krylov_row_init(b))
         out.append({
             "target_fraction": frac, "active_fraction": nA / n, "n_active": nA, "lin_iters": stt.lin_iters,
             "k7_ms": m["k7"], "k7_gbs": by7 / m["k7"] / 1e6,
@@ -439,17 +751,16 @@ def eos_flash_line(pkg, n, reps, no_cpu):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--configs", default="1,2,3", help="per-config lines besides the headline ('' to skip)")
     ap.add_argument("--c5", default="0.01,0.05,0.2,0.5,1.0", help="config-5 active fractions ('' to skip)")
     ap.add_argument("--c5-ilu", default="0.05", help="fractions that also get the ILU(0) row ('' to skip)")
     ap.add_argument("--c5-reps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--direct", type=int, default=1, help="time the exact dense-LU solve at N = 2048 / 4096 (0 to skip)")
     ap.add_argument("--flash-cells", type=int, default=1 << 22, help="PR flash bench cells (0 to skip)")
-    ap.add_argument("--precond", type=int, default=None,
-                    help="0 block-Jacobi, 2 block-Jacobi + first-order Neumann polynomial (default: case default)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, ws, lr = dist_env()
@@ -458,174 +769,89 @@ def main():
 
     dist = init_dist(ws, lr)
     import paper_2008_01539_b200 as pkg
-    import ctypes as C
-    from paper_2008_01539_b200 import _abi as A
     pkg._abi.lib().rsim_gpu_set_device(lr)
     hbm, peak_kind = peaks()
+    cores = len(os.sched_getaffinity(0))
 
-    case = pkg.Case(WORKLOAD["config"])
-    s0 = case.init_state()
-    dts = case.schedule()
-    opts = case.solver_opts()
-    if args.precond is not None:
-        opts.precond = args.precond
-    sim = pkg.GpuSimulator(case)
-    L, ctx = sim.L, sim._ctx
-    b, D = case.b, (3 if case.nz > 1 else 2)
-    s = 2 * D
-    sim.set_state(s0, float(dts[0]))
-    L.rsim_gpu_checkpoint(ctx, 0)
-    d = np.ascontiguousarray(dts, np.float64)
-    it, lin, cuts = C.c_int32(), C.c_int32(), C.c_int32()
-    ma, na = C.c_double(), C.c_int64()
-
-    def run_dev():
-        rc = L.rsim_run_case_dev(ctx, WORKLOAD["solver"], A.ptr(d, C.c_double), len(d), C.byref(opts), C.byref(it),
-                                 C.byref(ma), C.byref(na), C.byref(lin), C.byref(cuts))
-        if rc != 0:
-            raise RuntimeError(f"run_case_dev failed rc={rc}: {L.rsim_gpu_last_error()}")
-        return na.value
-
-    for _ in range(args.warmup):
-        L.rsim_gpu_checkpoint(ctx, 1)
-        run_dev()
-    # ---- device-resident timed region (phase timers OFF: no extra events)
-    L.rsim_gpu_timers(ctx, 0, None, None)
-    cnt = np.zeros(5, np.int64)
-    L.rsim_gpu_counters(ctx, A.ptr(cnt, C.c_int64), 1)
-    launches0 = C.c_int32()
-    barrier(dist)
-    L.rsim_gpu_stats_get(ctx, C.byref(pkg.GpuStats()))
-    tot_ms, tot_na = 0.0, 0
-    with Clocks(lr) as clk:
-        L.rsim_gpu_timers(ctx, -1, None, C.byref(launches0))
-        for _ in range(args.steps):
-            L.rsim_gpu_checkpoint(ctx, 1)
-            L.rsim_gpu_flush_l2(ctx)
-            L.rsim_gpu_mark(ctx, 0)
-            tot_na += run_dev()
-            L.rsim_gpu_mark(ctx, 1)
-            v = C.c_double()
-            L.rsim_gpu_elapsed(ctx, 0, 1, C.byref(v))
-            tot_ms += v.value
-        launches1 = C.c_int32()
-        L.rsim_gpu_timers(ctx, -1, None, C.byref(launches1))
-    barrier(dist)
-    L.rsim_gpu_counters(ctx, A.ptr(cnt, C.c_int64), 1)
-    n_iters, n_lin, iters_per_run = it.value, lin.value, it.value
-    t_max = dist_max(dist, tot_ms)
-    na_all = dist_sum(dist, float(tot_na))
-    value = na_all / (t_max / 1e3)
-    n_launch = int(launches1.value - launches0.value)
-    # ---- phase breakdown (separate pass with per-phase CUDA events; not part of `value`)
-    L.rsim_gpu_timers(ctx, 1, None, None)
-    L.rsim_gpu_checkpoint(ctx, 1)
-    L.rsim_gpu_flush_l2(ctx)
-    run_dev()
-    phase_ms = np.zeros(4)
-    L.rsim_gpu_timers(ctx, 0, A.ptr(phase_ms, C.c_double), None)
-    phase_ms *= args.steps  # per-run breakdown scaled to the timed steps
-
-    # ---- e2e through the public C-ABI entry point with pinned host buffers
-    import torch
-    u_pin = torch.empty(len(s0.u), dtype=torch.float64, pin_memory=True).numpy()
-    st_pin = torch.empty(len(s0.status), dtype=torch.uint8, pin_memory=True).numpy()
-    e2e_t, e2e_na = 0.0, 0
-    for k in range(args.steps + 1):
-        u_pin[:] = s0.u
-        st_pin[:] = s0.status
-        L.rsim_gpu_flush_l2(ctx)
-        L.rsim_gpu_stats_get(ctx, C.byref(pkg.GpuStats()))
-        t0 = time.perf_counter()
-        rc = L.rsim_run_case(ctx, WORKLOAD["solver"], A.ptr(u_pin, C.c_double), A.ptr(st_pin, C.c_uint8),
-                             A.ptr(d, C.c_double), len(d), C.byref(opts), C.byref(it), C.byref(ma), C.byref(na),
-                             C.byref(lin), C.byref(cuts))
-        dt_ = time.perf_counter() - t0
-        if rc != 0:
-            raise RuntimeError("rsim_run_case failed")
-        if k > 0:
-            e2e_t += dt_
-            e2e_na += na.value
-    e2e_t = dist_max(dist, e2e_t)
-    e2e_v = dist_sum(dist, float(e2e_na)) / e2e_t
-    h2d = s0.u.nbytes + s0.status.nbytes + d.nbytes
-    d2h = s0.u.nbytes + s0.status.nbytes
-
-    # ---- roofline of the dominant kernel (per-phase CUDA-event time)
-    names = ["set_estimation_K7", "assembly_K1", "krylov_bicgstab_K3K5", "update_K6"]
-    dom = int(np.argmax(phase_ms))
-    row_iters, solves, krylov_rows, asm_rows = int(cnt[1]), int(cnt[2]), int(cnt[3]), int(cnt[0])
-    nnc_per_row = case.n_nnc / case.n
-    if dom == 2:
-        alg = row_iters * bytes_krylov_row_iter(b, s) + krylov_rows * bytes_krylov_row_init(b)
-        per_launch_units = f"{bytes_krylov_row_iter(b, s)} B per row-iteration + {bytes_krylov_row_init(b)} B per row init"
-    elif dom == 1:
-        alg = asm_rows * bytes_assembly_row(b, D, s, nnc_per_row)
-        per_launch_units = f"{bytes_assembly_row(b, D, s, nnc_per_row):.1f} B per active row"
-    else:
-        alg = int(cnt[4]) * bytes_k7(case.n, 0, 2)
-        per_launch_units = f"{bytes_k7(case.n, 0, 2)} B per full-grid set update"
-    achieved = alg / (phase_ms[dom] / 1e3) / 1e9
-    # measured DRAM traffic per launch of that kernel (ncu --set full, committed
-    # under profiles/): compare with the algorithmic bytes per launch
-    kern = {0: "k_scatter_rg", 1: "k_assemble", 2: "k_krylov_dsm", 3: "k_update"}[dom]
-    traffic = None
-    try:
-        tj = json.load(open(Path(__file__).resolve().parent / "profiles" / "r01_traffic.json"))
-        traffic = tj["dram_bytes_per_launch"].get(kern)
-    except (OSError, ValueError, KeyError):
-        pass
-    launches_dom = solves if dom == 2 else max(1, iters_per_run * args.steps)
-    roof = {"kernel": names[dom], "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": traffic,
-            "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/r01_ncu_summary.md)",
-            "algorithmic_bytes_per_launch": alg / launches_dom,
-            "algorithmic_bytes": per_launch_units,
-            "phase_ms_per_step": {k: float(v) / args.steps for k, v in zip(names, phase_ms)},
-            "krylov_solves_per_step": solves / args.steps, "krylov_row_iters_per_step": row_iters / args.steps}
-
+    # ---- headline: the largest full-Newton config (c4), whole 20-step schedule, localized Newton
+    h = measure_config(pkg, HEADLINE, args.steps, args.warmup, hbm, peak_kind, dist, lr, e2e_runs=2,
+                       compare=(rank == 0 and ws == 1))
+    R = h.pop("_R")
     line = {
-        "metric": "active-cell Newton iters/s", "value": value, "unit": "active-cell iters/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+        "metric": "active-cell Newton iters/s", "value": h["value"], "unit": "active-cell iters/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": h["ms_per_step"], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md App. A)",
-        "config": {"workload": WORKLOAD["name"], "n_cells": case.n, "timesteps": len(dts),
-                   "newton_iters_per_run": iters_per_run, "krylov_iters_per_run": n_lin,
-                   "sum_nA_per_run": tot_na // args.steps, "l2": "flushed (512 MB write) before every step",
-                   "parallelism": f"replicas x{ws}"},
-        "e2e": {"value": e2e_v, "unit": "active-cell iters/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "api": "rsim_run_case (C-ABI), pinned host buffers"},
-        "gpu_launches": n_launch,
-        "roofline": roof,
-        "clocks": clk.summary(),
+        "config": config_key(HEADLINE, R.case.n, len(R.dts), ws),
+        "e2e": h["e2e"], "gpu_launches": h["gpu_launches"], "roofline": h["roofline"], "clocks": h["clocks"],
+        "workload_detail": {"b": h["b"], "run": h["run"], "active_fraction_mean": h["active_fraction_mean"],
+                            "step": "one whole run of the schedule from the seeded initial state",
+                            "l2": "flushed (512 MB write) before every step"},
+        "parity_vs_oracle": h["parity_vs_oracle"],
     }
-    if rank == 0:  # the paper's comparison on the same workload (one timed run each, after the timed region)
-        cmp = {}
-        for sv, nm in ((0, "standard"), (1, "localized"), (2, "adaptive_dd")):
-            sim.run_case(sv, s0, dts, opts)
-            sim.L.rsim_gpu_mark(sim._ctx, 20)
-            r = sim.run_case(sv, s0, dts, opts)
-            sim.L.rsim_gpu_mark(sim._ctx, 21)
-            ms = C.c_double()
-            sim.L.rsim_gpu_elapsed(sim._ctx, 20, 21, C.byref(ms))
-            cmp[nm] = {"ms_per_run": ms.value, "newton_iters": r["iterations"], "krylov_iters": r["lin_iters"],
-                       "sum_nA": r["sum_na"], "total_MA": r["total_ma"], "status": r["status"]}
-        line["solver_comparison"] = cmp
-    sim.close()
-    if rank == 0 and args.c5:
+    if "solver_comparison" in h:
+        line["solver_comparison"] = h["solver_comparison"]
+    final = h.pop("_final")
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cb = cpu_sample(HEADLINE, cores)
+        same = gpu_same_sample(R, cb["_kind"], cb["_last"], final)
+        line["cpu_baseline"] = strip(cb)
+        line["cpu_baseline"]["gpu_same_sample"] = same
+        line["parity_vs_oracle"]["live_sample"] = same.get("live_oracle_match")
+    R.close()
+
+    # ---- the other named grids (c1..c3), each with its own value / e2e / roofline / CPU baseline
+    if rank == 0 and ws == 1 and args.configs:
+        per = {}
+        for cfg in (int(x) for x in args.configs.split(",") if x.strip()):
+            small = cfg in (1, 2)
+            m = measure_config(pkg, cfg, args.steps if not small else max(args.steps, 5), 3 if small else 1,
+                               hbm, peak_kind, None, lr, e2e_runs=None if small else 2)
+            Rc = m.pop("_R")
+            if not args.no_cpu:
+                cb = cpu_sample(cfg, cores)
+                same = gpu_same_sample(Rc, cb["_kind"], cb["_last"], m["_final"])
+                m["cpu_baseline"] = strip(cb)
+                m["cpu_baseline"]["gpu_same_sample"] = same
+                m["parity_vs_oracle"]["live_sample"] = same.get("live_oracle_match")
+                ser = cpu_serial(cfg)
+                if ser:
+                    m["cpu_baseline"]["serial"] = ser
+            if cfg == 3:  # BASELINE configs[2]: active fraction per Newton iteration, logged
+                m["active_fraction_per_iteration"] = active_fraction_log(pkg, cfg)
+            Rc.close()
+            m.pop("_final")
+            per[CONFIGS[cfg]["key"]] = m
+        line["per_config"] = per
+    if rank == 0 and ws == 1 and args.c5:
         fr = [float(x) for x in args.c5.split(",") if x]
         ilu_fr = [float(x) for x in args.c5_ilu.split(",") if x.strip()]
         line["c5_sweep"] = c5_sweep(pkg, fr, args.c5_reps, hbm, ilu_fr)
-    if rank == 0 and args.flash_cells > 0:
+    if rank == 0 and ws == 1 and args.flash_cells > 0:
         line["eos_flash"] = eos_flash_line(pkg, args.flash_cells, 5, args.no_cpu)
-    if rank == 0 and args.direct:
+    if rank == 0 and ws == 1 and args.direct:
         line["direct_solve"] = direct_line(pkg, args.no_cpu)
-    if rank == 0 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(case, s0, dts, opts)
     barrier(dist)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def active_fraction_log(pkg, cfg: int) -> dict:
+    """Per-iteration active fraction n_A/n of the config's whole run (the case runner's
+    iterations.csv, one row per Newton iteration of every committed timestep)."""
+    import tempfile
+    spec = CONFIGS[cfg]
+    with tempfile.TemporaryDirectory() as d:
+        pkg.simulate(cfg, spec["solvers"][0], d, write_fields=False)
+        rows = [ln.split(",") for ln in open(os.path.join(d, "iterations.csv")).read().splitlines()[1:]]
+    rows = [r for r in rows if r[2] == "1"]  # committed attempts
+    frac = [float(r[6]) for r in rows]
+    per_step = {}
+    for r in rows:
+        per_step.setdefault(int(r[0]), []).append(round(float(r[6]), 5))
+    return {"iterations": len(frac), "min": min(frac), "max": max(frac), "mean": float(np.mean(frac)),
+            "per_timestep": per_step, "source": "rsim_simulate iterations.csv (column n_active/n)"}
 
 
 if __name__ == "__main__":

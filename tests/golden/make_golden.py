@@ -35,18 +35,21 @@ GOLDEN = {
     "c2s_localized_bj": (dict(config=2, nx=48, ny=48, n_dfn=12), 1, 6, 0),
 }
 
-# Full-size BASELINE configs (the bench workload and the first timesteps of configs 3 and 4):
+# Full-size BASELINE configs (the bench workloads: whole schedules of configs 1-4):
 # the final state is stored as a digest (sha256 of the u / status bytes) plus every
 # SUBSAMPLE-th cell's unknowns, so the fixture stays small.  Generation takes minutes
-# (config 4: ~20 min on 8 host threads), so only c2 is re-checked on the CPU suite.
+# (config 4: ~20-40 min per solver on 8 host threads), so only c1 / c2 are re-checked on the CPU suite.
 FULL = {
     "c2_bench_localized": (dict(config=2), 1, 30, None),
     "c2_bench_dd": (dict(config=2), 2, 30, None),
     "c3_full_localized": (dict(config=3), 1, 20, None),
-    "c4_full_localized": (dict(config=4), 1, 2, None),
+    "c4_full_localized": (dict(config=4), 1, 20, None),
+    "c4_full_dd": (dict(config=4), 2, 20, None),
+    "c3_full_dd": (dict(config=3), 2, 20, None),
+    "c1_bench_standard": (dict(config=1), 0, 20, None),
 }
 SUBSAMPLE = 101
-CPU_RECHECK = ("c2_bench_localized", "c2_bench_dd")
+CPU_RECHECK = ("c2_bench_localized", "c2_bench_dd", "c1_bench_standard")
 
 REC_FIELDS = ["n_active", "lin_iters", "subdomain", "mode_expand", "dp_inf_A", "dp_inf_B", "f_norm2",
               "f_norminf", "lin_res"]
