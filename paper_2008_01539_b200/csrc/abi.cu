@@ -213,6 +213,7 @@ int rsim_gpu_create(rsim_gpu_ctx** out, const rsim_graph_desc* g, const rsim_flu
     TRY(dalloc(&c->tile_cnt, nt)); TRY(dalloc(&c->tile_off, nt));
   }
   TRY(dalloc(&c->ell_col, c->nslot * n)); TRY(dalloc(&c->ell_val, c->nslot * n * b * b));
+  c->ell_cap = n;
   TRY(dalloc(&c->nnc_lcol, c->nnc_total)); TRY(dalloc(&c->nnc_val, c->nnc_total * b * b));
   TRY(dalloc(&c->F_raw, n * b)); TRY(dalloc(&c->rhs, n * b));
   TRY(dalloc(&c->part_f2, nchunks));
@@ -504,7 +505,7 @@ int rsim_gpu_download_boundary(rsim_gpu_ctx* c, int32_t* vb, int32_t* n) {
 
 int64_t rsim_gpu_download_system(rsim_gpu_ctx* c, double* F_raw, double* rhs, int32_t* rowptr, int32_t* col,
                                  double* val, int64_t cap_nnzb) {
-  const int64_t nA = c->nA, b = c->b, bb = b * b, cap = c->n;
+  const int64_t nA = c->nA, b = c->b, bb = b * b, cap = c->ell_cap;
   TRY(launch_materialize_cols(c));
   RSIM_CUDA(cudaStreamSynchronize(c->stream));
   std::vector<int32_t> ecol(c->nslot * nA), act(nA);

@@ -607,7 +607,10 @@ int launch_assemble(rsim_gpu_ctx* c) {
   a.nx = c->nx; a.ny = c->ny; a.nz = c->nz;
   a.nslot = c->nslot;
   a.nA = c->nA;
-  a.cap = c->n;
+  // compact slot stride: the slot slabs of the current system are adjacent
+  // (one contiguous ~nslot·n_A·b²·8 B region instead of slabs n apart)
+  c->ell_cap = c->nA == c->n ? c->n : ((c->nA + 31) / 32) * 32;
+  a.cap = c->ell_cap;
   a.d3 = c->d3;
   a.has_nnc = c->has_nnc;
   a.tx = c->tx; a.ty = c->ty; a.tz = c->tz; a.pv = c->pv; a.wi = c->wi;

@@ -112,6 +112,7 @@ struct rsim_gpu_ctx {
 
   // local system (ELL [slot][cap] + global-NNC-slot values)
   int32_t* ell_col = nullptr;
+  int64_t ell_cap = 0;  // ELL slot stride of the current assembly: n_A rounded up to 32 (n for full sets)
   double* ell_val = nullptr;
   int32_t* nnc_lcol = nullptr;
   double* nnc_val = nullptr;

@@ -296,7 +296,7 @@ int launch_b(rsim_gpu_ctx* c) {
   a.nA = c->nA; a.nslot = c->nslot; a.b = B;
   a.nx = c->nx; a.ny = c->ny; a.nz = c->nz;
   a.d3 = c->d3; a.implicit = c->cols_implicit; a.has_nnc = c->has_nnc; a.f2_parts = c->f2_parts;
-  a.cap = c->n; a.N = N;
+  a.cap = c->ell_cap; a.N = N;
   a.ell_col = c->ell_col; a.act = c->act; a.nptr = c->nptr; a.nnc_lcol = c->nnc_lcol;
   a.ell_val = c->ell_val; a.nnc_val = c->nnc_val; a.rhs = c->rhs; a.F_raw = c->F_raw; a.part_f2 = c->part_f2;
   a.W = c->dn_W; a.colbuf = c->dn_colbuf; a.piv = c->dn_piv; a.x = c->x; a.dsc = c->dsc;

@@ -117,7 +117,7 @@ int ilu_prepare(rsim_gpu_ctx* c) {
   std::vector<int32_t> ecol((size_t)c->nslot * n), act(n), nlcol(c->nnc_total);
   RSIM_CUDA(cudaStreamSynchronize(c->stream));
   for (int s = 0; s < c->nslot; ++s)
-    RSIM_CUDA(cudaMemcpy(&ecol[(size_t)s * n], c->ell_col + (int64_t)s * c->n, sizeof(int32_t) * n,
+    RSIM_CUDA(cudaMemcpy(&ecol[(size_t)s * n], c->ell_col + (int64_t)s * c->ell_cap, sizeof(int32_t) * n,
                          cudaMemcpyDeviceToHost));
   if (c->has_nnc) {
     RSIM_CUDA(cudaMemcpy(act.data(), c->act, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
@@ -131,7 +131,7 @@ int ilu_prepare(rsim_gpu_ctx* c) {
     ent.clear();
     for (int s = 0; s < c->nslot; ++s) {
       const int32_t cl = ecol[(size_t)s * n + l];
-      if (cl >= 0) ent.emplace_back(cl, (int32_t)(s * c->n + l));  // ELL value index (slot-major)
+      if (cl >= 0) ent.emplace_back(cl, (int32_t)(s * c->ell_cap + l));  // ELL value index (slot-major)
     }
     if (c->has_nnc) {
       const int64_t i = act[l];

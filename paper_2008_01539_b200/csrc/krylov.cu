@@ -29,9 +29,34 @@ namespace cg = cooperative_groups;
 
 namespace {
 
-constexpr int KT = 1024;  // threads per CTA
-constexpr int CPR = KT / 256;  // canonical chunks per round
-constexpr int LCPR = CPR == 4 ? 2 : (CPR == 2 ? 1 : 0);
+// Threads per CTA per block size (template parameter of the kernel; one CTA
+// per SM, so KT fixes the register cap: 1024 -> 64, 512 -> 128).  Measured on
+// the config-3 / config-4 first Newton systems (100 Neumann-1 iterations,
+// scripts/krylov_c4.py): b = 2 66.2 -> 44.9 µs per iteration with 512 threads
+// and one slot per gather group, b = 3 551 -> 461 µs with 1024 threads and one
+// slot per group (512 threads: 454-588 µs, 256 threads for b = 2: 64-68 µs);
+// b = 1 (config 5 at 1-100 %) keeps 1024 threads and all six slots in flight.
+#ifndef RSIM_KT1
+#define RSIM_KT1 1024
+#endif
+#ifndef RSIM_KT2
+#define RSIM_KT2 512
+#endif
+#ifndef RSIM_KT3
+#define RSIM_KT3 1024
+#endif
+__host__ __device__ constexpr int kt_for(int B) { return B == 1 ? RSIM_KT1 : (B == 2 ? RSIM_KT2 : RSIM_KT3); }
+#ifndef RSIM_SPMV_SG1
+#define RSIM_SPMV_SG1 6
+#endif
+#ifndef RSIM_SPMV_SG2
+#define RSIM_SPMV_SG2 1
+#endif
+#ifndef RSIM_SPMV_SG3
+#define RSIM_SPMV_SG3 1
+#endif
+template <int CPR>
+__host__ __device__ constexpr int lcpr() { return CPR == 4 ? 2 : (CPR == 2 ? 1 : 0); }
 constexpr int64_t kFuseMaxRows = 1 << 20;  // recompute-fusion only while latency-bound
 
 struct KArgs {
@@ -60,6 +85,7 @@ struct KArgs {
   double* part2;  // [5][pstride2] level-2 partials (very large systems)
   int32_t pstride, pstride2;
   int32_t red_small_max;  // chunk partials reduced redundantly by every CTA up to this count
+  int32_t alt;            // sweep direction alternates between phases (L2 reuse of the previous sweep's tail)
   DevScalars* dsc;
 };
 
@@ -79,6 +105,7 @@ struct Red {
 // and after the CTA's last round, one barrier pair turns them into level-1
 // chunk partials (8-way trees, canonical).  Warps thus run ahead through up
 // to RSTAGE rounds of loads instead of meeting at two barriers per round.
+template <int CPR>
 __device__ __forceinline__ void stage_round(Red& R, int NQ, const double* val, int slot, int64_t rd, bool flush,
                                             int nstaged, int64_t nch, double* part, int pstride) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -90,7 +117,7 @@ __device__ __forceinline__ void stage_round(Red& R, int NQ, const double* val, i
   if (!flush) return;
   __syncthreads();
   for (int k = threadIdx.x; k < nstaged * CPR * NQ; k += blockDim.x) {
-    const int sl = k / (CPR * NQ), rem = k - sl * CPR * NQ, q = rem >> LCPR, g = rem & (CPR - 1);
+    const int sl = k / (CPR * NQ), rem = k - sl * CPR * NQ, q = rem >> lcpr<CPR>(), g = rem & (CPR - 1);
     const int64_t c = R.rid[sl] * CPR + g;
     if (c < nch) part[q * pstride + c] = tree8(&R.wsr[sl][q][8 * g]);
   }
@@ -99,6 +126,7 @@ __device__ __forceinline__ void stage_round(Red& R, int NQ, const double* val, i
 
 // Per-round commit: warp trees of up to 3 quantities -> 8-way trees -> level-1
 // partials of the 4 chunks of this round.
+template <int CPR>
 __device__ __forceinline__ void commit_round(Red& R, int NQ, const double* val, int64_t chunk0, int64_t nch,
                                              double* part, int pstride) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -108,7 +136,7 @@ __device__ __forceinline__ void commit_round(Red& R, int NQ, const double* val, 
   }
   __syncthreads();
   if ((int)threadIdx.x < CPR * NQ) {
-    const int g = threadIdx.x & (CPR - 1), q = threadIdx.x >> LCPR;
+    const int g = threadIdx.x & (CPR - 1), q = threadIdx.x >> lcpr<CPR>();
     if (chunk0 + g < nch) part[q * pstride + chunk0 + g] = tree8(&R.ws[q][8 * g]);
   }
   __syncthreads();
@@ -120,7 +148,7 @@ __device__ __forceinline__ void commit_round(Red& R, int NQ, const double* val, 
 // load + barrier steps).  src(q) gives quantity q's partials; results in
 // R.res[q].  Per quantity: warp trees + 8-way trees over chunks of 256
 // partials, then the same over the chunk results (blockops.h canonical tree).
-template <class SF>
+template <int CPR, class SF>
 __device__ __forceinline__ void reduce_small_multi(Red& R, int NQ, SF&& src, int P) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (P == 1) {
@@ -142,7 +170,7 @@ __device__ __forceinline__ void reduce_small_multi(Red& R, int NQ, SF&& src, int
       }
     __syncthreads();
     if ((int)threadIdx.x < CPR * NQ) {
-      const int g = threadIdx.x & (CPR - 1), q = threadIdx.x >> LCPR;
+      const int g = threadIdx.x & (CPR - 1), q = threadIdx.x >> lcpr<CPR>();
       if (c0 + g < P2) R.lvl[q][c0 + g] = tree8(&R.ws[q][8 * g]);
     }
     __syncthreads();
@@ -200,15 +228,26 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
     for (int s = 0; s < 6; ++s)
       if (s < a.nslot) cl[s] = __ldg(&col[s * a.cap + l]);
   }
-  double xv[6][B];
-#pragma unroll
-  for (int s = 0; s < 6; ++s)
-    if (cl[s] >= 0) nbr_val<B>(mode, X, cl[s], beta, omega, alpha, xv[s]);
+  // Slots in groups of SG: all gathers of a group in flight, then its blocks.
+  // Gathering all six neighbours first keeps 6·B doubles live and spills them
+  // to local memory at 64 registers (b = 3: ~1 KB of local traffic per row and
+  // SpMV, measured 1.4× the algorithmic DRAM bytes).  Accumulation order is
+  // unchanged (slots ascending), so the bits are the same.
+  constexpr int SG = B == 1 ? RSIM_SPMV_SG1 : (B == 2 ? RSIM_SPMV_SG2 : RSIM_SPMV_SG3);
 #pragma unroll
   for (int e = 0; e < B; ++e) acc[e] = own[e];
 #pragma unroll
-  for (int s = 0; s < 6; ++s)
-    if (cl[s] >= 0) rsim::blk::gemv_acc_flat<B>(&val[((int64_t)s * a.cap + l) * B * B], xv[s], acc);
+  for (int s0 = 0; s0 < 6; s0 += SG) {
+    double xv[SG][B];
+#pragma unroll
+    for (int k = 0; k < SG; ++k)
+      if (s0 + k < 6 && cl[s0 + k] >= 0) nbr_val<B>(mode, X, cl[s0 + k], beta, omega, alpha, xv[k]);
+#pragma unroll
+    for (int k = 0; k < SG; ++k)
+      if (s0 + k < 6 && cl[s0 + k] >= 0)
+        rsim::blk::gemv_acc_flat<B>(&val[((int64_t)(s0 + k) * a.cap + l) * B * B], xv[k], acc);
+    if (SG < 6) asm volatile("" ::: "memory");  // keep the next group's loads after this group's math
+  }
   if (a.has_nnc) {
     const int64_t i = a.act[l];
     const int32_t q0 = a.nptr[i], q1 = a.nptr[i + 1];
@@ -225,8 +264,9 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
 
 // FUSE is a template parameter: the two variants have different live state,
 // and one kernel holding both spills heavily at 64 registers / thread.
-template <int B, bool FUSE, bool ILU>
+template <int B, bool FUSE, bool ILU, int KT>
 __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
+  constexpr int CPR = KT / 256;  // canonical chunks per round
   __shared__ Red R;
   const bool single = gridDim.x == 1;
   auto sync = [&]() {
@@ -245,7 +285,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     const int P1 = (int)nch;
     auto src = [&](int q) { return (q == 1 && src1) ? src1 : a.part + q * a.pstride; };
     if (P1 <= a.red_small_max) {
-      reduce_small_multi(R, NQ, src, P1);
+      reduce_small_multi<CPR>(R, NQ, src, P1);
     } else {
       // distributed level 2, one more barrier, then the (small) rest per CTA
       const int P2 = (P1 + 255) / 256;
@@ -254,27 +294,36 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
         const int64_t idx = c2 * 256 + (tid & 255);
         double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         for (int q = 0; q < NQ; ++q) v[q] = idx < P1 ? src(q)[idx] : 0.0;
-        commit_round(R, NQ, v, rr * CPR, P2, a.part2, a.pstride2);
+        commit_round<CPR>(R, NQ, v, rr * CPR, P2, a.part2, a.pstride2);
       }
       sync();
-      reduce_small_multi(R, NQ, [&](int q) { return (const double*)(a.part2 + q * a.pstride2); }, P2);
+      reduce_small_multi<CPR>(R, NQ, [&](int q) { return (const double*)(a.part2 + q * a.pstride2); }, P2);
     }
   };
 
+  // Sweep order: with a.alt every phase walks the rounds in the direction
+  // opposite to the previous phase, so the rows it starts with are the ones the
+  // previous phase touched last (still in L2).  Row results do not depend on the
+  // order (reductions go through per-chunk partials), so the bits are unchanged.
+  bool rev = false;
+  auto rmap = [&](int64_t rd0) { return rev ? nrounds - 1 - rd0 : rd0; };
+  auto flip = [&]() { if (a.alt) rev = !rev; };
 #define ROUNDS_BEGIN                                                         \
   {                                                                          \
   int rloc = 0;                                                              \
-  for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x, ++rloc) {     \
+  for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x, ++rloc) {  \
+    const int64_t rd = rmap(rd0);                                            \
     const int64_t l = rd * KT + tid;                                         \
     const bool ok = l < nr;                                                  \
     double val[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #define ROUNDS_END(NQ)                                                       \
     {                                                                        \
       const int slot = rloc % a.stage;                                       \
-      const bool last = rd + gridDim.x >= nrounds;                           \
-      stage_round(R, NQ, val, slot, rd, slot == a.stage - 1 || last, slot + 1, nch, a.part, a.pstride); \
+      const bool last = rd0 + gridDim.x >= nrounds;                          \
+      stage_round<CPR>(R, NQ, val, slot, rd, slot == a.stage - 1 || last, slot + 1, nch, a.part, a.pstride); \
     }                                                                        \
   }                                                                          \
+  flip();                                                                    \
   }
 
   // ---- init: r = r0 = rhs, x = 0;  (rhs, rhs), (F, F) (the latter from the
@@ -329,8 +378,8 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   const bool prec = neu || ilu;  // ph = M^{-1} p, sh = M^{-1} s are stored
   if (ilu && ilu_bad) { status = RSIM_ENUM; it = 0; continue; }  // singular pivot: block-Jacobi only
   if (attempt) {
-    for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
-      const int64_t l = rd * KT + tid;
+    for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
+      const int64_t l = rmap(rd0) * KT + tid;
       if (l < nr)
 #pragma unroll
         for (int e = 0; e < B; ++e) {
@@ -354,8 +403,8 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     const Vecs V0{a.r, po, vo, a.s, a.t};  // p_j = (s_j − ω t_j) + β (p_old_j − ω v_old_j)
     if (!fuse) {  // p = r + β (p − ω v), stored, then visible to all
       if (!p_ready)  // (else already stored by the previous x/r update pass)
-      for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
-        const int64_t l = rd * KT + tid;
+      for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
+        const int64_t l = rmap(rd0) * KT + tid;
         if (l < nr) {
           double pown[B];
           nbr_val<B>(pmode, V0, l, beta, omega, 0.0, pown);
@@ -364,10 +413,11 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
         }
       }
       sync();
+      flip();
     }
     if (neu) {  // ph = p + (p − Â p), stored, barrier
-      for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
-        const int64_t l = rd * KT + tid;
+      for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
+        const int64_t l = rmap(rd0) * KT + tid;
         if (l < nr) {
           double pown[B], y[B];
           if (fuse) {
@@ -385,6 +435,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
         }
       }
       sync();
+      flip();
     }
     if (ilu) ilu_apply<B>(a.fa, pc, a.ph, sync);  // ph = (LU)^{-1} p (p stored: unfused)
     // ---- v = Â p (BJ) or v = Â ph (Neumann-1, ILU(0)); (r0, v) and the lagged (r, r)
@@ -421,17 +472,18 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     const Vecs V2{a.r, po, vc, a.s, a.t};  // s_j = r_j − α v_j
     const bool fs = fuse || (!prec && a.fuse_s);  // s recomputed where gathered, stored by its owner
     if (!fs) {  // s = r − α v, stored, barrier
-      for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
-        const int64_t l = rd * KT + tid;
+      for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
+        const int64_t l = rmap(rd0) * KT + tid;
         if (l < nr)
 #pragma unroll
           for (int e = 0; e < B; ++e) a.s[l * B + e] = a.r[l * B + e] - alpha * vc[l * B + e];
       }
       sync();
+      flip();
     }
     if (neu) {  // sh = s + (s − Â s), stored, barrier
-      for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
-        const int64_t l = rd * KT + tid;
+      for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
+        const int64_t l = rmap(rd0) * KT + tid;
         if (l < nr) {
           double sv[B], y[B];
           if (fuse) {
@@ -447,6 +499,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
         }
       }
       sync();
+      flip();
     }
     if (ilu) ilu_apply<B>(a.fa, a.s, a.sh, sync);  // sh = (LU)^{-1} s
     // ---- t = Â s (BJ) or t = Â sh (Neumann-1, ILU(0)); (s,s), (t,s), (t,t), (r0,s), (r0,t)
@@ -484,8 +537,8 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     const double* phv = prec ? a.ph : pc;
     const double* shv = prec ? a.sh : a.s;
     if (!fixed && sqrt(ss) <= tol) {
-      for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
-        const int64_t l = rd * KT + tid;
+      for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
+        const int64_t l = rmap(rd0) * KT + tid;
         if (l < nr)
 #pragma unroll
           for (int e = 0; e < B; ++e) a.x[l * B + e] = a.x[l * B + e] + alpha * phv[l * B + e];
@@ -496,7 +549,8 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     }
     if (tt == 0.0 || !isfinite(tt)) { status = RSIM_ENUM; break; }
     omega = ts / tt;
-    // ---- x, r update (own rows, no barrier: neighbours recompute r from s, t
+    // ---- x, r update (own rows, no barrier — so it keeps the sweep direction of
+    //      the phase that follows it (same rows per CTA) — neighbours recompute r from s, t
     //      until the next reduction, and the next p-pass reads only its own r).
     //      Unfused: the next iterate's p = r + β' (p − ω v) is formed here from
     //      the same registers (own row only; β' needs only this iteration's
@@ -507,8 +561,8 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     const bool pfuse = !fuse && more;
     const double beta_next = pfuse ? (rho_next / rho_new) * (alpha / omega) : 0.0;
     double* pn = cur ? a.p : a.p2;  // the next iterate's p buffer
-    for (int64_t rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
-      const int64_t l = rd * KT + tid;
+    for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
+      const int64_t l = rmap(rd0) * KT + tid;
       if (l < nr)
 #pragma unroll
         for (int e = 0; e < B; ++e) {
@@ -565,7 +619,7 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
     return (e && *e) ? std::atoi(e) : 0;
   }();
   a.stage = 1;  // set below from the rounds per CTA
-  a.cap = c->n;
+  a.cap = c->ell_cap;
   a.has_nnc = c->has_nnc;
   a.rtol = o->lin_rtol;
   a.ell_col = c->ell_col; a.ell_val = c->ell_val;
@@ -598,18 +652,25 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
     return (e && *e) ? (int32_t)std::atoi(e) : 2048;
   }();
   a.red_small_max = red_small < 64 * 256 ? red_small : 64 * 256;
+  static const int alt_env = [] {  // experiment switch
+    const char* e = std::getenv("RSIM_KALT");
+    return (e && *e) ? std::atoi(e) : 0;
+  }();
+  a.alt = alt_env;
   a.pstride = (int32_t)((c->n + 255) / 256);
   a.pstride2 = (a.pstride + 255) / 256;
   a.part = c->part;
   a.part2 = c->part + 5 * (int64_t)a.pstride;
   a.dsc = c->dsc;
+  constexpr int KT = kt_for(B), CPR = KT / 256;
   const int64_t nrounds = ((c->nA + 255) / 256 + CPR - 1) / CPR;
-  auto kern = a.ilu ? k_bicgstab<B, false, true> : (a.fuse ? k_bicgstab<B, true, false> : k_bicgstab<B, false, false>);
+  auto kern = a.ilu ? k_bicgstab<B, false, true, KT>
+                    : (a.fuse ? k_bicgstab<B, true, false, KT> : k_bicgstab<B, false, false, KT>);
   if (c->max_coop_blocks[B] == 0) {
     int per_sm = 0, per_sm2 = 0, per_sm3 = 0;
-    RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bicgstab<B, true, false>, KT, 0));
-    RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_bicgstab<B, false, false>, KT, 0));
-    RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, k_bicgstab<B, false, true>, KT, 0));
+    RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bicgstab<B, true, false, KT>, KT, 0));
+    RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_bicgstab<B, false, false, KT>, KT, 0));
+    RSIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, k_bicgstab<B, false, true, KT>, KT, 0));
     if (per_sm2 < per_sm) per_sm = per_sm2;
     if (per_sm3 < per_sm) per_sm = per_sm3;
     c->max_coop_blocks[B] = per_sm * c->sm_count;

@@ -820,7 +820,7 @@ int launch_krylov_dsm(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.fixed = o->fixed_lin_iters;
   a.neu = o->precond == RSIM_PREC_NEUMANN1;
   a.nch = nch;
-  a.cap = c->n;
+  a.cap = c->ell_cap;
   a.has_nnc = c->has_nnc;
   a.rtol = o->lin_rtol;
   a.ell_col = c->ell_col;

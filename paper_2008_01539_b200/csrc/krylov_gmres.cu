@@ -393,7 +393,7 @@ int launch_g(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.neu = o->precond == RSIM_PREC_NEUMANN1;
   a.ilu = o->precond == RSIM_PREC_ILU0;
   a.fa = ilu_args(c);
-  a.cap = c->n;
+  a.cap = c->ell_cap;
   a.nx = c->nx; a.ny = c->ny; a.nz = c->nz; a.d3 = c->d3;
   a.has_nnc = c->has_nnc; a.implicit = c->cols_implicit; a.f2_parts = c->f2_parts;
   a.rtol = o->lin_rtol;

@@ -1,0 +1,17 @@
+#!/bin/bash
+# Build librsim variants with different krylov.cu compile-time tuning macros
+# into paper_2008_01539_b200/lib/ab/librsim_<name>.so (A/B experiments; load
+# with RSIM_LIB=...).  Usage: scripts/ab_krylov_build.sh name "-DMACRO=v ..." ...
+set -e
+cd "$(dirname "$0")/.."
+OBJ=paper_2008_01539_b200/lib/obj
+OUT=paper_2008_01539_b200/lib/ab
+mkdir -p $OUT
+NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --fmad=false -ccbin /usr/bin/g++ -Xcompiler -fPIC,-ffp-contract=off,-fopenmp,-O3 -Xptxas -O3 -I include -I paper_2008_01539_b200/csrc"
+while [ $# -ge 2 ]; do
+  name=$1; flags=$2; shift 2
+  $NV $flags -c paper_2008_01539_b200/csrc/krylov.cu -o $OUT/krylov_$name.o
+  objs=$(ls $OBJ/*.o | grep -v krylov.cu.o)
+  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -ccbin /usr/bin/g++ $objs $OUT/krylov_$name.o -o $OUT/librsim_$name.so -lgomp
+  echo built $OUT/librsim_$name.so
+done
