@@ -32,10 +32,11 @@ namespace {
 // Threads per CTA per block size (template parameter of the kernel; one CTA
 // per SM, so KT fixes the register cap: 1024 -> 64, 512 -> 128).  Measured on
 // the config-3 / config-4 first Newton systems (100 Neumann-1 iterations,
-// scripts/krylov_c4.py): b = 2 66.2 -> 44.9 µs per iteration with 512 threads
-// and one slot per gather group, b = 3 551 -> 461 µs with 1024 threads and one
-// slot per group (512 threads: 454-588 µs, 256 threads for b = 2: 64-68 µs);
-// b = 1 (config 5 at 1-100 %) keeps 1024 threads and all six slots in flight.
+// scripts/krylov_c4.py): b = 2 66.2 -> 44.9 µs per iteration and b = 3
+// 551 -> 454 µs with 512 threads and one slot per gather group (no spills;
+// b = 3 with 1024 threads: 461 µs and ~0.8 KB of local traffic per row-phase
+// left, 256 threads for b = 2: 64-68 µs); b = 1 (config 5 at 1-100 %) keeps
+// 1024 threads and all six slots in flight.
 #ifndef RSIM_KT1
 #define RSIM_KT1 1024
 #endif
@@ -43,7 +44,7 @@ namespace {
 #define RSIM_KT2 512
 #endif
 #ifndef RSIM_KT3
-#define RSIM_KT3 1024
+#define RSIM_KT3 512
 #endif
 __host__ __device__ constexpr int kt_for(int B) { return B == 1 ? RSIM_KT1 : (B == 2 ? RSIM_KT2 : RSIM_KT3); }
 #ifndef RSIM_SPMV_SG1
