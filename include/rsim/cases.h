@@ -46,6 +46,41 @@ int64_t    rsim_case_n_nnc(const rsim_case* c);                          /* dire
 double     rsim_case_c5_field(const rsim_case* c, double target, int32_t m, double eps,
                               double* dp, double* R_out);
 
+/* ---- case files and EDFM (csrc/edfm.cpp)
+ * A case file is the SPEC's flat structured text: "[section]" headers,
+ * "key = value" entries, "#" comments, and a [fractures] table of rows
+ * "x0 y0 x1 y1 aperture perm [porosity]" (m, m^2).  Sections and keys (units):
+ *   [case] name   [grid] nx ny dx dy thickness (m)
+ *   [rock] porosity  perm (m^2) | perm_lognormal = kg sigma_ln seed   c_r (1/psi)
+ *   [fluid] model = single|oilwater  mu_o mu_w (cP)  c_o c_w (1/psi)  rho_o rho_w (kg/m^3)  swc sor
+ *   [initial] pressure (psi)  sw      [well] bhp (psi)  wi (m^3)  trajectory = x0 y0 x1 y1 (m)
+ *   [time] total dt0 dt_max (days)  growth
+ *   [solver] solver = standard|localized|adaptive_dd  m  eps_p (psi)
+ * The fractures are discretized with the EDFM (one fracture cell per segment x
+ * crossed matrix cell) into fracture planes above the 2D matrix grid; unused
+ * plane positions are RSIM_KIND_DEAD.  NULL + message on a
+ * configuration error. */
+rsim_case* rsim_case_from_text(const char* text, char* err, int32_t errlen);
+rsim_case* rsim_case_from_file(const char* path, char* err, int32_t errlen);
+
+typedef struct {
+  int64_t n_live;    /* matrix + fracture cells (M_A's n)        */
+  int64_t n_frac;    /* EDFM fracture cells                      */
+  int64_t n_dead;    /* dead filler cells of the fracture planes */
+  int32_t solver, m; /* case-file defaults (seeded configs: 1, 2) */
+  double eps_p;      /* Pa                                       */
+  double total_time; /* s (0: n_steps schedule)                  */
+} rsim_case_info_t;
+int rsim_case_info(const rsim_case* c, rsim_case_info_t* out);
+
+/* Every connection (i < j, Υ > 0): Cartesian faces, then NNCs; returns the
+ * count (writes at most cap entries; pass cap 0 to count). */
+int64_t rsim_case_connections(const rsim_case* c, int32_t* i, int32_t* j, double* T, int64_t cap);
+
+/* EDFM ⟨d⟩: mean normal distance of cell [cx, cx+dx] x [cy, cy+dy] to the line
+ * through (x0,y0)-(x1,y1), 8 x 8 midpoint quadrature. */
+double rsim_edfm_avg_distance(double cx, double cy, double dx, double dy, double x0, double y0, double x1, double y1);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,6 +22,10 @@
  *   pressure_t<days>.txt / satwater_t / satgas_t / phasestatus_t
  *                row-major matrices (one row per y line, layers stacked) at
  *                every report time (report_every_days > 0) and at the end.
+ *   flags_t<days>_iter<k>.txt  (trace_flags) Fig. 8 category of every cell
+ *                after Newton iteration k of the step ending at <days>:
+ *                0 inactive, 1 active, 2 boundary, 3 active + updated,
+ *                4 boundary + updated, -1 dead EDFM filler position.
  * Units: SI inside, psi / days / bbl externally (SPEC.md design decision).
  * Surface rates: single phase and oil-water models conserve mass, so the
  * mass rate is divided by the phase reference density; the black-oil model
@@ -51,6 +55,7 @@ typedef struct {
   double report_every_days;  /* field dumps every this many days; 0 -> end only */
   int32_t write_fields;      /* 0: no field dumps at all                         */
   int32_t lin_method;        /* -1 -> case default (RSIM_LIN_*; DIRECT: n_A·b <= RSIM_DIRECT_MAX) */
+  int32_t trace_flags;       /* 1: flags_t<days>_iter<k>.txt after every Newton iteration (Fig. 8 categories) */
 } rsim_sim_opts;
 
 typedef struct {
@@ -74,6 +79,11 @@ int rsim_well_rates(const rsim_case* c, const double* u, const uint8_t* st, doub
 
 /* Run the case on the GPU; out_dir NULL or "" -> no files. */
 int rsim_simulate(const rsim_case_opts* co, const rsim_sim_opts* so, const char* out_dir, rsim_run_metrics* out);
+
+/* The same for a case file (rsim/cases.h grammar; EDFM fractures): so->solver
+ * -1 and so->m / so->eps_p <= 0 take the case file's [solver] defaults.
+ * RSIM_EARG (message in rsim_gpu_last_error) on a configuration error. */
+int rsim_simulate_file(const char* case_file, const rsim_sim_opts* so, const char* out_dir, rsim_run_metrics* out);
 
 #ifdef __cplusplus
 }

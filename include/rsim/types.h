@@ -32,7 +32,7 @@ enum {
 enum { RSIM_BO_UNDERSAT = 0, RSIM_BO_SAT = 1 };
 
 /* Cell kind (SPEC.md:38 cell_kind). Fracture cells are always active. */
-enum { RSIM_KIND_MATRIX = 0, RSIM_KIND_FRACTURE = 1 };
+enum { RSIM_KIND_MATRIX = 0, RSIM_KIND_FRACTURE = 1, RSIM_KIND_DEAD = 2 };  /* DEAD: EDFM fracture-plane filler (no connections, never active) */
 
 /* Linear solver selectors. */
 enum { RSIM_LIN_BICGSTAB = 0, RSIM_LIN_GMRES = 1, RSIM_LIN_DIRECT = 2 };

@@ -48,7 +48,8 @@ struct Graph {
   bool d3 = false;
   int nslot = 0;
   std::vector<double> tx, ty, tz, pv, wi;
-  std::vector<uint8_t> kind, pinned;
+  std::vector<uint8_t> kind, pinned, dead;  // dead: RSIM_KIND_DEAD filler cells (no connections)
+  int64_t n_live = 0;                       // cells of the model (n minus dead fillers): M_A's n
   std::vector<int32_t> nptr, nnbr;
   std::vector<double> nt;
   bool has_nnc = false;
@@ -68,6 +69,12 @@ struct Graph {
     if (d3 && iz < nz - 1) f(i + nxy, tz[i]);
     if (has_nnc)
       for (int32_t q = nptr[i]; q < nptr[i + 1]; ++q) f((int64_t)nnbr[q], nt[q]);
+  }
+  // Graph neighbours for the set logic: as each(), without the
+  // structural Cartesian neighbours that are dead filler cells (EDFM planes).
+  template <class F>
+  void each_live(int64_t i, F&& f) const {
+    each(i, [&](int64_t j, double T) { if (!dead[j]) f(j, T); });
   }
 };
 
@@ -146,7 +153,7 @@ static void dilate(const Graph& g, const std::vector<int32_t>& seeds, int m, std
     q.pop_front();
     mark[i] = 1;
     if (dist[i] >= m) continue;
-    g.each(i, [&](int64_t j, double) {
+    g.each_live(i, [&](int64_t j, double) {
       if (dist[j] < 0) { dist[j] = dist[i] + 1; q.push_back((int32_t)j); }
     });
   }
@@ -158,7 +165,7 @@ static std::vector<uint8_t> boundary_of(const Graph& g, const std::vector<uint8_
   for (int64_t i = 0; i < g.n; ++i) {
     if (!A[i]) continue;
     bool out = false;
-    g.each(i, [&](int64_t j, double) { if (!A[j]) out = true; });
+    g.each_live(i, [&](int64_t j, double) { if (!A[j]) out = true; });
     B[i] = out;
   }
   return B;
@@ -753,8 +760,9 @@ static std::vector<uint8_t> initial_flags(const Model& M, const int32_t* va, int
 
 // newton_standard: V_A = all cells every iteration.
 static int newton_standard(Model& M, const rsim_solver_opts& o, rsim_newton_report* rep) {
-  std::vector<int32_t> all(M.g.n);
-  for (int64_t i = 0; i < M.g.n; ++i) all[i] = (int32_t)i;
+  std::vector<int32_t> all;  // every live cell (dead filler cells are not cells of the model)
+  for (int64_t i = 0; i < M.g.n; ++i)
+    if (!M.g.dead[i]) all.push_back((int32_t)i);
   std::vector<double> x;
   for (int it = 0; it < o.max_newton; ++it) {
     rsim_iter_record rec{};
@@ -762,7 +770,7 @@ static int newton_standard(Model& M, const rsim_solver_opts& o, rsim_newton_repo
     int st = local_step(M, all, o, rec, x);
     rec.dp_inf_B = 0.0;
     rec.mode_expand = 0;
-    rep_push(rep, rec, M.g.n);
+    rep_push(rep, rec, M.g.n_live);
     if (st != RSIM_OK) { rep->status = st; return st; }
     if (rec.dp_inf_A < o.eps_p) { rep->converged = 1; return RSIM_OK; }
   }
@@ -810,14 +818,14 @@ static int newton_localized(Model& M, const int32_t* va_init, int32_t n_init, co
     rsim_iter_record rec{};
     rec.subdomain = -1;
     int st = local_step(M, act, o, rec, x);
-    if (st != RSIM_OK) { rep_push(rep, rec, M.g.n); rep->status = st; return st; }
+    if (st != RSIM_OK) { rep_push(rep, rec, M.g.n_live); rep->status = st; return st; }
     bool conv = rec.dp_inf_A < o.eps_p;
     double maxB = 0.0;
     bool expand = estimate_active(M, A, Bf, M.dp, o.eps_set, o.m, shrink_locked, &maxB);
     if (!expand) shrink_locked = true;
     rec.dp_inf_B = maxB;
     rec.mode_expand = expand ? 1 : 0;
-    rep_push(rep, rec, M.g.n);
+    rep_push(rep, rec, M.g.n_live);
     if (!expand && conv) { rep->converged = 1; return RSIM_OK; }
     Bf = boundary_of(M.g, A);
     act = to_list(A);
@@ -851,7 +859,7 @@ static int adaptive_dd(Model& M, const int32_t* va_init, int32_t n_init, const r
     rec.subdomain = -1;
     int st = local_step(M, act, o, rec, x);
     ++inner;
-    if (st != RSIM_OK) { rep_push(rep, rec, g.n); rep->status = st; return st; }
+    if (st != RSIM_OK) { rep_push(rep, rec, g.n_live); rep->status = st; return st; }
     double maxB = 0.0;
     std::vector<int32_t> seeds;
     for (int64_t i = 0; i < g.n; ++i)
@@ -863,7 +871,7 @@ static int adaptive_dd(Model& M, const int32_t* va_init, int32_t n_init, const r
     rec.dp_inf_B = maxB;
     bool expand = maxB >= o.eps_set;
     rec.mode_expand = expand;
-    rep_push(rep, rec, g.n);
+    rep_push(rep, rec, g.n_live);
     if (!expand) break;
     std::vector<uint8_t> mark(g.n, 0);
     dilate(g, seeds, o.m, mark);
@@ -881,7 +889,7 @@ static int adaptive_dd(Model& M, const int32_t* va_init, int32_t n_init, const r
     std::vector<uint8_t> in(g.n, 0), h(g.n, 0);
     for (int32_t i : sub[s]) in[i] = 1;
     for (int32_t i : sub[s])
-      g.each(i, [&](int64_t j, double) { if (!in[j]) h[j] = 1; });
+      g.each_live(i, [&](int64_t j, double) { if (!in[j]) h[j] = 1; });
     halo[s] = to_list(h);
   }
   std::vector<double> last(g.n, 0.0);
@@ -902,7 +910,7 @@ static int adaptive_dd(Model& M, const int32_t* va_init, int32_t n_init, const r
         rec.subdomain = s;
         int st = local_step(M, sub[s], o, rec, x);
         rec.dp_inf_B = hmax;
-        rep_push(rep, rec, g.n);
+        rep_push(rep, rec, g.n_live);
         if (st != RSIM_OK) { rep->outer_iterations = outer; rep->status = st; return st; }
         for (int32_t i : sub[s]) last[i] = std::fabs(M.dp[i]);
         normA[s] = rec.dp_inf_A;
@@ -990,7 +998,13 @@ void* orc_create(const rsim_graph_desc* gd, const rsim_fluid_params* f) {
     g.nt.assign(gd->nnc_t, gd->nnc_t + g.nptr[g.n]);
   }
   g.pinned.resize(g.n);
-  for (int64_t i = 0; i < g.n; ++i) g.pinned[i] = (uint8_t)(g.kind[i] == RSIM_KIND_FRACTURE || g.wi[i] > 0.0);
+  g.dead.resize(g.n);
+  g.n_live = 0;
+  for (int64_t i = 0; i < g.n; ++i) {
+    g.pinned[i] = (uint8_t)(g.kind[i] == RSIM_KIND_FRACTURE || g.wi[i] > 0.0);
+    g.dead[i] = (uint8_t)(g.kind[i] == RSIM_KIND_DEAD);
+    g.n_live += !g.dead[i];
+  }
   M->fl = phys::Fluid(*f);
   M->b = f->kind;
   M->u.assign(g.n * M->b, 0.0);
@@ -1078,7 +1092,7 @@ int32_t orc_outer_halo(void* h, const int32_t* va, int32_t n, int32_t* out) {
   std::vector<uint8_t> A(M.g.n, 0), H(M.g.n, 0);
   for (int32_t k = 0; k < n; ++k) A[va[k]] = 1;
   for (int32_t k = 0; k < n; ++k)
-    M.g.each(va[k], [&](int64_t j, double) { if (!A[j]) H[j] = 1; });
+    M.g.each_live(va[k], [&](int64_t j, double) { if (!A[j]) H[j] = 1; });
   std::vector<int32_t> l = to_list(H);
   std::copy(l.begin(), l.end(), out);
   return (int32_t)l.size();

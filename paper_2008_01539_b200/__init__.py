@@ -77,17 +77,24 @@ class Case:
     """Seeded synthetic input for one BASELINE.json config (include/rsim/cases.h)."""
 
     def __init__(self, config: int, nx: int = 0, ny: int = 0, nz: int = 0, seed: int = 0, n_dfn: int = -1,
-                 n_steps: int = -1, lib=None):
+                 n_steps: int = -1, lib=None, _handle=None):
         # lib: any library exporting include/rsim/cases.h (librsim.so by default; the
         # oracle's own liborsim.so links the same host-only generator, so the CPU
         # reference arm builds its inputs without loading the product library)
         L = lib if lib is not None else A.lib()
         self._L = L
-        o = A.CaseOpts(config, nx, ny, nz, seed, n_dfn, n_steps)
-        self._h = L.rsim_case_create(C.byref(o))
+        if _handle is not None:  # Case.from_file / Case.from_text
+            self._h = _handle
+        else:
+            o = A.CaseOpts(config, nx, ny, nz, seed, n_dfn, n_steps)
+            self._h = L.rsim_case_create(C.byref(o))
         if not self._h:
             raise RsimError(RSIM_EARG, f"bad case config {config}")
         self.config = config
+        info = A.CaseInfo()
+        L.rsim_case_info(self._h, C.byref(info))
+        self.n_live, self.n_frac, self.n_dead = int(info.n_live), int(info.n_frac), int(info.n_dead)
+        self.default_solver, self.default_m = int(info.solver), int(info.m)
         self.n = int(L.rsim_case_n(self._h))
         d = np.zeros(3, np.int32)
         s = np.zeros(3, np.float64)
@@ -100,6 +107,28 @@ class Case:
         L.rsim_case_fluid(self._h, C.byref(self.fluid))
         self.b = int(self.fluid.kind)
         self.n_nnc = int(L.rsim_case_n_nnc(self._h))
+
+    @classmethod
+    def from_text(cls, text: str, lib=None) -> "Case":
+        """A case file's text (grammar: include/rsim/cases.h; EDFM fractures)."""
+        L = lib if lib is not None else A.lib()
+        err = C.create_string_buffer(512)
+        h = L.rsim_case_from_text(text.encode(), err, 512)
+        if not h:
+            raise RsimError(RSIM_EARG, "case file: " + err.value.decode())
+        return cls(0, lib=L, _handle=h)
+
+    @classmethod
+    def from_file(cls, path: str, lib=None) -> "Case":
+        with open(path) as f:
+            return cls.from_text(f.read(), lib=lib)
+
+    def connections(self):
+        """(i, j, Υ) of every connection with Υ > 0, i < j (Cartesian faces, then NNCs)."""
+        k = int(self._L.rsim_case_connections(self._h, None, None, None, 0))
+        i, j, t = np.zeros(k, np.int32), np.zeros(k, np.int32), np.zeros(k)
+        self._L.rsim_case_connections(self._h, A.ptr(i, C.c_int32), A.ptr(j, C.c_int32), A.ptr(t, C.c_double), k)
+        return i, j, t
 
     def well_rates(self, states: "CellStates") -> np.ndarray:
         """Surface production rates (water, oil, gas) in m^3/s at `states`."""
@@ -368,15 +397,29 @@ SOLVERS = {"standard": 0, "localized": 1, "adaptive_dd": 2}
 def simulate(config: int, solver: str = "localized", out_dir: str | None = None, *, nx: int = 0, ny: int = 0,
              nz: int = 0, seed: int = 0, n_dfn: int = -1, m: int = 0, eps_p: float = 0.0, n_steps: int = 0,
              precond: int = -1, report_every_days: float = 0.0, write_fields: bool = True,
-             lin_method: int = -1) -> dict:
+             lin_method: int = -1, trace_flags: bool = False) -> dict:
     """Case runner (SPEC.md sim_driver_cli run_case, include/rsim/simulate.h): run a seeded
     config on the GPU with the named solver; writes rates.csv / metrics.csv / summary.txt
     (+ field dumps) into out_dir when given.  eps_p in Pa (0 -> case default)."""
     co = A.CaseOpts(config, nx, ny, nz, seed, n_dfn, -1)
-    so = A.SimOpts(SOLVERS[solver], m, eps_p, n_steps, precond, report_every_days, int(write_fields), lin_method)
+    so = A.SimOpts(SOLVERS[solver], m, eps_p, n_steps, precond, report_every_days, int(write_fields), lin_method,
+                   int(trace_flags))
     mt = A.RunMetrics()
     rc = A.lib().rsim_simulate(C.byref(co), C.byref(so), (out_dir or "").encode(), C.byref(mt))
     _check(rc, "simulate")
+    return {f: getattr(mt, f) for f, _ in A.RunMetrics._fields_ if f != "pad"}
+
+
+def simulate_file(case_file: str, solver: str | None = None, out_dir: str | None = None, *, m: int = 0,
+                  eps_p: float = 0.0, n_steps: int = 0, precond: int = -1, report_every_days: float = 0.0,
+                  write_fields: bool = True, lin_method: int = -1, trace_flags: bool = False) -> dict:
+    """Case runner on a case file (SPEC.md sim_driver_cli `simulate <case-file>`): EDFM
+    fractures, the file's schedule and [solver] defaults (solver None -> the file's)."""
+    so = A.SimOpts(SOLVERS[solver] if solver else -1, m, eps_p, n_steps, precond, report_every_days,
+                   int(write_fields), lin_method, int(trace_flags))
+    mt = A.RunMetrics()
+    rc = A.lib().rsim_simulate_file(case_file.encode(), C.byref(so), (out_dir or "").encode(), C.byref(mt))
+    _check(rc, "simulate_file")
     return {f: getattr(mt, f) for f, _ in A.RunMetrics._fields_ if f != "pad"}
 
 

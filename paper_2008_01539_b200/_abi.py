@@ -99,7 +99,14 @@ class SimOpts(C.Structure):
     _fields_ = [
         ("solver", C.c_int32), ("m", C.c_int32), ("eps_p", C.c_double), ("n_steps", C.c_int32),
         ("precond", C.c_int32), ("report_every_days", C.c_double), ("write_fields", C.c_int32),
-        ("lin_method", C.c_int32),
+        ("lin_method", C.c_int32), ("trace_flags", C.c_int32),
+    ]
+
+
+class CaseInfo(C.Structure):
+    _fields_ = [
+        ("n_live", C.c_int64), ("n_frac", C.c_int64), ("n_dead", C.c_int64), ("solver", C.c_int32),
+        ("m", C.c_int32), ("eps_p", C.c_double), ("total_time", C.c_double),
     ]
 
 
@@ -139,9 +146,15 @@ PROTOS: dict[str, tuple] = {
     "rsim_case_schedule": (C.c_int32, [P, dptr, C.c_int32]),
     "rsim_case_solver_opts": (C.c_int, [P, C.POINTER(SolverOpts)]),
     "rsim_case_n_nnc": (C.c_int64, [P]),
+    "rsim_case_from_text": (P, [C.c_char_p, C.c_char_p, C.c_int32]),
+    "rsim_case_from_file": (P, [C.c_char_p, C.c_char_p, C.c_int32]),
+    "rsim_case_info": (C.c_int, [P, C.POINTER(CaseInfo)]),
+    "rsim_case_connections": (C.c_int64, [P, i32ptr, i32ptr, dptr, C.c_int64]),
+    "rsim_edfm_avg_distance": (C.c_double, [C.c_double] * 8),
     # simulate.h (case runner, SPEC.md sim_driver_cli)
     "rsim_well_rates": (C.c_int, [P, dptr, u8ptr, dptr]),
     "rsim_simulate": (C.c_int, [C.POINTER(CaseOpts), C.POINTER(SimOpts), C.c_char_p, C.POINTER(RunMetrics)]),
+    "rsim_simulate_file": (C.c_int, [C.c_char_p, C.POINTER(SimOpts), C.c_char_p, C.POINTER(RunMetrics)]),
     # eos.h (Peng-Robinson flash)
     "rsim_eos_case3": (C.c_int, [C.POINTER(EosParams)]),
     "rsim_eos_flash": (C.c_int, [C.POINTER(EosParams), C.c_double, C.c_int64, dptr, dptr, u8ptr, dptr, dptr, dptr,

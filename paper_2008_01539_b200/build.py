@@ -33,7 +33,7 @@ NVFLAGS = ARCH + [
     "-Xptxas", "-v" if os.environ.get("RSIM_PTXAS_V") else "-O3",
     "-I", str(ROOT / "include"), "-I", str(CSRC),
 ]
-SOURCES = ["abi.cu", "assemble.cu", "krylov.cu", "krylov_dsm.cu", "krylov_gmres.cu", "ilu.cu", "sets.cu", "solvers.cpp", "cases.cpp", "simulate.cpp", "eos.cu", "direct.cu"]
+SOURCES = ["abi.cu", "assemble.cu", "krylov.cu", "krylov_dsm.cu", "krylov_gmres.cu", "ilu.cu", "sets.cu", "solvers.cpp", "cases.cpp", "edfm.cpp", "simulate.cpp", "eos.cu", "direct.cu"]
 CLI = PKG / "lib" / "simulate"
 
 
@@ -83,11 +83,12 @@ def build_oracle(force: bool = False) -> Path:
     # the oracle links its own copy of the host-only case generator (csrc/cases.cpp,
     # include/rsim/cases.h) so the CPU reference arm never loads librsim.so
     out = ORACLE / "_build" / "liborsim.so"
-    deps = [ORACLE / "oracle.cpp", ORACLE / "oracle_api.h", CSRC / "cases.cpp"] + _headers()
+    deps = [ORACLE / "oracle.cpp", ORACLE / "oracle_api.h", CSRC / "cases.cpp", CSRC / "edfm.cpp",
+            CSRC / "case_impl.h"] + _headers()
     if force or _stale(out, deps):
         out.parent.mkdir(parents=True, exist_ok=True)
         _run([HOSTCXX, "-O3", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off", "-shared",
-              "-I", str(ROOT / "include"), str(ORACLE / "oracle.cpp"), str(CSRC / "cases.cpp"), "-o", str(out)])
+              "-I", str(ROOT / "include"), str(ORACLE / "oracle.cpp"), str(CSRC / "cases.cpp"), str(CSRC / "edfm.cpp"), "-I", str(CSRC), "-o", str(out)])
     return out
 
 

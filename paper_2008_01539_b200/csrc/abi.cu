@@ -131,7 +131,16 @@ int rsim_internal_reset_scalars(rsim_gpu_ctx* c) {
   return RSIM_OK;
 }
 int rsim_internal_dd_begin(rsim_gpu_ctx* c) { return launch_dd_begin(c); }
-int64_t rsim_internal_n(const rsim_gpu_ctx* c) { return c->n; }
+void rsim_internal_set_iter_hook(rsim_gpu_ctx* c, int (*fn)(void*, int32_t, int32_t), void* user) {
+  c->iter_hook = fn;
+  c->iter_user = user;
+}
+double rsim_internal_dt(const rsim_gpu_ctx* c) { return c->dt; }
+int rsim_internal_iter_hook(rsim_gpu_ctx* c, int32_t iter, int32_t subdomain) {
+  return c->iter_hook ? c->iter_hook(c->iter_user, iter, subdomain) : RSIM_OK;
+}
+// cells of the graph for M_A = Σ n_A / n (dead filler cells are not cells of the model)
+int64_t rsim_internal_n(const rsim_gpu_ctx* c) { return c->n - c->n_dead; }
 int rsim_internal_b(const rsim_gpu_ctx* c) { return c->b; }
 int32_t rsim_internal_nA(const rsim_gpu_ctx* c) { return c->nA; }
 
@@ -190,6 +199,7 @@ int rsim_gpu_create(rsim_gpu_ctx** out, const rsim_graph_desc* g, const rsim_flu
   c->bhp = g->bhp;
   c->sm_count = sms;
   c->nnc_total = g->nnc_ptr ? g->nnc_ptr[c->n] : 0;
+  for (int64_t i = 0; i < c->n; ++i) c->n_dead += g->kind[i] == RSIM_KIND_DEAD;
   c->has_nnc = c->nnc_total > 0;
   const int64_t n = c->n, b = c->b;
   const int64_t nchunks = (n + RSIM_RED_CHUNK - 1) / RSIM_RED_CHUNK;

@@ -9,6 +9,7 @@
 // added to their shared face, or an NNC if they touch only at a corner.
 // Crossed cells are tagged fracture => always active.
 #include "rsim/cases.h"
+#include "case_impl.h"
 
 #include <omp.h>
 
@@ -23,9 +24,9 @@
 
 namespace {
 
-constexpr double kMilliDarcy = 9.869233e-16;  // m^2
-constexpr double kDay = 86400.0;
-constexpr double kCp = 1e-3;                  // Pa s
+using rsim_case_detail::kCp;
+using rsim_case_detail::kDay;
+using rsim_case_detail::kMilliDarcy;
 
 // SplitMix64 keyed by (seed, stream, index): counter-based, so every cell's
 // draw is independent of generation order.
@@ -49,25 +50,6 @@ struct Line {
 };
 
 }  // namespace
-
-struct rsim_case {
-  int config = 1;
-  int32_t nx = 0, ny = 0, nz = 0;
-  double dx = 10, dy = 10, dz = 1;
-  int64_t n = 0;
-  uint64_t seed = 0;
-  std::vector<double> kx, ky, kz, phi, tx, ty, tz, pv, wi;
-  std::vector<uint8_t> kind;
-  std::vector<int32_t> nptr, nnbr;
-  std::vector<double> nt;
-  rsim_fluid_params fl{};
-  double bhp = 0, p_init = 0, sw_init = 0;
-  int n_steps = 20;
-  double dt0 = 0.01 * kDay, growth = 1.5, dt_max = 1e30;
-  double eps = 0.2;
-  int m = 2;
-  std::map<std::pair<int64_t, int64_t>, double> nnc;
-};
 
 namespace {
 
@@ -342,6 +324,10 @@ void build_c5(rsim_case& c) {  // scaling stress, single phase, no Newton loop
 
 }  // namespace
 
+void rsim_case_finalize_nnc(rsim_case& c) { finalize_nnc(c); }
+void rsim_case_fluid_single(rsim_case& c) { set_fluid_single(c); }
+void rsim_case_fluid_oilwater(rsim_case& c) { set_fluid_oilwater(c); }
+
 extern "C" {
 
 rsim_case* rsim_case_create(const rsim_case_opts* o) {
@@ -407,9 +393,23 @@ int rsim_case_init_state(const rsim_case* c, double* u, uint8_t* st) {
   return 0;
 }
 
+// timestep_schedule: Δt_k = min(Δt_0·g^k, Δt_max); with a
+// total time T the ramp is truncated so that Σ Δt = T exactly (last step
+// shortened); otherwise n_steps steps.
 int32_t rsim_case_schedule(const rsim_case* c, double* dts, int32_t cap) {
   double dt = c->dt0;
   int32_t k = 0;
+  if (c->total_time > 0.0) {
+    double t = 0.0;
+    for (; t < c->total_time && k < cap; ++k) {
+      double d = std::min(dt, c->dt_max);
+      if (t + d >= c->total_time * (1.0 - 1e-12)) d = c->total_time - t;
+      dts[k] = d;
+      t += d;
+      dt *= c->growth;
+    }
+    return k;
+  }
   for (; k < c->n_steps && k < cap; ++k) {
     dts[k] = std::min(dt, c->dt_max);
     dt *= c->growth;

@@ -21,6 +21,7 @@ enum : uint8_t {
   F_T = 16,    // in V_T (DD total active set)
   F_D0 = 32,   // dilation ping-pong bits
   F_D1 = 64,
+  F_DEAD = 128,  // filler position of an EDFM fracture plane (RSIM_KIND_DEAD): no connections, never active
 };
 
 // Set-update modes of the final compaction pass.
@@ -61,6 +62,11 @@ struct rsim_gpu_ctx {
   int b = 1;
   int32_t nx = 0, ny = 0, nz = 0;
   int64_t n = 0;
+  int64_t n_dead = 0;
+  // per-Newton-iteration hook (case runner --trace-flags): called by the host
+  // solvers after each local solve + update, before the set update
+  int (*iter_hook)(void* user, int32_t iter, int32_t subdomain) = nullptr;
+  void* iter_user = nullptr;  // RSIM_KIND_DEAD cells (excluded from every set and from M_A's n)
   bool d3 = false;
   int nslot = 4;
   bool has_nnc = false;

@@ -29,11 +29,14 @@ struct Geo {
   int64_t n;
   bool d3, has_nnc;
   const int32_t *nptr, *nnbr;
+  const uint8_t* pin0;  // F_DEAD marks filler cells (only read when the graph has any)
+  bool has_dead;
 };
 
 __host__ Geo geo(const rsim_gpu_ctx* c) {
-  return Geo{c->nx, c->ny, c->nz, c->n, c->d3, c->has_nnc, c->nptr, c->nnbr};
+  return Geo{c->nx, c->ny, c->nz, c->n, c->d3, c->has_nnc, c->nptr, c->nnbr, c->pin0, c->n_dead > 0};
 }
+__device__ __forceinline__ bool is_dead(const Geo& g, int64_t i) { return g.has_dead && (g.pin0[i] & F_DEAD); }
 
 // Visit every graph neighbour of i (Cartesian + NNC).
 template <class F>
@@ -179,6 +182,7 @@ struct Geo4 {
   int64_t wplane;  // groups per plane (vec4)
   int32_t bs, nseg;
   bool d3, has_nnc, vec4;
+  bool has_dead;  // F_DEAD cells: never dilated into, count as kept in the boundary test
   const int32_t *nptr, *nnbr;
 };
 
@@ -192,6 +196,7 @@ __host__ Geo4 geo4(const rsim_gpu_ctx* c) {
   g.bs = g.wrow >= 256 ? 256 : ((g.wrow + 31) / 32) * 32;
   g.nseg = (g.wrow + g.bs - 1) / g.bs;
   g.d3 = c->d3; g.has_nnc = c->has_nnc;
+  g.has_dead = c->n_dead > 0;
   g.nptr = c->nptr; g.nnbr = c->nnbr;
   return g;
 }
@@ -285,6 +290,7 @@ __device__ __forceinline__ void dilate_tile(const Geo4& g, uint8_t* __restrict__
               if (flags[__ldg(&g.nnbr[q])] & bit_in) out |= 1u << (8 * k);
           }
         }
+        if (g.has_dead) out &= ~lanes(w, F_DEAD);  // graph distance over live cells only
         w = (w & ~(0x01010101u * bit_out)) | (out * bit_out);
         fw[p.t] = w;
       }
@@ -300,6 +306,7 @@ __device__ __forceinline__ void dilate_tile(const Geo4& g, uint8_t* __restrict__
         if (dil) {
           bool v = (f & bit_in) != 0;
           if (!v) each_nbr_xyz(g, i, ix, p.iy, p.iz, [&](int64_t j) { if (flags[j] & bit_in) v = true; });
+          if (f & F_DEAD) v = false;
           f = v ? (uint8_t)(f | bit_out) : (uint8_t)(f & ~bit_out);
           flags[i] = f;
         }
@@ -400,7 +407,11 @@ __device__ __forceinline__ void scatter_tile(const Geo4& g, const uint8_t* __res
       f4 = fw[p.t];
       keep = a_new4(f4, M.mode, ex, M.dbit);
       if (keep) {
-        auto L = [&](int64_t u) { return a_new4(__ldg(&fw[u]), M.mode, ex, M.dbit); };
+        // a dead neighbour is not a graph neighbour: it counts as kept
+        auto L = [&](int64_t u) {
+          const uint32_t w = __ldg(&fw[u]);
+          return a_new4(w, M.mode, ex, M.dbit) | (g.has_dead ? lanes(w, F_DEAD) : 0u);
+        };
         const uint32_t all = nbr_lanes4(g, p, keep, 0x01010101u, L, [](uint32_t x, uint32_t y) { return x & y; });
         bnd = keep & ~all & 0x01010101u;
         if (g.has_nnc)
@@ -424,7 +435,9 @@ __device__ __forceinline__ void scatter_tile(const Geo4& g, const uint8_t* __res
         if (a_new(f, M.mode, ex, M.dbit)) {
           keep |= 1u << (8 * k);
           bool b = false;
-          each_nbr_xyz(g, i, ix, p.iy, p.iz, [&](int64_t j) { if (!a_new(fin[j], M.mode, ex, M.dbit)) b = true; });
+          each_nbr_xyz(g, i, ix, p.iy, p.iz, [&](int64_t j) {
+            if (!(fin[j] & F_DEAD) && !a_new(fin[j], M.mode, ex, M.dbit)) b = true;
+          });
           if (b) bnd |= 1u << (8 * k);
         }
       }
@@ -450,7 +463,7 @@ __device__ __forceinline__ void scatter_tile(const Geo4& g, const uint8_t* __res
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const uint32_t f = (f4 >> (8 * k)) & 0xFFu;
-    uint32_t o = f & (F_PIN | F_T);
+    uint32_t o = f & (F_PIN | F_T | F_DEAD);
     gl[k] = -1;
     if ((keep >> (8 * k)) & 1u) {
       o |= F_A;
@@ -738,7 +751,7 @@ __global__ void __launch_bounds__(256) k_scatter_rg(Geo4 g, const uint8_t* __res
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const uint32_t f = (own[k] >> (8 * e)) & 0xFFu;
-      uint32_t o = f & (F_PIN | F_T);
+      uint32_t o = f & (F_PIN | F_T | F_DEAD);
       gl[e] = -1;
       if ((keep[k] >> (8 * e)) & 1u) {
         o |= F_A;
@@ -771,7 +784,7 @@ __global__ void k_pin_mask(int64_t n, const uint8_t* __restrict__ kind, const do
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   bool pin = kind[i] == RSIM_KIND_FRACTURE || wi[i] > 0.0;
-  pin0[i] = pin ? (uint8_t)(F_PIN | F_A) : (uint8_t)0;
+  pin0[i] = kind[i] == RSIM_KIND_DEAD ? (uint8_t)F_DEAD : (pin ? (uint8_t)(F_PIN | F_A) : (uint8_t)0);
 }
 
 // Reset flags to the pinned set (A|PIN), or to all-active: 16 cells per
@@ -782,13 +795,14 @@ __global__ void k_set_reset(int64_t n, const uint8_t* __restrict__ pin0, uint8_t
   const int64_t n16 = n / 16;
   if (t < n16) {
     uint4 v = reinterpret_cast<const uint4*>(pin0)[t];
-    if (all_active) {
-      const uint32_t a = 0x01010101u * F_A;
-      v.x |= a; v.y |= a; v.z |= a; v.w |= a;
+    if (all_active) {  // every live cell (dead filler cells stay out)
+      auto a = [](uint32_t w) { return (0x01010101u & ~((w >> 7) & 0x01010101u)) * F_A; };
+      v.x |= a(v.x); v.y |= a(v.y); v.z |= a(v.z); v.w |= a(v.w);
     }
     reinterpret_cast<uint4*>(flags)[t] = v;
   } else if (t == n16) {
-    for (int64_t i = 16 * n16; i < n; ++i) flags[i] = (uint8_t)(pin0[i] | (all_active ? F_A : 0));
+    for (int64_t i = 16 * n16; i < n; ++i)
+      flags[i] = (uint8_t)(pin0[i] | (all_active && !(pin0[i] & F_DEAD) ? F_A : 0));
   }
 }
 
@@ -872,7 +886,7 @@ __global__ void k_dd_begin(int64_t n, uint8_t* __restrict__ flags, int32_t* __re
 __device__ __forceinline__ bool dd_pred(const Geo& g, const int32_t* __restrict__ label, int64_t i, int k, int sel) {
   int32_t li = label[i];
   if (sel == 0) return li == k;
-  if (li == k) return false;
+  if (li == k || is_dead(g, i)) return false;
   bool h = false;
   each_nbr(g, i, [&](int64_t j) { if (label[j] == k) h = true; });
   return h;
@@ -892,6 +906,7 @@ __global__ void __launch_bounds__(256) k_dd_hist(Geo g, const int32_t* __restric
     if (i >= g.n) break;
     const int32_t li = label[i];
     if (li >= 0 && li < n_sub) atomicAdd(&sh[li], 1);
+    if (is_dead(g, i)) continue;
     // each distinct neighbour label counts once: the j-th neighbour counts
     // unless an earlier neighbour (enumeration order) carries the same label
     int idx = 0;
@@ -1252,7 +1267,7 @@ __global__ void __launch_bounds__(256) k_scatter_kb(Geo4 g, const uint8_t* __res
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const uint32_t f = (own[k] >> (8 * e)) & 0xFFu;
-      uint32_t o = f & (F_PIN | F_T);
+      uint32_t o = f & (F_PIN | F_T | F_DEAD);
       gl[e] = -1;
       if ((keep[k] >> (8 * e)) & 1u) {
         o |= F_A;
@@ -1369,7 +1384,7 @@ int launch_set_update(rsim_gpu_ctx* c, int mode, int round, double eps, int m, i
   const dim3 grg = rg_grid(g);
   // row groups reuse the ±y words RG-fold but give RG-fold fewer blocks: only
   // for grids large enough to fill the GPU many times over
-  const bool use_rg = g.vec4 && (int64_t)grg.x * grg.y >= 16 * 148;
+  const bool use_rg = g.vec4 && !g.has_dead && (int64_t)grg.x * grg.y >= 16 * 148;
   if (!use_rg && ntiles <= kCoopMaxTiles && coop_set_update_enabled()) {
     static int per_sm = 0;
     if (per_sm == 0) {

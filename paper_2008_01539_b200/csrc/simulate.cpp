@@ -20,6 +20,8 @@
 // hook after every timestep attempt: committed = 1 (accepted) or 0 (failed, about to be cut)
 typedef int (*rsim_step_cb)(void* user, double dt, const rsim_newton_report* rep, int committed);
 extern "C" void rsim_set_error_c(const char* msg);
+void rsim_internal_set_iter_hook(rsim_gpu_ctx* c, int (*fn)(void*, int32_t, int32_t), void* user);
+double rsim_internal_dt(const rsim_gpu_ctx* c);
 extern "C" int rsim_internal_run_case_cb(rsim_gpu_ctx* c, int32_t solver, const double* dts, int32_t nsteps,
                                          const rsim_solver_opts* o, int32_t* total_iters, double* total_ma,
                                          int64_t* total_na, int32_t* total_lin, int32_t* n_cuts, rsim_step_cb cb,
@@ -77,6 +79,8 @@ struct Run {
   FILE* iters = nullptr;
   int attempt = 0;
   rsim_run_metrics* m = nullptr;
+  bool trace = false;            // --trace-flags: flags_t<days>_iter<k>.txt per Newton iteration
+  std::vector<uint8_t> cat;      // Fig. 8 categories of the last iteration
 };
 
 bool mkdir_p(const std::string& d) {
@@ -106,6 +110,34 @@ int dump(const Run& R, const char* what, F&& val) {
     for (int64_t x = 0; x < nx; ++x) {
       if (x) std::fputc(' ', f);
       val(f, r * nx + x);
+    }
+    std::fputc('\n', f);
+  }
+  std::fclose(f);
+  return RSIM_OK;
+}
+
+// --trace-flags (Figs. 8-9, 11): the Fig. 8 category of every cell
+// after Newton iteration k of the timestep ending at t days — 0 inactive,
+// 1 active, 2 boundary layer, 3 active + updated (|δp| >= ε), 4 boundary +
+// updated; -1 marks dead EDFM filler positions.  Integer matrix, same layout
+// as the field dumps.  DD local solves are numbered in solve order.
+int trace_flags(void* user, int32_t iter, int32_t subdomain) {
+  (void)subdomain;
+  Run& R = *static_cast<Run*>(user);
+  R.cat.resize((size_t)R.n);
+  int r = rsim_gpu_download_flags(R.ctx, R.cat.data());
+  if (r != RSIM_OK) return r;
+  char name[512];
+  std::snprintf(name, sizeof(name), "%s/flags_t%.6g_iter%d.txt", R.dir.c_str(),
+                (R.t + rsim_internal_dt(R.ctx)) / kDay, iter);
+  FILE* f = std::fopen(name, "w");
+  if (!f) return RSIM_EARG;
+  const int64_t nx = R.nxyz[0], rows = R.n / nx;
+  for (int64_t row = 0; row < rows; ++row) {
+    for (int64_t x = 0; x < nx; ++x) {
+      const int64_t i = row * nx + x;
+      std::fprintf(f, x ? " %d" : "%d", R.g.kind[i] == RSIM_KIND_DEAD ? -1 : (int)R.cat[i]);
     }
     std::fputc('\n', f);
   }
@@ -189,15 +221,17 @@ int rsim_well_rates(const rsim_case* c, const double* u, const uint8_t* st, doub
   return RSIM_OK;
 }
 
-int rsim_simulate(const rsim_case_opts* co, const rsim_sim_opts* so, const char* out_dir, rsim_run_metrics* out) {
-  if (!co || !so || !out || so->solver < 0 || so->solver > 2) return RSIM_EARG;
-  if (so->precond < -1 || so->precond > RSIM_PREC_NEUMANN1 || so->lin_method < -1 || so->lin_method > RSIM_LIN_DIRECT) {
-    rsim_set_error_c("rsim_simulate: precond / lin_method out of range");
-    return RSIM_EARG;
-  }
-  std::memset(out, 0, sizeof(*out));
-  rsim_case* cs = rsim_case_create(co);
-  if (!cs) return RSIM_EARG;
+}  // extern "C"
+
+namespace {
+
+// run_case(cfg) of an already built case; takes ownership of cs.
+int run_sim(rsim_case* cs, const char* label, const rsim_sim_opts* so_in, const char* out_dir, rsim_run_metrics* out) {
+  rsim_case_info_t info;
+  rsim_case_info(cs, &info);
+  rsim_sim_opts sov = *so_in;
+  const rsim_sim_opts* so = &sov;
+  if (sov.solver < 0) sov.solver = info.solver;  // case default (case files: [solver] solver)
   Run R;
   R.cs = cs;
   R.m = out;
@@ -218,7 +252,7 @@ int rsim_simulate(const rsim_case_opts* co, const rsim_sim_opts* so, const char*
   rsim_solver_opts o;
   rsim_case_solver_opts(cs, &o);
   if (so->eps_p > 0.0) o.eps_p = o.eps_set = so->eps_p;
-  o.m = so->m > 0 ? so->m : (so->solver == 2 ? 4 : o.m);
+  o.m = so->m > 0 ? so->m : (so->solver == 2 && info.solver != 2 ? 4 : o.m);  // DD: m = 4
   if (so->precond >= 0) o.precond = so->precond;
   if (so->lin_method >= 0) o.lin_method = so->lin_method;
   int r = RSIM_OK;
@@ -240,8 +274,10 @@ int rsim_simulate(const rsim_case_opts* co, const rsim_sim_opts* so, const char*
                             "mode_expand,dp_inf_A,dp_inf_B,f_norm2,f_norminf,lin_relres\n");
     if (R.rates) std::fprintf(R.rates, "time_days,oil_rate,gas_rate,bhp,water_rate,oil_rate_bbl\n");
     if (R.metrics) std::fprintf(R.metrics, "step,time_days,dt_days,iterations,sum_nA_over_n,sum_nA,lin_iters,n_subdomains\n");
+    R.trace = so->trace_flags != 0;
   }
   if (r == RSIM_OK) r = rsim_gpu_create(&R.ctx, &R.g, &fp);
+  if (r == RSIM_OK && R.trace) rsim_internal_set_iter_hook(R.ctx, trace_flags, &R);
   if (r == RSIM_OK) r = rsim_gpu_set_state(R.ctx, R.u.data(), R.st.data(), dts[0]);
   if (r == RSIM_OK) {
     const auto t0 = std::chrono::steady_clock::now();
@@ -258,8 +294,9 @@ int rsim_simulate(const rsim_case_opts* co, const rsim_sim_opts* so, const char*
     FILE* f = std::fopen((R.dir + "/summary.txt").c_str(), "w");
     if (f) {
       static const char* names[3] = {"standard", "localized", "adaptive_dd"};
-      std::fprintf(f, "config %d  grid %dx%dx%d  n %lld  solver %s  m %d  eps_p %.6g Pa\n", co->config, R.nxyz[0],
-                   R.nxyz[1], R.nxyz[2], (long long)R.n, names[so->solver], o.m, o.eps_p);
+      std::fprintf(f, "case %s  grid %dx%dx%d  n %lld  live %lld  fracture_cells %lld  solver %s  m %d  eps_p %.6g Pa\n",
+                   label, R.nxyz[0], R.nxyz[1], R.nxyz[2], (long long)R.n, (long long)info.n_live,
+                   (long long)info.n_frac, names[so->solver], o.m, o.eps_p);
       std::fprintf(f, "status %d\ntimesteps %d\nsimulated_days %.10g\ncuts %d\n", r, out->timesteps, out->sim_days,
                    out->cuts);
       std::fprintf(f, "total_iterations %d\ntotal_linear_iterations %d\n", out->total_iters, out->total_lin);
@@ -277,6 +314,41 @@ int rsim_simulate(const rsim_case_opts* co, const rsim_sim_opts* so, const char*
   if (R.ctx) rsim_gpu_destroy(R.ctx);
   rsim_case_destroy(cs);
   return r;
+}
+
+bool opts_ok(const rsim_sim_opts* so) {
+  if (so->solver < -1 || so->solver > 2 || so->precond < -1 || so->precond > RSIM_PREC_NEUMANN1 ||
+      so->lin_method < -1 || so->lin_method > RSIM_LIN_DIRECT) {
+    rsim_set_error_c("rsim_simulate: solver / precond / lin_method out of range");
+    return false;
+  }
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rsim_simulate(const rsim_case_opts* co, const rsim_sim_opts* so, const char* out_dir, rsim_run_metrics* out) {
+  if (!co || !so || !out || so->solver < 0 || !opts_ok(so)) return RSIM_EARG;
+  std::memset(out, 0, sizeof(*out));
+  rsim_case* cs = rsim_case_create(co);
+  if (!cs) return RSIM_EARG;
+  char label[32];
+  std::snprintf(label, sizeof(label), "config%d", co->config);
+  return run_sim(cs, label, so, out_dir, out);
+}
+
+int rsim_simulate_file(const char* case_file, const rsim_sim_opts* so, const char* out_dir, rsim_run_metrics* out) {
+  if (!case_file || !so || !out || !opts_ok(so)) return RSIM_EARG;
+  std::memset(out, 0, sizeof(*out));
+  char err[512] = {0};
+  rsim_case* cs = rsim_case_from_file(case_file, err, sizeof(err));
+  if (!cs) {
+    rsim_set_error_c(err);
+    return RSIM_EARG;
+  }
+  return run_sim(cs, case_file, so, out_dir, out);
 }
 
 }  // extern "C"

@@ -1,14 +1,15 @@
 // simulate_main.cpp — command-line front end of the case runner
 // (SPEC.md sim_driver_cli "External Interfaces"):
 //
-//   simulate --config N [--nx X --ny Y --nz Z --seed S --n-dfn K]
+//   simulate <case-file> | --config N [--nx X --ny Y --nz Z --seed S --n-dfn K]
 //            [--solver standard|localized|adaptive_dd] [--m N] [--eps-p PSI]
 //            [--steps K] [--precond bj|neumann1|ilu0] [--lin bicgstab|gmres|direct] [--out DIR]
-//            [--report-every DAYS] [--no-fields]
+//            [--report-every DAYS] [--no-fields] [--trace-flags]
 //
-// The reference's case-file grammar was never written (geometry
-// "read from figures only"), so a case is one of the seeded synthetic
-// configs of BASELINE.json (rsim/cases.h) with optional overrides.
+// A case is either a case file (the SPEC's key = value + fracture-table text,
+// grammar in rsim/cases.h; EDFM fractures; cases/*.case hold the paper's
+// Case 1 / Case 2 and the grid-sensitivity models) or one of the seeded
+// synthetic configs of BASELINE.json with optional overrides.
 // Exit codes: 0 success, 2 configuration error, 3 solver failure.
 #include <cstdio>
 #include <cstdlib>
@@ -20,9 +21,10 @@
 static int usage(const char* msg) {
   if (msg) std::fprintf(stderr, "simulate: %s\n", msg);
   std::fprintf(stderr,
-               "usage: simulate --config N [--nx X --ny Y --nz Z --seed S --n-dfn K] "
+               "usage: simulate <case-file> | --config N [--nx X --ny Y --nz Z --seed S --n-dfn K] "
                "[--solver standard|localized|adaptive_dd] [--m N] [--eps-p PSI] [--steps K] "
-               "[--precond bj|neumann1|ilu0] [--lin bicgstab|gmres|direct] [--out DIR] [--report-every DAYS] [--no-fields]\n");
+               "[--precond bj|neumann1|ilu0] [--lin bicgstab|gmres|direct] [--out DIR] [--report-every DAYS] "
+               "[--no-fields] [--trace-flags]\n");
   return 2;
 }
 
@@ -33,16 +35,22 @@ int main(int argc, char** argv) {
   co.n_steps = -1;
   rsim_sim_opts so;
   std::memset(&so, 0, sizeof(so));
-  so.solver = 1;
+  so.solver = -1;  // case default (seeded configs: localized)
   so.precond = -1;
   so.lin_method = -1;
   so.write_fields = 1;
-  std::string out;
+  std::string out, case_file;
   for (int k = 1; k < argc; ++k) {
     const std::string a = argv[k];
     auto next = [&]() -> const char* { return k + 1 < argc ? argv[++k] : nullptr; };
     const char* v = nullptr;
     if (a == "--no-fields") { so.write_fields = 0; continue; }
+    if (a == "--trace-flags") { so.trace_flags = 1; continue; }
+    if (a.size() && a[0] != '-') {
+      if (!case_file.empty()) return usage("more than one case file");
+      case_file = a;
+      continue;
+    }
     if (a == "-h" || a == "--help") return usage(nullptr), 0;
     if (!(v = next())) return usage(("missing value for " + a).c_str());
     char* end = nullptr;
@@ -83,11 +91,18 @@ int main(int argc, char** argv) {
     }
     if (!end || *end) return usage(("bad value for " + a).c_str());
   }
-  if (co.config < 1 || co.config > 4) return usage("--config must be 1..4 (config 5 has no time loop)");
+  if (case_file.empty() == (co.config == 0)) return usage("give either a case file or --config N");
+  if (case_file.empty() && (co.config < 1 || co.config > 4))
+    return usage("--config must be 1..4 (config 5 has no time loop)");
   if (so.eps_p < 0.0 || so.report_every_days < 0.0) return usage("negative --eps-p / --report-every");
+  if (case_file.empty() && so.solver < 0) so.solver = 1;
   rsim_run_metrics m;
-  const int r = rsim_simulate(&co, &so, out.c_str(), &m);
-  if (r == RSIM_EARG) return usage("invalid case or output directory");
+  const int r = case_file.empty() ? rsim_simulate(&co, &so, out.c_str(), &m)
+                                  : rsim_simulate_file(case_file.c_str(), &so, out.c_str(), &m);
+  if (r == RSIM_EARG) {
+    const std::string why = std::string("invalid case or output directory: ") + rsim_gpu_last_error();
+    return usage(why.c_str());
+  }
   if (r != RSIM_OK) {
     std::fprintf(stderr, "simulate: solver failure (code %d): %s\n", r, rsim_gpu_last_error());
     return 3;

@@ -22,6 +22,7 @@ int rsim_internal_begin_step(rsim_gpu_ctx* c, double dt);
 int rsim_internal_commit_step(rsim_gpu_ctx* c);
 int rsim_internal_dd_begin(rsim_gpu_ctx* c);
 int64_t rsim_internal_n(const rsim_gpu_ctx* c);
+int rsim_internal_iter_hook(rsim_gpu_ctx* c, int32_t iter, int32_t subdomain);
 int rsim_internal_b(const rsim_gpu_ctx* c);
 int32_t rsim_internal_nA(const rsim_gpu_ctx* c);
 extern "C" int rsim_internal_add_row_iters(rsim_gpu_ctx* c, int64_t v);
@@ -76,6 +77,7 @@ int standard_dev(rsim_gpu_ctx* c, const rsim_solver_opts* o, rsim_newton_report*
   TRY(rsim_gpu_set_active(c, nullptr, -1, &s));
   for (int it = 0; it < o->max_newton; ++it) {
     TRY(local_step(c, o));
+    TRY(rsim_internal_iter_hook(c, it, -1));
     TRY(rsim_gpu_stats_get(c, &s));
     rsim_iter_record rec{};
     rec.subdomain = -1;
@@ -98,6 +100,7 @@ int localized_dev(rsim_gpu_ctx* c, const rsim_solver_opts* o, rsim_newton_report
   for (int it = 0; it < o->max_newton; ++it) {
     const int32_t nA = rsim_internal_nA(c);
     TRY(local_step(c, o));
+    TRY(rsim_internal_iter_hook(c, it, -1));
     // set update for the next iteration (device-side mode decision) + the
     // single scalar D2H of this iteration
     TRY(rsim_gpu_estimate_active(c, o->eps_set, o->m, shrink_locked, &s));
@@ -127,6 +130,7 @@ int dd_dev(rsim_gpu_ctx* c, const rsim_solver_opts* o, rsim_newton_report* rep) 
     if (inner >= o->max_newton) { rep->status = RSIM_ENOCONV; return RSIM_ENOCONV; }
     const int32_t nA = rsim_internal_nA(c);
     TRY(local_step(c, o));
+    TRY(rsim_internal_iter_hook(c, inner, -1));
     ++inner;
     TRY(rsim_gpu_dd_expand(c, o->eps_set, o->m, k + 1, &s));
     rsim_iter_record rec{};
@@ -154,6 +158,7 @@ int dd_dev(rsim_gpu_ctx* c, const rsim_solver_opts* o, rsim_newton_report* rep) 
       const double hmax = s.halo_max;
       if (first || normA[sd] >= o->eps_set || hmax >= o->eps_set) {
         TRY(local_step(c, o));
+        TRY(rsim_internal_iter_hook(c, rep->iterations, sd));
         TRY(rsim_gpu_stats_get(c, &s));
         rsim_iter_record rec{};
         rec.subdomain = sd;

@@ -1,0 +1,296 @@
+"""EDFM fracture discretization, case files and the paper's Cases 1 / 2
+(SPEC.md:52-60 discretize_fractures, :463-466 / :522-524 case files, :535-544
+acceptance criteria; §5).
+
+CPU: the SPEC's discretize_fractures examples (1x1 grid -> 1 fracture cell +
+1 matrix-fracture connection; <d> of a bisecting fracture = a/4; fracture-cell
+count = cells crossed by each segment from an independent line walk),
+refinement consistency of the fracture volume, graph positivity / symmetry,
+the total-time schedule, the oracle's neighbor_set on an EDFM graph against a
+BFS over the connection list (dead filler cells are not graph neighbours),
+case-file errors and the CLI's exit code 2.
+GPU: the sm_100a path equals the oracle bit for bit on the paper cases (all
+three solvers), the --trace-flags maps, and the SPEC acceptance criteria on
+the paper's cases (each checked value is reported by the assertion message).
+"""
+import hashlib
+import os
+import subprocess
+from collections import deque
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2008_01539_b200 as pkg
+from oracle import Oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CASES = os.path.join(ROOT, "cases")
+CLI = os.path.join(ROOT, "paper_2008_01539_b200", "lib", "simulate")
+PSI = 6894.757293168361
+DAY = 86400.0
+
+BASE = """
+[grid]
+nx = {nx}
+ny = {ny}
+dx = {dx}
+dy = {dy}
+thickness = 1
+[rock]
+porosity = 0.05
+perm = 1e-19
+c_r = 3.4e-4
+[fluid]
+model = oilwater
+[initial]
+pressure = 2500
+sw = 0.2
+[well]
+bhp = 1000
+trajectory = {well}
+[time]
+total = 1500
+dt0 = 0.1
+growth = 1.2
+dt_max = 100
+[solver]
+solver = localized
+m = 2
+eps_p = 0.3
+[fractures]
+{fracs}
+"""
+
+
+def case_text(nx=10, ny=10, dx=1.0, dy=1.0, well="0.05 5.05 9.95 5.05", fracs="5.3 1.1 5.3 8.9 1e-3 1e-10"):
+    return BASE.format(nx=nx, ny=ny, dx=dx, dy=dy, well=well, fracs=fracs)
+
+
+def test_one_cell_segment_gives_one_fracture_cell_and_one_connection():
+    c = oracle.case_from_text(case_text(nx=1, ny=1, dx=2.0, dy=2.0, well="0 1 2 1", fracs="1 0 1 2 1e-3 1e-10"))
+    assert (c.n_frac, c.n_live, c.n_dead) == (1, 2, 0)
+    i, j, t = c.connections()
+    assert list(zip(i, j)) == [(0, 1)] and t[0] > 0  # the matrix-fracture NNC (a z-face of plane 1)
+    # k_eff A_f / <d>: k_eff = harmonic mean of k_m, k_f; A_f = 2 L h; <d> = a/4 (bisecting)
+    keff = 2 * 1e-19 * 1e-10 / (1e-19 + 1e-10)
+    np.testing.assert_allclose(t[0], keff * 2 * 2.0 * 1.0 / 0.5, rtol=1e-14)
+
+
+def test_avg_distance_of_bisecting_fracture_is_a_over_4():
+    L = pkg._abi.lib()
+    for a in (0.5, 1.0, 3.0):
+        assert L.rsim_edfm_avg_distance(0.0, 0.0, a, a, a / 2, 0.0, a / 2, a) == pytest.approx(a / 4, rel=1e-15)
+        assert L.rsim_edfm_avg_distance(0.0, 0.0, a, a, 0.0, a / 2, a, a / 2) == pytest.approx(a / 4, rel=1e-15)
+    # diagonal through the cell: the 8x8 midpoint rule (numpy restatement) and, within 2 %,
+    # the analytic mean distance a / (3 sqrt 2)
+    d = L.rsim_edfm_avg_distance(0.0, 0.0, 1.0, 1.0, 0.0, 0.0, 1.0, 1.0)
+    g = (np.arange(8) + 0.5) / 8
+    X, Y = np.meshgrid(g, g)
+    assert d == pytest.approx(np.mean(np.abs(X - Y)) / np.sqrt(2), rel=1e-14)
+    assert d == pytest.approx(1 / (3 * np.sqrt(2)), rel=2e-2)
+
+
+def crossed_cells(x0, y0, x1, y1, dx, dy, nx, ny, samples=200000):
+    """Independent line walk: cells visited by a finely sampled segment (grid-corner touches excluded)."""
+    t = (np.arange(samples) + 0.5) / samples
+    x, y = x0 + (x1 - x0) * t, y0 + (y1 - y0) * t
+    ix, iy = np.clip(np.floor(x / dx).astype(int), 0, nx - 1), np.clip(np.floor(y / dy).astype(int), 0, ny - 1)
+    return len(set(zip(ix.tolist(), iy.tolist())))
+
+
+@pytest.mark.parametrize("name", ["paper_case1", "paper_case2", "paper_case1_grid20", "paper_case1_grid50"])
+def test_fracture_cell_count_volume_and_graph(name):
+    path = os.path.join(CASES, name + ".case")
+    c = oracle.case_from_file(path)
+    rows = []
+    sec = None
+    for ln in open(path):
+        ln = ln.split("#")[0].strip()
+        if ln.startswith("["):
+            sec = ln
+        elif ln and sec == "[fractures]":
+            rows.append([float(v) for v in ln.split()])
+    # one fracture cell per (segment x crossed matrix cell)
+    assert c.n_frac == sum(crossed_cells(r[0], r[1], r[2], r[3], c.dx, c.dy, c.nx, c.ny) for r in rows)
+    # refinement consistency: total fracture volume = Σ L · aperture · thickness
+    vol = sum(np.hypot(r[2] - r[0], r[3] - r[1]) * r[4] * c.dz for r in rows)
+    np.testing.assert_allclose(c.pv[c.kind == 1].sum(), vol, rtol=1e-12)
+    # graph: positive Υ, every fracture cell connected, dead cells isolated, NNC CSR symmetric
+    i, j, t = c.connections()
+    assert np.all(t > 0) and np.all(i < j)
+    deg = np.bincount(np.concatenate([i, j]), minlength=c.n)
+    assert np.all(deg[c.kind == 1] >= 2)  # its matrix cell + a fracture neighbour
+    assert np.all(deg[c.kind == 2] == 0)
+    assert c.n_live + c.n_dead == c.n and c.n_live == c.nx * c.ny + c.n_frac
+    if c.n_nnc:
+        ptr, nbr, nt = c.nnc()
+        pairs = {}
+        for a in range(c.n):
+            for q in range(ptr[a], ptr[a + 1]):
+                pairs[(a, int(nbr[q]))] = nt[q]
+        assert all(pairs.get((b, a)) == v for (a, b), v in pairs.items())
+
+
+def test_total_time_schedule():
+    c = oracle.case_from_file(os.path.join(CASES, "paper_case1.case"))
+    d = c.schedule()
+    assert d.sum() == pytest.approx(1500 * DAY, rel=1e-14)
+    assert 48 <= len(d) <= 55  # "≈ 48–55 steps"
+    assert np.all(d[:-1] <= 100 * DAY * (1 + 1e-12)) and d[0] == pytest.approx(0.1 * DAY)
+
+
+def bfs(n, i, j, src, m):
+    adj = [[] for _ in range(n)]
+    for a, b in zip(i.tolist(), j.tolist()):
+        adj[a].append(b)
+        adj[b].append(a)
+    dist = {src: 0}
+    q = deque([src])
+    while q:
+        u = q.popleft()
+        if dist[u] == m:
+            continue
+        for v in adj[u]:
+            if v not in dist:
+                dist[v] = dist[u] + 1
+                q.append(v)
+    return sorted(dist)
+
+
+def test_oracle_neighbor_set_is_graph_distance_over_live_cells():
+    """neighbor_set on an EDFM graph = BFS over the connection list: the
+    dead positions of the fracture plane are structural neighbours but not graph ones."""
+    c = oracle.case_from_file(os.path.join(CASES, "paper_case1_grid20.case"))
+    o = Oracle(c)
+    i, j, _ = c.connections()
+    rng = np.random.default_rng(3)
+    live = np.flatnonzero(c.kind != 2)
+    for src in list(rng.choice(live, 12, replace=False)) + list(np.flatnonzero(c.kind == 1)[:4]):
+        for m in (1, 2, 3):
+            got = sorted(o.neighbor_set(int(src), m).tolist())
+            assert got == bfs(c.n, i, j, int(src), m), (src, m)
+
+
+@pytest.mark.parametrize("bad, why", [
+    (case_text().replace("nx = 10", ""), "missing [grid] nx"),
+    (case_text(fracs="5.3 1.1 5.3 18.9 1e-3 1e-10"), "outside the grid"),
+    (case_text(fracs="5.3 1.1 5.3 8.9 0 1e-10"), "aperture"),
+    (case_text(fracs="5.3 1.1 5.3"), "fracture row"),
+    (case_text(well="0 0.5 10 0.5"), "crosses no fracture"),
+    (case_text().replace("solver = localized", "solver = newtonian"), "solver"),
+    (case_text().replace("dt_max = 100", "dt_max = 5000"), "[time]"),
+])
+def test_case_file_errors(bad, why):
+    with pytest.raises(pkg.RsimError) as e:
+        oracle.case_from_text(bad)
+    assert why in str(e.value)
+
+
+def test_cli_bad_case_file_exits_2(tmp_path):
+    p = tmp_path / "bad.case"
+    p.write_text(case_text(fracs="5.3 1.1 5.3 18.9 1e-3 1e-10"))
+    r = subprocess.run([CLI, str(p), "--out", str(tmp_path / "o")], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 2 and "outside the grid" in r.stderr, r.stderr
+    r = subprocess.run([CLI, str(p), "--config", "1"], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 2
+
+
+# ------------------------------------------------------------------ GPU
+def digest(s):
+    return hashlib.sha256(s.u.tobytes()).hexdigest(), hashlib.sha256(s.status.tobytes()).hexdigest()
+
+
+def run_both(name, solver):
+    path = os.path.join(CASES, name + ".case")
+    oracle.set_threads(len(os.sched_getaffinity(0)))
+    co = oracle.case_from_file(path)
+    opts = co.solver_opts()
+    if solver == 2:
+        opts.m = 4
+    ro = Oracle(co).run_case(solver, co.init_state(), co.schedule(), opts)
+    cg = pkg.Case.from_file(path)
+    sim = pkg.GpuSimulator(cg)
+    rg = sim.run_case(solver, cg.init_state(), cg.schedule(), opts)
+    sim.close()
+    return co, ro, rg
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["paper_case1_grid20", "paper_case1_grid50", "paper_case1", "paper_case2"])
+@pytest.mark.parametrize("solver", [0, 1, 2])
+def test_gpu_paper_cases_bit_exact(name, solver):
+    co, ro, rg = run_both(name, solver)
+    for k in ("status", "iterations", "sum_na", "lin_iters", "cuts"):
+        assert rg[k] == ro[k], (k, rg[k], ro[k])
+    assert rg["total_ma"] == ro["total_ma"]
+    assert digest(rg["states"]) == digest(ro["states"])
+
+
+def sim_file(name, tmp_path, solver=None, **kw):
+    out = tmp_path / f"{name}_{solver}"
+    m = pkg.simulate_file(os.path.join(CASES, name + ".case"), solver, str(out), **kw)
+    return m, out
+
+
+@pytest.mark.gpu
+def test_gpu_trace_flags(tmp_path):
+    m, out = sim_file("paper_case1_grid20", tmp_path, "localized", trace_flags=True, write_fields=False,
+                      n_steps=3)
+    files = sorted(p for p in os.listdir(out) if p.startswith("flags_t"))
+    assert len(files) == m["total_iters"] > 0
+    c = oracle.case_from_file(os.path.join(CASES, "paper_case1_grid20.case"))
+    for f in files:
+        a = np.loadtxt(out / f, dtype=int)
+        assert a.shape == (c.ny * c.nz, c.nx)
+        v = a.reshape(-1)
+        assert set(np.unique(v)) <= {-1, 0, 1, 2, 3, 4}
+        assert np.array_equal(v == -1, c.kind == 2)  # dead filler positions
+        assert np.all(v[c.kind == 1] > 0)  # fracture cells are always active
+
+
+@pytest.mark.gpu
+def test_gpu_acceptance_case1_single_50_day_step(tmp_path):
+    """SPEC acceptance 8 (Figs. 8-9): one 50-day timestep of Case 1 with localized Newton
+    converges in <= 6 iterations, |V_A| nondecreasing while expanding, decreasing after."""
+    text = open(os.path.join(CASES, "paper_case1.case")).read()
+    text = text.replace("total = 1500", "total = 50").replace("dt0 = 0.1", "dt0 = 50").replace(
+        "dt_max = 100", "dt_max = 50")
+    p = tmp_path / "c1_50d.case"
+    p.write_text(text)
+    m = pkg.simulate_file(str(p), "localized", str(tmp_path / "o"), write_fields=False)
+    rows = [r.split(",") for r in open(tmp_path / "o" / "iterations.csv").read().splitlines()[1:]]
+    na = [int(r[5]) for r in rows]
+    mode = [int(r[9]) for r in rows]
+    assert m["status"] == 0 and m["timesteps"] == 1 and len(rows) <= 6, (len(rows), na, mode)
+    ex = [k for k, e in enumerate(mode) if e]
+    assert all(na[k + 1] >= na[k] for k in ex if k + 1 < len(na)), (na, mode)
+    sh = [k for k, e in enumerate(mode) if not e]
+    assert all(na[k + 1] < na[k] for k in sh if k + 1 < len(na)), (na, mode)
+
+
+@pytest.mark.gpu
+def test_gpu_acceptance_grid_sensitivity(tmp_path):
+    """SPEC acceptance 9 (§5.1, Fig. 4): cumulative oil at 1500 days
+    20x20 < 50x50 < 200x200, each gap > 2 %."""
+    oil = [sim_file(n, tmp_path, "standard", write_fields=False)[0]["cum_oil_m3"]
+           for n in ("paper_case1_grid20", "paper_case1_grid50", "paper_case1")]
+    assert oil[0] * 1.02 < oil[1] and oil[1] * 1.02 < oil[2], oil
+
+
+@pytest.mark.gpu
+def test_gpu_acceptance_solution_equivalence_case1(tmp_path):
+    """SPEC acceptance 1: localized and adaptive DD match standard Newton on Case 1 —
+    pressure within 2 eps_p = 0.6 psi at the end, oil rates within 0.5 % at every step."""
+    res = {}
+    for sv in ("standard", "localized", "adaptive_dd"):
+        m, out = sim_file("paper_case1", tmp_path, sv)
+        rates = np.loadtxt(out / "rates.csv", delimiter=",", skiprows=1)
+        pf = sorted(p for p in os.listdir(out) if p.startswith("pressure_t"))[-1]
+        res[sv] = (rates[:, 1], np.loadtxt(out / pf))
+    for sv in ("localized", "adaptive_dd"):
+        dp = np.abs(res[sv][1] - res["standard"][1]).max()
+        assert dp <= 0.6, (sv, dp)
+        rel = np.abs(res[sv][0] - res["standard"][0]) / np.abs(res["standard"][0])
+        assert rel.max() <= 5e-3, (sv, rel.max())
