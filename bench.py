@@ -755,6 +755,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--configs", default="1,2,3", help="per-config lines besides the headline ('' to skip)")
+    ap.add_argument("--paper", type=int, default=1, help="paper Tables 2/3/5/6 on the EDFM case files (0 to skip)")
     ap.add_argument("--c5", default="0.01,0.05,0.2,0.5,1.0", help="config-5 active fractions ('' to skip)")
     ap.add_argument("--c5-ilu", default="0.05", help="fractions that also get the ILU(0) row ('' to skip)")
     ap.add_argument("--c5-reps", type=int, default=3)
@@ -822,6 +823,8 @@ def main():
             m.pop("_final")
             per[CONFIGS[cfg]["key"]] = m
         line["per_config"] = per
+    if rank == 0 and ws == 1 and args.paper:
+        line["paper_tables"] = paper_tables(pkg)
     if rank == 0 and ws == 1 and args.c5:
         fr = [float(x) for x in args.c5.split(",") if x]
         ilu_fr = [float(x) for x in args.c5_ilu.split(",") if x.strip()]
@@ -835,6 +838,42 @@ def main():
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+# Paper Tables 2 / 3 / 5 / 6 (§5) with the SPEC acceptance bands 2, 3, 5, 6
+# on the EDFM case files (cases/*.case; geometry is a [choice]).
+PAPER = {"paper_case1": {"table": 2, "localized": (159, 11.4, 0.072), "standard": (156, 156, 1.0),
+                         "dd_table": 5, "adaptive_dd": (804, 20.8, 0.026)},
+         "paper_case2": {"table": 3, "localized": (155, 10.1, 0.065), "standard": (153, 153, 1.0),
+                         "dd_table": 6, "adaptive_dd": (255, 13.6, 0.053)}}
+
+
+def paper_tables(pkg) -> dict:
+    out = {}
+    for name, ref in PAPER.items():
+        path = os.path.join(ROOT, "cases", name + ".case")
+        r = {}
+        for sv in ("standard", "localized", "adaptive_dd"):
+            m = pkg.simulate_file(path, sv, None, write_fields=False)
+            r[sv] = {"timesteps": m["timesteps"], "iterations": m["total_iters"], "total_MA": m["total_ma"],
+                     "avg_MA": m["avg_ma"], "outer_iterations": m["total_outer"], "krylov_iters": m["total_lin"],
+                     "cuts": m["cuts"], "solver_wall_s": m["wall_s"], "status": m["status"],
+                     "paper_iterations_totalMA_avgMA": ref[sv]}
+        std, loc, dd = r["standard"], r["localized"], r["adaptive_dd"]
+        bands = {"localized_total_MA <= standard/6": loc["total_MA"] <= std["total_MA"] / 6,
+                 "localized_avg_MA <= 0.15": loc["avg_MA"] <= 0.15}
+        if name == "paper_case1":
+            bands["localized_iterations <= 1.25 x standard"] = loc["iterations"] <= 1.25 * std["iterations"]
+            bands["dd_total_MA <= standard/5"] = dd["total_MA"] <= std["total_MA"] / 5
+            bands["dd_inner <= 8 x standard"] = dd["iterations"] <= 8 * std["iterations"]
+            bands["dd_outer_per_step <= 2 x standard_per_step"] = \
+                dd["outer_iterations"] / dd["timesteps"] <= 2 * std["iterations"] / std["timesteps"]
+        else:
+            bands["dd_total_MA <= standard/6"] = dd["total_MA"] <= std["total_MA"] / 6
+            bands["dd_inner <= 3 x standard"] = dd["iterations"] <= 3 * std["iterations"]
+        r["spec_acceptance"] = {"tables": (ref["table"], ref["dd_table"]), "bands": bands}
+        out[name] = r
+    return out
 
 
 def active_fraction_log(pkg, cfg: int) -> dict:

@@ -71,6 +71,7 @@ typedef struct {
   double sim_days;
   double cum_oil_m3, cum_water_m3, cum_gas_m3;  /* surface volumes               */
   double wall_s;             /* host wall time of the solver loop                */
+  int64_t total_outer;       /* DD outer (Schwarz sweep) iterations of the committed steps */
 } rsim_run_metrics;
 
 /* Surface-condition production rates of the case's producer at state (u, st):

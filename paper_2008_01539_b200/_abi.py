@@ -116,6 +116,7 @@ class RunMetrics(C.Structure):
         ("cuts", C.c_int32), ("pad", C.c_int32), ("sum_na", C.c_int64), ("total_ma", C.c_double),
         ("avg_ma", C.c_double), ("sim_days", C.c_double), ("cum_oil_m3", C.c_double),
         ("cum_water_m3", C.c_double), ("cum_gas_m3", C.c_double), ("wall_s", C.c_double),
+        ("total_outer", C.c_int64),
     ]
 
 

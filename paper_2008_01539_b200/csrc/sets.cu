@@ -412,7 +412,9 @@ __device__ __forceinline__ void scatter_tile(const Geo4& g, const uint8_t* __res
           const uint32_t w = __ldg(&fw[u]);
           return a_new4(w, M.mode, ex, M.dbit) | (g.has_dead ? lanes(w, F_DEAD) : 0u);
         };
-        const uint32_t all = nbr_lanes4(g, p, keep, 0x01010101u, L, [](uint32_t x, uint32_t y) { return x & y; });
+        // (the word's own lanes feed the ±x neighbours inside the word: dead ones count as kept too)
+        const uint32_t self = keep | (g.has_dead ? lanes(f4, F_DEAD) : 0u);
+        const uint32_t all = nbr_lanes4(g, p, self, 0x01010101u, L, [](uint32_t x, uint32_t y) { return x & y; });
         bnd = keep & ~all & 0x01010101u;
         if (g.has_nnc)
 #pragma unroll

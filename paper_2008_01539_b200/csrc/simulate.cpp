@@ -188,6 +188,7 @@ int on_step(void* user, double dt, const rsim_newton_report* rep, int committed)
   m.cum_oil_m3 += q[1] * dt;
   m.cum_gas_m3 += q[2] * dt;
   m.timesteps += 1;
+  m.total_outer += rep->outer_iterations;
   if (R.rates)
     std::fprintf(R.rates, "%.10g,%.10g,%.10g,%.10g,%.10g,%.10g\n", R.t / kDay, q[1] * kDay, q[2] * kDay,
                  R.g.bhp / kPsi, q[0] * kDay, q[1] * kDay / kBbl);

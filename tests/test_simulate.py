@@ -89,7 +89,7 @@ def _summary(path):
     out = {}
     for line in open(path):
         k, _, v = line.strip().partition(" ")
-        if k and v and k != "config":
+        if k and v and k not in ("config", "case"):  # the first line describes the case
             out[k] = float(v)
     return out
 
