@@ -208,8 +208,8 @@ print(json.dumps({{"a": sim.active().tolist(), "b": sim.boundary().tolist(), "ex
                                   (256, 64, 19),    # 3D full set: z-marching tile kernel, partial last z-chunk
                                   (512, 32, 24)])
 def test_full_set_tile_assembly_bit_exact(dims):
-    """Full-set b=1 assembly above the row-kernel threshold runs the tile kernels
-    (k_assemble_full1 in 2D, k_assemble_full1z in 3D): F, rhs, the scaled
+    """Full-set b=1 assembly above the row-kernel threshold runs the tile kernel
+    (k_assemble_tile1<D3, false>, 256 x 4 tiles of a plane): F, rhs, the scaled
     blocks and the canonical (F,F) partials must equal the oracle's."""
     nx, ny, nz = dims
     case = pkg.Case(5, nx=nx, ny=ny, nz=nz)
@@ -239,6 +239,46 @@ def test_full_set_tile_assembly_bit_exact(dims):
     assert g.lin_iters == it_o
     assert np.array_equal(sim.solution(case.n), xo)
     assert g.lin_relres == rr_o
+    sim.close()
+
+
+@pytest.mark.parametrize("dims", [(1024, 512, 1), (256, 64, 32)])
+def test_partial_set_tile_assembly_bit_exact(dims):
+    """Partial-set b=1 assembly above the row-kernel threshold runs the tile kernel with
+    staged g2l (k_assemble_tile1<D3, true>): an irregular active set (blocks + sprinkled
+    cells, so tiles are full, partial and empty) — F, rhs, the ELL columns (frozen
+    neighbours -1), the scaled blocks and a 2-iteration Krylov solve equal the oracle's."""
+    nx, ny, nz = dims
+    case = pkg.Case(5, nx=nx, ny=ny, nz=nz)
+    s = perturbed_state(case, 7)
+    dt = 86400.0
+    i = np.arange(case.n)
+    ix, iy, iz = i % nx, (i // nx) % ny, i // (nx * ny)
+    rng = np.random.default_rng(11)
+    mask = ((ix // 37 + iy // 11 + iz) % 3 != 0) | (rng.random(case.n) < 0.02)
+    act = np.flatnonzero(mask).astype(np.int32)
+    assert len(act) >= 148 * 2048 and len(act) < case.n
+    orc = Oracle(case)
+    orc.set_state(s, dt)
+    Fo, ro, rpo, co, vo = orc.assemble(act)
+    sim = pkg.GpuSimulator(case)
+    assert sim.L.rsim_gpu_set_debug(sim._ctx, 1) == 0
+    sim.set_state(s, dt)
+    sim.set_active(act)
+    sim.assemble()
+    Fg, rg, rpg, cg, vg = sim.system(len(act))
+    assert np.array_equal(rpg, rpo) and np.array_equal(cg, co)
+    assert np.array_equal(Fg, Fo), np.abs(Fg - Fo).max()
+    assert np.array_equal(rg, ro)
+    assert np.array_equal(vg, vo), np.abs(vg - vo).max()
+    sim.L.rsim_gpu_set_debug(sim._ctx, 0)
+    sim.assemble()
+    opts = case.solver_opts(precond=pkg.PREC_BJACOBI, fixed_lin_iters=2, lin_maxit=2)
+    rc_o, xo, it_o, rr_o = orc.linear_solve(len(act), opts)
+    sim.linear_solve(opts)
+    g = sim.stats()
+    assert g.lin_iters == it_o and g.lin_relres == rr_o
+    assert np.array_equal(sim.solution(len(act)), xo)
     sim.close()
 
 
