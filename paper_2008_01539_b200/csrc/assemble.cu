@@ -409,39 +409,28 @@ __global__ void __launch_bounds__(256, B == 1 ? RSIM_K1ROW_MINB : 1) k_assemble_
   if (threadIdx.x == 0) a.part_f2[blockIdx.x] = tree8(wsf);
 }
 
-// b = 1, no NNC, nx % 256 == 0, ny % FRY == 0 (config 5, single-phase grids):
-// one 256-thread block per tile of 256 (x) × FRY (y) cells of one plane.  The
-// properties of every tile cell and of a one-cell halo are evaluated ONCE into
-// shared memory (each needs an exp), instead of once per referencing row as in
-// the row kernel (up to 7 per row, and warps pay for divergent upwind
-// choices); the ±z neighbours are evaluated as in the row kernel.  Same
-// physics.h calls and the same canonical order per row => the same bits.
-// FULL set (PART = false): row l = cell i, each tile row is one canonical
+// FULL set, b = 1, no NNC, nx % 256 == 0, ny % FRY == 0 (config 5, standard
+// Newton on single-phase grids): one 256-thread block per tile of 256 (x) ×
+// FRY (y) cells of one plane.  The properties of every tile cell and of a
+// one-cell halo are evaluated ONCE into shared memory (each needs an exp),
+// instead of once per referencing row as in the row kernel (up to 7 per row,
+// and warps pay for divergent upwind choices); the ±z neighbours are
+// evaluated as in the row kernel.  Same physics.h calls and the same
+// canonical order per row => the same bits.  Each tile row is one canonical
 // 256-row chunk, so the (F,F) chunk partials come out as in the row kernel.
-// Partial set (PART = true): the tile's g2l decides which cells are rows
-// (tiles without an active cell return after one coalesced g2l read); rows
-// go to their local index, neighbour columns from the staged g2l, frozen
-// neighbours get no column; F is stored for the Krylov init's (F,F).
 constexpr int FRY = 4;
-template <bool D3, bool PART>
-__global__ void __launch_bounds__(256) k_assemble_tile1(const AsmArgs a) {
+template <bool D3>
+__global__ void __launch_bounds__(256) k_assemble_full1(const AsmArgs a) {
   // p and ρ per tile/halo cell; dρ/dp = c·ρ and λρ = ρ·(1/μ) are re-formed
   // with the same multiplications props<1> uses (same bits).  Slots are
   // compile-time (no dynamically indexed arrays: nothing goes to local memory).
   __shared__ double su[FRY + 2][258], sA[FRY + 2][258];
-  __shared__ int32_t sg[PART ? FRY + 2 : 1][PART ? 258 : 1];  // g2l of tile + halo (partial sets)
   __shared__ double wsf[FRY][8];
   using rsim::phys::Props;
   const int t = threadIdx.x, lane = t & 31;
   const int x0 = blockIdx.x * 256, y0 = blockIdx.y * FRY, z = blockIdx.z;
   const int64_t nxy = (int64_t)a.nx * a.ny;
   const double cf = a.fl.c_f[1], imu = a.fl.inv_mu[1];
-  if (PART) {  // any active cell in the tile?
-    int any = 0;
-#pragma unroll
-    for (int r = 0; r < FRY; ++r) any |= __ldg(&a.g2l[(int64_t)z * nxy + (int64_t)(y0 + r) * a.nx + x0 + t]) >= 0;
-    if (!__syncthreads_or(any)) return;
-  }
   auto rho_of = [&](double p) {
     double ui[1] = {p};
     Props<1> P;
@@ -450,35 +439,26 @@ __global__ void __launch_bounds__(256) k_assemble_tile1(const AsmArgs a) {
   };
   {
     double pr[FRY + 2];
-    int32_t gr[FRY + 2];
 #pragma unroll
     for (int r = 0; r < FRY + 2; ++r) {  // tile rows + halo rows, thread t = column x0 + t
       const int y = y0 - 1 + r;
-      const bool in = y >= 0 && y < a.ny;
-      const int64_t i = (int64_t)z * nxy + (int64_t)y * a.nx + x0 + t;
-      pr[r] = in ? __ldg(&a.u[i]) : 0.0;
-      gr[r] = (PART && in) ? __ldg(&a.g2l[i]) : -1;
+      pr[r] = (y >= 0 && y < a.ny) ? __ldg(&a.u[(int64_t)z * nxy + (int64_t)y * a.nx + x0 + t]) : 0.0;
     }
     double ph = 0.0;
-    int32_t gh = -1;
     int hr = -1, hc = 0;
     if (t < 2 * (FRY + 2)) {  // x halo columns x0-1 / x0+256
       const int r = t >> 1, y = y0 - 1 + r, x = (t & 1) ? x0 + 256 : x0 - 1;
       if (y >= 0 && y < a.ny && x >= 0 && x < a.nx) {
         hr = r; hc = (t & 1) ? 257 : 0;
-        const int64_t i = (int64_t)z * nxy + (int64_t)y * a.nx + x;
-        ph = __ldg(&a.u[i]);
-        if (PART) gh = __ldg(&a.g2l[i]);
+        ph = __ldg(&a.u[(int64_t)z * nxy + (int64_t)y * a.nx + x]);
       }
     }
 #pragma unroll
     for (int r = 0; r < FRY + 2; ++r) {
       const int y = y0 - 1 + r;
       if (y >= 0 && y < a.ny) { su[r][t + 1] = pr[r]; sA[r][t + 1] = rho_of(pr[r]); }
-      if (PART) sg[r][t + 1] = gr[r];
     }
     if (hr >= 0) { su[hr][hc] = ph; sA[hr][hc] = rho_of(ph); }
-    if (PART && t < 2 * (FRY + 2)) sg[t >> 1][(t & 1) ? 257 : 0] = gh;  // -1 off the grid
   }
   __syncthreads();
   const int x = x0 + t, c = t + 1;
@@ -487,104 +467,85 @@ __global__ void __launch_bounds__(256) k_assemble_tile1(const AsmArgs a) {
 #pragma unroll 1
   for (int ry = 0; ry < FRY; ++ry) {
     const int y = y0 + ry, r = ry + 1;
-    const int64_t i = (int64_t)z * nxy + (int64_t)y * a.nx + x;
-    const int64_t l = PART ? (int64_t)sg[r][c] : i;  // local row (full set: = cell)
-    const bool row = !PART || l >= 0;
+    const int64_t i = (int64_t)z * nxy + (int64_t)y * a.nx + x;  // = local row l (full set)
     const bool h0 = D3 && z > 0, h5 = D3 && z < a.nz - 1;
     const double txi = __ldg(&a.tx[i]), tyi = __ldg(&a.ty[i]);
+    const double tzi = h5 ? __ldg(&a.tz[i]) : 0.0, tzm = h0 ? __ldg(&a.tz[i - nxy]) : 0.0;
+    const double pzm = h0 ? __ldg(&a.u[i - nxy]) : 0.0, pzp = h5 ? __ldg(&a.u[i + nxy]) : 0.0;
     double txl = __shfl_up_sync(0xffffffffu, txi, 1);
     if (lane == 0) txl = x > 0 ? __ldg(&a.tx[i - 1]) : 0.0;
-    double R[1] = {0.0};
-    if (row) {
-      const double tzi = h5 ? __ldg(&a.tz[i]) : 0.0, tzm = h0 ? __ldg(&a.tz[i - nxy]) : 0.0;
-      const double pzm = h0 ? __ldg(&a.u[i - nxy]) : 0.0, pzp = h5 ? __ldg(&a.u[i + nxy]) : 0.0;
-      const int32_t gzm = (PART && h0) ? __ldg(&a.g2l[i - nxy]) : 0, gzp = (PART && h5) ? __ldg(&a.g2l[i + nxy]) : 0;
-      const double pi = su[r][c], Ai = sA[r][c];
-      Props<1> Pi;
-      Pi.A[0] = Ai; Pi.dA[0][0] = cf * Ai; Pi.L[0] = Ai * imu; Pi.dL[0][0] = (cf * Ai) * imu;
-      double D[1][1], Mo[1] = {__ldg(&a.mold[i])};
-      rsim::phys::accum_row<1>(a.fl, __ldg(&a.pv[i]), pi, Pi, Mo, a.inv_dt, R, D);
-      auto cn = [&](double T, double pj, double Aj) -> double {  // neighbour with known ρ
-        double Oo[1][1];
-        const double dp = pi - pj;
-        if (!(dp < 0.0)) {
-          rsim::phys::flux_conn<1>(T, dp, true, Pi, R, D, Oo);
-        } else {
-          Props<1> Pj;
-          Pj.A[0] = Aj; Pj.dA[0][0] = cf * Aj; Pj.L[0] = Aj * imu; Pj.dL[0][0] = (cf * Aj) * imu;
-          rsim::phys::flux_conn<1>(T, dp, false, Pj, R, D, Oo);
-        }
-        return Oo[0][0];
-      };
-      auto cz = [&](double T, double pj) -> double {  // ±z neighbour: ρ evaluated only when it is upwind
-        double Oo[1][1];
-        const double dp = pi - pj;
-        if (!(dp < 0.0)) {
-          rsim::phys::flux_conn<1>(T, dp, true, Pi, R, D, Oo);
-        } else {
-          double uj[1] = {pj};
-          Props<1> Pj;
-          rsim::phys::props(a.fl, uj, (uint8_t)0, Pj);
-          rsim::phys::flux_conn<1>(T, dp, false, Pj, R, D, Oo);
-        }
-        return Oo[0][0];
-      };
-      // canonical slot order -z, -y, -x, +x, +y, +z (2D: no z slots)
-      double O0 = 0.0, O1 = 0.0, O2 = 0.0, O3 = 0.0, O4 = 0.0, O5 = 0.0;
-      const bool h1 = y > 0, h2 = x > 0, h3 = x < a.nx - 1, h4 = y < a.ny - 1;
-      if (h0) O0 = cz(tzm, pzm);
-      if (h1) O1 = cn(ty_prev, su[r - 1][c], sA[r - 1][c]);
-      if (h2) O2 = cn(txl, su[r][c - 1], sA[r][c - 1]);
-      if (h3) O3 = cn(txi, su[r][c + 1], sA[r][c + 1]);
-      if (h4) O4 = cn(tyi, su[r + 1][c], sA[r + 1][c]);
-      if (h5) O5 = cz(tzi, pzp);
-      rsim::phys::well_row<1>(__ldg(&a.wi[i]), pi, a.bhp, Pi, R, D);
-      double Di[1][1];
-      if (!rsim::blk::inv(D, Di)) {
-        atomicMin(&a.dsc->bad_cell, (int32_t)i);
-        a.dsc->status = RSIM_ENUM;
-        Di[0][0] = 0.0;
-      }
-      double yv[1];
-      rsim::blk::gemv<1>(Di, R, yv);
-      if (PART || a.keep_F) __stcs(&a.F_raw[l], R[0]);
-      __stcs(&a.rhs[l], -yv[0]);
-      finf = fmax(finf, fabs(R[0]));
-      // full set: structural columns (not stored); partial: g2l of the neighbour, -1 = frozen
-      auto st = [&](int q, bool h, int32_t gc, double O) {
-        if (PART) {
-          const int32_t col = h ? gc : -1;
-          __stcs(&a.ell_col[(int64_t)q * a.cap + l], col);
-          if (col < 0) return;
-        } else if (!h) {
-          return;
-        }
-        double Oq[1][1] = {{O}}, S[1][1];
-        rsim::blk::gemm<1>(Di, Oq, S);
-        __stcs(&a.ell_val[(int64_t)q * a.cap + l], S[0][0]);
-      };
-      auto G = [&](int rr, int cc) { return PART ? sg[rr][cc] : 0; };
-      if (D3) {
-        st(0, h0, gzm, O0); st(1, h1, G(r - 1, c), O1); st(2, h2, G(r, c - 1), O2);
-        st(3, h3, G(r, c + 1), O3); st(4, h4, G(r + 1, c), O4); st(5, h5, gzp, O5);
+    const double pi = su[r][c], Ai = sA[r][c];
+    Props<1> Pi;
+    Pi.A[0] = Ai; Pi.dA[0][0] = cf * Ai; Pi.L[0] = Ai * imu; Pi.dL[0][0] = (cf * Ai) * imu;
+    double R[1], D[1][1], Mo[1] = {__ldg(&a.mold[i])};
+    rsim::phys::accum_row<1>(a.fl, __ldg(&a.pv[i]), pi, Pi, Mo, a.inv_dt, R, D);
+    auto cn = [&](double T, double pj, double Aj) -> double {  // neighbour with known ρ
+      double Oo[1][1];
+      const double dp = pi - pj;
+      if (!(dp < 0.0)) {
+        rsim::phys::flux_conn<1>(T, dp, true, Pi, R, D, Oo);
       } else {
-        st(0, h1, G(r - 1, c), O1); st(1, h2, G(r, c - 1), O2); st(2, h3, G(r, c + 1), O3); st(3, h4, G(r + 1, c), O4);
+        Props<1> Pj;
+        Pj.A[0] = Aj; Pj.dA[0][0] = cf * Aj; Pj.L[0] = Aj * imu; Pj.dL[0][0] = (cf * Aj) * imu;
+        rsim::phys::flux_conn<1>(T, dp, false, Pj, R, D, Oo);
       }
+      return Oo[0][0];
+    };
+    auto cz = [&](double T, double pj) -> double {  // ±z neighbour: ρ evaluated only when it is upwind
+      double Oo[1][1];
+      const double dp = pi - pj;
+      if (!(dp < 0.0)) {
+        rsim::phys::flux_conn<1>(T, dp, true, Pi, R, D, Oo);
+      } else {
+        double uj[1] = {pj};
+        Props<1> Pj;
+        rsim::phys::props(a.fl, uj, (uint8_t)0, Pj);
+        rsim::phys::flux_conn<1>(T, dp, false, Pj, R, D, Oo);
+      }
+      return Oo[0][0];
+    };
+    // canonical slot order -z, -y, -x, +x, +y, +z (2D: no z slots)
+    double O0 = 0.0, O1 = 0.0, O2 = 0.0, O3 = 0.0, O4 = 0.0, O5 = 0.0;
+    const bool h1 = y > 0, h2 = x > 0, h3 = x < a.nx - 1, h4 = y < a.ny - 1;
+    if (h0) O0 = cz(tzm, pzm);
+    if (h1) O1 = cn(ty_prev, su[r - 1][c], sA[r - 1][c]);
+    if (h2) O2 = cn(txl, su[r][c - 1], sA[r][c - 1]);
+    if (h3) O3 = cn(txi, su[r][c + 1], sA[r][c + 1]);
+    if (h4) O4 = cn(tyi, su[r + 1][c], sA[r + 1][c]);
+    if (h5) O5 = cz(tzi, pzp);
+    rsim::phys::well_row<1>(__ldg(&a.wi[i]), pi, a.bhp, Pi, R, D);
+    double Di[1][1];
+    if (!rsim::blk::inv(D, Di)) {
+      atomicMin(&a.dsc->bad_cell, (int32_t)i);
+      a.dsc->status = RSIM_ENUM;
+      Di[0][0] = 0.0;
     }
-    if (!PART) {
-      const double ws = warp_tree(rsim::blk::rowdot<1>(R, R));
-      if (lane == 0) wsf[ry][t >> 5] = ws;
+    double yv[1];
+    rsim::blk::gemv<1>(Di, R, yv);
+    if (a.keep_F) __stcs(&a.F_raw[i], R[0]);
+    __stcs(&a.rhs[i], -yv[0]);
+    finf = fmax(finf, fabs(R[0]));
+    auto st = [&](int q, bool h, double O) {
+      if (!h) return;
+      double Oq[1][1] = {{O}}, S[1][1];
+      rsim::blk::gemm<1>(Di, Oq, S);
+      __stcs(&a.ell_val[(int64_t)q * a.cap + i], S[0][0]);
+    };
+    if (D3) {
+      st(0, h0, O0); st(1, h1, O1); st(2, h2, O2); st(3, h3, O3); st(4, h4, O4); st(5, h5, O5);
+    } else {
+      st(0, h1, O1); st(1, h2, O2); st(2, h3, O3); st(3, h4, O4);
     }
+    const double ws = warp_tree(rsim::blk::rowdot<1>(R, R));
+    if (lane == 0) wsf[ry][t >> 5] = ws;
     ty_prev = tyi;
   }
   const double wm = warp_max(finf);
   if (lane == 0 && wm > 0.0) atomic_max_bits(&a.dsc->finf, wm);
-  if (!PART) {
-    __syncthreads();
-    if (t < FRY) {  // canonical chunk partial of each tile row (256 consecutive rows)
-      const int64_t row0 = (int64_t)z * nxy + (int64_t)(y0 + t) * a.nx + x0;
-      a.part_f2[row0 >> 8] = tree8(wsf[t]);
-    }
+  __syncthreads();
+  if (t < FRY) {  // canonical chunk partial of each tile row (256 consecutive rows)
+    const int64_t row0 = (int64_t)z * nxy + (int64_t)(y0 + t) * a.nx + x0;
+    a.part_f2[row0 >> 8] = tree8(wsf[t]);
   }
 }
 
@@ -675,13 +636,9 @@ int launch_assemble(rsim_gpu_ctx* c) {
     const int64_t nblocks = (c->nA + 255) / 256;
     const bool full = c->nA == c->n;
     c->cols_implicit = full;
-    if (c->b == 1 && !c->has_nnc && c->nx % 256 == 0 && c->ny % FRY == 0 && tile_full1_enabled()) {
-      const dim3 grid(c->nx / 256, c->ny / FRY, c->nz);
-      if (!full) c->f2_parts = false;  // partial tiles store F; the Krylov init reduces (F,F) itself
-      if (full && c->d3) k_assemble_tile1<true, false><<<grid, 256, 0, c->stream>>>(a);
-      else if (full) k_assemble_tile1<false, false><<<grid, 256, 0, c->stream>>>(a);
-      else if (c->d3) k_assemble_tile1<true, true><<<grid, 256, 0, c->stream>>>(a);
-      else k_assemble_tile1<false, true><<<grid, 256, 0, c->stream>>>(a);
+    if (full && c->b == 1 && !c->has_nnc && c->nx % 256 == 0 && c->ny % FRY == 0 && tile_full1_enabled()) {
+      if (c->d3) k_assemble_full1<true><<<dim3(c->nx / 256, c->ny / FRY, c->nz), 256, 0, c->stream>>>(a);
+      else k_assemble_full1<false><<<dim3(c->nx / 256, c->ny / FRY, c->nz), 256, 0, c->stream>>>(a);
       c->launches++;
       RSIM_CUDA(cudaGetLastError());
       return RSIM_OK;

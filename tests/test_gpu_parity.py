@@ -209,7 +209,7 @@ print(json.dumps({{"a": sim.active().tolist(), "b": sim.boundary().tolist(), "ex
                                   (512, 32, 24)])
 def test_full_set_tile_assembly_bit_exact(dims):
     """Full-set b=1 assembly above the row-kernel threshold runs the tile kernel
-    (k_assemble_tile1<D3, false>, 256 x 4 tiles of a plane): F, rhs, the scaled
+    (k_assemble_full1, 256 x 4 tiles of a plane): F, rhs, the scaled
     blocks and the canonical (F,F) partials must equal the oracle's."""
     nx, ny, nz = dims
     case = pkg.Case(5, nx=nx, ny=ny, nz=nz)
@@ -244,10 +244,10 @@ def test_full_set_tile_assembly_bit_exact(dims):
 
 @pytest.mark.parametrize("dims", [(1024, 512, 1), (256, 64, 32)])
 def test_partial_set_tile_assembly_bit_exact(dims):
-    """Partial-set b=1 assembly above the row-kernel threshold runs the tile kernel with
-    staged g2l (k_assemble_tile1<D3, true>): an irregular active set (blocks + sprinkled
-    cells, so tiles are full, partial and empty) — F, rhs, the ELL columns (frozen
-    neighbours -1), the scaled blocks and a 2-iteration Krylov solve equal the oracle's."""
+    """Partial-set b=1 assembly above the row-kernel threshold (k_assemble_row<1, false>,
+    canonical (F,F) chunk partials) on an irregular active set (blocks + sprinkled cells):
+    F, rhs, the ELL columns (frozen neighbours -1), the scaled blocks and a 2-iteration
+    Krylov solve equal the oracle's."""
     nx, ny, nz = dims
     case = pkg.Case(5, nx=nx, ny=ny, nz=nz)
     s = perturbed_state(case, 7)
