@@ -32,8 +32,10 @@ namespace {
 // Threads per CTA per block size (template parameter of the kernel; one CTA
 // per SM, so KT fixes the register cap: 1024 -> 64, 512 -> 128).  Measured on
 // the config-3 / config-4 first Newton systems (100 Neumann-1 iterations,
-// scripts/krylov_c4.py): b = 2 66.2 -> 44.9 µs per iteration and b = 3
-// 551 -> 454 µs with 512 threads and one slot per gather group (no spills;
+// scripts/krylov_c4.py): b = 2 66.2 -> 44.9 µs per iteration with 512 threads
+// and one slot per gather group, b = 3 551 -> 454 µs with 512 threads (no spills)
+// and 440 µs with 768 (80 registers, 3 chunks per round; 768 threads for b = 2:
+// 58.6 µs;
 // b = 3 with 1024 threads: 461 µs and ~0.8 KB of local traffic per row-phase
 // left, 256 threads for b = 2: 64-68 µs); b = 1 (config 5 at 1-100 %) keeps
 // 1024 threads and all six slots in flight.
@@ -44,7 +46,7 @@ namespace {
 #define RSIM_KT2 512
 #endif
 #ifndef RSIM_KT3
-#define RSIM_KT3 512
+#define RSIM_KT3 768
 #endif
 __host__ __device__ constexpr int kt_for(int B) { return B == 1 ? RSIM_KT1 : (B == 2 ? RSIM_KT2 : RSIM_KT3); }
 #ifndef RSIM_SPMV_SG1
@@ -56,8 +58,6 @@ __host__ __device__ constexpr int kt_for(int B) { return B == 1 ? RSIM_KT1 : (B 
 #ifndef RSIM_SPMV_SG3
 #define RSIM_SPMV_SG3 1
 #endif
-template <int CPR>
-__host__ __device__ constexpr int lcpr() { return CPR == 4 ? 2 : (CPR == 2 ? 1 : 0); }
 constexpr int64_t kFuseMaxRows = 1 << 20;  // recompute-fusion only while latency-bound
 
 struct KArgs {
@@ -118,7 +118,7 @@ __device__ __forceinline__ void stage_round(Red& R, int NQ, const double* val, i
   if (!flush) return;
   __syncthreads();
   for (int k = threadIdx.x; k < nstaged * CPR * NQ; k += blockDim.x) {
-    const int sl = k / (CPR * NQ), rem = k - sl * CPR * NQ, q = rem >> lcpr<CPR>(), g = rem & (CPR - 1);
+    const int sl = k / (CPR * NQ), rem = k - sl * CPR * NQ, q = rem / CPR, g = rem % CPR;
     const int64_t c = R.rid[sl] * CPR + g;
     if (c < nch) part[q * pstride + c] = tree8(&R.wsr[sl][q][8 * g]);
   }
@@ -137,7 +137,7 @@ __device__ __forceinline__ void commit_round(Red& R, int NQ, const double* val, 
   }
   __syncthreads();
   if ((int)threadIdx.x < CPR * NQ) {
-    const int g = threadIdx.x & (CPR - 1), q = threadIdx.x >> lcpr<CPR>();
+    const int g = threadIdx.x % CPR, q = threadIdx.x / CPR;
     if (chunk0 + g < nch) part[q * pstride + chunk0 + g] = tree8(&R.ws[q][8 * g]);
   }
   __syncthreads();
@@ -171,7 +171,7 @@ __device__ __forceinline__ void reduce_small_multi(Red& R, int NQ, SF&& src, int
       }
     __syncthreads();
     if ((int)threadIdx.x < CPR * NQ) {
-      const int g = threadIdx.x & (CPR - 1), q = threadIdx.x >> lcpr<CPR>();
+      const int g = threadIdx.x % CPR, q = threadIdx.x / CPR;
       if (c0 + g < P2) R.lvl[q][c0 + g] = tree8(&R.ws[q][8 * g]);
     }
     __syncthreads();

@@ -27,6 +27,7 @@ if cfg == 5:  # the bench's config-5 set: Gaussian-decay field at KC4_FRAC activ
     sim.upload_dp(dp)
     sim.L.rsim_gpu_state_from_dp(sim._ctx, 30e6, 20e6)
     sim.L.rsim_gpu_support_active(sim._ctx, 1e-3, 2, None)
+    sim.stats()  # syncs n_A to the host before the assembly (as bench.c5_sweep does)
     precond = pkg.PREC_BJACOBI if precond is None else precond
 else:
     sim.set_state(s0, float(dts[0]))
@@ -50,7 +51,7 @@ for r in range(reps + 1):
 x = sim.solution(nA)
 b = case.b
 nnc = case.n_nnc * 2 / case.n
-per = bench.bytes_krylov_row_iter(b, 6 if case.nz > 1 else 4, nnc, o.precond == pkg.PREC_NEUMANN1)
+per = bench.bytes_krylov_row_iter(b, 6 if case.nz > 1 else 4, nnc, o.precond == pkg.PREC_NEUMANN1, cols=nA < case.n)
 m = float(np.median(ms))
 print(json.dumps({"config": cfg, "frac": os.environ.get("KC4_FRAC"), "n_active": nA, "iters": iters, "ms": m, "us_per_iter": 1e3 * m / iters,
                   "alg_GBs": nA * (iters * per + bench.bytes_krylov_row_init(b)) / (m / 1e3) / 1e9,
