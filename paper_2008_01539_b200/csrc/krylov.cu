@@ -34,8 +34,8 @@ namespace {
 // the config-3 / config-4 first Newton systems (100 Neumann-1 iterations,
 // scripts/krylov_c4.py): b = 2 66.2 -> 44.9 µs per iteration with 512 threads
 // and one slot per gather group, b = 3 551 -> 454 µs with 512 threads (no spills)
-// and 440 µs with 768 (80 registers, 3 chunks per round; 768 threads for b = 2:
-// 58.6 µs;
+// (768 threads: 440 µs on that system but 10.19 vs 9.63 s for the whole config-4
+// run, whose smaller systems lose more to round imbalance; 768 for b = 2: 58.6 µs;
 // b = 3 with 1024 threads: 461 µs and ~0.8 KB of local traffic per row-phase
 // left, 256 threads for b = 2: 64-68 µs); b = 1 (config 5 at 1-100 %) keeps
 // 1024 threads and all six slots in flight.
@@ -46,7 +46,7 @@ namespace {
 #define RSIM_KT2 512
 #endif
 #ifndef RSIM_KT3
-#define RSIM_KT3 768
+#define RSIM_KT3 512
 #endif
 __host__ __device__ constexpr int kt_for(int B) { return B == 1 ? RSIM_KT1 : (B == 2 ? RSIM_KT2 : RSIM_KT3); }
 #ifndef RSIM_SPMV_SG1
