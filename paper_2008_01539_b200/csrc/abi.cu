@@ -243,6 +243,11 @@ int rsim_gpu_create(rsim_gpu_ctx** out, const rsim_graph_desc* g, const rsim_flu
     TRY(h2d(c, c->nt, g->nnc_t, c->nnc_total));
     c->h_nptr.assign(g->nnc_ptr, g->nnc_ptr + n + 1);
     c->h_nnbr.assign(g->nnc_nbr, g->nnc_nbr + c->nnc_total);
+    std::vector<uint32_t> nb((size_t)(n + 31) / 32, 0u);
+    for (int64_t i = 0; i < n; ++i)
+      if (g->nnc_ptr[i + 1] > g->nnc_ptr[i]) nb[(size_t)(i >> 5)] |= 1u << (i & 31);
+    TRY(dalloc(&c->nnc_bits, (int64_t)nb.size()));
+    TRY(h2d(c, c->nnc_bits, nb.data(), (int64_t)nb.size()));
   } else {
     RSIM_CUDA(cudaMemsetAsync(c->nptr, 0, sizeof(int32_t) * (n + 1), c->stream));
   }
@@ -282,7 +287,7 @@ int rsim_gpu_destroy(rsim_gpu_ctx* c) {
                   c->mold, c->p_prev, c->st, c->st_start, c->flags, c->flags_alt, c->act_buf, c->g2l, c->label,
                   c->list_buf, c->dp, c->last_dp, c->tile_cnt, c->tile_off, c->ell_col, c->ell_val, c->nnc_lcol,
                   c->nnc_val, c->F_raw, c->rhs, c->part_f2, c->x, c->r, c->r0, c->p, c->v, c->s, c->t, c->p2, c->v2, c->ph, c->sh, c->part,
-                  c->dsc, c->dd.sub_cells, c->dd.halo_cells, c->u_ckpt, c->st_ckpt, c->l2_scratch, c->pin0, c->ktrace,
+                  c->dsc, c->dd.sub_cells, c->dd.halo_cells, c->u_ckpt, c->st_ckpt, c->l2_scratch, c->pin0, c->ktrace, c->nnc_bits,
                   c->gm_V, c->gm_part, c->dd.hist, c->bits[0], c->bits[1], c->dn_W, c->dn_colbuf, c->dn_piv};
   for (void* p : ptrs)
     if (p) cudaFree(p);

@@ -152,6 +152,7 @@ struct rsim_gpu_ctx {
   int64_t counters[5] = {0, 0, 0, 0, 0};
   uint8_t* pin0 = nullptr;  // F_PIN|F_A for pinned cells, 0 elsewhere (reset source)
   unsigned long long* ktrace = nullptr;  // Krylov phase cycle counters (debug, RSIM_KTRACE=1)
+  uint32_t* nnc_bits = nullptr;  // bit i: cell i has NNC entries (small-grid K7: skips the nptr reads)
   uint32_t* bits[2] = {nullptr, nullptr};  // K7 bitmap dilation ping-pong (n/32 words each; nx % 32 == 0)
   bool seed_bits_ready = false;            // bits[0] holds the D0 seed (written by the fused reset + seed)
 };

@@ -556,6 +556,158 @@ __global__ void __launch_bounds__(256) k_set_update_coop(Geo4 g, uint8_t* __rest
   }
 }
 
+// Whole set update of a TINY vec4 grid (n <= kSmemK7MaxCells) in ONE CTA:
+// the flag words are staged in shared memory, the dilation rounds, the count
+// and the scatter run from there separated by __syncthreads (no grid
+// barriers; the cooperative kernel above pays ~5 of them per update).  Thread
+// t owns the contiguous word range [t·W, (t+1)·W), so its block-scan offset
+// orders the compacted list by cell.  Same predicates (a_new4, nbr_lanes4,
+// the NNC and dead-cell rules) as dilate_tile / scatter_tile => same sets.
+// Measured (one update = 2 dilations + count + scatter): config 1 (10 k cells)
+// 4.39 -> 4.10 ms per run; config 2 (65 k cells, DFN NNCs) 27.3 -> 33.9 ms and
+// paper Case 1 (80 k) 0.124 -> 0.146 s: one SM is too slow past ~16 k cells.
+constexpr int64_t kSmemK7MaxCells = 16 * 1024;
+__global__ void __launch_bounds__(1024) k_set_update_smem(Geo4 g, const uint8_t* __restrict__ fin,
+                                                          uint8_t* __restrict__ fout, SetMode M, int rounds,
+                                                          int32_t round, DevScalars* dsc, int32_t* __restrict__ act,
+                                                          int32_t* __restrict__ g2l, int32_t* __restrict__ label,
+                                                          const uint32_t* __restrict__ nnc_bits) {
+  // the flag bytes (one 32-bit word per 4-cell group), then one bit per cell
+  // telling which cells have NNC entries (so nptr is read only for those)
+  extern __shared__ uint32_t sw[];
+  uint32_t* snb = sw + g.n / 4;
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t tot[3];
+  const uint8_t* sb = reinterpret_cast<const uint8_t*>(sw);
+  const int64_t nw = g.n / 4;
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wp = tid >> 5;
+  for (int64_t t = tid; t < nw; t += nth) sw[t] = reinterpret_cast<const uint32_t*>(fin)[t];
+  if (g.has_nnc)
+    for (int64_t t = tid; t < (g.n + 31) / 32; t += nth) snb[t] = nnc_bits[t];
+  if (tid < 3) tot[tid] = 0;
+  __syncthreads();
+  const bool ex = decide_expand(M, dsc);
+  const bool dil = (M.mode == MODE_DEVICE || M.mode == MODE_DD) ? ex : true;
+  const int64_t per = (nw + nth - 1) / nth, t0 = tid * per, t1 = t0 + per < nw ? t0 + per : nw;
+  auto pos = [&](int64_t t) {
+    Pos4 p;
+    p.row = (int32_t)(t / g.wrow);
+    p.xw = (int32_t)(t - (int64_t)p.row * g.wrow);
+    p.iz = p.row / g.ny;
+    p.iy = p.row - p.iz * g.ny;
+    p.t = t;
+    p.ok = true;
+    return p;
+  };
+  if (dil)
+    for (int r = 0; r < rounds; ++r) {
+      const uint8_t bin = (r % 2 == 0) ? F_D0 : F_D1, bout = (r % 2 == 0) ? F_D1 : F_D0;
+      // bit_in is not written in this round, so reading a neighbour word while its
+      // owner rewrites bit_out sees the same bit_in either way
+      auto L = [&](int64_t u) { return lanes(sw[u], bin); };
+      for (int64_t t = t0; t < t1; ++t) {
+        uint32_t w = sw[t];
+        const uint32_t in = lanes(w, bin);
+        uint32_t out = in | nbr_lanes4(g, pos(t), in, 0u, L, [](uint32_t x, uint32_t y) { return x | y; });
+        if (g.has_nnc && ((snb[t >> 3] >> (4 * (t & 7))) & 0xFu))
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int64_t i = 4 * t + k;
+            if (!((snb[i >> 5] >> (i & 31)) & 1u)) continue;
+            const int32_t q0 = __ldg(&g.nptr[i]), q1 = __ldg(&g.nptr[i + 1]);
+            for (int32_t q = q0; q < q1; ++q)
+              if (sb[__ldg(&g.nnbr[q])] & bin) out |= 1u << (8 * k);
+          }
+        if (g.has_dead) out &= ~lanes(w, F_DEAD);
+        w = (w & ~(0x01010101u * bout)) | (out * bout);
+        sw[t] = w;
+      }
+      __syncthreads();
+    }
+  // ---- count + block exclusive scan of the per-thread counts (cell order)
+  int cnt = 0;
+  for (int64_t t = t0; t < t1; ++t) cnt += __popc(a_new4(sw[t], M.mode, ex, M.dbit));
+  int x = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wp] = x;
+  __syncthreads();
+  if (wp == 0) {
+    int z = lane < (nth >> 5) ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    wsum[lane] = z;
+  }
+  __syncthreads();
+  int32_t posn = (wp > 0 ? wsum[wp - 1] : 0) + x - cnt;
+  // ---- scatter: A, V_B, V_T / labels, g2l, the sorted list
+  auto L2 = [&](int64_t u) {
+    const uint32_t w = sw[u];
+    return a_new4(w, M.mode, ex, M.dbit) | (g.has_dead ? lanes(w, F_DEAD) : 0u);
+  };
+  int nb = 0, nn = 0;
+  for (int64_t t = t0; t < t1; ++t) {
+    const uint32_t f4 = sw[t];
+    const uint32_t keep = a_new4(f4, M.mode, ex, M.dbit);
+    uint32_t bnd = 0;
+    if (keep) {
+      const uint32_t self = keep | (g.has_dead ? lanes(f4, F_DEAD) : 0u);
+      const uint32_t all = nbr_lanes4(g, pos(t), self, 0x01010101u, L2, [](uint32_t a, uint32_t b) { return a & b; });
+      bnd = keep & ~all & 0x01010101u;
+      if (g.has_nnc && ((snb[t >> 3] >> (4 * (t & 7))) & 0xFu))
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t i = 4 * t + k;
+          if (!((keep >> (8 * k)) & 1u) || ((bnd >> (8 * k)) & 1u) || !((snb[i >> 5] >> (i & 31)) & 1u)) continue;
+          const int32_t q0 = __ldg(&g.nptr[i]), q1 = __ldg(&g.nptr[i + 1]);
+          for (int32_t q = q0; q < q1; ++q)
+            if (!a_new(sb[__ldg(&g.nnbr[q])], M.mode, ex, M.dbit)) { bnd |= 1u << (8 * k); break; }
+        }
+    }
+    int32_t gl[4];
+    uint32_t out = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t f = (f4 >> (8 * k)) & 0xFFu;
+      uint32_t o = f & (F_PIN | F_T | F_DEAD);
+      gl[k] = -1;
+      if ((keep >> (8 * k)) & 1u) {
+        o |= F_A;
+        if ((bnd >> (8 * k)) & 1u) o |= F_B;
+        if (M.mode == MODE_DD) {
+          if (!(f & F_T)) { label[4 * t + k] = round; ++nn; }
+          o |= F_T;
+        }
+        act[posn] = (int32_t)(4 * t + k);
+        gl[k] = posn++;
+      }
+      out |= o << (8 * k);
+    }
+    nb += __popc(bnd);
+    reinterpret_cast<uint32_t*>(fout)[t] = out;
+    reinterpret_cast<int4*>(g2l)[t] = make_int4(gl[0], gl[1], gl[2], gl[3]);
+  }
+  nb = __reduce_add_sync(0xffffffffu, nb);
+  nn = __reduce_add_sync(0xffffffffu, nn);
+  if (lane == 0) {
+    if (nb) atomicAdd(&tot[0], nb);
+    if (nn) atomicAdd(&tot[1], nn);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    dsc->nA = wsum[(nth >> 5) - 1];
+    dsc->expand = ex ? 1 : 0;
+    dsc->nB = tot[0];
+    dsc->n_new = tot[1];
+  }
+}
+
 // ---- row-group variants (vec4 grids): a thread owns the same 4-cell group in
 // RG consecutive x-rows of one plane.  The ±y neighbour words of the group
 // column are loaded once and reused by the RG rows, the ±x neighbours come
@@ -1345,6 +1497,15 @@ static bool keepbits_enabled() {
   return v == 1;
 }
 
+static bool smem_set_update_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("RSIM_NO_SMEM_K7");
+    v = (e && *e == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static bool coop_set_update_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -1387,6 +1548,21 @@ int launch_set_update(rsim_gpu_ctx* c, int mode, int round, double eps, int m, i
   // row groups reuse the ±y words RG-fold but give RG-fold fewer blocks: only
   // for grids large enough to fill the GPU many times over
   const bool use_rg = g.vec4 && !g.has_dead && (int64_t)grg.x * grg.y >= 16 * 148;
+  if (g.vec4 && c->n <= kSmemK7MaxCells && smem_set_update_enabled()) {  // small grid: one CTA, flags in smem
+    const size_t smem = (size_t)(c->n / 4 + (c->n + 31) / 32) * sizeof(uint32_t);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && attr < 220 * 1024) {
+      RSIM_CUDA(cudaFuncSetAttribute(k_set_update_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+      attr = 220 * 1024;
+    }
+    k_set_update_smem<<<1, 1024, smem, c->stream>>>(g, c->flags, c->flags_alt, M, rounds, round, c->dsc, c->act_buf,
+                                                     c->g2l, c->label, c->nnc_bits);
+    c->launches++;
+    RSIM_CUDA(cudaGetLastError());
+    std::swap(c->flags, c->flags_alt);
+    c->act = c->act_buf;
+    return RSIM_OK;
+  }
   if (!use_rg && ntiles <= kCoopMaxTiles && coop_set_update_enabled()) {
     static int per_sm = 0;
     if (per_sm == 0) {

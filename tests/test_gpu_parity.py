@@ -196,7 +196,7 @@ print(json.dumps({{"a": sim.active().tolist(), "b": sim.boundary().tolist(), "ex
 """
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for env in ({}, {"RSIM_NO_COOP_K7": "1"}):
+    for env in ({}, {"RSIM_NO_SMEM_K7": "1"}, {"RSIM_NO_SMEM_K7": "1", "RSIM_NO_COOP_K7": "1"}):
         e = dict(os.environ, **env, PYTHONPATH=root)
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=e, cwd=root, timeout=600)
         assert r.returncode == 0, r.stderr
