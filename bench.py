@@ -167,6 +167,17 @@ def bytes_krylov_row_iter(b, s, nnc=0.0, neumann=False, cols=True):
     return (4 if neumann else 2) * bytes_spmv_row(b, s, nnc, cols) + 112 * b
 
 
+def bytes_krylov_counted(b, s, rows_its, blk_its, po_its, neumann=False):
+    # b > 1, partial sets, from the work counters (rsim_gpu_block_counters): per row and
+    # SpMV the s column indices + 1 B pressure-only mask + own x read + y write; per stored
+    # block (active Cartesian neighbour; frozen neighbours have no block) b² values, or its
+    # b column-0 values when it is pressure-only (the other b² − b are zero and never read);
+    # + the 14 vector passes.  NNC blocks (rare) are left out.
+    k = 4 if neumann else 2
+    return k * (rows_its * (4 * s + 1 + 16 * b) + 8 * b * b * blk_its - 8 * (b * b - b) * po_its) \
+        + 112 * b * rows_its
+
+
 def bytes_krylov_row_init(b):
     return 8 * b * 4  # read rhs, write r, r0, x
 
@@ -337,10 +348,13 @@ def measure_config(pkg, cfg: int, steps: int, warmup: int, hbm: float, peak_kind
     L.rsim_gpu_checkpoint(ctx, 1)
     L.rsim_gpu_flush_l2(ctx)
     L.rsim_gpu_counters(ctx, None, 1)
+    L.rsim_gpu_block_counters(ctx, None, 1)
     R.run_dev(restore=False)
     phase_ms = np.zeros(4)
     L.rsim_gpu_timers(ctx, 0, A.ptr(phase_ms, C.c_double), None)
     L.rsim_gpu_counters(ctx, A.ptr(cnt, C.c_int64), 1)  # work counters of this one run
+    bcnt = np.zeros(2, dtype=np.int64)
+    L.rsim_gpu_block_counters(ctx, A.ptr(bcnt, C.c_int64), 1)
     # ---- e2e through the public C-ABI entry point with pinned host buffers
     import torch
     u_pin = torch.empty(len(R.s0.u), dtype=torch.float64, pin_memory=True).numpy()
@@ -375,10 +389,19 @@ def measure_config(pkg, cfg: int, steps: int, warmup: int, hbm: float, peak_kind
     nnc = case.n_nnc * 2 / case.n  # NNC entries per row (each NNC is stored in both rows)
     neu = R.opts.precond == pkg.PREC_NEUMANN1
     if dom == 2:
-        per = bytes_krylov_row_iter(b, s, nnc, neu)
-        alg = row_iters * per + krylov_rows * bytes_krylov_row_init(b)
+        if b > 1:  # counted: stored blocks only, pressure-only blocks at b of b² values
+            blk_its, po_its = int(bcnt[0]), int(bcnt[1])
+            alg_it = bytes_krylov_counted(b, s, row_iters, blk_its, po_its, neu)
+            per = alg_it / max(1, row_iters)
+            extra = f"; {blk_its / max(1, row_iters):.2f} stored blocks per row, " \
+                    f"{po_its / max(1, blk_its):.3f} of them pressure-only; all {s} blocks dense: " \
+                    f"{bytes_krylov_row_iter(b, s, nnc, neu):.1f} B"
+        else:
+            per = bytes_krylov_row_iter(b, s, nnc, neu)
+            alg_it, extra = row_iters * per, ""
+        alg = alg_it + krylov_rows * bytes_krylov_row_init(b)
         units = f"{per:.1f} B per row-iteration ({'Neumann-1: 4' if neu else '2'} SpMVs) + " \
-                f"{bytes_krylov_row_init(b)} B per row init"
+                f"{bytes_krylov_row_init(b)} B per row init" + extra
         launches_dom = solves
     elif dom == 1:
         per = bytes_assembly_row(b, D, s, nnc)

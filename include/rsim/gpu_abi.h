@@ -120,6 +120,10 @@ int rsim_gpu_timers(rsim_gpu_ctx* ctx, int32_t enable, double* ms4, int32_t* lau
  * [0] rows assembled, [1] Krylov row-iterations Σ n_A·its, [2] Krylov solves,
  * [3] Krylov launches' rows Σ n_A, [4] set-update passes (full-grid scans). */
 int rsim_gpu_counters(rsim_gpu_ctx* ctx, int64_t* out5, int32_t reset);
+/* b > 1, accumulated with the counters above: [0] Σ its · off-diagonal ELL
+ * blocks stored by the assembly (active Cartesian neighbours), [1] Σ its · the
+ * pressure-only ones among them (blockops.h col0_only: b of b² entries read). */
+int rsim_gpu_block_counters(rsim_gpu_ctx* ctx, int64_t* out2, int32_t reset);
 
 /* Debug flags: bit 0 = the large-set assembly also stores the raw residual F
  * (otherwise only ‖F‖ partials are kept; rsim_gpu_download_system needs F). */

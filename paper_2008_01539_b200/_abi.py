@@ -167,6 +167,7 @@ PROTOS: dict[str, tuple] = {
     # gpu_abi.h
     "rsim_gpu_set_device": (C.c_int, [C.c_int32]),
     "rsim_gpu_counters": (C.c_int, [P, i64ptr, C.c_int32]),
+    "rsim_gpu_block_counters": (C.c_int, [P, i64ptr, C.c_int32]),
     "rsim_gpu_create": (C.c_int, [C.POINTER(P), C.POINTER(GraphDesc), C.POINTER(FluidParams)]),
     "rsim_gpu_destroy": (C.c_int, [P]),
     "rsim_gpu_last_error": (C.c_char_p, []),

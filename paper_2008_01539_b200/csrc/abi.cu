@@ -99,6 +99,8 @@ __global__ void k_reset_scalars(DevScalars* d) {
   d->finf = 0ull;
   d->maxA = 0ull;  // ‖δp‖∞ of the coming update (a fused update has no memset of its own)
   d->maxB = 0ull;
+  d->nblk = 0ull;
+  d->npo = 0ull;
 }
 
 // p component of the interleaved state: dst[i] = u[i*b]
@@ -175,6 +177,12 @@ int rsim_gpu_counters(rsim_gpu_ctx* c, int64_t* out5, int32_t reset) {
   return RSIM_OK;
 }
 
+int rsim_gpu_block_counters(rsim_gpu_ctx* c, int64_t* out2, int32_t reset) {
+  if (out2) { out2[0] = c->counters[5]; out2[1] = c->counters[6]; }
+  if (reset) c->counters[5] = c->counters[6] = 0;
+  return RSIM_OK;
+}
+
 int rsim_gpu_create(rsim_gpu_ctx** out, const rsim_graph_desc* g, const rsim_fluid_params* f) {
   if (!out || !g || !f || f->kind < 1 || f->kind > 3 || g->nx < 1 || g->ny < 1 || g->nz < 1 ||
       (int64_t)g->nx * g->ny * g->nz >= ((int64_t)1 << 31)) {  // cell ids are int32 (CSR, act, g2l)
@@ -223,6 +231,7 @@ int rsim_gpu_create(rsim_gpu_ctx** out, const rsim_graph_desc* g, const rsim_flu
     TRY(dalloc(&c->tile_cnt, nt)); TRY(dalloc(&c->tile_off, nt));
   }
   TRY(dalloc(&c->ell_col, c->nslot * n)); TRY(dalloc(&c->ell_val, c->nslot * n * b * b));
+  TRY(dalloc(&c->ell_po, n));
   c->ell_cap = n;
   TRY(dalloc(&c->nnc_lcol, c->nnc_total)); TRY(dalloc(&c->nnc_val, c->nnc_total * b * b));
   TRY(dalloc(&c->F_raw, n * b)); TRY(dalloc(&c->rhs, n * b));
@@ -285,7 +294,7 @@ int rsim_gpu_destroy(rsim_gpu_ctx* c) {
   cudaStreamSynchronize(c->stream);
   void* ptrs[] = {c->tx, c->ty, c->tz, c->pv, c->wi, c->kind, c->nptr, c->nnbr, c->nt, c->u, c->u_start,
                   c->mold, c->p_prev, c->st, c->st_start, c->flags, c->flags_alt, c->act_buf, c->g2l, c->label,
-                  c->list_buf, c->dp, c->last_dp, c->tile_cnt, c->tile_off, c->ell_col, c->ell_val, c->nnc_lcol,
+                  c->list_buf, c->dp, c->last_dp, c->tile_cnt, c->tile_off, c->ell_col, c->ell_val, c->ell_po, c->nnc_lcol,
                   c->nnc_val, c->F_raw, c->rhs, c->part_f2, c->x, c->r, c->r0, c->p, c->v, c->s, c->t, c->p2, c->v2, c->ph, c->sh, c->part,
                   c->dsc, c->dd.sub_cells, c->dd.halo_cells, c->u_ckpt, c->st_ckpt, c->l2_scratch, c->pin0, c->ktrace, c->nnc_bits,
                   c->gm_V, c->gm_part, c->dd.hist, c->bits[0], c->bits[1], c->dn_W, c->dn_colbuf, c->dn_piv};
@@ -441,8 +450,10 @@ int rsim_gpu_stats_get(rsim_gpu_ctx* c, rsim_gpu_stats* st) {
   return RSIM_OK;
 }
 
-int rsim_internal_add_row_iters(rsim_gpu_ctx* c, int64_t v) {
-  c->counters[1] += v;
+int rsim_internal_add_row_iters(rsim_gpu_ctx* c, int64_t nA, int64_t its) {  // after the stats sync of the solve
+  c->counters[1] += nA * its;
+  c->counters[5] += (int64_t)c->hsc->nblk * its;
+  c->counters[6] += (int64_t)c->hsc->npo * its;
   return RSIM_OK;
 }
 
@@ -527,8 +538,15 @@ int64_t rsim_gpu_download_system(rsim_gpu_ctx* c, double* F_raw, double* rhs, in
   std::vector<double> eval(c->nslot * nA * bb);
   for (int s = 0; s < c->nslot; ++s) {
     RSIM_CUDA(cudaMemcpy(&ecol[s * nA], c->ell_col + s * cap, sizeof(int32_t) * nA, cudaMemcpyDeviceToHost));
-    RSIM_CUDA(cudaMemcpy(&eval[s * nA * bb], c->ell_val + s * cap * bb, sizeof(double) * nA * bb,
-                         cudaMemcpyDeviceToHost));
+  }
+  {  // planar [slot][element][cap] on the device -> [slot][row][element] for the CSR copy below
+    std::vector<double> plane(nA);
+    for (int s = 0; s < c->nslot; ++s)
+      for (int e = 0; e < bb; ++e) {
+        RSIM_CUDA(cudaMemcpy(plane.data(), c->ell_val + ell_at(cap, (int)bb, s, e, 0), sizeof(double) * nA,
+                             cudaMemcpyDeviceToHost));
+        for (int64_t l = 0; l < nA; ++l) eval[(s * nA + l) * bb + e] = plane[l];
+      }
   }
   RSIM_CUDA(cudaMemcpy(act.data(), c->act, sizeof(int32_t) * nA, cudaMemcpyDeviceToHost));
   std::vector<int32_t> nlcol(c->nnc_total);

@@ -34,6 +34,7 @@ struct AsmArgs {
   const int32_t *__restrict__ act, *__restrict__ g2l;
   int32_t* ell_col;
   double* ell_val;
+  uint8_t* ell_po;
   int32_t* nnc_lcol;
   double* nnc_val;
   double *F_raw, *rhs, *part_f2;
@@ -88,6 +89,24 @@ __device__ __forceinline__ void store_scaled(double* dst, const double (*Di)[B],
   for (int r = 0; r < B; ++r)
 #pragma unroll
     for (int c = 0; c < B; ++c) dst[r * B + c] = S[r][c];
+}
+
+// Scaled block D_ii^{-1}·O of (slot s, row l) into the planar ELL values;
+// returns whether it is pressure-only (blockops.h col0_only).
+template <int B, bool STREAM>
+__device__ __forceinline__ bool store_scaled_ell(const AsmArgs& a, int s, int64_t l, const double (*Di)[B],
+                                                 const double (*O)[B]) {
+  double S[B][B];
+  rsim::blk::gemm<B>(Di, O, S);
+  double* dst = a.ell_val + (int64_t)s * (B * B) * a.cap + l;
+#pragma unroll
+  for (int r = 0; r < B; ++r)
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+      if (STREAM) __stcs(&dst[(int64_t)(r * B + c) * a.cap], S[r][c]);
+      else dst[(int64_t)(r * B + c) * a.cap] = S[r][c];
+    }
+  return rsim::blk::col0_only<B>(&S[0][0]);
 }
 
 // 8 lanes per active row: lanes 0..nslot-1 evaluate one Cartesian connection
@@ -217,13 +236,23 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
     }
   }
   __syncwarp();
+  bool po = false;
   if (valid && q < a.nslot && lcol >= 0) {
     double Di[B][B];
 #pragma unroll
     for (int r = 0; r < B; ++r)
 #pragma unroll
       for (int c = 0; c < B; ++c) Di[r][c] = sDi[rg][r * B + c];
-    store_scaled<B>(&a.ell_val[((int64_t)q * a.cap + l) * B * B], Di, O);
+    po = store_scaled_ell<B, false>(a, q, l, Di, O);
+  }
+  if (B > 1) {  // lane q of the row group holds slot q's bit
+    const unsigned bal = __ballot_sync(0xffffffffu, po);
+    const unsigned stored = __ballot_sync(0xffffffffu, valid && q < a.nslot && lcol >= 0);
+    if (valid && q == 0) a.ell_po[l] = (uint8_t)((bal >> (threadIdx.x & 24)) & 0x3fu);
+    if ((threadIdx.x & 31) == 0 && stored) {
+      atomicAdd(&a.dsc->nblk, (unsigned long long)__popc(stored));
+      if (bal) atomicAdd(&a.dsc->npo, (unsigned long long)__popc(bal));
+    }
   }
   const double wm = warp_max(finf);
   if ((threadIdx.x & 31) == 0 && wm > 0.0) atomic_max_bits(&a.dsc->finf, wm);
@@ -244,6 +273,7 @@ __global__ void __launch_bounds__(256, B == 1 ? RSIM_K1ROW_MINB : 1) k_assemble_
   constexpr bool KEEP = (B == 1);
   __shared__ double wsf[8];
   double finf = 0.0, ff = 0.0;
+  uint32_t nblk = 0, npo = 0;
   const int64_t l = (int64_t)blockIdx.x * 256 + threadIdx.x;
   if (l < a.nA) {
     const int64_t i = FULL ? l : (int64_t)a.act[l];
@@ -350,10 +380,10 @@ __global__ void __launch_bounds__(256, B == 1 ? RSIM_K1ROW_MINB : 1) k_assemble_
       finf = fmax(finf, fabs(R[e]));
     }
     ff = rsim::blk::rowdot<B>(R, R);
+    uint32_t pom = 0;
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       if (!has[s] || gn[s] < 0) continue;
-      double* dst = &a.ell_val[((int64_t)s * a.cap + l) * B * B];
       double O[B][B];
       if (KEEP) {
 #pragma unroll
@@ -377,13 +407,11 @@ __global__ void __launch_bounds__(256, B == 1 ? RSIM_K1ROW_MINB : 1) k_assemble_
           rsim::phys::flux_conn<B>(Tn[s], dp, false, Pj, Rd, Dd, O);
         }
       }
-      double S[B][B];
-      rsim::blk::gemm<B>(Di, O, S);
-#pragma unroll
-      for (int r = 0; r < B; ++r)
-#pragma unroll
-        for (int c = 0; c < B; ++c) __stcs(&dst[r * B + c], S[r][c]);
+      ++nblk;
+      if (store_scaled_ell<B, true>(a, s, l, Di, O)) pom |= 1u << s;
     }
+    if (B > 1) __stcs(&a.ell_po[l], (uint8_t)pom);
+    npo = __popc(pom);
     for (int32_t q = q0; q < q1; ++q) {
       const int64_t j = __ldg(&a.nnbr[q]);
       if (__ldg(&a.g2l[j]) < 0) continue;
@@ -400,6 +428,13 @@ __global__ void __launch_bounds__(256, B == 1 ? RSIM_K1ROW_MINB : 1) k_assemble_
   }
   const double wm = warp_max(finf);
   if ((threadIdx.x & 31) == 0 && wm > 0.0) atomic_max_bits(&a.dsc->finf, wm);
+  if (B > 1) {
+    const uint32_t wb = __reduce_add_sync(0xffffffffu, nblk), wp = __reduce_add_sync(0xffffffffu, npo);
+    if ((threadIdx.x & 31) == 0 && wb) {
+      atomicAdd(&a.dsc->nblk, (unsigned long long)wb);
+      if (wp) atomicAdd(&a.dsc->npo, (unsigned long long)wp);
+    }
+  }
   // canonical chunk partial of (F, F): this block IS local chunk blockIdx.x
   // (256 rows; rows past n_A hold +0.0) — the Krylov init reduces these
   // instead of re-reading F
@@ -617,7 +652,7 @@ int launch_assemble(rsim_gpu_ctx* c) {
   a.nptr = c->nptr; a.nnbr = c->nnbr; a.nt = c->nt;
   a.u = c->u; a.mold = c->mold; a.st = c->st;
   a.act = c->act; a.g2l = c->g2l;
-  a.ell_col = c->ell_col; a.ell_val = c->ell_val;
+  a.ell_col = c->ell_col; a.ell_val = c->ell_val; a.ell_po = c->ell_po;
   a.nnc_lcol = c->nnc_lcol; a.nnc_val = c->nnc_val;
   a.F_raw = c->F_raw; a.rhs = c->rhs; a.part_f2 = c->part_f2;
   a.keep_F = c->keep_F;

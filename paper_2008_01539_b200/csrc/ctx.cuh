@@ -45,6 +45,8 @@ struct DevScalars {
   unsigned long long halo;
   int32_t part_count;       // number of K1 F-norm partials
   int32_t ilu_bad;          // ILU(0) factorisation hit a singular pivot (=> block-Jacobi fallback)
+  unsigned long long nblk;  // b > 1: ELL blocks the last assembly stored (active Cartesian neighbours)
+  unsigned long long npo;   // ... of which pressure-only (bench: bytes the Krylov kernels actually need)
 };
 
 struct DDLists {
@@ -116,10 +118,14 @@ struct rsim_gpu_ctx {
   int32_t *tile_cnt = nullptr, *tile_off = nullptr;
   int32_t* list_buf = nullptr;  // uploaded lists
 
-  // local system (ELL [slot][cap] + global-NNC-slot values)
+  // local system (ELL + global-NNC-slot values).  Columns [slot][cap]; values
+  // planar [slot][element e = r·b + c][cap], so a warp's load of one element is
+  // one contiguous 256 B run and the zero columns of pressure-only blocks
+  // (blockops.h col0_only, one bit per slot in ell_po) are never touched.
   int32_t* ell_col = nullptr;
   int64_t ell_cap = 0;  // ELL slot stride of the current assembly: n_A rounded up to 32 (n for full sets)
   double* ell_val = nullptr;
+  uint8_t* ell_po = nullptr;  // [cap] bit s: the block of slot s is pressure-only (b > 1)
   int32_t* nnc_lcol = nullptr;
   double* nnc_val = nullptr;
   double *F_raw = nullptr, *rhs = nullptr;
@@ -149,7 +155,7 @@ struct rsim_gpu_ctx {
   double* u_ckpt = nullptr;
   uint8_t* st_ckpt = nullptr;
   void* l2_scratch = nullptr;
-  int64_t counters[5] = {0, 0, 0, 0, 0};
+  int64_t counters[7] = {0, 0, 0, 0, 0, 0, 0};  // [5], [6]: Σ its · stored / pressure-only ELL blocks (b > 1)
   uint8_t* pin0 = nullptr;  // F_PIN|F_A for pinned cells, 0 elsewhere (reset source)
   unsigned long long* ktrace = nullptr;  // Krylov phase cycle counters (debug, RSIM_KTRACE=1)
   uint32_t* nnc_bits = nullptr;  // bit i: cell i has NNC entries (small-grid K7: skips the nptr reads)
@@ -233,6 +239,18 @@ __device__ __forceinline__ void implicit_cols(int32_t nx, int32_t ny, int32_t nz
   } else {
     cl[0] = ym; cl[1] = xm; cl[2] = xp; cl[3] = yp;
   }
+}
+
+// Planar ELL values: element e of the block of (slot s, local row l).
+__host__ __device__ __forceinline__ int64_t ell_at(int64_t cap, int bb, int s, int e, int64_t l) {
+  return ((int64_t)s * bb + e) * cap + l;
+}
+// The whole block of (slot s, row l) as a flat row-major b×b array.
+template <int B>
+__device__ __forceinline__ void ell_load(const double* __restrict__ val, int64_t cap, int s, int64_t l, double* M) {
+  const double* __restrict__ vp = val + (int64_t)s * (B * B) * cap + l;
+#pragma unroll
+  for (int e = 0; e < B * B; ++e) M[e] = vp[(int64_t)e * cap];
 }
 
 __device__ __forceinline__ double warp_tree(double v) {

@@ -70,7 +70,11 @@ __global__ void k_direct_build(const DArgs a) {
     for (int s = 0; s < a.nslot; ++s) cl[s] = a.ell_col[s * a.cap + l];
   }
   for (int s = 0; s < a.nslot; ++s)
-    if (cl[s] >= 0) add(cl[s], &a.ell_val[((int64_t)s * a.cap + l) * B * B]);
+    if (cl[s] >= 0) {
+      double M[B * B];
+      ell_load<B>(a.ell_val, a.cap, s, l, M);
+      add(cl[s], M);
+    }
   if (a.has_nnc) {
     const int64_t i = a.act[l];
     for (int32_t q = a.nptr[i]; q < a.nptr[i + 1]; ++q)

@@ -25,7 +25,7 @@ namespace {
 
 template <int B>
 __global__ void __launch_bounds__(256) k_ilu_factor(IluArgs f, const int32_t* __restrict__ src, int32_t nnz,
-                                                    const double* __restrict__ ell_val,
+                                                    const double* __restrict__ ell_val, int64_t ell_cap,
                                                     const double* __restrict__ nnc_val, DevScalars* dsc) {
   constexpr int BB = B * B;
   auto grid = cg::this_grid();
@@ -36,9 +36,16 @@ __global__ void __launch_bounds__(256) k_ilu_factor(IluArgs f, const int32_t* __
   if (gtid == 0) dsc->ilu_bad = 0;
   for (int64_t p = gtid; p < nnz; p += gstride) {  // gather the scaled blocks into CSR order
     const int32_t s = src[p];
-    const double* from = s >= 0 ? &ell_val[(int64_t)s * BB] : &nnc_val[(int64_t)(-s - 1) * BB];
+    if (s >= 0) {  // s = slot · cap + local row (planar ELL values)
+      const int32_t slot = s / (int32_t)ell_cap;
+      const int64_t l = s - (int64_t)slot * ell_cap;
 #pragma unroll
-    for (int q = 0; q < BB; ++q) val[(int64_t)p * BB + q] = from[q];
+      for (int q = 0; q < BB; ++q) val[(int64_t)p * BB + q] = ell_val[ell_at(ell_cap, BB, slot, q, l)];
+    } else {
+      const double* from = &nnc_val[(int64_t)(-s - 1) * BB];
+#pragma unroll
+      for (int q = 0; q < BB; ++q) val[(int64_t)p * BB + q] = from[q];
+    }
   }
   grid.sync();
   for (int lv = 0; lv < f.nf; ++lv) {
@@ -98,9 +105,10 @@ int factor_launch(rsim_gpu_ctx* c) {
   int32_t nnz = c->ilu.nnz;
   const int32_t* src = c->ilu.src;
   const double* ev = c->ell_val;
+  int64_t ecap = c->ell_cap;
   const double* nv = c->nnc_val;
   DevScalars* dsc = c->dsc;
-  void* args[] = {&f, &src, &nnz, &ev, &nv, &dsc};
+  void* args[] = {&f, &src, &nnz, &ev, &ecap, &nv, &dsc};
   RSIM_CUDA(cudaLaunchCooperativeKernel((void*)k_ilu_factor<B>, grid, 256, args, 0, c->stream));
   c->launches++;
   RSIM_CUDA(cudaGetLastError());

@@ -70,6 +70,7 @@ struct KArgs {
   double rtol;
   const int32_t* ell_col;
   const double* ell_val;
+  const uint8_t* ell_po;
   const int32_t* act;
   const int32_t* nptr;
   const int32_t* nnc_lcol;
@@ -203,9 +204,10 @@ struct Vecs {
 // mode 2: s_j = r_j − α v_j (vo = current v);  mode 3: x_j read directly from `po`.
 template <int B>
 __device__ __forceinline__ void nbr_val(int mode, const Vecs& X, int64_t j, double beta, double omega, double alpha,
-                                        double* out) {
+                                        double* out, bool only0 = false) {
 #pragma unroll
   for (int e = 0; e < B; ++e) {
+    if (e > 0 && only0) break;  // a pressure-only block multiplies component 0 only
     const int64_t q = j * B + e;
     if (mode == 3) out[e] = X.po[q];
     else if (mode == 1) out[e] = X.r[q];
@@ -229,6 +231,11 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
     for (int s = 0; s < 6; ++s)
       if (s < a.nslot) cl[s] = __ldg(&col[s * a.cap + l]);
   }
+  // bit s: slot s holds a pressure-only block (columns >= 1 are zero, set by the
+  // assembly with blockops.h col0_only): its b² − b zero entries are not loaded
+  // and only component 0 of the neighbour is gathered.  Values are planar
+  // ([slot][element][cap]), so a warp whose rows agree skips whole sectors.
+  const uint32_t pom = B > 1 ? (uint32_t)__ldg(&a.ell_po[l]) : 0u;
   // Slots in groups of SG: all gathers of a group in flight, then its blocks.
   // Gathering all six neighbours first keeps 6·B doubles live and spills them
   // to local memory at 64 registers (b = 3: ~1 KB of local traffic per row and
@@ -242,11 +249,24 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
     double xv[SG][B];
 #pragma unroll
     for (int k = 0; k < SG; ++k)
-      if (s0 + k < 6 && cl[s0 + k] >= 0) nbr_val<B>(mode, X, cl[s0 + k], beta, omega, alpha, xv[k]);
+      if (s0 + k < 6 && cl[s0 + k] >= 0)
+        nbr_val<B>(mode, X, cl[s0 + k], beta, omega, alpha, xv[k], B > 1 && ((pom >> (s0 + k)) & 1u));
 #pragma unroll
     for (int k = 0; k < SG; ++k)
-      if (s0 + k < 6 && cl[s0 + k] >= 0)
-        rsim::blk::gemv_acc_flat<B>(&val[((int64_t)(s0 + k) * a.cap + l) * B * B], xv[k], acc);
+      if (s0 + k < 6 && cl[s0 + k] >= 0) {
+        const double* __restrict__ vp = val + (int64_t)(s0 + k) * (B * B) * a.cap + l;
+        if (B > 1 && ((pom >> (s0 + k)) & 1u)) {
+          double M0[B];
+#pragma unroll
+          for (int r = 0; r < B; ++r) M0[r] = vp[(int64_t)(r * B) * a.cap];
+          rsim::blk::gemv_acc_col0<B>(M0, xv[k][0], acc);
+        } else {
+          double M[B * B];
+#pragma unroll
+          for (int e = 0; e < B * B; ++e) M[e] = vp[(int64_t)e * a.cap];
+          rsim::blk::gemv_acc_full<B>(M, xv[k], acc);
+        }
+      }
     if (SG < 6) asm volatile("" ::: "memory");  // keep the next group's loads after this group's math
   }
   if (a.has_nnc) {
@@ -363,6 +383,10 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   double relres = 0.0;
   int cur = 0;  // which (p, v) buffer pair holds the current iterate
   bool p_ready = false;  // unfused: the next p was stored by the x/r update pass
+  // fused: the x/r update of iteration k is own-row work with no barrier before the
+  // first pass of iteration k+1, so it rides on that pass (one sweep over the rows
+  // and the re-read of s, t, p, v less per iteration); pending between the two
+  bool xr_pending = false;
   // fuse: neighbours' p and s are recomputed at the gather site (fewer grid
   // barriers, latency regime); !fuse: owners store p and s, then a barrier,
   // then plain gathers (less memory traffic, bandwidth regime).
@@ -391,6 +415,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     rho = 1.0; alpha = 1.0; omega = 1.0; rho_new = bb;
     cur = 0;
     p_ready = false;
+    xr_pending = false;
     status = RSIM_ENOCONV;
     sync();
   }
@@ -402,6 +427,22 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     const double* vo = cur ? a.v : a.v2;
     const int pmode = it == 1 ? 1 : 0;
     const Vecs V0{a.r, po, vo, a.s, a.t};  // p_j = (s_j − ω t_j) + β (p_old_j − ω v_old_j)
+    // deferred x/r update of the previous iteration + this iteration's own p from the
+    // same registers (the expressions of the x/r pass and of nbr_val mode 0: same bits)
+    const bool xr_def = xr_pending;
+    const bool prev_prec = (a.neu && attempt == 0);  // ph / sh hold M⁻¹p / M⁻¹s of the previous iteration
+    auto own_xr_p = [&](int64_t l, double* pown) {
+#pragma unroll
+      for (int e = 0; e < B; ++e) {
+        const int64_t q = l * B + e;
+        const double pq = po[q], sq = a.s[q];
+        a.x[q] = (a.x[q] + alpha * (prev_prec ? a.ph[q] : pq)) + omega * (prev_prec ? a.sh[q] : sq);
+        const double rq = sq - omega * a.t[q];
+        a.r[q] = rq;
+        pown[e] = rq + beta * (pq - omega * vo[q]);
+      }
+    };
+    xr_pending = false;
     if (!fuse) {  // p = r + β (p − ω v), stored, then visible to all
       if (!p_ready)  // (else already stored by the previous x/r update pass)
       for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
@@ -422,7 +463,8 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
         if (l < nr) {
           double pown[B], y[B];
           if (fuse) {
-            nbr_val<B>(pmode, V0, l, beta, omega, 0.0, pown);
+            if (xr_def) own_xr_p(l, pown);
+            else nbr_val<B>(pmode, V0, l, beta, omega, 0.0, pown);
             spmv_row<B>(a, l, pmode, V0, beta, omega, 0.0, pown, y);
 #pragma unroll
             for (int e = 0; e < B; ++e) pc[l * B + e] = pown[e];
@@ -447,7 +489,8 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
         spmv_row<B>(a, l, 3, Vecs{a.r, a.ph, vo, a.s, a.t}, 0.0, 0.0, 0.0, &a.ph[l * B], y);
       } else if (fuse) {
         double pown[B];
-        nbr_val<B>(pmode, V0, l, beta, omega, 0.0, pown);
+        if (xr_def) own_xr_p(l, pown);
+        else nbr_val<B>(pmode, V0, l, beta, omega, 0.0, pown);
 #pragma unroll
         for (int e = 0; e < B; ++e) pc[l * B + e] = pown[e];
         spmv_row<B>(a, l, pmode, V0, beta, omega, 0.0, pown, y);
@@ -562,6 +605,8 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     const bool pfuse = !fuse && more;
     const double beta_next = pfuse ? (rho_next / rho_new) * (alpha / omega) : 0.0;
     double* pn = cur ? a.p : a.p2;  // the next iterate's p buffer
+    xr_pending = fuse && more && (neu || !prec);
+    if (!xr_pending)
     for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
       const int64_t l = rmap(rd0) * KT + tid;
       if (l < nr)
@@ -623,7 +668,7 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.cap = c->ell_cap;
   a.has_nnc = c->has_nnc;
   a.rtol = o->lin_rtol;
-  a.ell_col = c->ell_col; a.ell_val = c->ell_val;
+  a.ell_col = c->ell_col; a.ell_val = c->ell_val; a.ell_po = c->ell_po;
   a.act = c->act; a.nptr = c->nptr; a.nnc_lcol = c->nnc_lcol; a.nnc_val = c->nnc_val;
   a.rhs = c->rhs; a.F_raw = c->F_raw;
   a.part_f2 = c->part_f2;

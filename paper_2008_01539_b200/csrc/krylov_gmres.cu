@@ -67,7 +67,11 @@ __device__ __forceinline__ void spmv_row(const GArgs& a, int64_t l, const double
   for (int e = 0; e < B; ++e) y[e] = xv[l * B + e];
 #pragma unroll
   for (int s = 0; s < 6; ++s)
-    if (cl[s] >= 0) rsim::blk::gemv_acc_flat<B>(&a.ell_val[((int64_t)s * a.cap + l) * B * B], &xv[(int64_t)cl[s] * B], y);
+    if (cl[s] >= 0) {
+      double M[B * B];
+      ell_load<B>(a.ell_val, a.cap, s, l, M);
+      rsim::blk::gemv_acc_flat<B>(M, &xv[(int64_t)cl[s] * B], y);
+    }
   if (a.has_nnc) {
     const int64_t i = a.act[l];
     const int32_t q0 = a.nptr[i], q1 = a.nptr[i + 1];

@@ -25,7 +25,7 @@ int64_t rsim_internal_n(const rsim_gpu_ctx* c);
 int rsim_internal_iter_hook(rsim_gpu_ctx* c, int32_t iter, int32_t subdomain);
 int rsim_internal_b(const rsim_gpu_ctx* c);
 int32_t rsim_internal_nA(const rsim_gpu_ctx* c);
-extern "C" int rsim_internal_add_row_iters(rsim_gpu_ctx* c, int64_t v);
+extern "C" int rsim_internal_add_row_iters(rsim_gpu_ctx* c, int64_t nA, int64_t its);
 extern "C" int rsim_internal_solve_update(rsim_gpu_ctx* c, const rsim_solver_opts* o, double eps);
 // hook after every timestep attempt: committed = 1 (accepted) or 0 (failed, about to be cut)
 typedef int (*rsim_step_cb)(void* user, double dt, const rsim_newton_report* rep, int committed);
@@ -60,7 +60,7 @@ int local_step(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
 }
 
 void fill_rec(rsim_iter_record& rec, int32_t nA, const rsim_gpu_stats& s, rsim_gpu_ctx* c) {
-  rsim_internal_add_row_iters(c, (int64_t)nA * s.lin_iters);
+  rsim_internal_add_row_iters(c, nA, s.lin_iters);
   rec.n_active = nA;
   rec.lin_iters = s.lin_iters;
   rec.dp_inf_A = s.dp_inf_A;

@@ -49,10 +49,12 @@ for r in range(reps + 1):
     if r:
         ms.append(v.value)
 x = sim.solution(nA)
+import hashlib  # noqa: E402
+x_sha = hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest()[:16]
 b = case.b
 nnc = case.n_nnc * 2 / case.n
 per = bench.bytes_krylov_row_iter(b, 6 if case.nz > 1 else 4, nnc, o.precond == pkg.PREC_NEUMANN1, cols=nA < case.n)
 m = float(np.median(ms))
 print(json.dumps({"config": cfg, "frac": os.environ.get("KC4_FRAC"), "n_active": nA, "iters": iters, "ms": m, "us_per_iter": 1e3 * m / iters,
                   "alg_GBs": nA * (iters * per + bench.bytes_krylov_row_init(b)) / (m / 1e3) / 1e9,
-                  "x_sum": float(np.sum(x)), "env": {k: v for k, v in os.environ.items() if k.startswith("RSIM_")}}))
+                  "x_sum": float(np.sum(x)), "x_sha": x_sha, "env": {k: v for k, v in os.environ.items() if k.startswith("RSIM_")}}))
