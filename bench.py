@@ -167,15 +167,14 @@ def bytes_krylov_row_iter(b, s, nnc=0.0, neumann=False, cols=True):
     return (4 if neumann else 2) * bytes_spmv_row(b, s, nnc, cols) + 112 * b
 
 
-def bytes_krylov_counted(b, s, rows_its, blk_its, po_its, neumann=False):
+def bytes_krylov_counted(b, s, rows_its, blk_its, neumann=False):
     # b > 1, partial sets, from the work counters (rsim_gpu_block_counters): per row and
-    # SpMV the s column indices + 1 B pressure-only mask + own x read + y write; per stored
-    # block (active Cartesian neighbour; frozen neighbours have no block) b² values, or its
-    # b column-0 values when it is pressure-only (the other b² − b are zero and never read);
+    # SpMV the s column indices + own x read + y write; per STORED block (active Cartesian
+    # neighbour; frozen neighbours have no block and their value slots are not read) its b²
+    # values — pressure-only blocks included: the kernels load them whole;
     # + the 14 vector passes.  NNC blocks (rare) are left out.
     k = 4 if neumann else 2
-    return k * (rows_its * (4 * s + 1 + 16 * b) + 8 * b * b * blk_its - 8 * (b * b - b) * po_its) \
-        + 112 * b * rows_its
+    return k * (rows_its * (4 * s + 16 * b) + 8 * b * b * blk_its) + 112 * b * rows_its
 
 
 def bytes_krylov_row_init(b):
@@ -389,12 +388,12 @@ def measure_config(pkg, cfg: int, steps: int, warmup: int, hbm: float, peak_kind
     nnc = case.n_nnc * 2 / case.n  # NNC entries per row (each NNC is stored in both rows)
     neu = R.opts.precond == pkg.PREC_NEUMANN1
     if dom == 2:
-        if b > 1:  # counted: stored blocks only, pressure-only blocks at b of b² values
+        if b > 1:  # counted: the blocks actually stored (frozen neighbours have none)
             blk_its, po_its = int(bcnt[0]), int(bcnt[1])
-            alg_it = bytes_krylov_counted(b, s, row_iters, blk_its, po_its, neu)
+            alg_it = bytes_krylov_counted(b, s, row_iters, blk_its, neu)
             per = alg_it / max(1, row_iters)
             extra = f"; {blk_its / max(1, row_iters):.2f} stored blocks per row, " \
-                    f"{po_its / max(1, blk_its):.3f} of them pressure-only; all {s} blocks dense: " \
+                    f"{po_its / max(1, blk_its):.3f} of them pressure-only (loaded whole); all {s} slots filled: " \
                     f"{bytes_krylov_row_iter(b, s, nnc, neu):.1f} B"
         else:
             per = bytes_krylov_row_iter(b, s, nnc, neu)

@@ -74,10 +74,10 @@ RSIM_HD void gemv(const double (*M)[B], const double* x, double* y) {
 /* "Pressure-only" block: every entry outside column 0 is (±)0.  This is the
  * off-diagonal block of a row whose own cell is the upwind side of the
  * connection (physics.h flux_terms: ∂F_ij/∂u_j then has the p_j column only),
- * about half of all off-diagonal blocks.  The sm_100a kernels keep one bit per
- * block (set by the assembly with exactly this test) and neither load nor
- * multiply the zero columns; the rule below makes that the definition of the
- * block product on both sides, so the bits agree whatever x holds. */
+ * about half of all off-diagonal blocks.  The assembly counts them with exactly
+ * this test (one bit per block in ell_po).  They are multiplied like any other
+ * block: skipping their zero columns in the Krylov kernels was measured in round 2
+ * and loses on whole runs (lanes of a warp disagree on the block shape). */
 template <int B>
 RSIM_HD bool col0_only(const double* M) {
   bool z = B > 1;
@@ -86,32 +86,13 @@ RSIM_HD bool col0_only(const double* M) {
   return z;
 }
 
-/* y += M x over all columns (row r: y_r + (((M_r0 x_0) + M_r1 x_1) + ...)). */
+/* y += M x, flat row-major block (as stored in the BSR/ELL value arrays). */
 template <int B>
-RSIM_HD void gemv_acc_full(const double* M, const double* x, double* y) {
+RSIM_HD void gemv_acc_flat(const double* M, const double* x, double* y) {
   for (int r = 0; r < B; ++r) {
     double s = M[r * B] * x[0];
     for (int c = 1; c < B; ++c) s = s + M[r * B + c] * x[c];
     y[r] = y[r] + s;
-  }
-}
-
-/* y += M x for a pressure-only block: y_r + M_r0 x_0.  M0[r] = M_r0. */
-template <int B>
-RSIM_HD void gemv_acc_col0(const double* M0, double x0, double* y) {
-  for (int r = 0; r < B; ++r) y[r] = y[r] + M0[r] * x0;
-}
-
-/* y += M x, flat row-major block (as stored in the BSR/ELL value arrays):
- * the column-0 product for a pressure-only block, the full one otherwise. */
-template <int B>
-RSIM_HD void gemv_acc_flat(const double* M, const double* x, double* y) {
-  const bool po = col0_only<B>(M);
-  for (int r = 0; r < B; ++r) {  /* both products, then a select (no branch on the device) */
-    const double s0 = M[r * B] * x[0];
-    double s = s0;
-    for (int c = 1; c < B; ++c) s = s + M[r * B + c] * x[c];
-    y[r] = y[r] + (po ? s0 : s);
   }
 }
 

@@ -230,7 +230,10 @@ int rsim_gpu_create(rsim_gpu_ctx** out, const rsim_graph_desc* g, const rsim_flu
     const int64_t nt = (k7 > nchunks ? k7 : nchunks) + 1;
     TRY(dalloc(&c->tile_cnt, nt)); TRY(dalloc(&c->tile_off, nt));
   }
-  TRY(dalloc(&c->ell_col, c->nslot * n)); TRY(dalloc(&c->ell_val, c->nslot * n * b * b));
+  {  // slot stride = n_A rounded up to the 32-row tiles of the value layout (ctx.cuh ell_at)
+    const int64_t ncap = ((n + 31) / 32) * 32;
+    TRY(dalloc(&c->ell_col, c->nslot * ncap)); TRY(dalloc(&c->ell_val, c->nslot * ncap * b * b));
+  }
   TRY(dalloc(&c->ell_po, n));
   c->ell_cap = n;
   TRY(dalloc(&c->nnc_lcol, c->nnc_total)); TRY(dalloc(&c->nnc_val, c->nnc_total * b * b));
@@ -539,14 +542,12 @@ int64_t rsim_gpu_download_system(rsim_gpu_ctx* c, double* F_raw, double* rhs, in
   for (int s = 0; s < c->nslot; ++s) {
     RSIM_CUDA(cudaMemcpy(&ecol[s * nA], c->ell_col + s * cap, sizeof(int32_t) * nA, cudaMemcpyDeviceToHost));
   }
-  {  // planar [slot][element][cap] on the device -> [slot][row][element] for the CSR copy below
-    std::vector<double> plane(nA);
+  {  // device layout (ctx.cuh ell_at) -> [slot][row][element] for the CSR copy below
+    std::vector<double> dev((size_t)c->nslot * cap * bb);
+    RSIM_CUDA(cudaMemcpy(dev.data(), c->ell_val, sizeof(double) * dev.size(), cudaMemcpyDeviceToHost));
     for (int s = 0; s < c->nslot; ++s)
-      for (int e = 0; e < bb; ++e) {
-        RSIM_CUDA(cudaMemcpy(plane.data(), c->ell_val + ell_at(cap, (int)bb, s, e, 0), sizeof(double) * nA,
-                             cudaMemcpyDeviceToHost));
-        for (int64_t l = 0; l < nA; ++l) eval[(s * nA + l) * bb + e] = plane[l];
-      }
+      for (int64_t l = 0; l < nA; ++l)
+        for (int e = 0; e < bb; ++e) eval[(s * nA + l) * bb + e] = dev[ell_at(cap, (int)bb, s, e, l)];
   }
   RSIM_CUDA(cudaMemcpy(act.data(), c->act, sizeof(int32_t) * nA, cudaMemcpyDeviceToHost));
   std::vector<int32_t> nlcol(c->nnc_total);

@@ -91,20 +91,20 @@ __device__ __forceinline__ void store_scaled(double* dst, const double (*Di)[B],
     for (int c = 0; c < B; ++c) dst[r * B + c] = S[r][c];
 }
 
-// Scaled block D_ii^{-1}·O of (slot s, row l) into the planar ELL values;
+// Scaled block D_ii^{-1}·O of (slot s, row l) into the ELL values (ctx.cuh ell_at);
 // returns whether it is pressure-only (blockops.h col0_only).
 template <int B, bool STREAM>
 __device__ __forceinline__ bool store_scaled_ell(const AsmArgs& a, int s, int64_t l, const double (*Di)[B],
                                                  const double (*O)[B]) {
   double S[B][B];
   rsim::blk::gemm<B>(Di, O, S);
-  double* dst = a.ell_val + (int64_t)s * (B * B) * a.cap + l;
+  double* dst = a.ell_val + ell_at(a.cap, B * B, s, 0, l);
 #pragma unroll
   for (int r = 0; r < B; ++r)
 #pragma unroll
     for (int c = 0; c < B; ++c) {
-      if (STREAM) __stcs(&dst[(int64_t)(r * B + c) * a.cap], S[r][c]);
-      else dst[(int64_t)(r * B + c) * a.cap] = S[r][c];
+      if (STREAM) __stcs(&dst[(r * B + c) * ell_es(B * B)], S[r][c]);
+      else dst[(r * B + c) * ell_es(B * B)] = S[r][c];
     }
   return rsim::blk::col0_only<B>(&S[0][0]);
 }
@@ -602,13 +602,13 @@ __global__ void k_mold(rsim::phys::Fluid fl, int64_t n, const double* __restrict
 }
 
 // debug download of an implicit-column assembly: write the structural columns
-__global__ void k_materialize_cols(int32_t nx, int32_t ny, int32_t nz, bool d3, int nslot, int64_t n,
+__global__ void k_materialize_cols(int32_t nx, int32_t ny, int32_t nz, bool d3, int nslot, int64_t n, int64_t cap,
                                    int32_t* __restrict__ ell_col) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int32_t cl[6];
   implicit_cols(nx, ny, nz, d3, i, cl);
-  for (int s = 0; s < nslot; ++s) ell_col[s * n + i] = cl[s];
+  for (int s = 0; s < nslot; ++s) ell_col[s * cap + i] = cl[s];
 }
 
 }  // namespace
@@ -616,7 +616,7 @@ __global__ void k_materialize_cols(int32_t nx, int32_t ny, int32_t nz, bool d3, 
 int launch_materialize_cols(rsim_gpu_ctx* c) {
   if (!c->cols_implicit) return RSIM_OK;
   k_materialize_cols<<<(c->n + 255) / 256, 256, 0, c->stream>>>(c->nx, c->ny, c->nz, c->d3, c->nslot, c->n,
-                                                                c->ell_col);
+                                                                c->ell_cap, c->ell_col);
   c->launches++;
   c->cols_implicit = false;
   RSIM_CUDA(cudaGetLastError());
@@ -644,7 +644,7 @@ int launch_assemble(rsim_gpu_ctx* c) {
   a.nA = c->nA;
   // compact slot stride: the slot slabs of the current system are adjacent
   // (one contiguous ~nslot·n_A·b²·8 B region instead of slabs n apart)
-  c->ell_cap = c->nA == c->n ? c->n : ((c->nA + 31) / 32) * 32;
+  c->ell_cap = ((c->nA + 31) / 32) * 32;
   a.cap = c->ell_cap;
   a.d3 = c->d3;
   a.has_nnc = c->has_nnc;

@@ -118,12 +118,12 @@ struct rsim_gpu_ctx {
   int32_t *tile_cnt = nullptr, *tile_off = nullptr;
   int32_t* list_buf = nullptr;  // uploaded lists
 
-  // local system (ELL + global-NNC-slot values).  Columns [slot][cap]; values
-  // planar [slot][element e = r·b + c][cap], so a warp's load of one element is
-  // one contiguous 256 B run and the zero columns of pressure-only blocks
-  // (blockops.h col0_only, one bit per slot in ell_po) are never touched.
+  // local system (ELL + global-NNC-slot values).  Columns [slot][cap]; values in the
+  // per-block-size layout of ell_at() below; ell_po marks the pressure-only blocks
+  // (blockops.h col0_only, one bit per slot) for the cluster kernel's product select
+  // and the bench's block counters.
   int32_t* ell_col = nullptr;
-  int64_t ell_cap = 0;  // ELL slot stride of the current assembly: n_A rounded up to 32 (n for full sets)
+  int64_t ell_cap = 0;  // ELL slot stride of the current assembly: n_A rounded up to 32
   double* ell_val = nullptr;
   uint8_t* ell_po = nullptr;  // [cap] bit s: the block of slot s is pressure-only (b > 1)
   int32_t* nnc_lcol = nullptr;
@@ -241,16 +241,27 @@ __device__ __forceinline__ void implicit_cols(int32_t nx, int32_t ny, int32_t nz
   }
 }
 
-// Planar ELL values: element e of the block of (slot s, local row l).
+// ELL block values of (slot s, local row l), element e = r·b + c.
+//  * b <= 2: warp-tiled planar, [slot][l / 32][e][l % 32] (cap is a multiple of 32):
+//    a warp's load of one element is one contiguous 256 B run and the b² runs of its
+//    32 rows are adjacent, so a slot is ONE address stream.  Whole config-3 run (b = 2,
+//    round 2, same box): 1.33 s with row-major blocks, 1.23 s tiled.
+//  * b = 3: row-major blocks, [slot][l][e] (72 B per row).  Measured on the whole
+//    config-4 run: row-major 9.7-9.9 s, fully planar [slot][e][cap] 12.7-13.4 s (54
+//    address streams), warp-tiled 12.4 s (nine loads per block held in registers
+//    before the product: the b = 3 kernel then spills at its 128-register cap).
+// ell_es(b²) is the distance between consecutive elements of one block.
+__host__ __device__ constexpr int ell_es(int bb) { return bb > 4 ? 1 : 32; }
 __host__ __device__ __forceinline__ int64_t ell_at(int64_t cap, int bb, int s, int e, int64_t l) {
-  return ((int64_t)s * bb + e) * cap + l;
+  if (bb > 4) return ((int64_t)s * cap + l) * bb + e;
+  return ((((int64_t)s * (cap >> 5) + (l >> 5)) * bb + e) << 5) + (l & 31);
 }
 // The whole block of (slot s, row l) as a flat row-major b×b array.
 template <int B>
 __device__ __forceinline__ void ell_load(const double* __restrict__ val, int64_t cap, int s, int64_t l, double* M) {
-  const double* __restrict__ vp = val + (int64_t)s * (B * B) * cap + l;
+  const double* __restrict__ vp = val + ell_at(cap, B * B, s, 0, l);
 #pragma unroll
-  for (int e = 0; e < B * B; ++e) M[e] = vp[(int64_t)e * cap];
+  for (int e = 0; e < B * B; ++e) M[e] = vp[e * ell_es(B * B)];
 }
 
 __device__ __forceinline__ double warp_tree(double v) {

@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(256) k_ilu_factor(IluArgs f, const int32_t* __
   if (gtid == 0) dsc->ilu_bad = 0;
   for (int64_t p = gtid; p < nnz; p += gstride) {  // gather the scaled blocks into CSR order
     const int32_t s = src[p];
-    if (s >= 0) {  // s = slot · cap + local row (planar ELL values)
+    if (s >= 0) {  // s = slot · cap + local row (ELL value layout: ctx.cuh ell_at)
       const int32_t slot = s / (int32_t)ell_cap;
       const int64_t l = s - (int64_t)slot * ell_cap;
 #pragma unroll

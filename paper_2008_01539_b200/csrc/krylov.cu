@@ -70,7 +70,6 @@ struct KArgs {
   double rtol;
   const int32_t* ell_col;
   const double* ell_val;
-  const uint8_t* ell_po;
   const int32_t* act;
   const int32_t* nptr;
   const int32_t* nnc_lcol;
@@ -204,10 +203,9 @@ struct Vecs {
 // mode 2: s_j = r_j − α v_j (vo = current v);  mode 3: x_j read directly from `po`.
 template <int B>
 __device__ __forceinline__ void nbr_val(int mode, const Vecs& X, int64_t j, double beta, double omega, double alpha,
-                                        double* out, bool only0 = false) {
+                                        double* out) {
 #pragma unroll
   for (int e = 0; e < B; ++e) {
-    if (e > 0 && only0) break;  // a pressure-only block multiplies component 0 only
     const int64_t q = j * B + e;
     if (mode == 3) out[e] = X.po[q];
     else if (mode == 1) out[e] = X.r[q];
@@ -231,16 +229,16 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
     for (int s = 0; s < 6; ++s)
       if (s < a.nslot) cl[s] = __ldg(&col[s * a.cap + l]);
   }
-  // bit s: slot s holds a pressure-only block (columns >= 1 are zero, set by the
-  // assembly with blockops.h col0_only): its b² − b zero entries are not loaded
-  // and only component 0 of the neighbour is gathered.  Values are planar
-  // ([slot][element][cap]), so a warp whose rows agree skips whole sectors.
-  const uint32_t pom = B > 1 ? (uint32_t)__ldg(&a.ell_po[l]) : 0u;
   // Slots in groups of SG: all gathers of a group in flight, then its blocks.
   // Gathering all six neighbours first keeps 6·B doubles live and spills them
   // to local memory at 64 registers (b = 3: ~1 KB of local traffic per row and
   // SpMV, measured 1.4× the algorithmic DRAM bytes).  Accumulation order is
   // unchanged (slots ascending), so the bits are the same.
+  // Pressure-only blocks (blockops.h col0_only, K1's ell_po bits) are NOT special-cased.
+  // Measured on the whole config-3 / config-4 runs (round 2, scripts/ab_r02_s5.sh):
+  // skipping their zero columns per lane (K1's ell_po bit) makes warps whose rows
+  // disagree run both block shapes (avg 14 / 22 active lanes, 9.7 -> 13.0 s on
+  // config 4); predicated loads + select 11.3 s; a warp-uniform choice 11.0 s.
   constexpr int SG = B == 1 ? RSIM_SPMV_SG1 : (B == 2 ? RSIM_SPMV_SG2 : RSIM_SPMV_SG3);
 #pragma unroll
   for (int e = 0; e < B; ++e) acc[e] = own[e];
@@ -249,22 +247,16 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
     double xv[SG][B];
 #pragma unroll
     for (int k = 0; k < SG; ++k)
-      if (s0 + k < 6 && cl[s0 + k] >= 0)
-        nbr_val<B>(mode, X, cl[s0 + k], beta, omega, alpha, xv[k], B > 1 && ((pom >> (s0 + k)) & 1u));
+      if (s0 + k < 6 && cl[s0 + k] >= 0) nbr_val<B>(mode, X, cl[s0 + k], beta, omega, alpha, xv[k]);
 #pragma unroll
     for (int k = 0; k < SG; ++k)
       if (s0 + k < 6 && cl[s0 + k] >= 0) {
-        const double* __restrict__ vp = val + (int64_t)(s0 + k) * (B * B) * a.cap + l;
-        if (B > 1 && ((pom >> (s0 + k)) & 1u)) {
-          double M0[B];
-#pragma unroll
-          for (int r = 0; r < B; ++r) M0[r] = vp[(int64_t)(r * B) * a.cap];
-          rsim::blk::gemv_acc_col0<B>(M0, xv[k][0], acc);
+        if (ell_es(B * B) == 1) {  // row-major blocks: the product reads them in place
+          rsim::blk::gemv_acc_flat<B>(&val[ell_at(a.cap, B * B, s0 + k, 0, l)], xv[k], acc);
         } else {
           double M[B * B];
-#pragma unroll
-          for (int e = 0; e < B * B; ++e) M[e] = vp[(int64_t)e * a.cap];
-          rsim::blk::gemv_acc_full<B>(M, xv[k], acc);
+          ell_load<B>(val, a.cap, s0 + k, l, M);
+          rsim::blk::gemv_acc_flat<B>(M, xv[k], acc);
         }
       }
     if (SG < 6) asm volatile("" ::: "memory");  // keep the next group's loads after this group's math
@@ -280,6 +272,31 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
         rsim::blk::gemv_acc_flat<B>(&a.nnc_val[(int64_t)q * B * B], xn, acc);
       }
     }
+  }
+}
+
+// L2 prefetch of the matrix rows (block values + column indices) a warp will read in
+// its NEXT round, issued before the current round's loads: the value stream is
+// ~3/4 of the bytes of an SpMV pass and each round otherwise starts with one exposed
+// DRAM round trip.  A warp's 32 rows of one slot are one contiguous run of
+// 32·b²·8 B in both value layouts (ctx.cuh ell_at); lanes take its 128 B lines.
+#ifndef RSIM_PF
+#define RSIM_PF 0
+#endif
+template <int B>
+__device__ __forceinline__ void prefetch_rows(const KArgs& a, int64_t l) {
+  const int lane = threadIdx.x & 31;
+  const int64_t l0 = l - lane;
+  if (l0 >= a.nA) return;
+  constexpr int LPS = 2 * B * B;  // 128 B lines per slot and warp
+  for (int idx = lane; idx < a.nslot * LPS; idx += 32) {
+    const int sl = idx / LPS, ln = idx - sl * LPS;
+    const double* q = a.ell_val + ell_at(a.cap, B * B, sl, 0, l0) + ln * 16;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+  }
+  if (!a.implicit && lane < a.nslot) {
+    const int32_t* q = a.ell_col + (int64_t)lane * a.cap + l0;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
   }
 }
 
@@ -329,6 +346,9 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   bool rev = false;
   auto rmap = [&](int64_t rd0) { return rev ? nrounds - 1 - rd0 : rd0; };
   auto flip = [&]() { if (a.alt) rev = !rev; };
+  auto pf = [&](int64_t rd0) {  // matrix rows of this CTA's next round (SpMV passes)
+    if (RSIM_PF && rd0 + gridDim.x < nrounds) prefetch_rows<B>(a, rmap(rd0 + gridDim.x) * KT + tid);
+  };
 #define ROUNDS_BEGIN                                                         \
   {                                                                          \
   int rloc = 0;                                                              \
@@ -383,10 +403,8 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   double relres = 0.0;
   int cur = 0;  // which (p, v) buffer pair holds the current iterate
   bool p_ready = false;  // unfused: the next p was stored by the x/r update pass
-  // fused: the x/r update of iteration k is own-row work with no barrier before the
-  // first pass of iteration k+1, so it rides on that pass (one sweep over the rows
-  // and the re-read of s, t, p, v less per iteration); pending between the two
-  bool xr_pending = false;
+  // (fused: riding the x/r update of iteration k on the first pass of iteration k+1 was
+  // measured and rejected in round 2: config 3 run 1.27 -> 1.39 s, config 4 11.1 -> 11.3 s)
   // fuse: neighbours' p and s are recomputed at the gather site (fewer grid
   // barriers, latency regime); !fuse: owners store p and s, then a barrier,
   // then plain gathers (less memory traffic, bandwidth regime).
@@ -415,7 +433,6 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     rho = 1.0; alpha = 1.0; omega = 1.0; rho_new = bb;
     cur = 0;
     p_ready = false;
-    xr_pending = false;
     status = RSIM_ENOCONV;
     sync();
   }
@@ -427,22 +444,6 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     const double* vo = cur ? a.v : a.v2;
     const int pmode = it == 1 ? 1 : 0;
     const Vecs V0{a.r, po, vo, a.s, a.t};  // p_j = (s_j − ω t_j) + β (p_old_j − ω v_old_j)
-    // deferred x/r update of the previous iteration + this iteration's own p from the
-    // same registers (the expressions of the x/r pass and of nbr_val mode 0: same bits)
-    const bool xr_def = xr_pending;
-    const bool prev_prec = (a.neu && attempt == 0);  // ph / sh hold M⁻¹p / M⁻¹s of the previous iteration
-    auto own_xr_p = [&](int64_t l, double* pown) {
-#pragma unroll
-      for (int e = 0; e < B; ++e) {
-        const int64_t q = l * B + e;
-        const double pq = po[q], sq = a.s[q];
-        a.x[q] = (a.x[q] + alpha * (prev_prec ? a.ph[q] : pq)) + omega * (prev_prec ? a.sh[q] : sq);
-        const double rq = sq - omega * a.t[q];
-        a.r[q] = rq;
-        pown[e] = rq + beta * (pq - omega * vo[q]);
-      }
-    };
-    xr_pending = false;
     if (!fuse) {  // p = r + β (p − ω v), stored, then visible to all
       if (!p_ready)  // (else already stored by the previous x/r update pass)
       for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
@@ -460,11 +461,11 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     if (neu) {  // ph = p + (p − Â p), stored, barrier
       for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
         const int64_t l = rmap(rd0) * KT + tid;
+        pf(rd0);
         if (l < nr) {
           double pown[B], y[B];
           if (fuse) {
-            if (xr_def) own_xr_p(l, pown);
-            else nbr_val<B>(pmode, V0, l, beta, omega, 0.0, pown);
+            nbr_val<B>(pmode, V0, l, beta, omega, 0.0, pown);
             spmv_row<B>(a, l, pmode, V0, beta, omega, 0.0, pown, y);
 #pragma unroll
             for (int e = 0; e < B; ++e) pc[l * B + e] = pown[e];
@@ -483,14 +484,14 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     if (ilu) ilu_apply<B>(a.fa, pc, a.ph, sync);  // ph = (LU)^{-1} p (p stored: unfused)
     // ---- v = Â p (BJ) or v = Â ph (Neumann-1, ILU(0)); (r0, v) and the lagged (r, r)
     ROUNDS_BEGIN
+    pf(rd0);
     if (ok) {
       double y[B];
       if (prec) {
         spmv_row<B>(a, l, 3, Vecs{a.r, a.ph, vo, a.s, a.t}, 0.0, 0.0, 0.0, &a.ph[l * B], y);
       } else if (fuse) {
         double pown[B];
-        if (xr_def) own_xr_p(l, pown);
-        else nbr_val<B>(pmode, V0, l, beta, omega, 0.0, pown);
+        nbr_val<B>(pmode, V0, l, beta, omega, 0.0, pown);
 #pragma unroll
         for (int e = 0; e < B; ++e) pc[l * B + e] = pown[e];
         spmv_row<B>(a, l, pmode, V0, beta, omega, 0.0, pown, y);
@@ -528,6 +529,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     if (neu) {  // sh = s + (s − Â s), stored, barrier
       for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
         const int64_t l = rmap(rd0) * KT + tid;
+        pf(rd0);
         if (l < nr) {
           double sv[B], y[B];
           if (fuse) {
@@ -548,6 +550,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     if (ilu) ilu_apply<B>(a.fa, a.s, a.sh, sync);  // sh = (LU)^{-1} s
     // ---- t = Â s (BJ) or t = Â sh (Neumann-1, ILU(0)); (s,s), (t,s), (t,t), (r0,s), (r0,t)
     ROUNDS_BEGIN
+    pf(rd0);
     if (ok) {
       double sv[B], y[B];
       if (prec) {
@@ -605,8 +608,8 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     const bool pfuse = !fuse && more;
     const double beta_next = pfuse ? (rho_next / rho_new) * (alpha / omega) : 0.0;
     double* pn = cur ? a.p : a.p2;  // the next iterate's p buffer
-    xr_pending = fuse && more && (neu || !prec);
-    if (!xr_pending)
+    // (two rounds of loads in flight per thread in this pass and in the s pass were
+    //  measured on config 5 and are slower: 20 %: 28.1 -> 29.1 ms, 100 %: 115.7 -> 118.4 ms)
     for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
       const int64_t l = rmap(rd0) * KT + tid;
       if (l < nr)
@@ -668,7 +671,7 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.cap = c->ell_cap;
   a.has_nnc = c->has_nnc;
   a.rtol = o->lin_rtol;
-  a.ell_col = c->ell_col; a.ell_val = c->ell_val; a.ell_po = c->ell_po;
+  a.ell_col = c->ell_col; a.ell_val = c->ell_val;
   a.act = c->act; a.nptr = c->nptr; a.nnc_lcol = c->nnc_lcol; a.nnc_val = c->nnc_val;
   a.rhs = c->rhs; a.F_raw = c->F_raw;
   a.part_f2 = c->part_f2;

@@ -64,7 +64,6 @@ struct DArgs {
   double rtol;
   const int32_t* ell_col;
   const double* ell_val;
-  const uint8_t* ell_po;
   const int32_t* act;
   const int32_t* nptr;
   const int32_t* nnc_lcol;
@@ -337,7 +336,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
   // neighbour rows: cluster address per Cartesian slot (bit s of nmask = present)
   const double* na[NS];
   uint32_t nmask = 0;
-  uint32_t pmask = 0;  // bit s: slot s is a pressure-only block (K1's ell_po; blockops.h col0_only)
 #pragma unroll
   for (int s = 0; s < NS; ++s) na[s] = nullptr;
 
@@ -394,22 +392,14 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
       for (int k = 0; k < SG; ++k) {
         const int s = s0 + k;
         if (s < NS && (nmask & (1u << s))) {
-          const bool po = B > 1 && ((pmask >> s) & 1u);
-          // branch-free (the loads of all slots stay batched): both products, then a select
-          double M[B * B];
           if (MS) {
-#pragma unroll
-            for (int e = 0; e < B * B; ++e) M[e] = mval[((size_t)s * RC + lam) * B * B + e];
+            rsim::blk::gemv_acc_flat<B>(&mval[((size_t)s * RC + lam) * B * B], xv[k], acc);
+          } else if (ell_es(B * B) == 1) {
+            rsim::blk::gemv_acc_flat<B>(&a.ell_val[ell_at(a.cap, B * B, s, 0, l)], xv[k], acc);
           } else {
+            double M[B * B];
             ell_load<B>(a.ell_val, a.cap, s, l, M);
-          }
-#pragma unroll
-          for (int r = 0; r < B; ++r) {
-            const double s0v = M[r * B] * xv[k][0];
-            double sf = s0v;
-#pragma unroll
-            for (int c = 1; c < B; ++c) sf = sf + M[r * B + c] * xv[k][c];
-            acc[r] = acc[r] + (po ? s0v : sf);
+            rsim::blk::gemv_acc_flat<B>(M, xv[k], acc);
           }
         }
       }
@@ -495,7 +485,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_krylov_dsm(const DArgs a) {
           nrng[lam] = make_int2(q0, q1 | NNC_GLOBAL);
         }
       }
-      if (B > 1) pmask = a.ell_po[l];
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         const int32_t cl = a.ell_col[s * a.cap + l];
@@ -843,7 +832,6 @@ int launch_krylov_dsm(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.rtol = o->lin_rtol;
   a.ell_col = c->ell_col;
   a.ell_val = c->ell_val;
-  a.ell_po = c->ell_po;
   a.act = c->act;
   a.nptr = c->nptr;
   a.nnc_lcol = c->nnc_lcol;
