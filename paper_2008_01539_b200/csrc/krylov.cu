@@ -276,12 +276,16 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
 }
 
 // L2 prefetch of the matrix rows (block values + column indices) a warp will read in
-// its NEXT round, issued before the current round's loads: the value stream is
-// ~3/4 of the bytes of an SpMV pass and each round otherwise starts with one exposed
-// DRAM round trip.  A warp's 32 rows of one slot are one contiguous run of
-// 32·b²·8 B in both value layouts (ctx.cuh ell_at); lanes take its 128 B lines.
+// its NEXT round, issued before the current round's loads: the value stream is the
+// bulk of an SpMV pass and each round otherwise starts with one exposed DRAM round
+// trip.  A warp's 32 rows of one slot are one contiguous run of 32·b²·8 B in both
+// value layouts (ctx.cuh ell_at); lanes take its 128 B lines.  Used for b = 1 partial
+// sets only.  Measured (round 2, same box, 50 iterations on config 5): 5 % 9.11 -> 8.89 ms,
+// 20 % 28.1 -> 26.9, 50 % 64.6 -> 62.4, 100 % (structural columns) 114.4 -> 114.5; b = 2 / 3
+// whole runs get slower (config 3 1.25 -> 1.31 s, config 4 9.7 -> 10.8 s: the prefetched
+// blocks push the gathered vectors out of L2).
 #ifndef RSIM_PF
-#define RSIM_PF 0
+#define RSIM_PF 1
 #endif
 template <int B>
 __device__ __forceinline__ void prefetch_rows(const KArgs& a, int64_t l) {
@@ -347,7 +351,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   auto rmap = [&](int64_t rd0) { return rev ? nrounds - 1 - rd0 : rd0; };
   auto flip = [&]() { if (a.alt) rev = !rev; };
   auto pf = [&](int64_t rd0) {  // matrix rows of this CTA's next round (SpMV passes)
-    if (RSIM_PF && rd0 + gridDim.x < nrounds) prefetch_rows<B>(a, rmap(rd0 + gridDim.x) * KT + tid);
+    if (RSIM_PF && B == 1 && !a.implicit && rd0 + gridDim.x < nrounds) prefetch_rows<B>(a, rmap(rd0 + gridDim.x) * KT + tid);
   };
 #define ROUNDS_BEGIN                                                         \
   {                                                                          \
@@ -701,11 +705,19 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
     return (e && *e) ? (int32_t)std::atoi(e) : 2048;
   }();
   a.red_small_max = red_small < 64 * 256 ? red_small : 64 * 256;
-  static const int alt_env = [] {  // experiment switch
+  // Alternating sweep direction: every pass starts on the rows the previous pass
+  // touched last, which are still in L2.  It pays when the solve's working set (matrix
+  // + 11 vectors) is larger than L2, and costs a little when everything fits.  Whole
+  // runs, round 2, same box: config 4 (b = 3, 0.2-0.8 M rows, 150-600 MB) 9.71 -> 9.03 s;
+  // config 3 (b = 2, 150 k rows, 60 MB) 1.25 -> 1.31 s; config 5 at 20-100 % -0.2..-0.8 %.
+  static const int alt_env = [] {  // env override: tuning only
     const char* e = std::getenv("RSIM_KALT");
-    return (e && *e) ? std::atoi(e) : 0;
+    return (e && *e) ? std::atoi(e) : -1;
   }();
-  a.alt = alt_env;
+  {
+    const int64_t row_bytes = (int64_t)c->nslot * (8 * B * B + 4) + 11 * 8 * B;
+    a.alt = alt_env >= 0 ? alt_env : ((int64_t)c->nA * row_bytes > (int64_t)100e6 ? 1 : 0);
+  }
   a.pstride = (int32_t)((c->n + 255) / 256);
   a.pstride2 = (a.pstride + 255) / 256;
   a.part = c->part;
