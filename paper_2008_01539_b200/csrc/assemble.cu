@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
   }
   double O[B][B];
   int32_t lcol = -1;
+  bool nnc_act = false;  // owner lane: the row has an NNC block with an active column
   if (valid && q < a.nslot) {
     int64_t j;
     double T;
@@ -196,7 +197,9 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
         const int64_t j = __ldg(&a.nnbr[qq]);
         double On[B][B];
         conn<B>(a, ui, Pi, j, __ldg(&a.nt[qq]), R, D, On);
-        a.nnc_lcol[qq] = __ldg(&a.g2l[j]);
+        const int32_t lc = __ldg(&a.g2l[j]);
+        a.nnc_lcol[qq] = lc;
+        nnc_act = nnc_act || lc >= 0;
       }
     }
     rsim::phys::well_row<B>(__ldg(&a.wi[i]), ui[0], a.bhp, Pi, R, D);
@@ -245,11 +248,14 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
       for (int c = 0; c < B; ++c) Di[r][c] = sDi[rg][r * B + c];
     po = store_scaled_ell<B, false>(a, q, l, Di, O);
   }
-  if (B > 1) {  // lane q of the row group holds slot q's bit
+  if (B > 1 || a.has_nnc) {  // lane q of the row group holds slot q's bit, its owner lane the NNC bit
     const unsigned bal = __ballot_sync(0xffffffffu, po);
     const unsigned stored = __ballot_sync(0xffffffffu, valid && q < a.nslot && lcol >= 0);
-    if (valid && q == 0) a.ell_po[l] = (uint8_t)((bal >> (threadIdx.x & 24)) & 0x3fu);
-    if ((threadIdx.x & 31) == 0 && stored) {
+    const unsigned nnb = __ballot_sync(0xffffffffu, nnc_act);
+    const int base = threadIdx.x & 24;
+    if (valid && q == 0)
+      a.ell_po[l] = (uint8_t)(((bal >> base) & 0x3fu) | (((nnb >> (base + LPR - 1)) & 1u) ? ELL_ROW_NNC : 0u));
+    if (B > 1 && (threadIdx.x & 31) == 0 && stored) {
       atomicAdd(&a.dsc->nblk, (unsigned long long)__popc(stored));
       if (bal) atomicAdd(&a.dsc->npo, (unsigned long long)__popc(bal));
     }
@@ -351,6 +357,7 @@ __global__ void __launch_bounds__(256, B == 1 ? RSIM_K1ROW_MINB : 1) k_assemble_
       for (int s = 0; s < 6; ++s)
         if (s < a.nslot) __stcs(&a.ell_col[s * a.cap + l], has[s] ? gn[s] : -1);
     int32_t q0 = 0, q1 = 0;
+    bool nnc_act = false;  // the row has an NNC block with an active column
     if (a.has_nnc) {
       q0 = __ldg(&a.nptr[i]);
       q1 = __ldg(&a.nptr[i + 1]);
@@ -358,7 +365,9 @@ __global__ void __launch_bounds__(256, B == 1 ? RSIM_K1ROW_MINB : 1) k_assemble_
         const int64_t j = __ldg(&a.nnbr[q]);
         double O[B][B];
         conn<B>(a, ui, Pi, j, __ldg(&a.nt[q]), R, D, O);
-        a.nnc_lcol[q] = __ldg(&a.g2l[j]);
+        const int32_t lc = __ldg(&a.g2l[j]);
+        a.nnc_lcol[q] = lc;
+        nnc_act = nnc_act || lc >= 0;
       }
     }
     rsim::phys::well_row<B>(wi, ui[0], a.bhp, Pi, R, D);
@@ -410,7 +419,7 @@ __global__ void __launch_bounds__(256, B == 1 ? RSIM_K1ROW_MINB : 1) k_assemble_
       ++nblk;
       if (store_scaled_ell<B, true>(a, s, l, Di, O)) pom |= 1u << s;
     }
-    if (B > 1) __stcs(&a.ell_po[l], (uint8_t)pom);
+    if (B > 1 || a.has_nnc) __stcs(&a.ell_po[l], (uint8_t)(pom | (nnc_act ? ELL_ROW_NNC : 0u)));
     npo = __popc(pom);
     for (int32_t q = q0; q < q1; ++q) {
       const int64_t j = __ldg(&a.nnbr[q]);

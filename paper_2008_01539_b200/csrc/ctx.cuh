@@ -251,6 +251,10 @@ __device__ __forceinline__ void implicit_cols(int32_t nx, int32_t ny, int32_t nz
 //    address streams), warp-tiled 12.4 s (nine loads per block held in registers
 //    before the product: the b = 3 kernel then spills at its 128-register cap).
 // ell_es(b²) is the distance between consecutive elements of one block.
+// ell_po[l]: bits 0..5 pressure-only block per slot (b > 1); bit 7 (ELL_ROW_NNC): the
+// row has at least one NNC block with an active column (written when the graph has
+// NNCs), so the Krylov kernels walk act -> nptr -> nnc_lcol only for such rows.
+constexpr unsigned ELL_ROW_NNC = 0x80u;
 __host__ __device__ constexpr int ell_es(int bb) { return bb > 4 ? 1 : 32; }
 __host__ __device__ __forceinline__ int64_t ell_at(int64_t cap, int bb, int s, int e, int64_t l) {
   if (bb > 4) return ((int64_t)s * cap + l) * bb + e;

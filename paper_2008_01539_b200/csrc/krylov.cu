@@ -20,6 +20,7 @@
 //   p = r + β (p − ω v);  s = r − α v;  x = (x + α p) + ω s;  r = s − ω t.
 #include <cooperative_groups.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "ctx.cuh"
@@ -70,6 +71,7 @@ struct KArgs {
   double rtol;
   const int32_t* ell_col;
   const double* ell_val;
+  const uint8_t* ell_po;
   const int32_t* act;
   const int32_t* nptr;
   const int32_t* nnc_lcol;
@@ -229,6 +231,10 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
     for (int s = 0; s < 6; ++s)
       if (s < a.nslot) cl[s] = __ldg(&col[s * a.cap + l]);
   }
+  // row flags (K1): is there any NNC block to multiply?  Loaded with the columns, so
+  // the act -> nptr chain (two dependent gathers per row and pass that almost always
+  // found an empty range: 7 % of the stall samples on a config-4 solve) is gone.
+  const uint32_t rowf = a.has_nnc ? (uint32_t)__ldg(&a.ell_po[l]) : 0u;
   // Slots in groups of SG: all gathers of a group in flight, then its blocks.
   // Gathering all six neighbours first keeps 6·B doubles live and spills them
   // to local memory at 64 registers (b = 3: ~1 KB of local traffic per row and
@@ -261,7 +267,7 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
       }
     if (SG < 6) asm volatile("" ::: "memory");  // keep the next group's loads after this group's math
   }
-  if (a.has_nnc) {
+  if (a.has_nnc && (rowf & ELL_ROW_NNC)) {  // rare: rows of fracture cells and the cells they cross
     const int64_t i = a.act[l];
     const int32_t q0 = a.nptr[i], q1 = a.nptr[i + 1];
     for (int32_t q = q0; q < q1; ++q) {
@@ -304,6 +310,12 @@ __device__ __forceinline__ void prefetch_rows(const KArgs& a, int64_t l) {
   }
 }
 
+// Per-pass wall time of one solve (debug builds, -DRSIM_KTIME=1; scripts/ab_krylov_build.sh):
+// block 0 accumulates globaltimer deltas at the grid barriers that end each pass and prints
+// them when the kernel ends.  Adds one barrier after the x/r pass; never on in the product.
+#ifndef RSIM_KTIME
+#define RSIM_KTIME 0
+#endif
 // FUSE is a template parameter: the two variants have different live state,
 // and one kernel holding both spills heavily at 64 registers / thread.
 template <int B, bool FUSE, bool ILU, int KT>
@@ -350,6 +362,15 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   bool rev = false;
   auto rmap = [&](int64_t rd0) { return rev ? nrounds - 1 - rd0 : rd0; };
   auto flip = [&]() { if (a.alt) rev = !rev; };
+  unsigned long long kt_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, kt_last = 0;
+  auto tick = [&](int ph) {
+    if (RSIM_KTIME && blockIdx.x == 0 && tid == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (ph >= 0) kt_acc[ph] += t - kt_last;
+      kt_last = t;
+    }
+  };
   auto pf = [&](int64_t rd0) {  // matrix rows of this CTA's next round (SpMV passes)
     if (RSIM_PF && B == 1 && !a.implicit && rd0 + gridDim.x < nrounds) prefetch_rows<B>(a, rmap(rd0 + gridDim.x) * KT + tid);
   };
@@ -391,6 +412,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   }
   ROUNDS_END(nq_init)
   reduce(2, a.f2_parts ? a.part_f2 : nullptr);
+  tick(-1);
   const double bb = R.res[0];
   if (blockIdx.x == 0 && tid == 0) a.dsc->f2 = sqrt(R.res[1]);
   const double bnorm = sqrt(bb);
@@ -461,6 +483,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       }
       sync();
       flip();
+      tick(0);
     }
     if (neu) {  // ph = p + (p − Â p), stored, barrier
       for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
@@ -484,6 +507,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       }
       sync();
       flip();
+      tick(1);
     }
     if (ilu) ilu_apply<B>(a.fa, pc, a.ph, sync);  // ph = (LU)^{-1} p (p stored: unfused)
     // ---- v = Â p (BJ) or v = Â ph (Neumann-1, ILU(0)); (r0, v) and the lagged (r, r)
@@ -509,6 +533,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     }
     ROUNDS_END(2)
     reduce(2);
+    tick(2);
     if (it > 1 && !fixed && sqrt(R.res[1]) <= tol) {  // previous iterate converged
       relres = sqrt(R.res[1]) / bnorm;
       status = RSIM_OK;
@@ -529,6 +554,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       }
       sync();
       flip();
+      tick(3);
     }
     if (neu) {  // sh = s + (s − Â s), stored, barrier
       for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
@@ -550,6 +576,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       }
       sync();
       flip();
+      tick(4);
     }
     if (ilu) ilu_apply<B>(a.fa, a.s, a.sh, sync);  // sh = (LU)^{-1} s
     // ---- t = Â s (BJ) or t = Â sh (Neumann-1, ILU(0)); (s,s), (t,s), (t,t), (r0,s), (r0,t)
@@ -584,6 +611,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     }
     ROUNDS_END(5)
     reduce(5);
+    tick(5);
     const double ss = R.res[0], ts = R.res[1], tt = R.res[2], r0s = R.res[3], r0t = R.res[4];
     const double* phv = prec ? a.ph : pc;
     const double* shv = prec ? a.sh : a.s;
@@ -626,6 +654,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
           if (pfuse) pn[q] = rq + beta_next * (pc[q] - omega * vc[q]);
         }
     }
+    if (RSIM_KTIME) { sync(); tick(6); }
     p_ready = pfuse;
     rho = rho_new;
     rho_new = rho_next;
@@ -645,6 +674,10 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   if (!(prec && (status == RSIM_ENUM || status == RSIM_ENOCONV))) break;
   }
   it = it_total;
+  if (RSIM_KTIME && blockIdx.x == 0 && tid == 0)
+    printf("KTIME rows %d its %d us: p %.1f ph %.1f v+red %.1f s %.1f sh %.1f t+red %.1f xr %.1f\n", a.nA, it,
+           kt_acc[0] * 1e-3, kt_acc[1] * 1e-3, kt_acc[2] * 1e-3, kt_acc[3] * 1e-3, kt_acc[4] * 1e-3,
+           kt_acc[5] * 1e-3, kt_acc[6] * 1e-3);
   if (blockIdx.x == 0 && tid == 0) {
     a.dsc->lin_iters = it;
     a.dsc->lin_relres = relres;
@@ -675,7 +708,7 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.cap = c->ell_cap;
   a.has_nnc = c->has_nnc;
   a.rtol = o->lin_rtol;
-  a.ell_col = c->ell_col; a.ell_val = c->ell_val;
+  a.ell_col = c->ell_col; a.ell_val = c->ell_val; a.ell_po = c->ell_po;
   a.act = c->act; a.nptr = c->nptr; a.nnc_lcol = c->nnc_lcol; a.nnc_val = c->nnc_val;
   a.rhs = c->rhs; a.F_raw = c->F_raw;
   a.part_f2 = c->part_f2;

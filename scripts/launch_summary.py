@@ -2,9 +2,11 @@
   python scripts/launch_summary.py launches.csv [N]"""
 import collections
 import csv
+import gzip
 import sys
 
-lines = [l for l in open(sys.argv[1]) if l.startswith('"')]
+_open = gzip.open if sys.argv[1].endswith(".gz") else open
+lines = [l for l in _open(sys.argv[1], "rt") if l.startswith('"')]
 rows = list(csv.reader(lines))
 h = rows[0]
 ik, iv, iu = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
