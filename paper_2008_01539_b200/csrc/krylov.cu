@@ -88,6 +88,7 @@ struct KArgs {
   double* part2;  // [5][pstride2] level-2 partials (very large systems)
   int32_t pstride, pstride2;
   int32_t red_small_max;  // chunk partials reduced redundantly by every CTA up to this count
+  int32_t kblk;           // consecutive rounds per CTA (blocked-cyclic distribution; 1 = round-robin)
   int32_t alt;            // sweep direction alternates between phases (L2 reuse of the previous sweep's tail)
   DevScalars* dsc;
 };
@@ -108,14 +109,26 @@ struct Red {
 // and after the CTA's last round, one barrier pair turns them into level-1
 // chunk partials (8-way trees, canonical).  Warps thus run ahead through up
 // to RSTAGE rounds of loads instead of meeting at two barriers per round.
-template <int CPR>
-__device__ __forceinline__ void stage_round(Red& R, int NQ, const double* val, int slot, int64_t rd, bool flush,
+template <int CPR, int NQ>
+__device__ __forceinline__ void stage_round(Red& R, const double* val, int slot, int64_t rd, bool flush,
                                             int nstaged, int64_t nch, double* part, int pstride) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int q = 0; q < NQ; ++q) {
-    double v = warp_tree(val[q]);
-    if (lane == 0) R.wsr[slot][q][w] = v;
-  }
+#ifdef RSIM_DBG_NORED  // timing experiment only (wrong numerics): no warp trees
+  if (lane == 0) for (int q = 0; q < NQ; ++q) R.wsr[slot][q][w] = val[q];
+#else
+  // the NQ warp trees level by level (each quantity: v + shfl_down(v, 16), 8, 4, 2, 1 as in
+  // warp_tree, so the same bits): 5 dependent shuffle steps instead of 5·NQ
+  double v[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) v[q] = val[q];
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) v[q] = v[q] + __shfl_down_sync(0xffffffffu, v[q], off);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) R.wsr[slot][q][w] = v[q];
+#endif
   if (threadIdx.x == 0) R.rid[slot] = rd;
   if (!flush) return;
   __syncthreads();
@@ -216,15 +229,51 @@ __device__ __forceinline__ void nbr_val(int mode, const Vecs& X, int64_t j, doub
   }
 }
 
+// b = 1: matrix row (columns + values) loaded one round ahead.  In the passes that end
+// with a reduction a warp otherwise runs load -> wait -> math -> 5-step shuffle trees ->
+// next round's loads, i.e. nothing in flight during the trees (measured on config 5 at
+// 100 %: the trees cost 16 % of the v pass, 14 % of the t pass).  The next round's row is
+// requested BEFORE the trees; its columns are then known when the round starts, so the
+// gathers no longer wait for a column load either.
+#ifndef RSIM_PRE1
+#define RSIM_PRE1 1
+#endif
+struct Pre1 {
+  double m[6];
+  int32_t c[6];
+};
+__device__ __forceinline__ void pre_load1(const KArgs& a, int64_t l, bool ok, Pre1& P) {
+#pragma unroll
+  for (int s = 0; s < 6; ++s) { P.c[s] = -1; P.m[s] = 0.0; }
+  if (!ok) return;
+  if (a.implicit) {
+    implicit_cols(a.nx, a.ny, a.nz, a.d3, l, P.c);
+#pragma unroll
+    for (int s = 0; s < 6; ++s)
+      if (P.c[s] >= 0) P.m[s] = a.ell_val[(int64_t)s * a.cap + l];
+  } else {  // columns not known yet: the value slot of an absent neighbour is loaded and ignored
+#pragma unroll
+    for (int s = 0; s < 6; ++s)
+      if (s < a.nslot) {
+        P.c[s] = __ldg(&a.ell_col[(int64_t)s * a.cap + l]);
+        P.m[s] = a.ell_val[(int64_t)s * a.cap + l];
+      }
+  }
+}
+
 template <int B>
 __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, const Vecs& X, double beta,
-                                         double omega, double alpha, const double* own, double* acc) {
+                                         double omega, double alpha, const double* own, double* acc,
+                                         const Pre1* pre = nullptr) {
   const int32_t* __restrict__ col = a.ell_col;
   const double* __restrict__ val = a.ell_val;
   int32_t cl[6];
 #pragma unroll
   for (int s = 0; s < 6; ++s) cl[s] = -1;
-  if (a.implicit) {
+  if (B == 1 && pre) {
+#pragma unroll
+    for (int s = 0; s < 6; ++s) cl[s] = pre->c[s];
+  } else if (a.implicit) {
     implicit_cols(a.nx, a.ny, a.nz, a.d3, l, cl);
   } else {
 #pragma unroll
@@ -253,11 +302,17 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
     double xv[SG][B];
 #pragma unroll
     for (int k = 0; k < SG; ++k)
+#ifdef RSIM_DBG_NOGATHER  // timing experiment only (wrong numerics): neighbour := own row
+      if (s0 + k < 6 && cl[s0 + k] >= 0) nbr_val<B>(mode, X, l, beta, omega, alpha, xv[k]);
+#else
       if (s0 + k < 6 && cl[s0 + k] >= 0) nbr_val<B>(mode, X, cl[s0 + k], beta, omega, alpha, xv[k]);
+#endif
 #pragma unroll
     for (int k = 0; k < SG; ++k)
       if (s0 + k < 6 && cl[s0 + k] >= 0) {
-        if (ell_es(B * B) == 1) {  // row-major blocks: the product reads them in place
+        if (B == 1 && pre) {
+          rsim::blk::gemv_acc_flat<B>(&pre->m[s0 + k], xv[k], acc);
+        } else if (ell_es(B * B) == 1) {  // row-major blocks: the product reads them in place
           rsim::blk::gemv_acc_flat<B>(&val[ell_at(a.cap, B * B, s0 + k, 0, l)], xv[k], acc);
         } else {
           double M[B * B];
@@ -360,7 +415,19 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
   // previous phase touched last (still in L2).  Row results do not depend on the
   // order (reductions go through per-chunk partials), so the bits are unchanged.
   bool rev = false;
-  auto rmap = [&](int64_t rd0) { return rev ? nrounds - 1 - rd0 : rd0; };
+  // Blocked-cyclic rounds (a.kblk > 1): CTA b takes kblk consecutive rounds, then jumps
+  // grid·kblk ahead, so the ±y neighbours of a round are rows the same SM has just read
+  // (L1) while all CTAs still work inside one window of grid·kblk rounds (L2).  The ragged
+  // tail past the last full window stays round-robin.  A bijection on the rounds, so the
+  // bits are unchanged.
+  const int64_t GK = (int64_t)gridDim.x * a.kblk, NF = (nrounds / GK) * GK;
+  auto rmap = [&](int64_t rd0) {
+    const int64_t v = rev ? nrounds - 1 - rd0 : rd0;
+    if (a.kblk <= 1 || v >= NF) return v;
+    const int64_t sb = v / GK, w = v - sb * GK;
+    const int64_t jj = w / gridDim.x, b = w - jj * gridDim.x;
+    return sb * GK + b * a.kblk + jj;
+  };
   auto flip = [&]() { if (a.alt) rev = !rev; };
   unsigned long long kt_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, kt_last = 0;
   auto tick = [&](int ph) {
@@ -386,15 +453,30 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     {                                                                        \
       const int slot = rloc % a.stage;                                       \
       const bool last = rd0 + gridDim.x >= nrounds;                          \
-      stage_round<CPR>(R, NQ, val, slot, rd, slot == a.stage - 1 || last, slot + 1, nch, a.part, a.pstride); \
+      stage_round<CPR, NQ>(R, val, slot, rd, slot == a.stage - 1 || last, slot + 1, nch, a.part, a.pstride); \
     }                                                                        \
   }                                                                          \
   flip();                                                                    \
   }
 
+  constexpr bool PRE = B == 1 && RSIM_PRE1;
+  Pre1 P1;
+  const Pre1* pre = PRE ? &P1 : nullptr;
+  auto pre_first = [&]() {  // before a reducing SpMV pass: this CTA's first round
+    if (PRE) {
+      const int64_t l = rmap(blockIdx.x) * KT + tid;
+      pre_load1(a, l, (int64_t)blockIdx.x < nrounds && l < nr, P1);
+    }
+  };
+  auto pre_next = [&](int64_t rd0) {  // at the end of a round, before its shuffle trees
+    if (PRE) {
+      const bool more = rd0 + gridDim.x < nrounds;
+      const int64_t l = more ? rmap(rd0 + gridDim.x) * KT + tid : 0;
+      pre_load1(a, l, more && l < nr, P1);
+    }
+  };
   // ---- init: r = r0 = rhs, x = 0;  (rhs, rhs), (F, F) (the latter from the
   //      assembly's canonical chunk partials when it left them)
-  const int nq_init = a.f2_parts ? 1 : 2;
   ROUNDS_BEGIN
   if (ok) {
     double bv[B];
@@ -410,7 +492,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       val[1] = rsim::blk::rowdot<B>(fv, fv);
     }
   }
-  ROUNDS_END(nq_init)
+  ROUNDS_END(2)  // (F,F) staged as zeros when the assembly left its chunk partials
   reduce(2, a.f2_parts ? a.part_f2 : nullptr);
   tick(-1);
   const double bb = R.res[0];
@@ -511,26 +593,28 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     }
     if (ilu) ilu_apply<B>(a.fa, pc, a.ph, sync);  // ph = (LU)^{-1} p (p stored: unfused)
     // ---- v = Â p (BJ) or v = Â ph (Neumann-1, ILU(0)); (r0, v) and the lagged (r, r)
+    pre_first();
     ROUNDS_BEGIN
     pf(rd0);
     if (ok) {
       double y[B];
       if (prec) {
-        spmv_row<B>(a, l, 3, Vecs{a.r, a.ph, vo, a.s, a.t}, 0.0, 0.0, 0.0, &a.ph[l * B], y);
+        spmv_row<B>(a, l, 3, Vecs{a.r, a.ph, vo, a.s, a.t}, 0.0, 0.0, 0.0, &a.ph[l * B], y, pre);
       } else if (fuse) {
         double pown[B];
         nbr_val<B>(pmode, V0, l, beta, omega, 0.0, pown);
 #pragma unroll
         for (int e = 0; e < B; ++e) pc[l * B + e] = pown[e];
-        spmv_row<B>(a, l, pmode, V0, beta, omega, 0.0, pown, y);
+        spmv_row<B>(a, l, pmode, V0, beta, omega, 0.0, pown, y, pre);
       } else {
-        spmv_row<B>(a, l, 3, Vecs{a.r, pc, vo, a.s, a.t}, 0.0, 0.0, 0.0, &pc[l * B], y);
+        spmv_row<B>(a, l, 3, Vecs{a.r, pc, vo, a.s, a.t}, 0.0, 0.0, 0.0, &pc[l * B], y, pre);
       }
 #pragma unroll
       for (int e = 0; e < B; ++e) vc[l * B + e] = y[e];
       val[0] = rsim::blk::rowdot<B>(&a.r0[l * B], y);
       val[1] = rsim::blk::rowdot<B>(&a.r[l * B], &a.r[l * B]);
     }
+    pre_next(rd0);
     ROUNDS_END(2)
     reduce(2);
     tick(2);
@@ -580,6 +664,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     }
     if (ilu) ilu_apply<B>(a.fa, a.s, a.sh, sync);  // sh = (LU)^{-1} s
     // ---- t = Â s (BJ) or t = Â sh (Neumann-1, ILU(0)); (s,s), (t,s), (t,t), (r0,s), (r0,t)
+    pre_first();
     ROUNDS_BEGIN
     pf(rd0);
     if (ok) {
@@ -589,14 +674,14 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
         else
 #pragma unroll
           for (int e = 0; e < B; ++e) sv[e] = a.s[l * B + e];
-        spmv_row<B>(a, l, 3, Vecs{a.r, a.sh, vc, a.s, a.t}, 0.0, 0.0, 0.0, &a.sh[l * B], y);
+        spmv_row<B>(a, l, 3, Vecs{a.r, a.sh, vc, a.s, a.t}, 0.0, 0.0, 0.0, &a.sh[l * B], y, pre);
       } else if (fs) {
         nbr_val<B>(2, V2, l, 0.0, 0.0, alpha, sv);
-        spmv_row<B>(a, l, 2, V2, 0.0, 0.0, alpha, sv, y);
+        spmv_row<B>(a, l, 2, V2, 0.0, 0.0, alpha, sv, y, pre);
       } else {
 #pragma unroll
         for (int e = 0; e < B; ++e) sv[e] = a.s[l * B + e];
-        spmv_row<B>(a, l, 3, Vecs{a.r, a.s, vc, a.s, a.t}, 0.0, 0.0, 0.0, sv, y);
+        spmv_row<B>(a, l, 3, Vecs{a.r, a.s, vc, a.s, a.t}, 0.0, 0.0, 0.0, sv, y, pre);
       }
       if (fs)
 #pragma unroll
@@ -609,6 +694,7 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       val[3] = rsim::blk::rowdot<B>(&a.r0[l * B], sv);
       val[4] = rsim::blk::rowdot<B>(&a.r0[l * B], y);
     }
+    pre_next(rd0);
     ROUNDS_END(5)
     reduce(5);
     tick(5);
@@ -751,6 +837,11 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
     const int64_t row_bytes = (int64_t)c->nslot * (8 * B * B + 4) + 11 * 8 * B;
     a.alt = alt_env >= 0 ? alt_env : ((int64_t)c->nA * row_bytes > (int64_t)100e6 ? 1 : 0);
   }
+  static const int kblk_env = [] {  // env override: tuning only
+    const char* e = std::getenv("RSIM_KBLK");
+    return (e && *e) ? std::atoi(e) : 0;
+  }();
+  a.kblk = kblk_env > 0 ? kblk_env : 1;
   a.pstride = (int32_t)((c->n + 255) / 256);
   a.pstride2 = (a.pstride + 255) / 256;
   a.part = c->part;
