@@ -59,7 +59,14 @@ __host__ __device__ constexpr int kt_for(int B) { return B == 1 ? RSIM_KT1 : (B 
 #ifndef RSIM_SPMV_SG3
 #define RSIM_SPMV_SG3 1
 #endif
-constexpr int64_t kFuseMaxRows = 1 << 20;  // recompute-fusion only while latency-bound
+// Recompute fusion (neighbours' p and s formed at the gather sites, two grid barriers and the
+// p / s store passes less per iteration) up to this many rows.  b = 1: 2^20 (config 5: above it the
+// extra gather traffic costs more than the barriers).  b >= 2: always — the per-row matrix work
+// dominates and the fused kernel wins at every size measured in round 2: config 3 standard Newton
+// (2.1 M rows, b = 2) 3.38 -> 2.66 s per 2 steps, config 4 standard Newton (4.2 M rows, b = 3)
+// 12.75 -> 11.90 s, config 4 adaptive DD (subdomain systems > 2^20 rows) 13.54 -> 12.97 s per run;
+// below 2^20 rows the unfused kernel is 10-18 % slower on the config-4 localized run.
+__host__ __device__ constexpr int64_t fuse_max_rows(int B) { return B == 1 ? ((int64_t)1 << 20) : ((int64_t)1 << 40); }
 
 struct KArgs {
   int32_t nA, nslot, maxit, fixed;
@@ -806,9 +813,9 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   a.fa = ilu_args(c);
   static const int64_t fuse_max = [] {  // env override: tuning only
     const char* e = std::getenv("RSIM_FUSE_MAX_ROWS");
-    return (e && *e) ? (int64_t)std::atoll(e) : kFuseMaxRows;
+    return (e && *e) ? (int64_t)std::atoll(e) : (int64_t)-1;
   }();
-  a.fuse = (c->nA <= fuse_max && !a.ilu) ? 1 : 0;
+  a.fuse = (c->nA <= (fuse_max >= 0 ? fuse_max : fuse_max_rows(B)) && !a.ilu) ? 1 : 0;
   // s recompute at the gather sites: measured on config 5 (50 iterations),
   // 9.50 -> 9.35 ms at 5 % (1.7 M rows), even at 20 %, 114.5 -> 119.1 ms at 100 %
   static const int64_t fuse_s_max = [] {  // env override: tuning only
