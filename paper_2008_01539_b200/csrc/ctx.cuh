@@ -224,9 +224,22 @@ __device__ __forceinline__ unsigned long long dbits(double a) {
 // of cell i are structural — the Cartesian neighbours in slot order, -1 off-grid.
 __device__ __forceinline__ void implicit_cols(int32_t nx, int32_t ny, int32_t nz, bool d3, int64_t i, int32_t* cl) {
   const uint32_t nxy = (uint32_t)nx * (uint32_t)ny;
-  const uint32_t iz = (uint32_t)i / nxy;
-  const uint32_t rem = (uint32_t)i - iz * nxy;
-  const uint32_t iy = rem / (uint32_t)nx, ix = rem - iy * (uint32_t)nx;
+  uint32_t ix, iy, iz;
+#ifndef RSIM_NO_POW2  // A/B switch
+  if ((((uint32_t)nx & ((uint32_t)nx - 1u)) | ((uint32_t)ny & ((uint32_t)ny - 1u))) == 0u) {
+    // power-of-two nx, ny (configs 2-5): shifts and masks instead of two integer divisions
+    const int sx = 31 - __clz(nx), sy = 31 - __clz(ny);
+    ix = (uint32_t)i & ((uint32_t)nx - 1u);
+    iy = ((uint32_t)i >> sx) & ((uint32_t)ny - 1u);
+    iz = (uint32_t)i >> (sx + sy);
+  } else
+#endif
+  {
+    iz = (uint32_t)i / nxy;
+    const uint32_t rem = (uint32_t)i - iz * nxy;
+    iy = rem / (uint32_t)nx;
+    ix = rem - iy * (uint32_t)nx;
+  }
   const int32_t ii = (int32_t)i;
   // constant indices only: a runtime slot counter would force cl[] (and the
   // caller's gathers) into local memory

@@ -245,6 +245,15 @@ __device__ __forceinline__ void nbr_val(int mode, const Vecs& X, int64_t j, doub
 #ifndef RSIM_PRE1
 #define RSIM_PRE1 1
 #endif
+#ifndef RSIM_EARLY_R0  // b = 1: r0 / r of a row requested before its product (see the v pass)
+#define RSIM_EARLY_R0 1
+#endif
+#ifndef RSIM_EARLY_R0_BMAX  // ... for block sizes up to this one
+#define RSIM_EARLY_R0_BMAX 1
+#endif
+#ifndef RSIM_XR_LOADFIRST  // b >= 2: x/r update pass loads all components before its first store
+#define RSIM_XR_LOADFIRST 1    // (config 4 run 8.86 -> 8.73 s; early r0 / r for b = 3: 8.86 -> 9.01 s, so BMAX stays 1)
+#endif
 struct Pre1 {
   double m[6];
   int32_t c[6];
@@ -268,10 +277,32 @@ __device__ __forceinline__ void pre_load1(const KArgs& a, int64_t l, bool ok, Pr
   }
 }
 
+// Columns (and the NNC row flag) of a warp's NEXT round, requested at the start of the
+// current one (b = 2, partial sets).  Without it every round of every SpMV pass
+// starts with two dependent DRAM round trips — the column load, then the block values
+// (guarded by column >= 0) and the gathers — and the passes are latency-bound.
+#ifndef RSIM_COLPRE
+#define RSIM_COLPRE 1
+#endif
+struct ColPre {
+  int32_t c[6];
+  uint32_t f;
+};
+__device__ __forceinline__ void cols_load(const KArgs& a, int64_t l, bool ok, ColPre& C) {
+#pragma unroll
+  for (int s = 0; s < 6; ++s) C.c[s] = -1;
+  C.f = 0u;
+  if (!ok) return;
+#pragma unroll
+  for (int s = 0; s < 6; ++s)
+    if (s < a.nslot) C.c[s] = __ldg(&a.ell_col[(int64_t)s * a.cap + l]);
+  if (a.has_nnc) C.f = (uint32_t)__ldg(&a.ell_po[l]);
+}
+
 template <int B>
 __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, const Vecs& X, double beta,
                                          double omega, double alpha, const double* own, double* acc,
-                                         const Pre1* pre = nullptr) {
+                                         const Pre1* pre = nullptr, const ColPre* cpre = nullptr) {
   const int32_t* __restrict__ col = a.ell_col;
   const double* __restrict__ val = a.ell_val;
   int32_t cl[6];
@@ -280,6 +311,9 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
   if (B == 1 && pre) {
 #pragma unroll
     for (int s = 0; s < 6; ++s) cl[s] = pre->c[s];
+  } else if (cpre) {
+#pragma unroll
+    for (int s = 0; s < 6; ++s) cl[s] = cpre->c[s];
   } else if (a.implicit) {
     implicit_cols(a.nx, a.ny, a.nz, a.d3, l, cl);
   } else {
@@ -290,7 +324,7 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
   // row flags (K1): is there any NNC block to multiply?  Loaded with the columns, so
   // the act -> nptr chain (two dependent gathers per row and pass that almost always
   // found an empty range: 7 % of the stall samples on a config-4 solve) is gone.
-  const uint32_t rowf = a.has_nnc ? (uint32_t)__ldg(&a.ell_po[l]) : 0u;
+  const uint32_t rowf = cpre ? cpre->f : (a.has_nnc ? (uint32_t)__ldg(&a.ell_po[l]) : 0u);
   // Slots in groups of SG: all gathers of a group in flight, then its blocks.
   // Gathering all six neighbours first keeps 6·B doubles live and spills them
   // to local memory at 64 registers (b = 3: ~1 KB of local traffic per row and
@@ -343,17 +377,14 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
   }
 }
 
-// L2 prefetch of the matrix rows (block values + column indices) a warp will read in
-// its NEXT round, issued before the current round's loads: the value stream is the
-// bulk of an SpMV pass and each round otherwise starts with one exposed DRAM round
-// trip.  A warp's 32 rows of one slot are one contiguous run of 32·b²·8 B in both
-// value layouts (ctx.cuh ell_at); lanes take its 128 B lines.  Used for b = 1 partial
-// sets only.  Measured (round 2, same box, 50 iterations on config 5): 5 % 9.11 -> 8.89 ms,
-// 20 % 28.1 -> 26.9, 50 % 64.6 -> 62.4, 100 % (structural columns) 114.4 -> 114.5; b = 2 / 3
-// whole runs get slower (config 3 1.25 -> 1.31 s, config 4 9.7 -> 10.8 s: the prefetched
-// blocks push the gathered vectors out of L2).
+// L2 prefetch (prefetch.global.L2) of the matrix rows a warp will read in its NEXT round.
+// Off.  History (round 2, config 5, 50 iterations, same box each): alone it gained 2.5-4 % on
+// b = 1 partial sets (5 % 9.11 -> 8.89 ms, 20 % 28.1 -> 26.9, 50 % 64.6 -> 62.4); once the next
+// round's row is requested into registers before the shuffle trees (Pre1 below) it is redundant
+// and costs 6-7 % (20 %: 24.7 ms without vs 26.5 with, 50 %: 58.2 vs 62.2, 1 %: 2.30 vs 2.49).
+// For b = 2 / 3 it was slower from the start (config 3 1.25 -> 1.31 s, config 4 9.7 -> 10.8 s).
 #ifndef RSIM_PF
-#define RSIM_PF 1
+#define RSIM_PF 0
 #endif
 template <int B>
 __device__ __forceinline__ void prefetch_rows(const KArgs& a, int64_t l) {
@@ -482,6 +513,28 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       pre_load1(a, l, more && l < nr, P1);
     }
   };
+  // generic column preload (partial sets; b = 1 uses Pre1 in the reducing passes instead)
+  ColPre Ccur, Cnx;
+  // b = 2 only (measured on whole runs, same box: config 3 1.358 -> 1.290 s; for b = 3 the 14
+  // extra live registers cost more than the round trip saves, config 4 8.85 -> 9.79 s, and the
+  // b = 1 kernel, which needs it only in the Neumann passes, slows down by 3-5 % on config 5)
+  const bool use_cp = RSIM_COLPRE && B == 2 && !a.implicit;
+  auto cp_first = [&](bool skip) {
+    if (use_cp && !skip) {
+      const int64_t l = rmap(blockIdx.x) * KT + tid;
+      cols_load(a, l, (int64_t)blockIdx.x < nrounds && l < nr, Ccur);
+    }
+  };
+  auto cp_next = [&](int64_t rd0, bool skip) {  // at the START of a round: the next round's columns
+    if (use_cp && !skip) {
+      const bool more = rd0 + gridDim.x < nrounds;
+      const int64_t l = more ? rmap(rd0 + gridDim.x) * KT + tid : 0;
+      cols_load(a, l, more && l < nr, Cnx);
+    }
+  };
+  auto cp_adv = [&](bool skip) { if (use_cp && !skip) Ccur = Cnx; };
+  const ColPre* cpa = use_cp ? &Ccur : nullptr;           // passes without a reduction
+  const ColPre* cpr = (use_cp && !PRE) ? &Ccur : nullptr;  // reducing passes (b = 1: Pre1 instead)
   // ---- init: r = r0 = rhs, x = 0;  (rhs, rhs), (F, F) (the latter from the
   //      assembly's canonical chunk partials when it left them)
   ROUNDS_BEGIN
@@ -575,24 +628,27 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       tick(0);
     }
     if (neu) {  // ph = p + (p − Â p), stored, barrier
+      cp_first(false);
       for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
         const int64_t l = rmap(rd0) * KT + tid;
         pf(rd0);
+        cp_next(rd0, false);
         if (l < nr) {
           double pown[B], y[B];
           if (fuse) {
             nbr_val<B>(pmode, V0, l, beta, omega, 0.0, pown);
-            spmv_row<B>(a, l, pmode, V0, beta, omega, 0.0, pown, y);
+            spmv_row<B>(a, l, pmode, V0, beta, omega, 0.0, pown, y, nullptr, cpa);
 #pragma unroll
             for (int e = 0; e < B; ++e) pc[l * B + e] = pown[e];
           } else {
 #pragma unroll
             for (int e = 0; e < B; ++e) pown[e] = pc[l * B + e];
-            spmv_row<B>(a, l, 3, Vecs{a.r, pc, vo, a.s, a.t}, 0.0, 0.0, 0.0, pown, y);
+            spmv_row<B>(a, l, 3, Vecs{a.r, pc, vo, a.s, a.t}, 0.0, 0.0, 0.0, pown, y, nullptr, cpa);
           }
 #pragma unroll
           for (int e = 0; e < B; ++e) a.ph[l * B + e] = pown[e] + (pown[e] - y[e]);
         }
+        cp_adv(false);
       }
       sync();
       flip();
@@ -601,26 +657,42 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     if (ilu) ilu_apply<B>(a.fa, pc, a.ph, sync);  // ph = (LU)^{-1} p (p stored: unfused)
     // ---- v = Â p (BJ) or v = Â ph (Neumann-1, ILU(0)); (r0, v) and the lagged (r, r)
     pre_first();
+    cp_first(PRE);
     ROUNDS_BEGIN
     pf(rd0);
+    cp_next(rd0, PRE);
     if (ok) {
       double y[B];
+      // b = 1: r0 and r of the row are requested before the product.  After it they sit
+      // behind the store of v (the vectors may alias as far as the compiler knows), i.e. one
+      // more exposed DRAM round trip per round (11 % of the stall samples at 100 % of config 5).
+      // b >= 2 keeps the late loads: 2·b more live doubles would spill at the 128-register cap.
+      double r0e[B], re[B];
+      if (B <= RSIM_EARLY_R0_BMAX && RSIM_EARLY_R0) {
+#pragma unroll
+        for (int e = 0; e < B; ++e) { r0e[e] = a.r0[l * B + e]; re[e] = a.r[l * B + e]; }
+      }
       if (prec) {
-        spmv_row<B>(a, l, 3, Vecs{a.r, a.ph, vo, a.s, a.t}, 0.0, 0.0, 0.0, &a.ph[l * B], y, pre);
+        spmv_row<B>(a, l, 3, Vecs{a.r, a.ph, vo, a.s, a.t}, 0.0, 0.0, 0.0, &a.ph[l * B], y, pre, cpr);
       } else if (fuse) {
         double pown[B];
         nbr_val<B>(pmode, V0, l, beta, omega, 0.0, pown);
 #pragma unroll
         for (int e = 0; e < B; ++e) pc[l * B + e] = pown[e];
-        spmv_row<B>(a, l, pmode, V0, beta, omega, 0.0, pown, y, pre);
+        spmv_row<B>(a, l, pmode, V0, beta, omega, 0.0, pown, y, pre, cpr);
       } else {
-        spmv_row<B>(a, l, 3, Vecs{a.r, pc, vo, a.s, a.t}, 0.0, 0.0, 0.0, &pc[l * B], y, pre);
+        spmv_row<B>(a, l, 3, Vecs{a.r, pc, vo, a.s, a.t}, 0.0, 0.0, 0.0, &pc[l * B], y, pre, cpr);
       }
 #pragma unroll
       for (int e = 0; e < B; ++e) vc[l * B + e] = y[e];
-      val[0] = rsim::blk::rowdot<B>(&a.r0[l * B], y);
-      val[1] = rsim::blk::rowdot<B>(&a.r[l * B], &a.r[l * B]);
+      if (!(B <= RSIM_EARLY_R0_BMAX && RSIM_EARLY_R0)) {
+#pragma unroll
+        for (int e = 0; e < B; ++e) { r0e[e] = a.r0[l * B + e]; re[e] = a.r[l * B + e]; }
+      }
+      val[0] = rsim::blk::rowdot<B>(r0e, y);
+      val[1] = rsim::blk::rowdot<B>(re, re);
     }
+    cp_adv(PRE);
     pre_next(rd0);
     ROUNDS_END(2)
     reduce(2);
@@ -648,22 +720,25 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       tick(3);
     }
     if (neu) {  // sh = s + (s − Â s), stored, barrier
+      cp_first(false);
       for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
         const int64_t l = rmap(rd0) * KT + tid;
         pf(rd0);
+        cp_next(rd0, false);
         if (l < nr) {
           double sv[B], y[B];
           if (fuse) {
             nbr_val<B>(2, V2, l, 0.0, 0.0, alpha, sv);
-            spmv_row<B>(a, l, 2, V2, 0.0, 0.0, alpha, sv, y);
+            spmv_row<B>(a, l, 2, V2, 0.0, 0.0, alpha, sv, y, nullptr, cpa);
           } else {
 #pragma unroll
             for (int e = 0; e < B; ++e) sv[e] = a.s[l * B + e];
-            spmv_row<B>(a, l, 3, Vecs{a.r, a.s, vc, a.s, a.t}, 0.0, 0.0, 0.0, sv, y);
+            spmv_row<B>(a, l, 3, Vecs{a.r, a.s, vc, a.s, a.t}, 0.0, 0.0, 0.0, sv, y, nullptr, cpa);
           }
 #pragma unroll
           for (int e = 0; e < B; ++e) a.sh[l * B + e] = sv[e] + (sv[e] - y[e]);
         }
+        cp_adv(false);
       }
       sync();
       flip();
@@ -672,23 +747,29 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     if (ilu) ilu_apply<B>(a.fa, a.s, a.sh, sync);  // sh = (LU)^{-1} s
     // ---- t = Â s (BJ) or t = Â sh (Neumann-1, ILU(0)); (s,s), (t,s), (t,t), (r0,s), (r0,t)
     pre_first();
+    cp_first(PRE);
     ROUNDS_BEGIN
     pf(rd0);
+    cp_next(rd0, PRE);
     if (ok) {
-      double sv[B], y[B];
+      double sv[B], y[B], r0e[B];
+      if (B <= RSIM_EARLY_R0_BMAX && RSIM_EARLY_R0) {  // as in the v pass: r0 before the product, not behind the stores of s and t
+#pragma unroll
+        for (int e = 0; e < B; ++e) r0e[e] = a.r0[l * B + e];
+      }
       if (prec) {
         if (fuse) nbr_val<B>(2, V2, l, 0.0, 0.0, alpha, sv);
         else
 #pragma unroll
           for (int e = 0; e < B; ++e) sv[e] = a.s[l * B + e];
-        spmv_row<B>(a, l, 3, Vecs{a.r, a.sh, vc, a.s, a.t}, 0.0, 0.0, 0.0, &a.sh[l * B], y, pre);
+        spmv_row<B>(a, l, 3, Vecs{a.r, a.sh, vc, a.s, a.t}, 0.0, 0.0, 0.0, &a.sh[l * B], y, pre, cpr);
       } else if (fs) {
         nbr_val<B>(2, V2, l, 0.0, 0.0, alpha, sv);
-        spmv_row<B>(a, l, 2, V2, 0.0, 0.0, alpha, sv, y, pre);
+        spmv_row<B>(a, l, 2, V2, 0.0, 0.0, alpha, sv, y, pre, cpr);
       } else {
 #pragma unroll
         for (int e = 0; e < B; ++e) sv[e] = a.s[l * B + e];
-        spmv_row<B>(a, l, 3, Vecs{a.r, a.s, vc, a.s, a.t}, 0.0, 0.0, 0.0, sv, y, pre);
+        spmv_row<B>(a, l, 3, Vecs{a.r, a.s, vc, a.s, a.t}, 0.0, 0.0, 0.0, sv, y, pre, cpr);
       }
       if (fs)
 #pragma unroll
@@ -698,9 +779,14 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
       val[0] = rsim::blk::rowdot<B>(sv, sv);
       val[1] = rsim::blk::rowdot<B>(y, sv);
       val[2] = rsim::blk::rowdot<B>(y, y);
-      val[3] = rsim::blk::rowdot<B>(&a.r0[l * B], sv);
-      val[4] = rsim::blk::rowdot<B>(&a.r0[l * B], y);
+      if (!(B <= RSIM_EARLY_R0_BMAX && RSIM_EARLY_R0)) {
+#pragma unroll
+        for (int e = 0; e < B; ++e) r0e[e] = a.r0[l * B + e];
+      }
+      val[3] = rsim::blk::rowdot<B>(r0e, sv);
+      val[4] = rsim::blk::rowdot<B>(r0e, y);
     }
+    cp_adv(PRE);
     pre_next(rd0);
     ROUNDS_END(5)
     reduce(5);
@@ -737,15 +823,39 @@ __global__ void __launch_bounds__(KT, 1) k_bicgstab(const KArgs a) {
     //  measured on config 5 and are slower: 20 %: 28.1 -> 29.1 ms, 100 %: 115.7 -> 118.4 ms)
     for (int64_t rd0 = blockIdx.x; rd0 < nrounds; rd0 += gridDim.x) {
       const int64_t l = rmap(rd0) * KT + tid;
-      if (l < nr)
+      if (l < nr) {
+        if (B > 1 && RSIM_XR_LOADFIRST) {
+          // b >= 2: all b components' loads before the first store — component by component, the
+          // stores of x and r (which may alias the other vectors as far as the compiler knows)
+          // fence the next component's loads: b dependent DRAM round trips per row
+          double xx[B], pp[B], hh[B], sq[B], tq[B], pq[B], vq[B];
 #pragma unroll
-        for (int e = 0; e < B; ++e) {
-          const int64_t q = l * B + e;
-          a.x[q] = (a.x[q] + alpha * phv[q]) + omega * shv[q];
-          const double rq = a.s[q] - omega * a.t[q];
-          a.r[q] = rq;
-          if (pfuse) pn[q] = rq + beta_next * (pc[q] - omega * vc[q]);
+          for (int e = 0; e < B; ++e) {
+            const int64_t q = l * B + e;
+            xx[e] = a.x[q]; pp[e] = phv[q]; hh[e] = shv[q];
+            sq[e] = prec ? a.s[q] : hh[e];
+            tq[e] = a.t[q];
+            if (pfuse) { pq[e] = prec ? pc[q] : pp[e]; vq[e] = vc[q]; }
+          }
+#pragma unroll
+          for (int e = 0; e < B; ++e) {
+            const int64_t q = l * B + e;
+            a.x[q] = (xx[e] + alpha * pp[e]) + omega * hh[e];
+            const double rq = sq[e] - omega * tq[e];
+            a.r[q] = rq;
+            if (pfuse) pn[q] = rq + beta_next * (pq[e] - omega * vq[e]);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < B; ++e) {
+            const int64_t q = l * B + e;
+            a.x[q] = (a.x[q] + alpha * phv[q]) + omega * shv[q];
+            const double rq = a.s[q] - omega * a.t[q];
+            a.r[q] = rq;
+            if (pfuse) pn[q] = rq + beta_next * (pc[q] - omega * vc[q]);
+          }
         }
+      }
     }
     if (RSIM_KTIME) { sync(); tick(6); }
     p_ready = pfuse;

@@ -90,6 +90,20 @@ def test_grid_path_full_set(cfg, precond):
 
 
 @pytest.mark.parametrize("precond", [pkg.PREC_BJACOBI, pkg.PREC_NEUMANN1])
+@pytest.mark.parametrize("cfg,nA", [(dict(config=4, nx=64, ny=64, nz=8, n_dfn=12), 20000),
+                                    (dict(config=2, nx=200, ny=200, n_dfn=40), 24000),
+                                    (dict(config=5, nx=128, ny=128, nz=4), 40000)])
+def test_grid_path_partial_set(cfg, nA, precond):
+    # partial sets on the cooperative-grid kernel (> 16384 rows): stored columns, the per-row
+    # NNC flag of the assembly (b = 2 / 3 cases have DFN NNCs), row-major (b = 3) and
+    # warp-tiled (b <= 2) block values, b = 1 next-round row preload and L2 prefetch
+    case = pkg.Case(**cfg)
+    rng = np.random.default_rng(nA)
+    act = np.sort(rng.choice(case.n, nA, replace=False)).astype(np.int32)
+    _check(case, act, precond=precond)
+
+
+@pytest.mark.parametrize("precond", [pkg.PREC_BJACOBI, pkg.PREC_NEUMANN1])
 def test_grid_path_distributed_level2_reduction(precond):
     # > 64*256*256 rows => level-2 partials reduced across CTAs (extra barrier);
     # > 2^20 rows => the unfused (store, barrier, gather) Krylov variant
@@ -100,7 +114,8 @@ def test_grid_path_distributed_level2_reduction(precond):
 
 @pytest.mark.parametrize("precond", [pkg.PREC_BJACOBI, pkg.PREC_NEUMANN1])
 def test_grid_path_unfused_converged(precond):
-    # unfused variant run to convergence (early-exit branch) on 1.3 M rows, b=2
+    # 1.3 M rows, b = 2, run to convergence (early-exit branch); b >= 2 uses the recompute-fused
+    # variant at every size since round 2 (b = 1 above 2^20 rows is the unfused one, see above)
     case = pkg.Case(3, nx=160, ny=128, nz=64)
     assert case.n > (1 << 20)
     _check(case, None, precond=precond)
