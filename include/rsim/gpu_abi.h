@@ -122,7 +122,8 @@ int rsim_gpu_timers(rsim_gpu_ctx* ctx, int32_t enable, double* ms4, int32_t* lau
 int rsim_gpu_counters(rsim_gpu_ctx* ctx, int64_t* out5, int32_t reset);
 /* b > 1, accumulated with the counters above: [0] Σ its · off-diagonal ELL
  * blocks stored by the assembly (active Cartesian neighbours), [1] Σ its · the
- * pressure-only ones among them (blockops.h col0_only: b of b² entries read). */
+ * pressure-only ones among them (blockops.h col0_only; statistics only: the
+ * Krylov kernels load and multiply them whole). */
 int rsim_gpu_block_counters(rsim_gpu_ctx* ctx, int64_t* out2, int32_t reset);
 
 /* Debug flags: bit 0 = the large-set assembly also stores the raw residual F
