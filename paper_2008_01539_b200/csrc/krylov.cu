@@ -95,6 +95,7 @@ struct KArgs {
   double* part2;  // [5][pstride2] level-2 partials (very large systems)
   int32_t pstride, pstride2;
   int32_t red_small_max;  // chunk partials reduced redundantly by every CTA up to this count
+  int32_t stream;         // b = 1: matrix values through streaming (evict-first) loads
   int32_t kblk;           // consecutive rounds per CTA (blocked-cyclic distribution; 1 = round-robin)
   int32_t alt;            // sweep direction alternates between phases (L2 reuse of the previous sweep's tail)
   DevScalars* dsc;
@@ -245,6 +246,9 @@ __device__ __forceinline__ void nbr_val(int mode, const Vecs& X, int64_t j, doub
 #ifndef RSIM_PRE1
 #define RSIM_PRE1 1
 #endif
+#ifndef RSIM_LDCS  // experiment: matrix values through streaming (evict-first) loads so the vectors keep L2
+#define RSIM_LDCS 0
+#endif
 #ifndef RSIM_EARLY_R0  // b = 1: r0 / r of a row requested before its product (see the v pass)
 #define RSIM_EARLY_R0 1
 #endif
@@ -266,13 +270,13 @@ __device__ __forceinline__ void pre_load1(const KArgs& a, int64_t l, bool ok, Pr
     implicit_cols(a.nx, a.ny, a.nz, a.d3, l, P.c);
 #pragma unroll
     for (int s = 0; s < 6; ++s)
-      if (P.c[s] >= 0) P.m[s] = a.ell_val[(int64_t)s * a.cap + l];
+      if (P.c[s] >= 0) P.m[s] = (RSIM_LDCS || a.stream) ? __ldcs(&a.ell_val[(int64_t)s * a.cap + l]) : a.ell_val[(int64_t)s * a.cap + l];
   } else {  // columns not known yet: the value slot of an absent neighbour is loaded and ignored
 #pragma unroll
     for (int s = 0; s < 6; ++s)
       if (s < a.nslot) {
         P.c[s] = __ldg(&a.ell_col[(int64_t)s * a.cap + l]);
-        P.m[s] = a.ell_val[(int64_t)s * a.cap + l];
+        P.m[s] = (RSIM_LDCS || a.stream) ? __ldcs(&a.ell_val[(int64_t)s * a.cap + l]) : a.ell_val[(int64_t)s * a.cap + l];
       }
   }
 }
@@ -354,10 +358,27 @@ __device__ __forceinline__ void spmv_row(const KArgs& a, int64_t l, int mode, co
         if (B == 1 && pre) {
           rsim::blk::gemv_acc_flat<B>(&pre->m[s0 + k], xv[k], acc);
         } else if (ell_es(B * B) == 1) {  // row-major blocks: the product reads them in place
-          rsim::blk::gemv_acc_flat<B>(&val[ell_at(a.cap, B * B, s0 + k, 0, l)], xv[k], acc);
+          const double* __restrict__ Mp = &val[ell_at(a.cap, B * B, s0 + k, 0, l)];
+#if RSIM_LDCS
+#pragma unroll
+          for (int r = 0; r < B; ++r) {  // gemv_acc_flat's expression order, streaming (evict-first) loads
+            double sm = __ldcs(&Mp[r * B]) * xv[k][0];
+#pragma unroll
+            for (int c = 1; c < B; ++c) sm = sm + __ldcs(&Mp[r * B + c]) * xv[k][c];
+            acc[r] = acc[r] + sm;
+          }
+#else
+          rsim::blk::gemv_acc_flat<B>(Mp, xv[k], acc);
+#endif
         } else {
           double M[B * B];
+#if RSIM_LDCS
+          const double* __restrict__ vp = val + ell_at(a.cap, B * B, s0 + k, 0, l);
+#pragma unroll
+          for (int e = 0; e < B * B; ++e) M[e] = __ldcs(&vp[e * ell_es(B * B)]);
+#else
           ell_load<B>(val, a.cap, s0 + k, l, M);
+#endif
           rsim::blk::gemv_acc_flat<B>(M, xv[k], acc);
         }
       }
@@ -953,6 +974,11 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
   {
     const int64_t row_bytes = (int64_t)c->nslot * (8 * B * B + 4) + 11 * 8 * B;
     a.alt = alt_env >= 0 ? alt_env : ((int64_t)c->nA * row_bytes > (int64_t)100e6 ? 1 : 0);
+    // b = 1, working set beyond L2: the matrix values (read once per pass) go through
+    // ld.global.cs so the gathered vectors keep L2 (config 5 at 100 %: 110.0 -> 107.4 ms per 50
+    // iterations, 20 %: 24.5 -> 24.3).  Not for b >= 2: config 3, whose matrix fits in L2,
+    // 1.28 -> 1.51 s per run; config 4 8.72 -> 8.77 s.
+    a.stream = (B == 1 && (int64_t)c->nA * row_bytes > (int64_t)100e6) ? 1 : 0;
   }
   static const int kblk_env = [] {  // env override: tuning only
     const char* e = std::getenv("RSIM_KBLK");
