@@ -1,4 +1,5 @@
 #!/bin/bash
+# Needs the comparison tree: git worktree add _prev a831c67 && (cd _prev && python -c "from paper_2008_01539_b200 import build; build.build()")
 # per-launch durations of the grid BiCGSTAB over the whole config-4 run, HEAD vs _prev
 O=gpurun_out/ab5; mkdir -p $O
 for d in . _prev; do

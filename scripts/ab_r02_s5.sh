@@ -1,4 +1,5 @@
 #!/bin/bash
+# Optional comparison tree: git worktree add _prev a831c67 && (cd _prev && python -c "from paper_2008_01539_b200 import build; build.build()")
 # A/B on one box: GPU test suite, then whole c3 / c4 localized runs of HEAD against the
 # tree of commit a831c67 (_prev/, when present) and optional lib/ab/librsim_<name>.so variants.
 O=gpurun_out/ab5; mkdir -p $O
