@@ -947,11 +947,13 @@ int launch_b(rsim_gpu_ctx* c, const rsim_solver_opts* o) {
     return (e && *e) ? (int64_t)std::atoll(e) : (int64_t)-1;
   }();
   a.fuse = (c->nA <= (fuse_max >= 0 ? fuse_max : fuse_max_rows(B)) && !a.ilu) ? 1 : 0;
-  // s recompute at the gather sites: measured on config 5 (50 iterations),
-  // 9.50 -> 9.35 ms at 5 % (1.7 M rows), even at 20 %, 114.5 -> 119.1 ms at 100 %
+  // s recompute at the gather sites (unfused block-Jacobi: no s pass, one grid barrier less), at
+  // every size.  Round 1 measured a loss above 4 M rows (config 5 at 100 %: 114.5 -> 119.1 ms per 50
+  // iterations) and capped it at 2^22; with the row preload and the early r0 / r loads of round 2
+  // it wins everywhere: 20 % (6.7 M rows) 24.85 -> 23.60 ms, 50 % 57.0 -> 56.6, 100 % 109.9 -> 108.2.
   static const int64_t fuse_s_max = [] {  // env override: tuning only
     const char* e = std::getenv("RSIM_FUSE_S_MAX_ROWS");
-    return (e && *e) ? (int64_t)std::atoll(e) : (int64_t)1 << 22;
+    return (e && *e) ? (int64_t)std::atoll(e) : (int64_t)1 << 40;
   }();
   a.fuse_s = c->nA <= fuse_s_max ? 1 : 0;
   static const int32_t red_small = [] {  // env override: tuning only
